@@ -1,0 +1,146 @@
+/*
+ * mpm.h -- C ABI of the B200-native differentiable MLS-MPM step
+ *          (ChainQueen, arXiv 1810.01054; library paper_1810_01054_b200/libmpm.so, sm_100a).
+ *
+ * The problem statement follows the paper: a "memo" holds a whole rollout plus the initial
+ * state p0 and the parameters used at every step (Fig. 2 caption P:173); the
+ * caller asks for the gradient of a loss on the final state with respect to the initial
+ * state and to the parameters, here the per-step actuation and the
+ * per-particle Young's modulus / Poisson ratio.
+ *
+ *   forward  = P2G (Eqs. 3-5, with S1 P:430) -> grid (Eq. 6, plus
+ *              gravity and wall friction) -> G2P (Eqs. 7-10);
+ *   backward = the supplement's steps A-L per step, chained from the last step
+ *              to the first.
+ * Readings of the paper where it is silent are DESIGN.md R1-R19 (neo-Hookean psi, quadratic
+ * B-spline, wall bands, epsilon, ...).
+ *
+ * Conventions
+ *  - Ownership: the context owns every device buffer it allocates.  Input pointers are
+ *    borrowed for the duration of the call and copied; they may be host (pageable or pinned)
+ *    or device pointers (UVA, detected by the CUDA runtime).  Output buffers belong to the
+ *    caller and may also be host or device.
+ *  - Layout of user arrays (row-major, fp32 unless stated):
+ *      x, v          [batch][n_particles][dim]
+ *      F, C          [batch][n_particles][dim][dim]   (F[p][row][col])
+ *      mass, vol, E, nu            [batch][n_particles]
+ *      actuator_id   [batch][n_particles] int32, -1 = not actuated, else in [0, n_actuators)
+ *      actuation a   [batch][max_steps][n_actuators][dim]   (sigma_pa = act_strength*Diag(a))
+ *    All user-visible arrays are in the user's particle order; the per-step sort is internal.
+ *  - Errors: status codes only; nothing throws across the ABI.  Device-side faults (particle
+ *    outside the domain, inverted element) are latched on the device as (code, step,
+ *    particle) and returned by the synchronising call that ends mpm_forward / mpm_backward.
+ *    After MPM_ERR_OUT_OF_DOMAIN / MPM_ERR_INVERTED the context refuses forward/backward
+ *    until mpm_set_state.  mpm_last_error() returns a human-readable message.
+ *  - Streams: all work is ordered on config.stream (a cudaStream_t; NULL = the legacy
+ *    default stream).  mpm_forward, mpm_backward, mpm_get_*, mpm_grad synchronise the stream
+ *    before returning.  One context per host thread.
+ */
+#ifndef MPM_H
+#define MPM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mpm_ctx_s* mpm_ctx;
+
+typedef enum {
+  MPM_OK = 0,
+  MPM_ERR_INVALID_ARG = 1,
+  MPM_ERR_OOM = 2,
+  MPM_ERR_CUDA = 3,
+  MPM_ERR_OUT_OF_DOMAIN = 4, /* base index outside [0, res-3] (DESIGN R14)          */
+  MPM_ERR_INVERTED = 5,      /* det F <= 0, ln J undefined (DESIGN R14)             */
+  MPM_ERR_TAPE_FULL = 6,     /* forward beyond max_steps, or grid-slot arena full    */
+  MPM_ERR_CALL_ORDER = 7,    /* e.g. backward before forward, grad before backward   */
+  MPM_ERR_COMM = 8
+} mpm_status;
+
+typedef struct {
+  int32_t dim;          /* 2 or 3                                                     */
+  int32_t res;          /* grid nodes per axis, power of two, 16..4096; dx = 1/res     */
+  int32_t batch;        /* B independent rollouts ...                                 */
+  int32_t n_particles;  /* ... of N particles each (N < 2^25)                         */
+  int32_t max_steps;    /* tape capacity T (the memo holds states 0..T)               */
+  int32_t n_actuators;  /* K (0..64)                                                  */
+  float dt;             /* time step                                                  */
+  float gravity[3];     /* added on the grid after Eq. 6 (R5)                         */
+  int32_t bound;        /* wall band width in nodes (R6), >= 0, 2*bound < res          */
+  float friction[6];    /* c per wall (-x,+x,-y,+y,-z,+z); c < 0 => sticky (R6)        */
+  float act_strength;   /* s in sigma_pa = s * Diag(a[t][k])  (R4)                    */
+  int32_t device;       /* CUDA device ordinal                                        */
+  void* stream;         /* cudaStream_t or NULL                                       */
+  int32_t grid_slots;   /* grid-block slots per step in the tape arena; 0 = automatic */
+} mpm_config;
+
+/* Create a context on config->device.  Validates the config (MPM_ERR_INVALID_ARG) and
+ * allocates the fixed-size buffers (MPM_ERR_OOM); the tape is allocated by mpm_set_state. */
+mpm_status mpm_create(const mpm_config* config, mpm_ctx* out);
+void mpm_destroy(mpm_ctx ctx);
+
+/* Initial state p0 and constant per-particle parameters; resets the tape to t = 0,
+ * clears every gradient and the error latch.  E > 0, 0 <= nu < 0.5, mass > 0, vol > 0. */
+mpm_status mpm_set_state(mpm_ctx ctx, const float* x, const float* v, const float* F,
+                         const float* C, const float* mass, const float* vol, const float* E,
+                         const float* nu, const int32_t* actuator_id);
+
+/* Open-loop actuation for every step, [batch][max_steps][n_actuators][dim]. */
+mpm_status mpm_set_actuation(mpm_ctx ctx, const float* a);
+
+/* Advance n_steps steps from the current tape end, appending states to the memo.
+ * MPM_ERR_TAPE_FULL if the tape would exceed max_steps.                                 */
+mpm_status mpm_forward(mpm_ctx ctx, int32_t n_steps);
+
+/* Number of steps currently on the tape. */
+int32_t mpm_tape_length(mpm_ctx ctx);
+
+/* Truncate the tape to its first t steps (0 <= t <= tape length), keeping states 0..t, so
+ * the rollout can be re-run from state t (e.g. with new actuation) without re-uploading.
+ * Clears the error latch and the gradients.                                               */
+mpm_status mpm_rewind(mpm_ctx ctx, int32_t t);
+
+/* State at tape step t (0 <= t <= tape length), user particle order.  NULL = skip. */
+mpm_status mpm_get_state(mpm_ctx ctx, int32_t t, float* x, float* v, float* F, float* C);
+
+/* Reverse mode over the whole tape: seed dL/dstate at t = tape length, user order,
+ * same layouts as x, v, F, C; NULL = zero.  Requires a forward tape (MPM_ERR_CALL_ORDER). */
+mpm_status mpm_backward(mpm_ctx ctx, const float* dLdx, const float* dLdv, const float* dLdF,
+                        const float* dLdC);
+
+/* Gradients from the last mpm_backward: w.r.t. the initial state (user order), E and nu
+ * [batch][n], and the actuation [batch][max_steps][n_actuators][dim] (steps beyond the tape
+ * length are 0).  NULL = skip.  MPM_ERR_CALL_ORDER before any backward.                 */
+mpm_status mpm_grad(mpm_ctx ctx, float* dx0, float* dv0, float* dF0, float* dC0, float* dE,
+                    float* dnu, float* da);
+
+const char* mpm_last_error(mpm_ctx ctx);
+
+/* ---- introspection, used by the parity tests (all synchronous) ---- */
+
+/* Binning of tape step t (north_star item 1): positions as stored for step t in the
+ * internal storage order (x_store [B*N][dim]), the storage-to-user map orig [B*N], the
+ * keys [B*N] computed from x_store, the stable sort perm [B*N] (sorted slot -> storage
+ * index) and block_start [B*nb + 1], nb = (res/Bb)^dim, Bb = 4 (3D) / 8 (2D).  t < tape
+ * length.  NULL = skip.                                                                  */
+mpm_status mpm_get_binning(mpm_ctx ctx, int32_t t, float* x_store, int32_t* orig,
+                           int32_t* key, int32_t* perm, int32_t* block_start);
+
+/* Grid of tape step t as stored in the memo, dense [B][res^dim]: node mass m and vbar =
+ * p/m + dt g (before the wall projection, R5/R6); 0 on untouched nodes.                 */
+mpm_status mpm_get_grid(mpm_ctx ctx, int32_t t, float* m, float* vbar);
+
+/* Per-kernel device time (ms) and launch counts accumulated while profiling is on; names
+ * are returned as a ';'-separated list.  n_kernels in/out. */
+mpm_status mpm_set_profiling(mpm_ctx ctx, int32_t on);
+mpm_status mpm_get_profile(mpm_ctx ctx, int32_t* n_kernels, float* ms, int64_t* launches,
+                           char* names, int32_t names_len);
+/* Total kernel launches issued by this context since creation. */
+int64_t mpm_launch_count(mpm_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MPM_H */

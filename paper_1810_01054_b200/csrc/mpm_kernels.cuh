@@ -1,0 +1,1414 @@
+// mpm_kernels.cuh -- sm_100a kernels of the differentiable MLS-MPM step
+// (ChainQueen, arXiv 1810.01054).  Product code: shares nothing with oracle/.
+//
+// Citations: P:<line> = PAPER.md line; R<k> = DESIGN.md reading k.
+//
+// Layout:
+//   particle state, tape step t: SoA, component-major, "storage order t"
+//       comp(x_a) = a, comp(v_a) = D + a, comp(C_ab) = 2D + aD + b, comp(F_ab) = 2D + D^2 + aD + b
+//       value of particle j = state[comp * NT + j]
+//     storage order t+1 == the sorted (block, cell, index) order of step t.
+//   grid: sparse, one 64-node slot (1 KiB, float4 per node) per touched block of Bb^D
+//     nodes (Bb = 4 in 3D, 8 in 2D); node float4 = (p_x, p_y, p_z, m) after P2G,
+//     (vbar_x, vbar_y, vbar_z, m) after the grid update; slots of step t live in the tape arena.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpm {
+
+constexpr int kCPB = 64;         // cells (and nodes) per grid block
+constexpr int kThreads = 256;    // CTA size of the block-tile kernels
+constexpr int kCap = 256;        // particles per producer chunk
+constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks use scratch)
+constexpr int kScanTile = 2048;  // grid blocks per scan tile
+constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
+
+enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6 };
+
+template <int D> struct Dim;
+template <> struct Dim<3> {
+  static constexpr int BB = 4, LOG_BB = 2, NS = 27, TE = 6, TN = 216, S = 24;
+};
+template <> struct Dim<2> {
+  static constexpr int BB = 8, LOG_BB = 3, NS = 9, TE = 10, TN = 100, S = 12;
+};
+
+// Step-invariant parameters, passed by value.
+struct KParams {
+  int res, B, N, NT, nbpa, nb, NBT, K, T;  // T = max_steps (actuation stride)
+  float dt, dx, fres;                       // dx = 1/res, fres = res
+  float g[3];
+  int bound;
+  float fric[6];
+  float act_s;
+  int slots_per_step;                       // per-step cap of touched blocks
+  int arena_slots;                          // capacity of the tape grid arena
+};
+
+// Per-step bookkeeping record, info[t * kInfo + field]
+constexpr int kInfo = 8;
+enum { I_NOCC = 0, I_NTOUCH = 1, I_BASE = 2, I_WORK = 3, I_WORK2 = 4, I_OK = 5 };
+
+struct ErrLatch { int code, step, particle, pad; };
+
+__device__ __forceinline__ void latch(ErrLatch* e, int code, int step, int particle) {
+  if (atomicCAS(&e->code, 0, code) == 0) {
+    e->step = step;
+    e->particle = particle;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// index helpers
+// ------------------------------------------------------------------------------------
+template <int D> __device__ __forceinline__ int comp_x(int a) { return a; }
+template <int D> __device__ __forceinline__ int comp_v(int a) { return D + a; }
+template <int D> __device__ __forceinline__ int comp_C(int a, int b) { return 2 * D + a * D + b; }
+template <int D> __device__ __forceinline__ int comp_F(int a, int b) { return 2 * D + D * D + a * D + b; }
+
+// block linear index inside one rollout from block coords (row-major, axis 0 slowest)
+template <int D> __device__ __forceinline__ int block_lin(const int* b, int nbpa) {
+  int l = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) l = l * nbpa + b[a];
+  return l;
+}
+template <int D> __device__ __forceinline__ int cell_lin(const int* c) {
+  int l = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) l = l * Dim<D>::BB + c[a];
+  return l;
+}
+
+// ------------------------------------------------------------------------------------
+// quadratic B-spline stencil (R2) in fp32.  xg = x * res is exact (res = 2^k); the base
+// decision floor(xg - 0.5f) is the binning decision of R17.
+// ------------------------------------------------------------------------------------
+template <int D> struct Stencil {
+  int base[D];
+  float fx[D];
+  float w[D][3];
+};
+
+__device__ __forceinline__ int base_of(float x, float fres) {
+  float xg = x * fres;
+  return (int)floorf(xg - 0.5f);
+}
+
+template <int D>
+__device__ __forceinline__ void make_stencil(const float* x, float fres, Stencil<D>& s) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float xg = x[a] * fres;
+    int b = (int)floorf(xg - 0.5f);
+    float f = xg - (float)b;  // in [0.5, 1.5), exact
+    s.base[a] = b;
+    s.fx[a] = f;
+    float u0 = 1.5f - f, u1 = f - 1.0f, u2 = f - 0.5f;
+    s.w[a][0] = 0.5f * u0 * u0;
+    s.w[a][1] = 0.75f - u1 * u1;
+    s.w[a][2] = 0.5f * u2 * u2;
+  }
+}
+
+// dN/du at the three nodes, u = fx - o:  (fx - 1.5, -2 (fx - 1), fx - 0.5)
+__device__ __forceinline__ void stencil_dw(float f, float* dw) {
+  dw[0] = f - 1.5f;
+  dw[1] = -2.0f * (f - 1.0f);
+  dw[2] = f - 0.5f;
+}
+
+// ------------------------------------------------------------------------------------
+// neo-Hookean Kirchhoff stress (R1) + actuation (S1, R3/R4):
+//   tau = mu (F F^T - I) + lam ln J I + F Diag(sig) F^T   ( = P_total F^T )
+// ------------------------------------------------------------------------------------
+template <int D> __device__ __forceinline__ float det(const float (&F)[D][D]);
+template <> __device__ __forceinline__ float det<2>(const float (&F)[2][2]) {
+  return F[0][0] * F[1][1] - F[0][1] * F[1][0];
+}
+template <> __device__ __forceinline__ float det<3>(const float (&F)[3][3]) {
+  return F[0][0] * (F[1][1] * F[2][2] - F[1][2] * F[2][1]) -
+         F[0][1] * (F[1][0] * F[2][2] - F[1][2] * F[2][0]) +
+         F[0][2] * (F[1][0] * F[2][1] - F[1][1] * F[2][0]);
+}
+
+// inverse transpose F^{-T}
+template <int D> __device__ __forceinline__ void inv_T(const float (&F)[D][D], float J, float (&G)[D][D]);
+template <> __device__ __forceinline__ void inv_T<2>(const float (&F)[2][2], float J, float (&G)[2][2]) {
+  float iJ = 1.0f / J;
+  G[0][0] = F[1][1] * iJ; G[0][1] = -F[1][0] * iJ;
+  G[1][0] = -F[0][1] * iJ; G[1][1] = F[0][0] * iJ;
+}
+template <> __device__ __forceinline__ void inv_T<3>(const float (&F)[3][3], float J, float (&G)[3][3]) {
+  float iJ = 1.0f / J;
+  // cofactor matrix / J = F^{-T}
+  G[0][0] = (F[1][1] * F[2][2] - F[1][2] * F[2][1]) * iJ;
+  G[0][1] = (F[1][2] * F[2][0] - F[1][0] * F[2][2]) * iJ;
+  G[0][2] = (F[1][0] * F[2][1] - F[1][1] * F[2][0]) * iJ;
+  G[1][0] = (F[0][2] * F[2][1] - F[0][1] * F[2][2]) * iJ;
+  G[1][1] = (F[0][0] * F[2][2] - F[0][2] * F[2][0]) * iJ;
+  G[1][2] = (F[0][1] * F[2][0] - F[0][0] * F[2][1]) * iJ;
+  G[2][0] = (F[0][1] * F[1][2] - F[0][2] * F[1][1]) * iJ;
+  G[2][1] = (F[0][2] * F[1][0] - F[0][0] * F[1][2]) * iJ;
+  G[2][2] = (F[0][0] * F[1][1] - F[0][1] * F[1][0]) * iJ;
+}
+
+template <int D>
+__device__ __forceinline__ void kirchhoff(const float (&F)[D][D], float mu, float lam,
+                                          const float* sig, float (&tau)[D][D], float lnJ) {
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = a; b < D; ++b) {
+      float ff = 0.f, fsf = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        ff = fmaf(F[a][c], F[b][c], ff);
+        fsf = fmaf(F[a][c] * sig[c], F[b][c], fsf);
+      }
+      float t = mu * (ff - (a == b ? 1.f : 0.f)) + fsf;
+      if (a == b) t += lam * lnJ;
+      tau[a][b] = t;
+      tau[b][a] = t;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Wall-band friction projection of step L (R6 band geometry, R7, R8), applied
+// to a node's vbar on read.  Walls are axis aligned: n = +e_a (low wall), -e_a (high).
+// ------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ bool in_band(const int* node, int res, int bound) {
+  bool b = false;
+#pragma unroll
+  for (int a = 0; a < D; ++a) b |= (node[a] < bound) | (node[a] >= res - bound);
+  return b;
+}
+
+// one wall: v <- proj(v), normal n = sgn * e_ax
+template <int D>
+__device__ __forceinline__ void project_wall(float* v, int ax, float sgn, float c) {
+  if (c < 0.f) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) v[a] = 0.f;
+    return;
+  }
+  float ln = sgn * v[ax];
+  if (ln >= 0.f) return;  // R8 identity branch
+  float s2 = 0.f;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    if (a != ax) s2 = fmaf(v[a], v[a], s2);
+  float lt = sqrtf(s2 + kEps);
+  float lts = fmaxf(lt + c * ln, 0.f);
+  float sc = lts / lt;
+#pragma unroll
+  for (int a = 0; a < D; ++a) v[a] = (a == ax) ? 0.f : v[a] * sc;
+}
+
+template <int D>
+__device__ __forceinline__ void project_node(float* v, const int* node, const KParams& P) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    if (node[a] < P.bound) project_wall<D>(v, a, 1.f, P.fric[2 * a]);
+    if (node[a] >= P.res - P.bound) project_wall<D>(v, a, -1.f, P.fric[2 * a + 1]);
+  }
+}
+
+// adjoint of project_wall: g (= dL/dv*) -> dL/dv, given the wall's input v
+template <int D>
+__device__ __forceinline__ void project_wall_adj(const float* v, float* g, int ax, float sgn, float c) {
+  if (c < 0.f) {
+#pragma unroll
+    for (int a = 0; a < D; ++a) g[a] = 0.f;
+    return;
+  }
+  float ln = sgn * v[ax];
+  if (ln >= 0.f) return;
+  float s2 = 0.f;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    if (a != ax) s2 = fmaf(v[a], v[a], s2);
+  float lt = sqrtf(s2 + kEps);
+  float R = lt + c * ln;
+  float H = (R >= 0.f) ? 1.f : 0.f;
+  float lts = fmaxf(R, 0.f);
+  float s = lts / lt;
+  // v* = s * v_t ;  s = max(R,0)/lt ; ds/dlt = (H lt - lts)/lt^2 ; ds/dln = H c / lt
+  float gs = 0.f;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    if (a != ax) gs = fmaf(g[a], v[a], gs);
+  float k1 = gs * (H * lt - lts) / (lt * lt * lt);
+  float gln = gs * H * c / lt;  // minus (g_vt . n) = 0 since v_t . n = 0 direction has g_vt_n = s g_n
+  float gvt[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) gvt[a] = (a == ax) ? s * g[a] : fmaf(s, g[a], k1 * v[a]);
+  // ln = sgn v_ax;  v_t = v - ln n  ->  dv = g_vt (I - n n^T) + (gln) n
+#pragma unroll
+  for (int a = 0; a < D; ++a) g[a] = (a == ax) ? sgn * gln : gvt[a];
+}
+
+// adjoint of project_node (reverse wall order, R6), g in/out, vbar = node input
+template <int D>
+__device__ __forceinline__ void project_node_adj(const float* vbar, float* g, const int* node,
+                                                 const KParams& P) {
+  // replay forward, storing the input of every active wall (at most 2 per axis, 1 in practice)
+  float vin[2 * D][D];
+  int wax[2 * D];
+  float wsg[2 * D], wc[2 * D];
+  int nw = 0;
+  float v[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) v[a] = vbar[a];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      bool act = side == 0 ? (node[a] < P.bound) : (node[a] >= P.res - P.bound);
+      if (act) {
+#pragma unroll
+        for (int q = 0; q < D; ++q) vin[nw][q] = v[q];
+        wax[nw] = a;
+        wsg[nw] = side == 0 ? 1.f : -1.f;
+        wc[nw] = P.fric[2 * a + side];
+        project_wall<D>(v, a, wsg[nw], wc[nw]);
+        ++nw;
+      }
+    }
+  }
+  for (int w = nw - 1; w >= 0; --w) project_wall_adj<D>(vin[w], g, wax[w], wsg[w], wc[w]);
+}
+
+// ------------------------------------------------------------------------------------
+// warp-aggregated histogram increment
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void warp_hist_add(int* cnt, int gb, bool valid) {
+  unsigned vm = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  unsigned peers = __match_any_sync(vm, gb);
+  int lane = threadIdx.x & 31;
+  if (lane == __ffs(peers) - 1) atomicAdd(&cnt[gb], __popc(peers));
+}
+
+// key of a particle from its fp32 position (north_star item 1, R17); returns false when
+// the base index is outside [0, res-3] (R14).
+template <int D>
+__device__ __forceinline__ bool key_of(const float* x, int r, const KParams& P, int& gb, int& key) {
+  int blk[D], cell[D];
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    int b = base_of(x[a], P.fres);
+    ok &= (b >= 0) & (b <= P.res - 3);
+    b = min(max(b, 0), P.res - 3);  // keep the bookkeeping in range; the error is latched
+    blk[a] = b >> Dim<D>::LOG_BB;
+    cell[a] = b & (Dim<D>::BB - 1);
+  }
+  gb = r * P.nb + block_lin<D>(blk, P.nbpa);
+  key = gb * kCPB + cell_lin<D>(cell);
+  return ok;
+}
+
+// ------------------------------------------------------------------------------------
+// set_state helpers
+// ------------------------------------------------------------------------------------
+// user AoS [NT][D], [NT][D][D] -> SoA state; params -> {m, V, mu, lam}
+template <int D>
+__global__ void k_user_to_soa(KParams P, const float* __restrict__ x, const float* __restrict__ v,
+                              const float* __restrict__ F, const float* __restrict__ C,
+                              float* __restrict__ st) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.NT) return;
+  const size_t NT = P.NT;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    st[comp_x<D>(a) * NT + j] = x[j * D + a];
+    st[comp_v<D>(a) * NT + j] = v ? v[j * D + a] : 0.f;
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      st[comp_C<D>(a, b) * NT + j] = C ? C[(j * D + a) * D + b] : 0.f;
+      st[comp_F<D>(a, b) * NT + j] = F ? F[(j * D + a) * D + b] : (a == b ? 1.f : 0.f);
+    }
+  }
+}
+
+__global__ void k_params(int NT, const float* __restrict__ m, const float* __restrict__ V,
+                         const float* __restrict__ E, const float* __restrict__ nu,
+                         float4* __restrict__ prm, int* __restrict__ bad) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= NT) return;
+  float e = E[j], n = nu[j];
+  // Lame parameters (R1)
+  float mu = e / (2.f * (1.f + n));
+  float lam = e * n / ((1.f + n) * (1.f - 2.f * n));
+  if (!(m[j] > 0.f) || !(V[j] > 0.f) || !(e > 0.f) || !(n >= 0.f) || !(n < 0.5f)) atomicExch(bad, 1);
+  prm[j] = make_float4(m[j], V[j], mu, lam);
+}
+
+// keys, histogram and orig for t = 0 (storage order 0 = user order)
+template <int D>
+__global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __restrict__ key,
+                            int* __restrict__ cnt, int* __restrict__ orig, ErrLatch* err) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = j < P.NT;
+  int gb = 0, k = 0;
+  if (valid) {
+    float x[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[a] = st[(size_t)comp_x<D>(a) * P.NT + j];
+    if (!key_of<D>(x, j / P.N, P, gb, k)) latch(err, E_DOMAIN, 0, j);
+    key[j] = k;
+    orig[j] = j;
+  }
+  warp_hist_add(cnt, gb, valid);
+}
+
+// ------------------------------------------------------------------------------------
+// block table of step t: exclusive scans of (count, occupied, touched) over all grid
+// blocks, the occupied list, touched list and slot map; zeroes the step's grid slots.
+// touched(b) = some block b - delta, delta in {0,1}^D, holds particles (a particle with
+// base in block b' touches nodes of b' and b' + delta only).
+// ------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ void block_flags(const KParams& P, const int* cnt, int gb, int& c,
+                                            int& o, int& tch) {
+  c = cnt[gb];
+  o = c > 0;
+  int r = gb / P.nb, bl = gb - r * P.nb;
+  int b[D];
+  int t = bl;
+#pragma unroll
+  for (int a = D - 1; a >= 0; --a) { b[a] = t % P.nbpa; t /= P.nbpa; }
+  int any = 0;
+#pragma unroll
+  for (int dl = 0; dl < (1 << D); ++dl) {
+    int nb_[D];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      nb_[a] = b[a] - ((dl >> (D - 1 - a)) & 1);
+      ok &= nb_[a] >= 0;
+    }
+    if (ok) any |= cnt[r * P.nb + block_lin<D>(nb_, P.nbpa)] > 0;
+  }
+  tch = any;
+}
+
+__device__ __forceinline__ int3 warp_incl_scan3(int3 v) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int a = __shfl_up_sync(0xffffffffu, v.x, o);
+    int b = __shfl_up_sync(0xffffffffu, v.y, o);
+    int c = __shfl_up_sync(0xffffffffu, v.z, o);
+    if (lane >= o) { v.x += a; v.y += b; v.z += c; }
+  }
+  return v;
+}
+
+// CTA-wide exclusive scan of an int3 (kThreads threads)
+__device__ __forceinline__ int3 cta_excl_scan3(int3 v, int3* s_warp, int3& total) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int3 inc = warp_incl_scan3(v);
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int3 t = lane < kThreads / 32 ? s_warp[lane] : make_int3(0, 0, 0);
+    int3 ti = warp_incl_scan3(t);
+    if (lane < kThreads / 32) s_warp[lane] = make_int3(ti.x - t.x, ti.y - t.y, ti.z - t.z);
+    if (lane == kThreads / 32 - 1) s_warp[kThreads / 32] = ti;
+  }
+  __syncthreads();
+  int3 wo = s_warp[w];
+  total = s_warp[kThreads / 32];
+  return make_int3(wo.x + inc.x - v.x, wo.y + inc.y - v.y, wo.z + inc.z - v.z);
+}
+
+template <int D>
+__global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __restrict__ cnt,
+                                                     int3* __restrict__ tile_sums) {
+  constexpr int PER = kScanTile / kThreads;
+  __shared__ int3 s_warp[kThreads / 32 + 1];
+  int3 sum = make_int3(0, 0, 0);
+  int g0 = blockIdx.x * kScanTile + threadIdx.x * PER;
+  for (int q = 0; q < PER; ++q) {
+    int gb = g0 + q;
+    if (gb < P.NBT) {
+      int c, o, t;
+      block_flags<D>(P, cnt, gb, c, o, t);
+      sum.x += c; sum.y += o; sum.z += t;
+    }
+  }
+  int3 tot;
+  cta_excl_scan3(sum, s_warp, tot);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
+}
+
+// single CTA: exclusive scan of tile sums, per-step counts, arena base, overflow check
+__global__ void k_scan_b(KParams P, int n_tiles, int3* __restrict__ tile_sums, int* __restrict__ info,
+                         int t, ErrLatch* err) {
+  __shared__ int3 s_warp[kThreads / 32 + 1];
+  __shared__ int3 s_carry;
+  if (threadIdx.x == 0) s_carry = make_int3(0, 0, 0);
+  __syncthreads();
+  for (int base = 0; base < n_tiles; base += kThreads) {
+    int i = base + threadIdx.x;
+    int3 v = i < n_tiles ? tile_sums[i] : make_int3(0, 0, 0);
+    int3 tot;
+    int3 ex = cta_excl_scan3(v, s_warp, tot);
+    int3 cr = s_carry;
+    if (i < n_tiles) tile_sums[i] = make_int3(ex.x + cr.x, ex.y + cr.y, ex.z + cr.z);
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = make_int3(cr.x + tot.x, cr.y + tot.y, cr.z + tot.z);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int* I = info + t * kInfo;
+    int base = t == 0 ? 0 : info[(t - 1) * kInfo + I_BASE] + info[(t - 1) * kInfo + I_NTOUCH];
+    int ntouch = s_carry.z;
+    int ok = 1;
+    if (ntouch > P.slots_per_step || base + ntouch > P.arena_slots) {
+      latch(err, E_TAPE_FULL, t, ntouch);
+      ok = 0;
+    }
+    I[I_NOCC] = ok ? s_carry.y : 0;
+    I[I_NTOUCH] = ok ? ntouch : 0;
+    I[I_BASE] = base;
+    I[I_WORK] = 0;
+    I[I_WORK2] = 0;
+    I[I_OK] = ok;
+  }
+}
+
+template <int D>
+__global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const int* __restrict__ cnt,
+                                                     const int3* __restrict__ tile_pre,
+                                                     const int* __restrict__ info_t,
+                                                     int* __restrict__ block_start,
+                                                     int* __restrict__ slot_of,
+                                                     int* __restrict__ occ_list,
+                                                     int* __restrict__ touched_list,
+                                                     float4* __restrict__ arena) {
+  constexpr int PER = kScanTile / kThreads;
+  __shared__ int3 s_warp[kThreads / 32 + 1];
+  int ok = info_t[I_OK];
+  int base = info_t[I_BASE];
+  int c[PER], o[PER], tc[PER];
+  int3 sum = make_int3(0, 0, 0);
+  int g0 = blockIdx.x * kScanTile + threadIdx.x * PER;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    int gb = g0 + q;
+    c[q] = o[q] = tc[q] = 0;
+    if (gb < P.NBT) block_flags<D>(P, cnt, gb, c[q], o[q], tc[q]);
+    sum.x += c[q]; sum.y += o[q]; sum.z += tc[q];
+  }
+  int3 tot;
+  int3 ex = cta_excl_scan3(sum, s_warp, tot);
+  int3 tp = tile_pre[blockIdx.x];
+  ex.x += tp.x; ex.y += tp.y; ex.z += tp.z;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    int gb = g0 + q;
+    if (gb < P.NBT) {
+      block_start[gb] = ex.x;
+      if (ok && o[q]) occ_list[ex.y] = gb;
+      slot_of[gb] = (ok && tc[q]) ? base + ex.z : -1;
+      if (ok && tc[q]) touched_list[ex.z] = gb;
+    }
+    ex.x += c[q]; ex.y += o[q]; ex.z += tc[q];
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kThreads - 1) block_start[P.NBT] = P.NT;
+  // zero this tile's contiguous range of slots
+  if (ok) {
+    float4* z = arena + (size_t)(base + tp.z) * kCPB;
+    int n = tot.z * kCPB;
+    for (int i = threadIdx.x; i < n; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// counting-sort scatter by block (positions inside a block are fixed up by k_p2g)
+__global__ void k_scatter(int NT, const int* __restrict__ key, const int* __restrict__ block_start,
+                          int* __restrict__ cnt, int* __restrict__ tmp_perm) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = j < NT;
+  int gb = valid ? key[j] / kCPB : 0;
+  unsigned vm = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  unsigned peers = __match_any_sync(vm, gb);
+  int lane = threadIdx.x & 31;
+  int leader = __ffs(peers) - 1;
+  int n = __popc(peers);
+  int old = 0;
+  if (lane == leader) old = atomicSub(&cnt[gb], n);
+  old = __shfl_sync(peers, old, leader);
+  int rank = __popc(peers & ((1u << lane) - 1));
+  tmp_perm[block_start[gb] + old - n + rank] = j;
+}
+
+// ------------------------------------------------------------------------------------
+// zero a run of grid slots (adjoint grid of a backward step)
+// ------------------------------------------------------------------------------------
+__global__ void k_zero_slots(int* __restrict__ info_t, float4* __restrict__ g) {
+  int n = info_t[I_NTOUCH] * kCPB;
+  if (blockIdx.x == 0 && threadIdx.x == 0) info_t[I_WORK2] = 0;  // adjoint work counter
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// ------------------------------------------------------------------------------------
+// Block-tile scatter: P2G (Eqs. 3-5, forward) and G2P^T (step C, adjoint).
+//
+// One CTA per occupied block (dynamic work counter).  Particles of the block, sorted by
+// cell, are turned into a payload by all threads (producer), then thread (cell c, ox)
+// accumulates the contributions of its cell's particles to the 3^(D-1) nodes with x
+// offset ox in registers (consumer), and writes them into tile copy ox in conflict-free
+// phases (no shared-memory atomics).  The 3 copies are summed and each non-zero tile node
+// is flushed with one vector RED (red.global.add.v4.f32) into its grid slot.
+//
+// forward payload:  node value w_o * (A + B o), A = m v - dx G fx, B = dx G, G = -k tau + m C
+//                   (Eq. 4 with P_total F^T = tau, k = 4 dt V / dx^2), plus mass w_o m;
+// adjoint payload:  A = g_v - B fx, B = 4 res g_C with g_v = dL/dv^{t+1} + dt dL/dx^{t+1}
+//                   (step A), g_C = dL/dC^{t+1} + dt dL/dF^{t+1} F^T (step B).
+// ------------------------------------------------------------------------------------
+template <int D, bool ADJ> struct Pay;
+template <int D> struct Pay<D, false> { static constexpr int W = 0, M = 3 * D, A = M + 1, B = A + D, N = B + D * D; };
+template <int D> struct Pay<D, true> { static constexpr int W = 0, M = -1, A = 3 * D, B = A + D, N = B + D * D; };
+
+struct StepArgs {
+  // forward and adjoint
+  const float* st;        // state t (SoA)
+  int* perm;              // sorted slot -> storage index (written by forward k_p2g)
+  const int* tmp_perm;    // block-grouped, unsorted (forward)
+  const int* key;         // storage-order keys of step t (forward)
+  int* scratch;           // sort scratch for oversize blocks
+  const int* orig;        // storage index -> user index, step t
+  const float4* prm;      // {m, V, mu, lam} user order
+  const int* aid;         // actuator id, user order
+  const float* act;       // [B][T][K][D]
+  const int* block_start;
+  const int* occ_list;
+  const int* slot_of;
+  const int* touched_list;
+  int* info_t;            // info of step t
+  float4* grid;           // tape arena (forward) ; adjoint grid (ADJ)
+  const float4* tgrid;    // tape arena (adjoint kernels read the forward grid)
+  const float* gin;       // incoming adjoint, storage order t+1 (ADJ)
+  float* gout;            // outgoing adjoint, storage order t (ADJ)
+  float* st_next;         // state t+1
+  int* orig_next;
+  int* key_next;          // keys of t+1 (in the single key buffer)
+  int* cnt;               // histogram of t+1
+  float* dmu;             // [NT] user order
+  float* dlam;
+  float* da;              // [B][T][K][D]
+  ErrLatch* err;
+  int t;
+};
+
+template <int D, bool ADJ>
+__global__ __launch_bounds__(kThreads, 2) void k_block_scatter(KParams P, StepArgs A) {
+  using DD = Dim<D>;
+  using PY = Pay<D, ADJ>;
+  constexpr int BB = DD::BB, TE = DD::TE, TN = DD::TN;
+  constexpr int NSUB = (D == 3) ? 9 : 3;  // nodes per (cell, ox) thread
+  __shared__ int s_hist[kCPB];
+  __shared__ int s_cstart[kCPB + 1];
+  __shared__ int s_cursor[kCPB];
+  __shared__ int s_sort[ADJ ? 1 : kSortCap];
+  __shared__ float s_pay[PY::N][kCap];
+  __shared__ float4 s_tile[3][TN];
+  __shared__ int s_blk;
+  const int tid = threadIdx.x;
+  const size_t NT = P.NT;
+  const int work_field = ADJ ? I_WORK2 : I_WORK;
+  const int n_occ = A.info_t[I_NOCC];
+  const int base_slot = A.info_t[I_BASE];
+
+  for (;;) {
+    if (tid == 0) s_blk = atomicAdd(&A.info_t[work_field], 1);
+    __syncthreads();
+    const int bi = s_blk;
+    if (bi >= n_occ) break;
+    const int gb = A.occ_list[bi];
+    const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
+    const int r = gb / P.nb;
+    int bc[D];
+    {
+      int t = gb - r * P.nb;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
+    }
+    if (tid < kCPB) s_hist[tid] = 0;
+    for (int i = tid; i < 3 * TN; i += kThreads) (&s_tile[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncthreads();
+
+    // ---- cell ranges (and, forward, the stable in-block sort by (cell, index)) ----
+    if (!ADJ) {
+      for (int i = tid; i < n; i += kThreads) {
+        int j = A.tmp_perm[s + i];
+        atomicAdd(&s_hist[A.key[j] & (kCPB - 1)], 1);
+      }
+    } else {
+      for (int i = tid; i < n; i += kThreads) {
+        int j = A.perm[s + i];
+        int cl[D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) cl[a] = base_of(A.st[(size_t)comp_x<D>(a) * NT + j], P.fres) & (BB - 1);
+        atomicAdd(&s_hist[cell_lin<D>(cl)], 1);
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      int v0 = s_hist[tid], v1 = s_hist[tid + 32];
+      int i0 = v0, i1 = v1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int a = __shfl_up_sync(0xffffffffu, i0, o);
+        int b = __shfl_up_sync(0xffffffffu, i1, o);
+        if (tid >= o) { i0 += a; i1 += b; }
+      }
+      int tot0 = __shfl_sync(0xffffffffu, i0, 31);
+      s_cstart[tid] = i0 - v0;
+      s_cstart[tid + 32] = tot0 + i1 - v1;
+      s_cursor[tid] = i0 - v0;
+      s_cursor[tid + 32] = tot0 + i1 - v1;
+      if (tid == 31) s_cstart[kCPB] = tot0 + i1;
+    }
+    __syncthreads();
+    if (!ADJ) {
+      int* buf = (n <= kSortCap) ? s_sort : (A.scratch + s);
+      for (int i = tid; i < n; i += kThreads) {
+        int j = A.tmp_perm[s + i];
+        int pos = atomicAdd(&s_cursor[A.key[j] & (kCPB - 1)], 1);
+        buf[pos] = j;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += kThreads) {
+        int j = buf[i];
+        int c = A.key[j] & (kCPB - 1);
+        int lo = s_cstart[c], hi = s_cstart[c + 1];
+        int rank = 0;
+        for (int q = lo; q < hi; ++q) rank += buf[q] < j;
+        A.perm[s + lo + rank] = j;  // stable: ties by storage index (R18)
+      }
+      __syncthreads();
+    }
+
+    // ---- chunks of kCap particles: produce payload, consume per (cell, ox), phase-write ----
+    for (int lo = 0; lo < n; lo += kCap) {
+      const int hi = min(n, lo + kCap);
+      if (tid < hi - lo) {
+        const int k = s + lo + tid;
+        const int j = A.perm[k];
+        float x[D], f[D];
+        Stencil<D> sc;
+#pragma unroll
+        for (int a = 0; a < D; ++a) x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
+        make_stencil<D>(x, P.fres, sc);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          f[a] = sc.fx[a];
+#pragma unroll
+          for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][tid] = sc.w[a][o];
+        }
+        float Av[D], Bm[D][D];
+        if (!ADJ) {
+          const int u = A.orig[j];
+          const float4 pr = A.prm[u];  // m, V, mu, lam
+          float F[D][D], Cm[D][D], v[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            v[a] = A.st[(size_t)comp_v<D>(a) * NT + j];
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+              F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
+              Cm[a][b] = A.st[(size_t)comp_C<D>(a, b) * NT + j];
+            }
+          }
+          float sig[D];
+          const int ai = A.aid[u];
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+            sig[a] = ai >= 0 ? P.act_s * A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a] : 0.f;
+          float J = det<D>(F);
+          if (!(J > 0.f)) latch(A.err, E_INVERTED, A.t, u);
+          float lnJ = logf(J);
+          float tau[D][D];
+          kirchhoff<D>(F, pr.z, pr.w, sig, tau, lnJ);
+          // B = dx G = -4 res dt V tau + m dx C ;  A = m v - B fx
+          const float kk = 4.f * P.fres * P.dt * pr.y;
+          const float mdx = pr.x * P.dx;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) Bm[a][b] = fmaf(-kk, tau[a][b], mdx * Cm[a][b]);
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            float acc = pr.x * v[a];
+#pragma unroll
+            for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], f[b], acc);
+            Av[a] = acc;
+          }
+          if (PY::M >= 0) s_pay[PY::M < 0 ? 0 : PY::M][tid] = pr.x;
+        } else {
+          // steps A and B: g_v = gv + dt gx ; g_C = gC + dt gF F^T
+          const float* gi = A.gin;
+          float F[D][D], gF[D][D], gC[D][D], gv[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            gv[a] = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+              F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
+              gF[a][b] = gi[(size_t)comp_F<D>(a, b) * NT + k];
+              gC[a][b] = gi[(size_t)comp_C<D>(a, b) * NT + k];
+            }
+          }
+          const float s4 = 4.f * P.fres;
+#pragma unroll
+          for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+              float acc = gC[a][b];
+#pragma unroll
+              for (int c = 0; c < D; ++c) acc = fmaf(P.dt * gF[a][c], F[b][c], acc);
+              Bm[a][b] = s4 * acc;
+            }
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            float acc = gv[a];
+#pragma unroll
+            for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], f[b], acc);
+            Av[a] = acc;
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          s_pay[PY::A + a][tid] = Av[a];
+#pragma unroll
+          for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][tid] = Bm[a][b];
+        }
+      }
+      __syncthreads();
+
+      // consumer: thread (ox, c), c = cell, accumulates NSUB nodes
+      float4 acc[NSUB];
+#pragma unroll
+      for (int q = 0; q < NSUB; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int ox = tid / kCPB, c = tid % kCPB;
+      if (tid < 3 * kCPB) {
+        const int i0 = max(s_cstart[c], lo) - lo, i1 = min(s_cstart[c + 1], hi) - lo;
+        for (int i = i0; i < i1; ++i) {
+          const float wx = s_pay[PY::W + ox][i];
+          float Ax[3];
+#pragma unroll
+          for (int a = 0; a < D; ++a) Ax[a] = s_pay[PY::A + a][i] + (float)ox * s_pay[PY::B + a * D + 0][i];
+          const float mp = ADJ ? 0.f : s_pay[PY::M < 0 ? 0 : PY::M][i];
+          if (D == 3) {
+            float B1[3], B2[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) { B1[a] = s_pay[PY::B + a * D + 1][i]; B2[a] = s_pay[PY::B + a * D + 2 % D][i]; }
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+              const float wxy = wx * s_pay[PY::W + 3 + oy][i];
+#pragma unroll
+              for (int oz = 0; oz < 3; ++oz) {
+                const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
+                float4& q = acc[oy * 3 + oz];
+                q.x = fmaf(W, Ax[0] + (float)oy * B1[0] + (float)oz * B2[0], q.x);
+                q.y = fmaf(W, Ax[1] + (float)oy * B1[1] + (float)oz * B2[1], q.y);
+                q.z = fmaf(W, Ax[2] + (float)oy * B1[2] + (float)oz * B2[2], q.z);
+                if (!ADJ) q.w = fmaf(W, mp, q.w);
+              }
+            }
+          } else {
+            float B1[2];
+#pragma unroll
+            for (int a = 0; a < 2; ++a) B1[a] = s_pay[PY::B + a * D + 1][i];
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+              const float W = wx * s_pay[PY::W + 3 + oy][i];
+              float4& q = acc[oy];
+              q.x = fmaf(W, Ax[0] + (float)oy * B1[0], q.x);
+              q.y = fmaf(W, Ax[1] + (float)oy * B1[1], q.y);
+              if (!ADJ) q.w = fmaf(W, mp, q.w);
+            }
+          }
+        }
+      }
+      // phase-write: in phase q all threads of copy ox write distinct nodes c + (ox, q)
+      int cc[D];
+      {
+        int t = c;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) { cc[a] = t % BB; t /= BB; }
+      }
+#pragma unroll
+      for (int q = 0; q < NSUB; ++q) {
+        if (tid < 3 * kCPB) {
+          int tl;
+          if (D == 3) tl = ((cc[0] + ox) * TE + cc[1] + q / 3) * TE + cc[D - 1] + q % 3;
+          else tl = (cc[0] + ox) * TE + cc[D - 1] + q;
+          float4 v = s_tile[ox][tl];
+          v.x += acc[q].x; v.y += acc[q].y; v.z += acc[q].z; v.w += acc[q].w;
+          s_tile[ox][tl] = v;
+        }
+        __syncthreads();
+      }
+    }
+
+    // ---- flush: one vector RED per non-zero tile node ----
+    for (int tn = tid; tn < TN; tn += kThreads) {
+      float4 v0 = s_tile[0][tn], v1 = s_tile[1][tn], v2 = s_tile[2][tn];
+      float4 v = make_float4(v0.x + v1.x + v2.x, v0.y + v1.y + v2.y, v0.z + v1.z + v2.z, v0.w + v1.w + v2.w);
+      if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+      int tl[D];
+      {
+        int t = tn;
+#pragma unroll
+        for (int a = D - 1; a >= 0; --a) { tl[a] = t % TE; t /= TE; }
+      }
+      int nb_[D], loc[D];
+      bool inside = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        int gnode = bc[a] * BB + tl[a];
+        inside &= gnode < P.res;
+        nb_[a] = gnode >> DD::LOG_BB;
+        loc[a] = gnode & (BB - 1);
+      }
+      if (!inside) continue;
+      int slot = A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)];
+      if (slot < 0) continue;  // cannot happen (touched by construction); defensive
+      float4* dst = A.grid + (size_t)(ADJ ? slot - base_slot : slot) * kCPB + cell_lin<D>(loc);
+      atomicAdd(dst, v);  // red.global.add.v4.f32
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Grid update (Eq. 6; gravity R5): (p, m) -> (vbar = p/m + dt g, m) in place.
+// The wall projection (R6) is applied when a node is read.
+// ------------------------------------------------------------------------------------
+__global__ void k_grid_update(KParams P, const int* __restrict__ info_t, float4* __restrict__ arena) {
+  const int n = info_t[I_NTOUCH] * kCPB;
+  float4* g = arena + (size_t)info_t[I_BASE] * kCPB;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float4 q = g[i];
+    if (q.w > 0.f) {
+      q.x = q.x / q.w + P.dt * P.g[0];
+      q.y = q.y / q.w + P.dt * P.g[1];
+      q.z = q.z / q.w + P.dt * P.g[2];
+      g[i] = q;
+    }
+  }
+}
+
+// node fetch helpers for the gathers: the 2^D grid blocks spanned by a stencil
+template <int D> struct StencilSlots {
+  int slot[1 << D];
+  int b0[D];
+};
+
+template <int D>
+__device__ __forceinline__ void stencil_slots(const KParams& P, int r, const Stencil<D>& sc,
+                                              const int* __restrict__ slot_of, StencilSlots<D>& ss) {
+#pragma unroll
+  for (int a = 0; a < D; ++a) ss.b0[a] = sc.base[a] >> Dim<D>::LOG_BB;
+#pragma unroll
+  for (int q = 0; q < (1 << D); ++q) {
+    int b[D];
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      b[a] = ss.b0[a] + ((q >> (D - 1 - a)) & 1);
+      ok &= b[a] < P.nbpa;
+    }
+    ss.slot[q] = ok ? slot_of[r * P.nb + block_lin<D>(b, P.nbpa)] : -1;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ size_t node_addr(const StencilSlots<D>& ss, const int* node) {
+  int q = 0, loc[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    q = q * 2 + ((node[a] >> Dim<D>::LOG_BB) - ss.b0[a]);
+    loc[a] = node[a] & (Dim<D>::BB - 1);
+  }
+  return (size_t)ss.slot[q] * kCPB + cell_lin<D>(loc);
+}
+
+// ------------------------------------------------------------------------------------
+// G2P (Eqs. 7-10): gather v and C, update F and x, write state t+1 in sorted
+// order, and the keys + block histogram of step t+1 (binning of the next step).
+// ------------------------------------------------------------------------------------
+template <int D>
+__global__ __launch_bounds__(256) void k_g2p(KParams P, StepArgs A) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  bool valid = k < P.NT;
+  int gbn = 0;
+  if (valid) {
+    const size_t NT = P.NT;
+    const int j = A.perm[k];
+    const int r = k / P.N;
+    float x[D], F[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
+#pragma unroll
+      for (int b = 0; b < D; ++b) F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
+    }
+    Stencil<D> sc;
+    make_stencil<D>(x, P.fres, sc);
+    StencilSlots<D> ss;
+    stencil_slots<D>(P, r, sc, A.slot_of, ss);
+    float vn[D], M[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      vn[a] = 0.f;
+#pragma unroll
+      for (int b = 0; b < D; ++b) M[a][b] = 0.f;
+    }
+#pragma unroll
+    for (int s = 0; s < Dim<D>::NS; ++s) {
+      int o[D], node[D];
+      float W = 1.f;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        o[a] = (D == 3) ? (a == 0 ? s / 9 : (a == 1 ? (s / 3) % 3 : s % 3)) : (a == 0 ? s / 3 : s % 3);
+        node[a] = sc.base[a] + o[a];
+        W *= sc.w[a][o[a]];
+      }
+      float4 g = A.grid[node_addr<D>(ss, node)];
+      float vi[D];
+      vi[0] = g.x; vi[1] = g.y;
+      if (D == 3) vi[D - 1] = g.z;
+      if (!(g.w > 0.f)) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) vi[a] = 0.f;
+      } else if (in_band<D>(node, P.res, P.bound)) {
+        project_node<D>(vi, node, P);
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        float wv = W * vi[a];
+        vn[a] += wv;
+#pragma unroll
+        for (int b = 0; b < D; ++b) M[a][b] = fmaf(wv, (float)o[b] - sc.fx[b], M[a][b]);
+      }
+    }
+    // C' = 4/dx^2 sum w v (x_i - x_p)^T = 4 res sum w v (o - fx)^T ; F' = (I + dt C') F
+    float Cn[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) Cn[a][b] = 4.f * P.fres * M[a][b];
+    float* out = A.st_next;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = F[a][b];
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[a][c], F[c][b], acc);
+        out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
+        out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[a][b];
+      }
+      out[(size_t)comp_v<D>(a) * NT + k] = vn[a];
+      x[a] = fmaf(P.dt, vn[a], x[a]);
+      out[(size_t)comp_x<D>(a) * NT + k] = x[a];
+    }
+    const int u = A.orig[j];
+    A.orig_next[k] = u;
+    int key;
+    if (!key_of<D>(x, r, P, gbn, key)) latch(A.err, E_DOMAIN, A.t + 1, u);
+    A.key_next[k] = key;
+  }
+  warp_hist_add(A.cnt, gbn, valid);
+}
+
+// ------------------------------------------------------------------------------------
+// grid^T: steps L (reverse wall order R6), D, E (R9).
+// adjoint node (dL/dv_i) -> (dL/dp_i, dL/dm_i) in place.
+// ------------------------------------------------------------------------------------
+template <int D>
+__global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int* __restrict__ touched_list,
+                           const float4* __restrict__ arena, float4* __restrict__ ag) {
+  const int n = info_t[I_NTOUCH] * kCPB;
+  const float4* g = arena + (size_t)info_t[I_BASE] * kCPB;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float4 q = g[i];
+    float4 a = ag[i];
+    float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (q.w > 0.f) {
+      const int gb = touched_list[i / kCPB];
+      const int r = gb / P.nb;
+      int node[D];
+      {
+        int t = gb - r * P.nb, l = i % kCPB;
+#pragma unroll
+        for (int d = D - 1; d >= 0; --d) {
+          node[d] = (t % P.nbpa) * Dim<D>::BB + l % Dim<D>::BB;
+          t /= P.nbpa;
+          l /= Dim<D>::BB;
+        }
+      }
+      float vb[D] = {}, gv[D] = {};
+      vb[0] = q.x; vb[1] = q.y; gv[0] = a.x; gv[1] = a.y;
+      if (D == 3) { vb[D - 1] = q.z; gv[D - 1] = a.z; }
+      if (in_band<D>(node, P.res, P.bound)) project_node_adj<D>(vb, gv, node, P);
+      // gravity adjoint = identity (R5); v = p/m + dt g -> dp = gv/m, dm = -(p . gv)/m^2
+      const float im = 1.f / q.w;
+      float pg = 0.f;
+#pragma unroll
+      for (int d = 0; d < D; ++d) pg = fmaf(vb[d] - P.dt * P.g[d], gv[d], pg);
+      out.x = gv[0] * im;
+      out.y = gv[1] * im;
+      if (D == 3) out.z = gv[D - 1] * im;
+      out.w = -pg * im;
+    }
+    ag[i] = out;
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// P2G^T gather (steps F-K and J; E/nu per R19) in the Kirchhoff form:
+//   T = dL/dtau = -k Q, Q = dL/dG = sum_i w dp_i (x_i - x_p)^T, k = 4 dt V / dx^2
+//   dv^t = m sum_i w dp_i ; dC^t = m Q
+//   dF^t = (I + dt C^{t+1})^T dF^{t+1} + mu (T + T^T) F + lam tr(T) F^{-T} + (T + T^T) F sigma
+//   dx^t = dx^{t+1} + sum_i dW_i s_i - 4 res^2 g_C^T v^{t+1} - G^T sum_i w dp_i
+//     s_i = v_i . (g_v + 4 res g_C (o - fx)) + dp_i . (m v + G d_i) + m dm_i
+//   dsigma = F^T T F (diag -> actuation); dmu = T : (F F^T - I); dlam = tr(T) ln J
+// ------------------------------------------------------------------------------------
+template <int D>
+__global__ __launch_bounds__(128) void k_p2g_adj(KParams P, StepArgs A) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = k < P.NT;
+  const size_t NT = P.NT;
+  int ai = -1;
+  float dsig[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) dsig[a] = 0.f;
+  int r = 0;
+  if (valid) {
+    const int j = A.perm[k];
+    r = k / P.N;
+    const int u = A.orig[j];
+    const float4 pr = A.prm[u];
+    const float m = pr.x;
+    float x[D], v[D], F[D][D], Cm[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
+      v[a] = A.st[(size_t)comp_v<D>(a) * NT + j];
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
+        Cm[a][b] = A.st[(size_t)comp_C<D>(a, b) * NT + j];
+      }
+    }
+    ai = A.aid[u];
+    float sig[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+      sig[a] = ai >= 0 ? P.act_s * A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a] : 0.f;
+    const float J = det<D>(F);
+    const float lnJ = logf(J);
+    float tau[D][D];
+    kirchhoff<D>(F, pr.z, pr.w, sig, tau, lnJ);
+    const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
+    float G[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) G[a][b] = fmaf(-kk, tau[a][b], m * Cm[a][b]);
+    // incoming adjoint (storage order t+1 = sorted index k), steps A and B
+    const float* gi = A.gin;
+    float gx[D], gvh[D], gF[D][D], gCh[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      gx[a] = gi[(size_t)comp_x<D>(a) * NT + k];
+      gvh[a] = fmaf(P.dt, gx[a], gi[(size_t)comp_v<D>(a) * NT + k]);
+#pragma unroll
+      for (int b = 0; b < D; ++b) gF[a][b] = gi[(size_t)comp_F<D>(a, b) * NT + k];
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = gi[(size_t)comp_C<D>(a, b) * NT + k];
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc = fmaf(P.dt * gF[a][c], F[b][c], acc);
+        gCh[a][b] = acc;
+      }
+
+    Stencil<D> sc;
+    make_stencil<D>(x, P.fres, sc);
+    float dw[D][3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) stencil_dw(sc.fx[a], dw[a]);
+    StencilSlots<D> ss;
+    stencil_slots<D>(P, r, sc, A.slot_of, ss);
+    const int base_slot = A.info_t[I_BASE];
+
+    float Sv[D], Sdp[D], Mv[D][D], Q[D][D], gradx[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      Sv[a] = Sdp[a] = gradx[a] = 0.f;
+#pragma unroll
+      for (int b = 0; b < D; ++b) Mv[a][b] = Q[a][b] = 0.f;
+    }
+    float msum = 0.f;  // sum_i w dm_i  (unused by the formulas; kept for symmetry checks)
+    (void)msum;
+#pragma unroll 1
+    for (int s = 0; s < Dim<D>::NS; ++s) {
+      int o[D], node[D];
+      float W = 1.f, dW[D], d[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        o[a] = (D == 3) ? (a == 0 ? s / 9 : (a == 1 ? (s / 3) % 3 : s % 3)) : (a == 0 ? s / 3 : s % 3);
+        node[a] = sc.base[a] + o[a];
+        W *= sc.w[a][o[a]];
+        d[a] = (float)o[a] - sc.fx[a];  // (x_i - x_p) / dx
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        float gw = P.fres * dw[a][o[a]];
+#pragma unroll
+        for (int b = 0; b < D; ++b)
+          if (b != a) gw *= sc.w[b][o[b]];
+        dW[a] = gw;  // dW/dx_p (R10)
+      }
+      const size_t addr = node_addr<D>(ss, node);
+      const float4 g = A.tgrid[addr];
+      const float4 ad = A.grid[addr - (size_t)base_slot * kCPB];
+      float vi[D], dp[D];
+      vi[0] = g.x; vi[1] = g.y; dp[0] = ad.x; dp[1] = ad.y;
+      if (D == 3) { vi[D - 1] = g.z; dp[D - 1] = ad.z; }
+      const float dm = ad.w;
+      if (!(g.w > 0.f)) {
+#pragma unroll
+        for (int a = 0; a < D; ++a) vi[a] = 0.f;
+      } else if (in_band<D>(node, P.res, P.bound)) {
+        project_node<D>(vi, node, P);
+      }
+      // s_i
+      float si = m * dm;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        float gcd = 0.f, Gd = 0.f;
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          gcd = fmaf(gCh[a][b], d[b], gcd);
+          Gd = fmaf(G[a][b], d[b], Gd);
+        }
+        si = fmaf(vi[a], fmaf(4.f * P.fres, gcd, gvh[a]), si);
+        si = fmaf(dp[a], fmaf(m, v[a], P.dx * Gd), si);
+      }
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        gradx[a] = fmaf(dW[a], si, gradx[a]);
+        const float wv = W * vi[a], wdp = W * dp[a];
+        Sv[a] += wv;
+        Sdp[a] += wdp;
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          Mv[a][b] = fmaf(wv, d[b], Mv[a][b]);
+          Q[a][b] = fmaf(wdp, d[b], Q[a][b]);
+        }
+      }
+    }
+    // Q = dL/dG = sum w dp (x_i - x_p)^T  -> scale by dx
+    float T[D][D], Cn[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        Q[a][b] *= P.dx;
+        T[a][b] = -kk * Q[a][b];
+        Cn[a][b] = 4.f * P.fres * Mv[a][b];  // C^{t+1}, Eq. 8 recomputed from the tape grid
+      }
+    float* go = A.gout;
+    // (F) dv = m sum w dp
+#pragma unroll
+    for (int a = 0; a < D; ++a) go[(size_t)comp_v<D>(a) * NT + j] = m * Sdp[a];
+    // (I) dC = m Q
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) go[(size_t)comp_C<D>(a, b) * NT + j] = m * Q[a][b];
+    // (J)
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float acc = gx[a] + gradx[a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        acc = fmaf(-4.f * P.fres * P.fres * gCh[b][a], Sv[b], acc);
+        acc = fmaf(-G[b][a], Sdp[b], acc);
+      }
+      go[(size_t)comp_x<D>(a) * NT + j] = acc;
+    }
+    // (H) in Kirchhoff form
+    float Ts[D][D], FiT[D][D];
+    inv_T<D>(F, J, FiT);
+    float trT = 0.f;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      trT += T[a][a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) Ts[a][b] = T[a][b] + T[b][a];
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = gF[a][b];
+        float tf = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          acc = fmaf(P.dt * Cn[c][a], gF[c][b], acc);
+          tf = fmaf(Ts[a][c], F[c][b], tf);
+        }
+        acc = fmaf(pr.z + sig[b], tf, acc);  // mu (T+T^T) F + (T+T^T) F sigma
+        acc = fmaf(pr.w * trT, FiT[a][b], acc);
+        go[(size_t)comp_F<D>(a, b) * NT + j] = acc;
+      }
+    // (K) dsigma = F^T T F (diagonal), material parameters (R19)
+    float dmu = 0.f;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float ds = 0.f;
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float tf = 0.f, ff = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          tf = fmaf(T[b][c], F[c][a], tf);
+          ff = fmaf(F[a][c], F[b][c], ff);
+        }
+        ds = fmaf(F[b][a], tf, ds);
+        dmu = fmaf(T[a][b], ff - (a == b ? 1.f : 0.f), dmu);
+      }
+      dsig[a] = P.act_s * ds;
+    }
+    A.dmu[u] += dmu;
+    A.dlam[u] += trT * lnJ;
+  }
+  // actuation gradient: warp-reduce when the warp shares one actuator, else per-lane atomics
+  const unsigned vm = __ballot_sync(0xffffffffu, valid && ai >= 0);
+  if (vm) {
+    const int lane = threadIdx.x & 31;
+    const int ai0 = __shfl_sync(0xffffffffu, ai, __ffs(vm) - 1);
+    const int r0 = __shfl_sync(0xffffffffu, r, __ffs(vm) - 1);
+    const bool uniform = __all_sync(0xffffffffu, !(valid && ai >= 0) || (ai == ai0 && r == r0));
+    if (uniform) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        float v = (valid && ai >= 0) ? dsig[a] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) atomicAdd(&A.da[(((size_t)r0 * P.T + A.t) * P.K + ai0) * D + a], v);
+      }
+    } else if (valid && ai >= 0) {
+#pragma unroll
+      for (int a = 0; a < D; ++a) atomicAdd(&A.da[(((size_t)r * P.T + A.t) * P.K + ai) * D + a], dsig[a]);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// seed, readback, finalize
+// ------------------------------------------------------------------------------------
+// user-order AoS seed -> SoA adjoint in storage order T (orig_T maps storage -> user)
+template <int D>
+__global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __restrict__ gx,
+                       const float* __restrict__ gv, const float* __restrict__ gF,
+                       const float* __restrict__ gC, float* __restrict__ g) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= P.NT) return;
+  const size_t NT = P.NT;
+  int u = orig[k];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    g[(size_t)comp_x<D>(a) * NT + k] = gx ? gx[u * D + a] : 0.f;
+    g[(size_t)comp_v<D>(a) * NT + k] = gv ? gv[u * D + a] : 0.f;
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      g[(size_t)comp_F<D>(a, b) * NT + k] = gF ? gF[(u * D + a) * D + b] : 0.f;
+      g[(size_t)comp_C<D>(a, b) * NT + k] = gC ? gC[(u * D + a) * D + b] : 0.f;
+    }
+  }
+}
+
+// SoA storage order -> user AoS (x, v, F, C), any may be null
+template <int D>
+__global__ void k_soa_to_user(KParams P, const int* __restrict__ orig, const float* __restrict__ st,
+                              float* x, float* v, float* F, float* C) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.NT) return;
+  const size_t NT = P.NT;
+  int u = orig ? orig[j] : j;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    if (x) x[u * D + a] = st[(size_t)comp_x<D>(a) * NT + j];
+    if (v) v[u * D + a] = st[(size_t)comp_v<D>(a) * NT + j];
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      if (F) F[(u * D + a) * D + b] = st[(size_t)comp_F<D>(a, b) * NT + j];
+      if (C) C[(u * D + a) * D + b] = st[(size_t)comp_C<D>(a, b) * NT + j];
+    }
+  }
+}
+
+__global__ void k_finalize_params(int NT, const float* __restrict__ E, const float* __restrict__ nu,
+                                  const float* __restrict__ dmu, const float* __restrict__ dlam,
+                                  float* dE, float* dnu) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= NT) return;
+  // R19: chain through the Lame parameters
+  float e = E[j], n = nu[j], gm = dmu[j], gl = dlam[j];
+  float a = 1.f + n, b = 1.f - 2.f * n;
+  if (dE) dE[j] = gm / (2.f * a) + gl * n / (a * b);
+  if (dnu) dnu[j] = -gm * e / (2.f * a * a) + gl * e * (1.f + 2.f * n * n) / (a * a * b * b);
+}
+
+// dense readback of the tape grid of one step: [B][res^D] (m, vbar)
+template <int D>
+__global__ void k_dense_grid(KParams P, const int* __restrict__ info_t, const int* __restrict__ touched_list,
+                             const float4* __restrict__ arena, float* m, float* vbar) {
+  const int n = info_t[I_NTOUCH] * kCPB;
+  const float4* g = arena + (size_t)info_t[I_BASE] * kCPB;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int gb = touched_list[i / kCPB];
+    const int r = gb / P.nb;
+    int t = gb - r * P.nb, l = i % kCPB;
+    int node[D];
+#pragma unroll
+    for (int d = D - 1; d >= 0; --d) {
+      node[d] = (t % P.nbpa) * Dim<D>::BB + l % Dim<D>::BB;
+      t /= P.nbpa;
+      l /= Dim<D>::BB;
+    }
+    size_t lin = 0;
+#pragma unroll
+    for (int d = 0; d < D; ++d) lin = lin * P.res + node[d];
+    size_t nn = 1;
+#pragma unroll
+    for (int d = 0; d < D; ++d) nn *= P.res;
+    size_t o = (size_t)r * nn + lin;
+    float4 q = g[i];
+    if (m) m[o] = q.w;
+    if (vbar) {
+      vbar[o * D + 0] = q.x;
+      vbar[o * D + 1] = q.y;
+      if (D == 3) vbar[o * D + D - 1] = q.z;
+    }
+  }
+}
+
+}  // namespace mpm

@@ -1,0 +1,271 @@
+"""Thin ctypes binding of the C ABI in ``include/mpm.h`` (library ``libmpm.so``, sm_100a).
+
+Argument marshalling only: every step of the differentiable MLS-MPM path runs in the CUDA
+kernels of ``csrc/``.  There is no CPU fallback: ``load()`` raises if the library is
+missing, and every call raises ``MPMError`` on a non-zero status.
+
+Arrays may be numpy arrays (host) or torch tensors (host or CUDA); they are passed to the
+library as raw pointers (the library detects host vs device memory).  Outputs default to
+new numpy arrays; pass ``out=`` tensors to keep results on the device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpm.so")
+
+STATUS = {0: "MPM_OK", 1: "MPM_ERR_INVALID_ARG", 2: "MPM_ERR_OOM", 3: "MPM_ERR_CUDA",
+          4: "MPM_ERR_OUT_OF_DOMAIN", 5: "MPM_ERR_INVERTED", 6: "MPM_ERR_TAPE_FULL",
+          7: "MPM_ERR_CALL_ORDER", 8: "MPM_ERR_COMM"}
+
+# every symbol include/mpm.h declares
+EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "mpm_forward",
+           "mpm_tape_length", "mpm_rewind", "mpm_get_state", "mpm_backward", "mpm_grad",
+           "mpm_last_error", "mpm_get_binning", "mpm_get_grid", "mpm_set_profiling",
+           "mpm_get_profile", "mpm_launch_count")
+
+
+class MPMError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+        super().__init__(f"{self.status}: {msg}")
+
+
+class _Config(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("res", C.c_int32), ("batch", C.c_int32),
+                ("n_particles", C.c_int32), ("max_steps", C.c_int32), ("n_actuators", C.c_int32),
+                ("dt", C.c_float), ("gravity", C.c_float * 3), ("bound", C.c_int32),
+                ("friction", C.c_float * 6), ("act_strength", C.c_float), ("device", C.c_int32),
+                ("stream", C.c_void_p), ("grid_slots", C.c_int32)]
+
+
+_lib = None
+
+
+def load():
+    """Load libmpm.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    L.mpm_create.argtypes = [C.POINTER(_Config), C.POINTER(vp)]
+    L.mpm_destroy.argtypes = [vp]
+    L.mpm_destroy.restype = None
+    L.mpm_set_state.argtypes = [vp] * 10
+    L.mpm_set_actuation.argtypes = [vp, vp]
+    L.mpm_forward.argtypes = [vp, i32]
+    L.mpm_tape_length.argtypes = [vp]
+    L.mpm_tape_length.restype = i32
+    L.mpm_rewind.argtypes = [vp, i32]
+    L.mpm_get_state.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.mpm_backward.argtypes = [vp, vp, vp, vp, vp]
+    L.mpm_grad.argtypes = [vp] * 8
+    L.mpm_last_error.argtypes = [vp]
+    L.mpm_last_error.restype = C.c_char_p
+    L.mpm_get_binning.argtypes = [vp, i32, vp, vp, vp, vp, vp]
+    L.mpm_get_grid.argtypes = [vp, i32, vp, vp]
+    L.mpm_set_profiling.argtypes = [vp, i32]
+    L.mpm_get_profile.argtypes = [vp, C.POINTER(i32), vp, vp, C.c_char_p, i32]
+    L.mpm_launch_count.argtypes = [vp]
+    L.mpm_launch_count.restype = i64
+    for name in EXPORTS:
+        getattr(L, name)
+    _lib = L
+    return L
+
+
+def _ptr(a):
+    """Raw pointer of a numpy array or torch tensor (None -> NULL)."""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return a.ctypes.data
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    raise TypeError(f"unsupported array type {type(a)}")
+
+
+def _in(a, dtype, shape):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        a = np.ascontiguousarray(a, dtype=dtype)
+        assert a.size == int(np.prod(shape)), (a.shape, shape)
+        return a
+    assert a.is_contiguous() and a.numel() == int(np.prod(shape)), (tuple(a.shape), shape)
+    return a
+
+
+@dataclass
+class Config:
+    dim: int
+    res: int
+    batch: int
+    n_particles: int
+    max_steps: int
+    dt: float
+    n_actuators: int = 0
+    gravity: tuple = (0.0, 0.0, 0.0)
+    bound: int = 3
+    friction: tuple = (0.0,) * 6
+    act_strength: float = 0.0
+    device: int = 0
+    stream: int = 0
+    grid_slots: int = 0
+
+    @classmethod
+    def from_scene(cls, sc, max_steps=None, **kw):
+        return cls(dim=sc.dim, res=sc.res, batch=sc.batch, n_particles=sc.n,
+                   max_steps=max_steps or sc.steps, dt=sc.dt, n_actuators=sc.n_act,
+                   gravity=tuple(sc.gravity), bound=sc.bound, friction=tuple(sc.friction),
+                   act_strength=sc.act_strength, **kw)
+
+    def c(self) -> _Config:
+        g = list(self.gravity) + [0.0] * (3 - len(self.gravity))
+        f = list(self.friction) + [0.0] * (6 - len(self.friction))
+        return _Config(self.dim, self.res, self.batch, self.n_particles, self.max_steps,
+                       self.n_actuators, self.dt, (C.c_float * 3)(*g[:3]), self.bound,
+                       (C.c_float * 6)(*f[:6]), self.act_strength, self.device,
+                       self.stream or None, self.grid_slots)
+
+
+class MPM:
+    """One simulation context (one GPU, B rollouts).  Mirrors the C ABI one to one."""
+
+    def __init__(self, cfg: Config):
+        self.L = load()
+        self.cfg = cfg
+        self._cc = cfg.c()
+        h = C.c_void_p()
+        self._check(self.L.mpm_create(C.byref(self._cc), C.byref(h)), h)
+        self.h = h
+
+    # -- plumbing -----------------------------------------------------------------------
+    def _check(self, rc, h=None):
+        if rc != 0:
+            hh = h if h is not None else self.h
+            msg = self.L.mpm_last_error(hh).decode() if hh and hh.value else "create failed"
+            raise MPMError(rc, msg)
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.L.mpm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def NT(self):
+        return self.cfg.batch * self.cfg.n_particles
+
+    # -- the path -----------------------------------------------------------------------
+    def set_state(self, x, v=None, F=None, C_=None, mass=None, vol=None, E=None, nu=None,
+                  actuator_id=None):
+        d, NT = self.cfg.dim, self.NT
+        arrs = [_in(x, np.float32, (NT, d)), _in(v, np.float32, (NT, d)),
+                _in(F, np.float32, (NT, d, d)), _in(C_, np.float32, (NT, d, d)),
+                _in(mass, np.float32, (NT,)), _in(vol, np.float32, (NT,)),
+                _in(E, np.float32, (NT,)), _in(nu, np.float32, (NT,)),
+                _in(actuator_id, np.int32, (NT,))]
+        self._check(self.L.mpm_set_state(self.h, *[_ptr(a) for a in arrs]))
+
+    def set_scene(self, sc):
+        self.set_state(sc.x, sc.v, sc.F, sc.C, sc.mass, sc.vol, sc.E, sc.nu, sc.actuator_id)
+        if sc.n_act > 0:
+            a = np.zeros((sc.batch, self.cfg.max_steps, sc.n_act, sc.dim), np.float32)
+            T = min(self.cfg.max_steps, sc.act.shape[1])
+            a[:, :T] = sc.act[:, :T]
+            self.set_actuation(a)
+
+    def set_actuation(self, a):
+        cfg = self.cfg
+        a = _in(a, np.float32, (cfg.batch, cfg.max_steps, cfg.n_actuators, cfg.dim))
+        self._check(self.L.mpm_set_actuation(self.h, _ptr(a)))
+
+    def forward(self, n_steps: int):
+        self._check(self.L.mpm_forward(self.h, int(n_steps)))
+
+    def rewind(self, t: int = 0):
+        self._check(self.L.mpm_rewind(self.h, int(t)))
+
+    @property
+    def tape_length(self) -> int:
+        return self.L.mpm_tape_length(self.h)
+
+    def get_state(self, t: int, out=None):
+        d, NT = self.cfg.dim, self.NT
+        if out is None:
+            out = (np.empty((NT, d), np.float32), np.empty((NT, d), np.float32),
+                   np.empty((NT, d, d), np.float32), np.empty((NT, d, d), np.float32))
+        self._check(self.L.mpm_get_state(self.h, int(t), *[_ptr(a) for a in out]))
+        return out
+
+    def backward(self, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
+        d, NT = self.cfg.dim, self.NT
+        arrs = [_in(dLdx, np.float32, (NT, d)), _in(dLdv, np.float32, (NT, d)),
+                _in(dLdF, np.float32, (NT, d, d)), _in(dLdC, np.float32, (NT, d, d))]
+        self._check(self.L.mpm_backward(self.h, *[_ptr(a) for a in arrs]))
+
+    def grad(self, out=None):
+        cfg = self.cfg
+        d, NT = cfg.dim, self.NT
+        if out is None:
+            out = dict(dx0=np.empty((NT, d), np.float32), dv0=np.empty((NT, d), np.float32),
+                       dF0=np.empty((NT, d, d), np.float32), dC0=np.empty((NT, d, d), np.float32),
+                       dE=np.empty(NT, np.float32), dnu=np.empty(NT, np.float32),
+                       da=np.empty((cfg.batch, cfg.max_steps, max(cfg.n_actuators, 0), d), np.float32))
+        keys = ("dx0", "dv0", "dF0", "dC0", "dE", "dnu", "da")
+        self._check(self.L.mpm_grad(self.h, *[_ptr(out.get(k)) for k in keys]))
+        return out
+
+    # -- introspection -------------------------------------------------------------------
+    def get_binning(self, t: int):
+        cfg = self.cfg
+        d, NT = cfg.dim, self.NT
+        Bb = 4 if d == 3 else 8
+        nb = (cfg.res // Bb) ** d
+        x = np.empty((NT, d), np.float32)
+        orig = np.empty(NT, np.int32)
+        key = np.empty(NT, np.int32)
+        perm = np.empty(NT, np.int32)
+        bs = np.empty(cfg.batch * nb + 1, np.int32)
+        self._check(self.L.mpm_get_binning(self.h, int(t), _ptr(x), _ptr(orig), _ptr(key),
+                                           _ptr(perm), _ptr(bs)))
+        return x, orig, key, perm, bs
+
+    def get_grid(self, t: int):
+        cfg = self.cfg
+        nn = cfg.res ** cfg.dim
+        m = np.empty((cfg.batch, nn), np.float32)
+        vbar = np.empty((cfg.batch, nn, cfg.dim), np.float32)
+        self._check(self.L.mpm_get_grid(self.h, int(t), _ptr(m), _ptr(vbar)))
+        return m, vbar
+
+    def set_profiling(self, on: bool):
+        self._check(self.L.mpm_set_profiling(self.h, 1 if on else 0))
+
+    def profile(self):
+        n = C.c_int32(32)
+        ms = np.zeros(32, np.float32)
+        cnt = np.zeros(32, np.int64)
+        names = C.create_string_buffer(1024)
+        self._check(self.L.mpm_get_profile(self.h, C.byref(n), _ptr(ms), _ptr(cnt), names, 1024))
+        keys = names.value.decode().split(";")
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys[:n.value])}
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.mpm_launch_count(self.h))

@@ -1,0 +1,58 @@
+"""The C-ABI library builds, loads and exports every symbol include/mpm.h declares; config
+validation happens before any CUDA call.  CPU only (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_1810_01054_b200 import build, mpm
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "mpm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mpm_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    build.build()
+    L = mpm.load()
+    names = _declared()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(names) == set(mpm.EXPORTS)
+
+
+@pytest.mark.parametrize("bad", [
+    dict(dim=4), dict(res=100), dict(res=8), dict(batch=0), dict(n_particles=0),
+    dict(max_steps=0), dict(n_actuators=-1), dict(dt=0.0), dict(bound=40),
+])
+def test_config_validation_is_host_side(bad):
+    kw = dict(dim=3, res=64, batch=1, n_particles=10, max_steps=4, dt=1e-4)
+    kw.update(bad)
+    cfg = mpm.Config(**kw)
+    with pytest.raises(mpm.MPMError) as e:
+        mpm.MPM(cfg)
+    assert e.value.status == "MPM_ERR_INVALID_ARG"
+
+
+def test_no_cpu_fallback(monkeypatch, tmp_path):
+    """The binding refuses to run without the CUDA library (no silent fallback)."""
+    monkeypatch.setattr(mpm, "LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(mpm, "_lib", None)
+    with pytest.raises(ImportError):
+        mpm.load()
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1810_01054_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "mpm_oracle" not in txt and "liboracle" not in txt, f
