@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""Benchmark of the differentiable MLS-MPM step (ChainQueen, arXiv 1810.01054) on B200.
+
+Metric (BASELINE.json): particle-steps/s, forward + backward, 3D, at N GPUs; HBM GB/s as a
+fraction of the measured peak for the dominant kernel.
+
+Workload (N = 1 and per rank for N > 1): configs[3] "C4" -- 3D 128^3 grid, 1,048,576-particle
+neo-Hookean slab (64x32x64 cells, 8 particles per cell, v0 = (0,-1,0), 8 octant actuators,
+dt = 1e-4).  One "step" = one forward MLS-MPM step (binning, P2G, grid update, G2P) plus its
+reverse-mode step (G2P^T, grid^T, P2G^T) -- every row of SURVEY 8(a).  K steps = forward K
+steps onto the tape, then the backward pass over those K steps (loss: final CoM x).
+Multi-GPU: each rank runs its own independent C4 rollout (weak scaling, no data-path
+collective); the barrier / max-over-ranks timing uses torch.distributed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1810_01054_b200 import scenes  # noqa: E402
+
+METRIC = "particle-steps/sec fwd and fwd+bwd (3D, 1/2/4/8 B200); HBM GB/s % peak"
+UNIT = "particle-steps/s"
+WORKLOAD = ("C4 (configs[3]): 3D 128^3 grid, 1,048,576-particle neo-Hookean slab, "
+            "forward+backward, loss = final CoM x")
+SEG = 200  # max steps per tape segment (tape memory ~ 100 MB per step at C4)
+
+
+def _cfg_dict(K, W, n_gpus, sc):
+    return {"workload": WORKLOAD, "particles_per_rank": int(sc.batch * sc.n), "grid": f"{sc.res}^3",
+            "dim": 3, "dt": sc.dt, "steps_per_pass": K, "warmup": W,
+            "parallelism": f"batch-sharded x{n_gpus} (independent rollouts)" if n_gpus > 1 else "single GPU",
+            "l2": "inputs larger than L2: per-step state 96 MiB read + 96 MiB written, tape of K states"}
+
+
+# ---------------------------------------------------------------------------------------
+# clocks during the timed region (NVML, sampled in a thread)
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+               0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# Algorithmic bytes per launch: what each kernel must move, per
+# particle (NT) and per touched grid node (TN), fp32.
+ALG_BYTES = {
+    "p2g": (96 + 20, 16),          # read x,v,C,F + m,V,mu,lam,aid ; write (p,m) per node
+    "g2p": (48 + 96, 16),          # read x,F + write x,v,C,F ; read (vbar,m) per node
+    "p2g_T": (96 + 20 + 96 + 96 + 16, 32),  # tape state, params, adj in, adj out, dmu/dlam RMW ; tape + adj node
+    "g2p_T": (48 + 96, 16),        # x,F + adj in ; write dv per node
+    "grid_update": (0, 32),
+    "grid_T": (0, 48),
+}
+
+
+def _traffic(kernel):
+    """dram bytes per launch from the committed ncu summary, if any (profiles/*.json)."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path))["per_launch_dram_bytes"][kernel]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1810_01054_b200 import mpm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    K, W = args.steps, args.warmup
+    seg = min(K, SEG)
+    tape = max(seg, min(W, SEG), 1)
+    sc = scenes.slab_3d(seed=rank, steps=tape)
+    stream = torch.cuda.current_stream(dev)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=tape, device=dev.index, stream=stream.cuda_stream))
+    NT = sc.batch * sc.n
+    m = torch.tensor(sc.mass.reshape(-1), device=dev, dtype=torch.float64)
+    seed = torch.zeros((NT, 3), device=dev, dtype=torch.float32)
+    seed[:, 0] = (m / m.sum()).float()
+    sim.set_scene(sc)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def passes(n_steps, fwd_events=None):
+        left = n_steps
+        while left > 0:
+            s = min(left, seg)
+            sim.rewind(0)
+            sim.forward(s)
+            if fwd_events is not None:
+                fwd_events.append(torch.cuda.Event(enable_timing=True))
+                fwd_events[-1].record(stream)
+            sim.backward(seed)
+            left -= s
+
+    # warm-up: W steps (forward + backward), untimed
+    passes(max(W, 1))
+    # timed region: exactly K steps
+    barrier()
+    n0 = sim.launches
+    with ClockSampler(dev.index) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        fwd_ev = []
+        e0.record(stream)
+        passes(K, fwd_ev)
+        e1.record(stream)
+        barrier()
+    launches = sim.launches - n0
+    ms = e0.elapsed_time(e1)
+    fwd_ms = e0.elapsed_time(fwd_ev[0]) if len(fwd_ev) == 1 else None
+    t = torch.tensor([ms, fwd_ms or 0.0], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, fwd_ms = float(t[0]), (float(t[1]) if fwd_ms is not None else None)
+    value = NT * K * world / (ms / 1e3)
+
+    # roofline: per-kernel CUDA-event times of a second, profiled pass of the same K steps
+    sim.set_profiling(True)
+    passes(K)
+    prof = sim.profile()
+    sim.set_profiling(False)
+    steps_info = [sim.step_info(t_)[1] for t_ in range(sim.tape_length)]
+    TN = float(np.mean(steps_info)) * 64
+    peak, peak_src = _peaks()
+    per_kernel = {}
+    for kname, (ms_k, n_k) in prof.items():
+        if n_k == 0:
+            continue
+        ent = {"ms_total": round(ms_k, 4), "launches": n_k, "us_per_launch": round(1e3 * ms_k / n_k, 2)}
+        if kname in ALG_BYTES:
+            bp, bn = ALG_BYTES[kname]
+            byt = bp * NT + bn * TN
+            ent["alg_bytes_per_launch"] = int(byt)
+            ent["gbs"] = round(byt / (ms_k / n_k * 1e-3) / 1e9, 1)
+        per_kernel[kname] = ent
+    dom = max((k for k in per_kernel if k in ALG_BYTES), key=lambda k: per_kernel[k]["ms_total"])
+    d = per_kernel[dom]
+    prof_total = sum(v["ms_total"] for v in per_kernel.values())
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": round(d["gbs"] / peak, 4), "traffic": _traffic(dom),
+                "peak_source": peak_src, "share_of_step": round(d["ms_total"] / prof_total, 3),
+                "alg_bytes_per_launch": d["alg_bytes_per_launch"],
+                "per_kernel": per_kernel}
+
+    # e2e through the public API with pinned host buffers: set_state (H2D), forward,
+    # backward (seed H2D), grad (D2H), every pass
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    h_in = [pin(a.reshape(NT, *a.shape[2:])) for a in (sc.x, sc.v, sc.F, sc.C, sc.mass, sc.vol, sc.E, sc.nu, sc.actuator_id)]
+    act = np.zeros((1, tape, sc.n_act, 3), np.float32)
+    act[:, :min(tape, sc.act.shape[1])] = sc.act[:, :tape]
+    h_act = pin(act)
+    h_seed = pin(seed.cpu().numpy())
+    h_out = {k: torch.empty(s, dtype=torch.float32).pin_memory() for k, s in
+             (("dx0", (NT, 3)), ("dv0", (NT, 3)), ("dF0", (NT, 3, 3)), ("dC0", (NT, 3, 3)),
+              ("dE", (NT,)), ("dnu", (NT,)), ("da", (1, tape, sc.n_act, 3)))}
+    h2d = sum(a.numel() * a.element_size() for a in h_in) + h_act.numel() * 4
+    d2h = sum(a.numel() * a.element_size() for a in h_out.values())
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    left = K
+    nseg = 0
+    while left > 0:
+        s = min(left, seg)
+        sim.set_state(*h_in)
+        sim.set_actuation(h_act)
+        sim.forward(s)
+        sim.backward(h_seed)
+        sim.grad(h_out)
+        left -= s
+        nseg += 1
+    e3.record(stream)
+    barrier()
+    e2e_ms = e2.elapsed_time(e3)
+    t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t[0])
+    e2e = {"value": NT * K * world / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int((h2d + h_seed.numel() * 4) * nseg / K),
+           "d2h_bytes_per_step": int(d2h * nseg / K)}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded jittered-lattice slab)",
+            "config": _cfg_dict(K, W, world, sc),
+            "fwd": {"value": (NT * K * world / (fwd_ms / 1e3)) if fwd_ms else None,
+                    "ms_per_step": (fwd_ms / K) if fwd_ms else None},
+            "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary()}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_full(sc)
+    sim.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------------
+# oracle legs (CPU): cpu_baseline of our line, and the --impl reference arm
+# ---------------------------------------------------------------------------------------
+def _oracle_fb(sc, n_steps):
+    import oracle
+    cfg = oracle.Config(dim=sc.dim, res=sc.res, dt=sc.dt, gravity=sc.gravity, bound=sc.bound,
+                        friction=sc.friction, act_strength=sc.act_strength, n_act=sc.n_act)
+    st = oracle.pack(sc.x[0], sc.v[0], sc.C[0], sc.F[0])
+    prm = [a[0].astype(np.float64) for a in (sc.mass, sc.vol, sc.E, sc.nu)]
+    t0 = time.perf_counter()
+    traj = oracle.forward(cfg, st, *prm, sc.actuator_id[0], sc.act[0][:n_steps].astype(np.float64), n_steps)
+    t1 = time.perf_counter()
+    seed = np.zeros_like(traj[-1])
+    seed[:, 0] = prm[0] / prm[0].sum()
+    oracle.backward(cfg, traj, *prm, sc.actuator_id[0], sc.act[0][:n_steps].astype(np.float64), seed)
+    t2 = time.perf_counter()
+    return t1 - t0, t2 - t0
+
+
+def cpu_baseline_full(sc):
+    """The oracle as it stands (fp64, single thread) on the full C4 state: 1 forward + 1
+    backward step (~10-30 s of CPU work)."""
+    f, fb = _oracle_fb(sc, 1)
+    n = sc.batch * sc.n
+    return {"value": n / fb, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"full C4 state ({n} particles), 1 forward + 1 backward step, fp64, 1 thread; "
+                      f"forward alone {n / f:.4g} particle-steps/s"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as it stands, on the same metric/config/unit; each
+    step is a bounded sample of the C4 workload (a sub-slab at the same density)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    cells = (32, 16, 32) if K + W <= 40 else (16, 16, 16)
+    sc = scenes.slab_3d(seed=0, steps=2, cells=cells)
+    n = sc.batch * sc.n
+    for _ in range(W):
+        _oracle_fb(sc, 1)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        _oracle_fb(sc, 1)
+    dt = time.perf_counter() - t0
+    value = n * K / dt
+    full = scenes.slab_3d(seed=0, steps=1)
+    sample = (f"sub-slab {cells[0]}x{cells[1]}x{cells[2]} cells of the C4 slab at the same density "
+              f"({n} particles, 128^3 grid), 1 forward + 1 backward step per step, fp64, 1 thread")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": K, "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded jittered-lattice slab)",
+            "config": _cfg_dict(K, W, args.gpus, full),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

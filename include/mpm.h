@@ -132,6 +132,10 @@ mpm_status mpm_get_binning(mpm_ctx ctx, int32_t t, float* x_store, int32_t* orig
  * p/m + dt g (before the wall projection, R5/R6); 0 on untouched nodes.                 */
 mpm_status mpm_get_grid(mpm_ctx ctx, int32_t t, float* m, float* vbar);
 
+/* Block table of tape step t: out[0] = occupied grid blocks, out[1] = touched blocks (grid
+ * slots, 64 nodes each), out[2] = first arena slot of the step.  t < tape length.        */
+mpm_status mpm_get_step_info(mpm_ctx ctx, int32_t t, int32_t out[3]);
+
 /* Per-kernel device time (ms) and launch counts accumulated while profiling is on; names
  * are returned as a ';'-separated list.  n_kernels in/out. */
 mpm_status mpm_set_profiling(mpm_ctx ctx, int32_t on);

@@ -695,6 +695,18 @@ mpm_status mpm_get_grid(mpm_ctx c, int32_t t, float* m, float* vbar) {
   return s;
 }
 
+mpm_status mpm_get_step_info(mpm_ctx c, int32_t t, int32_t out[3]) {
+  if (!c || !out) return MPM_ERR_INVALID_ARG;
+  if (!c->has_state || t < 0 || t >= c->tape_len) return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape");
+  cudaSetDevice(c->cfg.device);
+  int h[kInfo];
+  CK(cudaMemcpy(h, info_at(c, t), sizeof(h), cudaMemcpyDeviceToHost));
+  out[0] = h[I_NOCC];
+  out[1] = h[I_NTOUCH];
+  out[2] = h[I_BASE];
+  return MPM_OK;
+}
+
 mpm_status mpm_set_profiling(mpm_ctx c, int32_t on) {
   if (!c) return MPM_ERR_INVALID_ARG;
   if (!on && c->profiling) {

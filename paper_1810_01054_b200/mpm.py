@@ -27,7 +27,7 @@ STATUS = {0: "MPM_OK", 1: "MPM_ERR_INVALID_ARG", 2: "MPM_ERR_OOM", 3: "MPM_ERR_C
 EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "mpm_forward",
            "mpm_tape_length", "mpm_rewind", "mpm_get_state", "mpm_backward", "mpm_grad",
            "mpm_last_error", "mpm_get_binning", "mpm_get_grid", "mpm_set_profiling",
-           "mpm_get_profile", "mpm_launch_count")
+           "mpm_get_profile", "mpm_launch_count", "mpm_get_step_info")
 
 
 class MPMError(RuntimeError):
@@ -75,6 +75,7 @@ def load():
     L.mpm_get_grid.argtypes = [vp, i32, vp, vp]
     L.mpm_set_profiling.argtypes = [vp, i32]
     L.mpm_get_profile.argtypes = [vp, C.POINTER(i32), vp, vp, C.c_char_p, i32]
+    L.mpm_get_step_info.argtypes = [vp, i32, vp]
     L.mpm_launch_count.argtypes = [vp]
     L.mpm_launch_count.restype = i64
     for name in EXPORTS:
@@ -253,6 +254,12 @@ class MPM:
         vbar = np.empty((cfg.batch, nn, cfg.dim), np.float32)
         self._check(self.L.mpm_get_grid(self.h, int(t), _ptr(m), _ptr(vbar)))
         return m, vbar
+
+    def step_info(self, t: int):
+        """(occupied blocks, touched blocks, first arena slot) of tape step t."""
+        out = np.zeros(3, np.int32)
+        self._check(self.L.mpm_get_step_info(self.h, int(t), _ptr(out)))
+        return tuple(int(v) for v in out)
 
     def set_profiling(self, on: bool):
         self._check(self.L.mpm_set_profiling(self.h, 1 if on else 0))
