@@ -36,7 +36,7 @@ struct mpm_ctx_s {
   int D = 3, S = 24;
   cudaStream_t stream = nullptr;
   int n_sm = 148;
-  int occ_scatter = 2;
+  int occ_scatter = 2, occ_g2p = 2, occ_p2gT = 2;
   int tape_len = 0;
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
   std::string last_error;
@@ -263,7 +263,8 @@ void launch_forward_step(mpm_ctx c, int t) {
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
   launch(c, KI_P2G, [&] { k_block_scatter<D, false><<<nblk, kThreads, 0, c->stream>>>(P, A); });
   launch(c, KI_GRID, [&] { k_grid_update<<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), c->arena); });
-  launch(c, KI_G2P, [&] { k_g2p<D><<<grid1d(P.NT), 256, 0, c->stream>>>(P, A); });
+  const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
+  launch(c, KI_G2P, [&] { k_g2p<D><<<ng, kThreads, 0, c->stream>>>(P, A); });
 }
 
 template <int D>
@@ -279,7 +280,8 @@ void launch_backward_step(mpm_ctx c, int t, const float* gin, float* gout) {
   launch(c, KI_GRIDT, [&] {
     k_grid_adj<D><<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), touch_at(c, t), c->arena, c->agrid);
   });
-  launch(c, KI_P2GT, [&] { k_p2g_adj<D><<<grid1d(P.NT, 128), 128, 0, c->stream>>>(P, A); });
+  const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
+  launch(c, KI_P2GT, [&] { k_p2g_adj<D><<<na, kThreads, 0, c->stream>>>(P, A); });
 }
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
@@ -506,6 +508,17 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   if (k.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<3, false>, kThreads, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<2, false>, kThreads, 0);
   c->occ_scatter = std::max(1, occ);
+  if (k.dim == 3) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<3>, kThreads, 0);
+    c->occ_g2p = std::max(1, occ);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<3>, kThreads, 0);
+    c->occ_p2gT = std::max(1, occ);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<2>, kThreads, 0);
+    c->occ_g2p = std::max(1, occ);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<2>, kThreads, 0);
+    c->occ_p2gT = std::max(1, occ);
+  }
 
   const size_t NT = P.NT, T = k.max_steps, S = c->S, D = k.dim;
   mpm_status s = MPM_OK;

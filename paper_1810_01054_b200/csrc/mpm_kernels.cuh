@@ -15,6 +15,17 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// occupancy targets (min CTAs per SM) of the block kernels; tuned on B200
+#ifndef MPM_G2P_MINB
+#define MPM_G2P_MINB 4
+#endif
+#ifndef MPM_P2GT_MINB
+#define MPM_P2GT_MINB 2
+#endif
+#ifndef MPM_SCAT_MINB
+#define MPM_SCAT_MINB 4
+#endif
+
 namespace mpm {
 
 constexpr int kCPB = 64;         // cells (and nodes) per grid block
@@ -48,7 +59,7 @@ struct KParams {
 
 // Per-step bookkeeping record, info[t * kInfo + field]
 constexpr int kInfo = 8;
-enum { I_NOCC = 0, I_NTOUCH = 1, I_BASE = 2, I_WORK = 3, I_WORK2 = 4, I_OK = 5 };
+enum { I_NOCC = 0, I_NTOUCH = 1, I_BASE = 2, I_WORK = 3, I_WORK2 = 4, I_OK = 5, I_WORK3 = 6, I_WORK4 = 7 };
 
 struct ErrLatch { int code, step, particle, pad; };
 
@@ -478,6 +489,8 @@ __global__ void k_scan_b(KParams P, int n_tiles, int3* __restrict__ tile_sums, i
     I[I_BASE] = base;
     I[I_WORK] = 0;
     I[I_WORK2] = 0;
+    I[I_WORK3] = 0;
+    I[I_WORK4] = 0;
     I[I_OK] = ok;
   }
 }
@@ -553,7 +566,7 @@ __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __rest
 // ------------------------------------------------------------------------------------
 __global__ void k_zero_slots(int* __restrict__ info_t, float4* __restrict__ g) {
   int n = info_t[I_NTOUCH] * kCPB;
-  if (blockIdx.x == 0 && threadIdx.x == 0) info_t[I_WORK2] = 0;  // adjoint work counter
+  if (blockIdx.x == 0 && threadIdx.x == 0) info_t[I_WORK2] = info_t[I_WORK4] = 0;  // adjoint work counters
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
@@ -609,7 +622,7 @@ struct StepArgs {
 };
 
 template <int D, bool ADJ>
-__global__ __launch_bounds__(kThreads, 2) void k_block_scatter(KParams P, StepArgs A) {
+__global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
   using DD = Dim<D>;
   using PY = Pay<D, ADJ>;
   constexpr int BB = DD::BB, TE = DD::TE, TN = DD::TN;
@@ -908,128 +921,492 @@ __global__ void k_grid_update(KParams P, const int* __restrict__ info_t, float4*
   }
 }
 
-// node fetch helpers for the gathers: the 2^D grid blocks spanned by a stencil
-template <int D> struct StencilSlots {
-  int slot[1 << D];
-  int b0[D];
-};
-
+// ------------------------------------------------------------------------------------
+// Block-tile gathers (G2P, P2G^T).  One CTA per occupied grid block (dynamic work
+// counter).  The block's (Bb+2)^D node tile is staged once in shared memory -- node
+// velocity after the wall projection of step L (applied once per node), and
+// for P2G^T also the adjoint node (dL/dp_i, dL/dm_i) -- then every particle of the block
+// (contiguous in sorted order) reads its 3^D stencil from the tile.
+// Weights are separable, W = wx(ox) wy(oy) wz(oz); oz-sums are formed first and folded
+// per (ox, oy), so the moments sum_i W v_i o_b cost O(1) per node.
+// ------------------------------------------------------------------------------------
 template <int D>
-__device__ __forceinline__ void stencil_slots(const KParams& P, int r, const Stencil<D>& sc,
-                                              const int* __restrict__ slot_of, StencilSlots<D>& ss) {
+__device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, int* bc) {
+  r = gb / P.nb;
+  int t = gb - r * P.nb;
 #pragma unroll
-  for (int a = 0; a < D; ++a) ss.b0[a] = sc.base[a] >> Dim<D>::LOG_BB;
+  for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
+}
+
+// stage tile nodes: velocity (projected) into s_v; optional second grid (adjoint) into s_a
+template <int D, bool TWO>
+__device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, int r, const int* bc,
+                                           float4* s_v, float4* s_a, size_t abase) {
+  using DD = Dim<D>;
+  for (int tn = threadIdx.x; tn < DD::TN; tn += kThreads) {
+    int tl[D], node[D], nb_[D], loc[D];
+    int t = tn;
 #pragma unroll
-  for (int q = 0; q < (1 << D); ++q) {
-    int b[D];
-    bool ok = true;
+    for (int a = D - 1; a >= 0; --a) { tl[a] = t % DD::TE; t /= DD::TE; }
+    bool inside = true;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      b[a] = ss.b0[a] + ((q >> (D - 1 - a)) & 1);
-      ok &= b[a] < P.nbpa;
+      node[a] = bc[a] * DD::BB + tl[a];
+      inside &= node[a] < P.res;
+      nb_[a] = node[a] >> DD::LOG_BB;
+      loc[a] = node[a] & (DD::BB - 1);
     }
-    ss.slot[q] = ok ? slot_of[r * P.nb + block_lin<D>(b, P.nbpa)] : -1;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f), ad = v;
+    if (inside) {
+      const int slot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+      if (slot >= 0) {
+        const size_t addr = (size_t)slot * kCPB + cell_lin<D>(loc);
+        v = A.tgrid[addr];
+        if (v.w > 0.f && in_band<D>(node, P.res, P.bound)) {
+          float vv[D];
+          vv[0] = v.x; vv[1] = v.y;
+          if constexpr (D == 3) vv[2] = v.z;
+          project_node<D>(vv, node, P);
+          v.x = vv[0]; v.y = vv[1];
+          if constexpr (D == 3) v.z = vv[2];
+        }
+        if (TWO) ad = A.grid[addr - abase];
+      }
+    }
+    s_v[tn] = v;
+    if (TWO) s_a[tn] = ad;
   }
 }
 
-template <int D>
-__device__ __forceinline__ size_t node_addr(const StencilSlots<D>& ss, const int* node) {
-  int q = 0, loc[D];
+template <int D, int OX, int OY, int OZ>
+__device__ __forceinline__ int tile_idx(const int* lb) {
+  constexpr int TE = Dim<D>::TE;
+  if constexpr (D == 3) return ((lb[0] + OX) * TE + lb[1] + OY) * TE + lb[2] + OZ;
+  else return (lb[0] + OX) * TE + lb[1] + OY;
+}
+
+// ---- G2P (Eqs. 7-10): v' = S, C' = 4 res (M - S fx^T), F' = (I + dt C') F,
+//      x' = x + dt v'; writes state t+1 in sorted order + keys/histogram of step t+1 ----
+template <int D, int OX, int OY, int OZ>
+__device__ __forceinline__ void g2p_node(const float4* s_v, const int* lb, const Stencil<D>& sc,
+                                         float wxy, float* Sxy, float* Zxy) {
+  const float4 g = s_v[tile_idx<D, OX, OY, OZ>(lb)];
+  float vi[3] = {g.x, g.y, g.z};
+  const float W = (D == 3) ? wxy * sc.w[D - 1][OZ] : wxy;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    q = q * 2 + ((node[a] >> Dim<D>::LOG_BB) - ss.b0[a]);
-    loc[a] = node[a] & (Dim<D>::BB - 1);
+    const float wv = W * vi[a];
+    Sxy[a] += wv;
+    if (OZ == 1) Zxy[a] += wv;
+    if (OZ == 2) Zxy[a] = fmaf(2.f, wv, Zxy[a]);
   }
-  return (size_t)ss.slot[q] * kCPB + cell_lin<D>(loc);
 }
 
-// ------------------------------------------------------------------------------------
-// G2P (Eqs. 7-10): gather v and C, update F and x, write state t+1 in sorted
-// order, and the keys + block histogram of step t+1 (binning of the next step).
-// ------------------------------------------------------------------------------------
+template <int D, int OX, int OY>
+__device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const Stencil<D>& sc,
+                                        float* S, float (&M)[D][D]) {
+  const float wxy = sc.w[0][OX] * sc.w[1][OY];
+  float Sxy[D], Zxy[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) Sxy[a] = Zxy[a] = 0.f;
+  if constexpr (D == 3) {
+    g2p_node<D, OX, OY, 0>(s_v, lb, sc, wxy, Sxy, Zxy);
+    g2p_node<D, OX, OY, 1>(s_v, lb, sc, wxy, Sxy, Zxy);
+    g2p_node<D, OX, OY, 2>(s_v, lb, sc, wxy, Sxy, Zxy);
+  } else {
+    g2p_node<D, OX, OY, 0>(s_v, lb, sc, wxy, Sxy, Zxy);
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    S[a] += Sxy[a];
+    if (OX) M[a][0] = fmaf((float)OX, Sxy[a], M[a][0]);
+    if (OY) M[a][1] = fmaf((float)OY, Sxy[a], M[a][1]);
+    if constexpr (D == 3) M[a][2] += Zxy[a];
+  }
+}
+
 template <int D>
-__global__ __launch_bounds__(256) void k_g2p(KParams P, StepArgs A) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  bool valid = k < P.NT;
-  int gbn = 0;
-  if (valid) {
-    const size_t NT = P.NT;
-    const int j = A.perm[k];
-    const int r = k / P.N;
-    float x[D], F[D][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
-#pragma unroll
-      for (int b = 0; b < D; ++b) F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
-    }
-    Stencil<D> sc;
-    make_stencil<D>(x, P.fres, sc);
-    StencilSlots<D> ss;
-    stencil_slots<D>(P, r, sc, A.slot_of, ss);
-    float vn[D], M[D][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      vn[a] = 0.f;
-#pragma unroll
-      for (int b = 0; b < D; ++b) M[a][b] = 0.f;
-    }
-#pragma unroll
-    for (int s = 0; s < Dim<D>::NS; ++s) {
-      int o[D], node[D];
-      float W = 1.f;
+__global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepArgs A) {
+  __shared__ float4 s_v[Dim<D>::TN];
+  __shared__ int s_blk;
+  const size_t NT = P.NT;
+  const int n_occ = A.info_t[I_NOCC];
+  for (;;) {
+    if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK3], 1);
+    __syncthreads();
+    const int bi = s_blk;
+    if (bi >= n_occ) break;
+    const int gb = A.occ_list[bi];
+    const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
+    int r, bc[D];
+    block_coords<D>(P, gb, r, bc);
+    stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += kThreads) {
+      const int k = s + i;
+      const int j = __ldg(&A.perm[k]);
+      float x[D], F[D][D];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        o[a] = (D == 3) ? (a == 0 ? s / 9 : (a == 1 ? (s / 3) % 3 : s % 3)) : (a == 0 ? s / 3 : s % 3);
-        node[a] = sc.base[a] + o[a];
-        W *= sc.w[a][o[a]];
-      }
-      float4 g = A.grid[node_addr<D>(ss, node)];
-      float vi[D];
-      vi[0] = g.x; vi[1] = g.y;
-      if (D == 3) vi[D - 1] = g.z;
-      if (!(g.w > 0.f)) {
+        x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
 #pragma unroll
-        for (int a = 0; a < D; ++a) vi[a] = 0.f;
-      } else if (in_band<D>(node, P.res, P.bound)) {
-        project_node<D>(vi, node, P);
+        for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
       }
+      const int u = __ldg(&A.orig[j]);
+      Stencil<D> sc;
+      make_stencil<D>(x, P.fres, sc);
+      int lb[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) lb[a] = sc.base[a] - bc[a] * Dim<D>::BB;
+      float S[D], M[D][D];
 #pragma unroll
       for (int a = 0; a < D; ++a) {
-        float wv = W * vi[a];
-        vn[a] += wv;
+        S[a] = 0.f;
 #pragma unroll
-        for (int b = 0; b < D; ++b) M[a][b] = fmaf(wv, (float)o[b] - sc.fx[b], M[a][b]);
+        for (int b = 0; b < D; ++b) M[a][b] = 0.f;
+      }
+      g2p_row<D, 0, 0>(s_v, lb, sc, S, M); g2p_row<D, 0, 1>(s_v, lb, sc, S, M); g2p_row<D, 0, 2>(s_v, lb, sc, S, M);
+      g2p_row<D, 1, 0>(s_v, lb, sc, S, M); g2p_row<D, 1, 1>(s_v, lb, sc, S, M); g2p_row<D, 1, 2>(s_v, lb, sc, S, M);
+      g2p_row<D, 2, 0>(s_v, lb, sc, S, M); g2p_row<D, 2, 1>(s_v, lb, sc, S, M); g2p_row<D, 2, 2>(s_v, lb, sc, S, M);
+      float* out = A.st_next;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        float Cn[D];
+#pragma unroll
+        for (int b = 0; b < D; ++b) Cn[b] = 4.f * P.fres * fmaf(-S[a], sc.fx[b], M[a][b]);
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+          float acc = F[a][b];
+#pragma unroll
+          for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[c], F[c][b], acc);
+          out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
+          out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[b];
+        }
+        out[(size_t)comp_v<D>(a) * NT + k] = S[a];
+        x[a] = fmaf(P.dt, S[a], x[a]);
+        out[(size_t)comp_x<D>(a) * NT + k] = x[a];
+      }
+      A.orig_next[k] = u;
+      int gbn, key;
+      if (!key_of<D>(x, r, P, gbn, key)) latch(A.err, E_DOMAIN, A.t + 1, u);
+      A.key_next[k] = key;
+      // block histogram of step t+1 (threads of a warp mostly share one block)
+      const unsigned am = __activemask();
+      const unsigned peers = __match_any_sync(am, gbn);
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&A.cnt[gbn], __popc(peers));
+    }
+    __syncthreads();
+  }
+}
+
+// ---- P2G^T gather (steps F-K and J; E/nu per R19) in the Kirchhoff form:
+//   T = dL/dtau = -k Q, Q = dL/dG = sum_i w dp_i (x_i - x_p)^T, k = 4 dt V / dx^2
+//   dv^t = m sum_i w dp_i ; dC^t = m Q
+//   dF^t = (I + dt C^{t+1})^T dF^{t+1} + mu (T + T^T) F + lam tr(T) F^{-T} + (T + T^T) F sigma
+//   dx^t = dx^{t+1} + sum_i dW_i s_i - 4 res^2 g_C^T v^{t+1} - G^T sum_i w dp_i
+//     s_i = v_i . u(o) + dp_i . q(o) + m dm_i,  u(o) = g_v + 4 res g_C (o - fx)  (the G2P^T
+//     payload), q(o) = m v + dx G (o - fx) (the P2G payload) -- both affine in o
+//   dsigma = F^T T F (diag -> actuation); dmu = T : (F F^T - I); dlam = tr(T) ln J
+template <int D> struct AdjAcc {
+  float S[D], Sd[D];          // sum W v_i, sum W dp_i
+  float Mv[D][D], Md[D][D];   // sum W v_i o_b, sum W dp_i o_b
+  float gx[D];                // sum dW s_i
+};
+
+template <int D> struct AdjPay {
+  float u0[D], U[D][D];       // u(o) = u0 + U o
+  float q0[D], Qm[D][D];      // q(o) = q0 + Qm o
+  float m;
+  float dw[D][3];             // res * dN
+};
+
+template <int D, int OX, int OY, int OZ>
+__device__ __forceinline__ void adj_node(const float4* s_v, const float4* s_a, const int* lb,
+                                         const Stencil<D>& sc, const AdjPay<D>& Y, const float* uxy,
+                                         const float* qxy, float wxy, float* Sxy, float* Zxy,
+                                         float* Dxy, float* Exy, float& t1, float& t2) {
+  const int ti = tile_idx<D, OX, OY, OZ>(lb);
+  const float4 g = s_v[ti];
+  const float4 ad = s_a[ti];
+  float vi[3] = {g.x, g.y, g.z}, dp[3] = {ad.x, ad.y, ad.z};
+  float s = Y.m * ad.w;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float u = uxy[a], q = qxy[a];
+    if constexpr (D == 3) {
+      if (OZ) {
+        u = fmaf((float)OZ, Y.U[a][2], u);
+        q = fmaf((float)OZ, Y.Qm[a][2], q);
       }
     }
-    // C' = 4/dx^2 sum w v (x_i - x_p)^T = 4 res sum w v (o - fx)^T ; F' = (I + dt C') F
-    float Cn[D][D];
+    s = fmaf(vi[a], u, s);
+    s = fmaf(dp[a], q, s);
+  }
+  const float wz = (D == 3) ? sc.w[D - 1][OZ] : 1.f;
+  const float W = wxy * wz;
+  t1 = fmaf(wz, s, t1);
+  if constexpr (D == 3) t2 = fmaf(Y.dw[2][OZ], s, t2);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    const float wv = W * vi[a], wd = W * dp[a];
+    Sxy[a] += wv;
+    Dxy[a] += wd;
+    if (OZ == 1) { Zxy[a] += wv; Exy[a] += wd; }
+    if (OZ == 2) { Zxy[a] = fmaf(2.f, wv, Zxy[a]); Exy[a] = fmaf(2.f, wd, Exy[a]); }
+  }
+}
+
+template <int D, int OX, int OY>
+__device__ __forceinline__ void adj_row(const float4* s_v, const float4* s_a, const int* lb,
+                                        const Stencil<D>& sc, const AdjPay<D>& Y, AdjAcc<D>& R) {
+  float uxy[D], qxy[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    uxy[a] = Y.u0[a];
+    qxy[a] = Y.q0[a];
+    if (OX) { uxy[a] = fmaf((float)OX, Y.U[a][0], uxy[a]); qxy[a] = fmaf((float)OX, Y.Qm[a][0], qxy[a]); }
+    if (OY) { uxy[a] = fmaf((float)OY, Y.U[a][1], uxy[a]); qxy[a] = fmaf((float)OY, Y.Qm[a][1], qxy[a]); }
+  }
+  const float wx = sc.w[0][OX], wy = sc.w[1][OY];
+  const float wxy = wx * wy;
+  float Sxy[D], Zxy[D], Dxy[D], Exy[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) Sxy[a] = Zxy[a] = Dxy[a] = Exy[a] = 0.f;
+  float t1 = 0.f, t2 = 0.f;
+  if constexpr (D == 3) {
+    adj_node<D, OX, OY, 0>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
+    adj_node<D, OX, OY, 1>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
+    adj_node<D, OX, OY, 2>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
+    R.gx[0] = fmaf(Y.dw[0][OX] * wy, t1, R.gx[0]);
+    R.gx[1] = fmaf(wx * Y.dw[1][OY], t1, R.gx[1]);
+    R.gx[2] = fmaf(wxy, t2, R.gx[2]);
+  } else {
+    adj_node<D, OX, OY, 0>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
+    R.gx[0] = fmaf(Y.dw[0][OX] * wy, t1, R.gx[0]);
+    R.gx[1] = fmaf(wx * Y.dw[1][OY], t1, R.gx[1]);
+  }
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    R.S[a] += Sxy[a];
+    R.Sd[a] += Dxy[a];
+    if (OX) { R.Mv[a][0] = fmaf((float)OX, Sxy[a], R.Mv[a][0]); R.Md[a][0] = fmaf((float)OX, Dxy[a], R.Md[a][0]); }
+    if (OY) { R.Mv[a][1] = fmaf((float)OY, Sxy[a], R.Mv[a][1]); R.Md[a][1] = fmaf((float)OY, Dxy[a], R.Md[a][1]); }
+    if constexpr (D == 3) { R.Mv[a][2] += Zxy[a]; R.Md[a][2] += Exy[a]; }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArgs& A, const float4* s_v,
+                                                 const float4* s_a, const int* bc, int r, int k,
+                                                 int& aid_out, float* dsig_out) {
+  const size_t NT = P.NT;
+  const int j = __ldg(&A.perm[k]);
+  const int u = __ldg(&A.orig[j]);
+  const float4 pr = __ldg(&A.prm[u]);
+  const float* gi = A.gin;
+  float x[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
+  Stencil<D> sc;
+  make_stencil<D>(x, P.fres, sc);
+  const int ai = __ldg(&A.aid[u]);
+  float sig[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    sig[a] = ai >= 0 ? P.act_s * __ldg(&A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a]) : 0.f;
+  const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
+  AdjPay<D> Y;
+  Y.m = pr.x;
+  {
+    float F[D][D], tau[D][D];
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
-      for (int b = 0; b < D; ++b) Cn[a][b] = 4.f * P.fres * M[a][b];
-    float* out = A.st_next;
+      for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
+    const float lnJ = logf(det<D>(F));
+    kirchhoff<D>(F, pr.z, pr.w, sig, tau, lnJ);
+    // q(o) = m v + dx G (o - fx), G = -kk tau + m C  (Eq. 4-5)
 #pragma unroll
     for (int a = 0; a < D; ++a) {
+      float q0 = pr.x * __ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]);
 #pragma unroll
       for (int b = 0; b < D; ++b) {
-        float acc = F[a][b];
-#pragma unroll
-        for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[a][c], F[c][b], acc);
-        out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
-        out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[a][b];
+        const float Gab = fmaf(-kk, tau[a][b], pr.x * __ldg(&A.st[(size_t)comp_C<D>(a, b) * NT + j]));
+        Y.Qm[a][b] = P.dx * Gab;
+        q0 = fmaf(-Y.Qm[a][b], sc.fx[b], q0);
       }
-      out[(size_t)comp_v<D>(a) * NT + k] = vn[a];
-      x[a] = fmaf(P.dt, vn[a], x[a]);
-      out[(size_t)comp_x<D>(a) * NT + k] = x[a];
+      Y.q0[a] = q0;
     }
-    const int u = A.orig[j];
-    A.orig_next[k] = u;
-    int key;
-    if (!key_of<D>(x, r, P, gbn, key)) latch(A.err, E_DOMAIN, A.t + 1, u);
-    A.key_next[k] = key;
+    // u(o) = g_v + 4 res g_C (o - fx); g_v = gv + dt gx (step A), g_C = gC + dt gF F^T (step B)
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float u0 = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
+      float gF[D];
+#pragma unroll
+      for (int c = 0; c < D; ++c) gF[c] = gi[(size_t)comp_F<D>(a, c) * NT + k];
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float gc = gi[(size_t)comp_C<D>(a, b) * NT + k];
+#pragma unroll
+        for (int c = 0; c < D; ++c) gc = fmaf(P.dt * gF[c], F[b][c], gc);
+        Y.U[a][b] = 4.f * P.fres * gc;
+        u0 = fmaf(-Y.U[a][b], sc.fx[b], u0);
+      }
+      Y.u0[a] = u0;
+    }
   }
-  warp_hist_add(A.cnt, gbn, valid);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float dw[3];
+    stencil_dw(sc.fx[a], dw);
+#pragma unroll
+    for (int o = 0; o < 3; ++o) Y.dw[a][o] = P.fres * dw[o];
+  }
+  int lb[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) lb[a] = sc.base[a] - bc[a] * Dim<D>::BB;
+  AdjAcc<D> R;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    R.S[a] = R.Sd[a] = R.gx[a] = 0.f;
+#pragma unroll
+    for (int b = 0; b < D; ++b) R.Mv[a][b] = R.Md[a][b] = 0.f;
+  }
+  adj_row<D, 0, 0>(s_v, s_a, lb, sc, Y, R); adj_row<D, 0, 1>(s_v, s_a, lb, sc, Y, R); adj_row<D, 0, 2>(s_v, s_a, lb, sc, Y, R);
+  adj_row<D, 1, 0>(s_v, s_a, lb, sc, Y, R); adj_row<D, 1, 1>(s_v, s_a, lb, sc, Y, R); adj_row<D, 1, 2>(s_v, s_a, lb, sc, Y, R);
+  adj_row<D, 2, 0>(s_v, s_a, lb, sc, Y, R); adj_row<D, 2, 1>(s_v, s_a, lb, sc, Y, R); adj_row<D, 2, 2>(s_v, s_a, lb, sc, Y, R);
+
+  float Q[D][D], Cn[D][D], T[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      Q[a][b] = P.dx * fmaf(-R.Sd[a], sc.fx[b], R.Md[a][b]);
+      Cn[a][b] = 4.f * P.fres * fmaf(-R.S[a], sc.fx[b], R.Mv[a][b]);  // C^{t+1}, Eq. 8
+      T[a][b] = -kk * Q[a][b];
+    }
+  float* go = A.gout;
+  const float m = pr.x;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    go[(size_t)comp_v<D>(a) * NT + j] = m * R.Sd[a];  // (F)
+#pragma unroll
+    for (int b = 0; b < D; ++b) go[(size_t)comp_C<D>(a, b) * NT + j] = m * Q[a][b];  // (I)
+  }
+  // (J): G^T = Qm^T / dx, g_C = U / (4 res)
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float acc = gi[(size_t)comp_x<D>(a) * NT + k] + R.gx[a];
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      acc = fmaf(-P.fres * Y.U[b][a], R.S[b], acc);
+      acc = fmaf(-P.fres * Y.Qm[b][a], R.Sd[b], acc);
+    }
+    go[(size_t)comp_x<D>(a) * NT + j] = acc;
+  }
+  // (H), (K), material parameters
+  float F[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
+  const float J = det<D>(F);
+  const float lnJ = logf(J);
+  float FiT[D][D];
+  inv_T<D>(F, J, FiT);
+  float trT = 0.f;
+#pragma unroll
+  for (int a = 0; a < D; ++a) trT += T[a][a];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      float acc = gi[(size_t)comp_F<D>(a, b) * NT + k];
+      float tf = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        acc = fmaf(P.dt * Cn[c][a], gi[(size_t)comp_F<D>(c, b) * NT + k], acc);
+        tf = fmaf(T[a][c] + T[c][a], F[c][b], tf);
+      }
+      acc = fmaf(pr.z + sig[b], tf, acc);  // mu (T+T^T) F + (T+T^T) F sigma
+      acc = fmaf(pr.w * trT, FiT[a][b], acc);
+      go[(size_t)comp_F<D>(a, b) * NT + j] = acc;
+    }
+  float dmu = 0.f, dsig[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float ds = 0.f;
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      float tf = 0.f, ff = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        tf = fmaf(T[b][c], F[c][a], tf);
+        ff = fmaf(F[a][c], F[b][c], ff);
+      }
+      ds = fmaf(F[b][a], tf, ds);
+      dmu = fmaf(T[a][b], ff - (a == b ? 1.f : 0.f), dmu);
+    }
+    dsig[a] = P.act_s * ds;
+  }
+  A.dmu[u] += dmu;
+  A.dlam[u] += trT * lnJ;
+  aid_out = ai;
+#pragma unroll
+  for (int a = 0; a < D; ++a) dsig_out[a] = dsig[a];
+}
+
+// Segmented warp reduction of the actuation gradient (step K -> dL/da[r][t][k]): one
+// butterfly sum and one global atomic per distinct actuator id in the warp.  Called by all
+// 32 lanes (key < 0 = no contribution).
+template <int D>
+__device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArgs& A, int r, int key,
+                                                 const float* v) {
+  const int lane = threadIdx.x & 31;
+  unsigned todo = __ballot_sync(0xffffffffu, key >= 0);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    const int k0 = __shfl_sync(0xffffffffu, key, src);
+    const bool mine = key == k0;
+    todo &= ~__ballot_sync(0xffffffffu, mine);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float s = mine ? v[a] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == src) atomicAdd(&A.da[(((size_t)r * P.T + A.t) * P.K + k0) * D + a], s);
+    }
+  }
+}
+
+template <int D>
+__global__ __launch_bounds__(kThreads, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
+  __shared__ float4 s_v[Dim<D>::TN];
+  __shared__ float4 s_a[Dim<D>::TN];
+  __shared__ int s_blk;
+  const int n_occ = A.info_t[I_NOCC];
+  const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
+  for (;;) {
+    if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
+    __syncthreads();
+    const int bi = s_blk;
+    if (bi >= n_occ) break;
+    const int gb = A.occ_list[bi];
+    const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
+    int r, bc[D];
+    block_coords<D>(P, gb, r, bc);
+    stage_tile<D, true>(P, A, r, bc, s_v, s_a, abase);
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += kThreads) {  // uniform trip count: whole warps reach the reduction
+      const int i = i0 + threadIdx.x;
+      int ai = -1;
+      float dsig[D] = {};
+      if (i < n) p2g_adj_particle<D>(P, A, s_v, s_a, bc, r, s + i, ai, dsig);
+      __syncwarp();
+      if (P.K > 0) reduce_actuation<D>(P, A, r, ai, dsig);
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -1073,251 +1450,6 @@ __global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int*
       out.w = -pg * im;
     }
     ag[i] = out;
-  }
-}
-
-// ------------------------------------------------------------------------------------
-// P2G^T gather (steps F-K and J; E/nu per R19) in the Kirchhoff form:
-//   T = dL/dtau = -k Q, Q = dL/dG = sum_i w dp_i (x_i - x_p)^T, k = 4 dt V / dx^2
-//   dv^t = m sum_i w dp_i ; dC^t = m Q
-//   dF^t = (I + dt C^{t+1})^T dF^{t+1} + mu (T + T^T) F + lam tr(T) F^{-T} + (T + T^T) F sigma
-//   dx^t = dx^{t+1} + sum_i dW_i s_i - 4 res^2 g_C^T v^{t+1} - G^T sum_i w dp_i
-//     s_i = v_i . (g_v + 4 res g_C (o - fx)) + dp_i . (m v + G d_i) + m dm_i
-//   dsigma = F^T T F (diag -> actuation); dmu = T : (F F^T - I); dlam = tr(T) ln J
-// ------------------------------------------------------------------------------------
-template <int D>
-__global__ __launch_bounds__(128) void k_p2g_adj(KParams P, StepArgs A) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = k < P.NT;
-  const size_t NT = P.NT;
-  int ai = -1;
-  float dsig[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) dsig[a] = 0.f;
-  int r = 0;
-  if (valid) {
-    const int j = A.perm[k];
-    r = k / P.N;
-    const int u = A.orig[j];
-    const float4 pr = A.prm[u];
-    const float m = pr.x;
-    float x[D], v[D], F[D][D], Cm[D][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
-      v[a] = A.st[(size_t)comp_v<D>(a) * NT + j];
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
-        Cm[a][b] = A.st[(size_t)comp_C<D>(a, b) * NT + j];
-      }
-    }
-    ai = A.aid[u];
-    float sig[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-      sig[a] = ai >= 0 ? P.act_s * A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a] : 0.f;
-    const float J = det<D>(F);
-    const float lnJ = logf(J);
-    float tau[D][D];
-    kirchhoff<D>(F, pr.z, pr.w, sig, tau, lnJ);
-    const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
-    float G[D][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) G[a][b] = fmaf(-kk, tau[a][b], m * Cm[a][b]);
-    // incoming adjoint (storage order t+1 = sorted index k), steps A and B
-    const float* gi = A.gin;
-    float gx[D], gvh[D], gF[D][D], gCh[D][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      gx[a] = gi[(size_t)comp_x<D>(a) * NT + k];
-      gvh[a] = fmaf(P.dt, gx[a], gi[(size_t)comp_v<D>(a) * NT + k]);
-#pragma unroll
-      for (int b = 0; b < D; ++b) gF[a][b] = gi[(size_t)comp_F<D>(a, b) * NT + k];
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        float acc = gi[(size_t)comp_C<D>(a, b) * NT + k];
-#pragma unroll
-        for (int c = 0; c < D; ++c) acc = fmaf(P.dt * gF[a][c], F[b][c], acc);
-        gCh[a][b] = acc;
-      }
-
-    Stencil<D> sc;
-    make_stencil<D>(x, P.fres, sc);
-    float dw[D][3];
-#pragma unroll
-    for (int a = 0; a < D; ++a) stencil_dw(sc.fx[a], dw[a]);
-    StencilSlots<D> ss;
-    stencil_slots<D>(P, r, sc, A.slot_of, ss);
-    const int base_slot = A.info_t[I_BASE];
-
-    float Sv[D], Sdp[D], Mv[D][D], Q[D][D], gradx[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      Sv[a] = Sdp[a] = gradx[a] = 0.f;
-#pragma unroll
-      for (int b = 0; b < D; ++b) Mv[a][b] = Q[a][b] = 0.f;
-    }
-    float msum = 0.f;  // sum_i w dm_i  (unused by the formulas; kept for symmetry checks)
-    (void)msum;
-#pragma unroll 1
-    for (int s = 0; s < Dim<D>::NS; ++s) {
-      int o[D], node[D];
-      float W = 1.f, dW[D], d[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        o[a] = (D == 3) ? (a == 0 ? s / 9 : (a == 1 ? (s / 3) % 3 : s % 3)) : (a == 0 ? s / 3 : s % 3);
-        node[a] = sc.base[a] + o[a];
-        W *= sc.w[a][o[a]];
-        d[a] = (float)o[a] - sc.fx[a];  // (x_i - x_p) / dx
-      }
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        float gw = P.fres * dw[a][o[a]];
-#pragma unroll
-        for (int b = 0; b < D; ++b)
-          if (b != a) gw *= sc.w[b][o[b]];
-        dW[a] = gw;  // dW/dx_p (R10)
-      }
-      const size_t addr = node_addr<D>(ss, node);
-      const float4 g = A.tgrid[addr];
-      const float4 ad = A.grid[addr - (size_t)base_slot * kCPB];
-      float vi[D], dp[D];
-      vi[0] = g.x; vi[1] = g.y; dp[0] = ad.x; dp[1] = ad.y;
-      if (D == 3) { vi[D - 1] = g.z; dp[D - 1] = ad.z; }
-      const float dm = ad.w;
-      if (!(g.w > 0.f)) {
-#pragma unroll
-        for (int a = 0; a < D; ++a) vi[a] = 0.f;
-      } else if (in_band<D>(node, P.res, P.bound)) {
-        project_node<D>(vi, node, P);
-      }
-      // s_i
-      float si = m * dm;
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        float gcd = 0.f, Gd = 0.f;
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          gcd = fmaf(gCh[a][b], d[b], gcd);
-          Gd = fmaf(G[a][b], d[b], Gd);
-        }
-        si = fmaf(vi[a], fmaf(4.f * P.fres, gcd, gvh[a]), si);
-        si = fmaf(dp[a], fmaf(m, v[a], P.dx * Gd), si);
-      }
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        gradx[a] = fmaf(dW[a], si, gradx[a]);
-        const float wv = W * vi[a], wdp = W * dp[a];
-        Sv[a] += wv;
-        Sdp[a] += wdp;
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          Mv[a][b] = fmaf(wv, d[b], Mv[a][b]);
-          Q[a][b] = fmaf(wdp, d[b], Q[a][b]);
-        }
-      }
-    }
-    // Q = dL/dG = sum w dp (x_i - x_p)^T  -> scale by dx
-    float T[D][D], Cn[D][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        Q[a][b] *= P.dx;
-        T[a][b] = -kk * Q[a][b];
-        Cn[a][b] = 4.f * P.fres * Mv[a][b];  // C^{t+1}, Eq. 8 recomputed from the tape grid
-      }
-    float* go = A.gout;
-    // (F) dv = m sum w dp
-#pragma unroll
-    for (int a = 0; a < D; ++a) go[(size_t)comp_v<D>(a) * NT + j] = m * Sdp[a];
-    // (I) dC = m Q
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) go[(size_t)comp_C<D>(a, b) * NT + j] = m * Q[a][b];
-    // (J)
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      float acc = gx[a] + gradx[a];
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        acc = fmaf(-4.f * P.fres * P.fres * gCh[b][a], Sv[b], acc);
-        acc = fmaf(-G[b][a], Sdp[b], acc);
-      }
-      go[(size_t)comp_x<D>(a) * NT + j] = acc;
-    }
-    // (H) in Kirchhoff form
-    float Ts[D][D], FiT[D][D];
-    inv_T<D>(F, J, FiT);
-    float trT = 0.f;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      trT += T[a][a];
-#pragma unroll
-      for (int b = 0; b < D; ++b) Ts[a][b] = T[a][b] + T[b][a];
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        float acc = gF[a][b];
-        float tf = 0.f;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          acc = fmaf(P.dt * Cn[c][a], gF[c][b], acc);
-          tf = fmaf(Ts[a][c], F[c][b], tf);
-        }
-        acc = fmaf(pr.z + sig[b], tf, acc);  // mu (T+T^T) F + (T+T^T) F sigma
-        acc = fmaf(pr.w * trT, FiT[a][b], acc);
-        go[(size_t)comp_F<D>(a, b) * NT + j] = acc;
-      }
-    // (K) dsigma = F^T T F (diagonal), material parameters (R19)
-    float dmu = 0.f;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      float ds = 0.f;
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        float tf = 0.f, ff = 0.f;
-#pragma unroll
-        for (int c = 0; c < D; ++c) {
-          tf = fmaf(T[b][c], F[c][a], tf);
-          ff = fmaf(F[a][c], F[b][c], ff);
-        }
-        ds = fmaf(F[b][a], tf, ds);
-        dmu = fmaf(T[a][b], ff - (a == b ? 1.f : 0.f), dmu);
-      }
-      dsig[a] = P.act_s * ds;
-    }
-    A.dmu[u] += dmu;
-    A.dlam[u] += trT * lnJ;
-  }
-  // actuation gradient: warp-reduce when the warp shares one actuator, else per-lane atomics
-  const unsigned vm = __ballot_sync(0xffffffffu, valid && ai >= 0);
-  if (vm) {
-    const int lane = threadIdx.x & 31;
-    const int ai0 = __shfl_sync(0xffffffffu, ai, __ffs(vm) - 1);
-    const int r0 = __shfl_sync(0xffffffffu, r, __ffs(vm) - 1);
-    const bool uniform = __all_sync(0xffffffffu, !(valid && ai >= 0) || (ai == ai0 && r == r0));
-    if (uniform) {
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        float v = (valid && ai >= 0) ? dsig[a] : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) atomicAdd(&A.da[(((size_t)r0 * P.T + A.t) * P.K + ai0) * D + a], v);
-      }
-    } else if (valid && ai >= 0) {
-#pragma unroll
-      for (int a = 0; a < D; ++a) atomicAdd(&A.da[(((size_t)r * P.T + A.t) * P.K + ai) * D + a], dsig[a]);
-    }
   }
 }
 

@@ -1,0 +1,41 @@
+"""Per-kernel device time of the C4 forward + backward step (CUDA events around every
+launch inside libmpm).  Usage: python tools/time_step.py [steps] [lib_path]"""
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_1810_01054_b200 import mpm, scenes  # noqa: E402
+
+
+def main():
+    K = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+    if len(sys.argv) > 2:
+        mpm.LIB_PATH = sys.argv[2]
+    sc = scenes.slab_3d(steps=K)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=K))
+    sim.set_scene(sc)
+    m = sc.mass.reshape(-1).astype(np.float64)
+    seed = np.zeros((sc.n, 3), np.float32)
+    seed[:, 0] = m / m.sum()
+    for _ in range(2):
+        sim.rewind(0)
+        sim.forward(K)
+        sim.backward(seed)
+    sim.set_profiling(True)
+    sim.rewind(0)
+    sim.forward(K)
+    sim.backward(seed)
+    prof = sim.profile()
+    tot = sum(v[0] for v in prof.values())
+    out = {k: round(1e3 * v[0] / max(v[1], 1), 2) for k, v in prof.items() if v[1]}
+    print(json.dumps({"lib": os.path.basename(mpm.LIB_PATH), "us_per_launch": out,
+                      "us_per_FB_step": round(1e3 * tot / K, 1)}))
+
+
+if __name__ == "__main__":
+    main()
