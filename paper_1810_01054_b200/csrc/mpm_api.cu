@@ -36,7 +36,7 @@ struct mpm_ctx_s {
   int D = 3, S = 24;
   cudaStream_t stream = nullptr;
   int n_sm = 148;
-  int occ_scatter = 2, occ_g2p = 2, occ_p2gT = 2;
+  int occ_scatter = 2, occ_scatter_adj = 2, occ_g2p = 2, occ_p2gT = 2;
   int tape_len = 0;
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
   std::string last_error;
@@ -70,6 +70,8 @@ struct mpm_ctx_s {
   float* gA = nullptr;
   float* gB = nullptr;
   float4* agrid = nullptr;
+  float4* agrid1 = nullptr;
+  unsigned* bflag = nullptr;
   float* dmu = nullptr;
   float* dlam = nullptr;
   float* da = nullptr;
@@ -246,13 +248,15 @@ StepArgs step_args(mpm_ctx c, int t) {
 template <int D>
 void launch_bin(mpm_ctx c, int t) {
   const KParams& P = c->P;
-  launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->tile_sums); });
+  launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->bflag, c->tile_sums); });
   launch(c, KI_SCAN_B, [&] { k_scan_b<<<1, kThreads, 0, c->stream>>>(P, c->n_tiles, c->tile_sums, c->info, t, c->err); });
   launch(c, KI_SCAN_C, [&] {
-    k_scan_c<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->tile_sums, info_at(c, t), bs_at(c, t),
-                                                         slot_at(c, t), occ_at(c, t), touch_at(c, t), c->arena);
+    k_scan_c<<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->bflag, c->tile_sums, info_at(c, t), bs_at(c, t),
+                                                      slot_at(c, t), occ_at(c, t), touch_at(c, t));
   });
-  launch(c, KI_SCATTER, [&] { k_scatter<<<grid1d(P.NT), 256, 0, c->stream>>>(P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_perm); });
+  launch(c, KI_SCATTER, [&] {
+    k_scatter<<<grid1d(P.NT), 256, 0, c->stream>>>(P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_perm, info_at(c, t), c->arena);
+  });
 }
 
 template <int D>
@@ -261,24 +265,30 @@ void launch_forward_step(mpm_ctx c, int t) {
   launch_bin<D>(c, t);
   StepArgs A = step_args(c, t);
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
-  launch(c, KI_P2G, [&] { k_block_scatter<D, false><<<nblk, kThreads, 0, c->stream>>>(P, A); });
+  launch(c, KI_P2G, [&] { k_block_scatter<D, false><<<nblk, kThreads, scatter_dyn_smem<D, false>(), c->stream>>>(P, A); });
   launch(c, KI_GRID, [&] { k_grid_update<<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), c->arena); });
   const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
   launch(c, KI_G2P, [&] { k_g2p<D><<<ng, kThreads, 0, c->stream>>>(P, A); });
 }
 
+// adjoint grid buffer of backward step t (double-buffered by step parity)
+float4* agrid_of(mpm_ctx c, int t) { return (t & 1) ? c->agrid1 : c->agrid; }
+
 template <int D>
 void launch_backward_step(mpm_ctx c, int t, const float* gin, float* gout) {
   const KParams& P = c->P;
   StepArgs A = step_args(c, t);
-  A.grid = c->agrid;
+  A.grid = agrid_of(c, t);
   A.gin = gin;
   A.gout = gout;
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
-  launch(c, KI_ZERO, [&] { k_zero_slots<<<c->n_sm * 4, 256, 0, c->stream>>>(info_at(c, t), c->agrid); });
-  launch(c, KI_G2PT, [&] { k_block_scatter<D, true><<<nblk, kThreads, 0, c->stream>>>(P, A); });
+  if (t == c->tape_len - 1)  // first backward step: prepare its buffer (later steps: by grid_T)
+    launch(c, KI_ZERO, [&] { k_zero_slots<<<c->n_sm * 4, 256, 0, c->stream>>>(info_at(c, t), A.grid); });
+  const int nbla = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter_adj));
+  launch(c, KI_G2PT, [&] { k_block_scatter<D, true><<<nbla, kThreads, scatter_dyn_smem<D, true>(), c->stream>>>(P, A); });
   launch(c, KI_GRIDT, [&] {
-    k_grid_adj<D><<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), touch_at(c, t), c->arena, c->agrid);
+    k_grid_adj<D><<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
+                                                       t > 0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
   launch(c, KI_P2GT, [&] { k_p2g_adj<D><<<na, kThreads, 0, c->stream>>>(P, A); });
@@ -320,7 +330,7 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   launch_keys<D>(c, 0);
   // automatic grid-slot capacity from the touched blocks of the initial state
   if (c->arena == nullptr) {
-    launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->tile_sums); });
+    launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->bflag, c->tile_sums); });
     std::vector<int3> ts(c->n_tiles);
     CK(cudaMemcpyAsync(ts.data(), c->tile_sums, ts.size() * sizeof(int3), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -334,6 +344,8 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
     mpm_status s = dalloc(c, &c->arena, c->arena_slots * kCPB);
     if (s) return s;
     s = dalloc(c, &c->agrid, (size_t)per * kCPB);
+    if (s) return s;
+    s = dalloc(c, &c->agrid1, (size_t)per * kCPB);
     if (s) return s;
   }
   CK(cudaMemsetAsync(c->dmu, 0, NT * sizeof(float), c->stream));
@@ -505,9 +517,22 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   P.act_s = k.act_strength;
   c->n_tiles = (P.NBT + kScanTile - 1) / kScanTile;
   int occ = 0;
-  if (k.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<3, false>, kThreads, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<2, false>, kThreads, 0);
-  c->occ_scatter = std::max(1, occ);
+  // dynamic shared memory of the block-tile scatter (payload buffer) above the 48 KB default
+  cudaFuncSetAttribute(k_block_scatter<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<3, false>());
+  cudaFuncSetAttribute(k_block_scatter<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<3, true>());
+  cudaFuncSetAttribute(k_block_scatter<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, false>());
+  cudaFuncSetAttribute(k_block_scatter<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, true>());
+  if (k.dim == 3) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<3, false>, kThreads, scatter_dyn_smem<3, false>());
+    c->occ_scatter = std::max(1, occ);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<3, true>, kThreads, scatter_dyn_smem<3, true>());
+    c->occ_scatter_adj = std::max(1, occ);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<2, false>, kThreads, scatter_dyn_smem<2, false>());
+    c->occ_scatter = std::max(1, occ);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<2, true>, kThreads, scatter_dyn_smem<2, true>());
+    c->occ_scatter_adj = std::max(1, occ);
+  }
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<3>, kThreads, 0);
     c->occ_g2p = std::max(1, occ);
@@ -538,6 +563,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   AL(scratch, NT);
   AL(hist2, (size_t)P.NBT);
   AL(tile_sums, (size_t)c->n_tiles);
+  AL(bflag, (size_t)P.NBT);
   AL(err, 1);
   AL(dbad, 1);
   AL(prm, NT);

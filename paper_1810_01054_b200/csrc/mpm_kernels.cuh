@@ -23,16 +23,19 @@
 #define MPM_P2GT_MINB 2
 #endif
 #ifndef MPM_SCAT_MINB
-#define MPM_SCAT_MINB 4
+#define MPM_SCAT_MINB 3
+#endif
+#ifndef MPM_SCATA_MINB
+#define MPM_SCATA_MINB 3
 #endif
 
 namespace mpm {
 
 constexpr int kCPB = 64;         // cells (and nodes) per grid block
 constexpr int kThreads = 256;    // CTA size of the block-tile kernels
-constexpr int kCap = 256;        // particles per producer chunk
+constexpr int kCap = 512;        // particles per producer chunk
 constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks use scratch)
-constexpr int kScanTile = 2048;  // grid blocks per scan tile
+constexpr int kScanTile = kThreads;  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
 
 enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6 };
@@ -378,9 +381,11 @@ __global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __rest
 
 // ------------------------------------------------------------------------------------
 // block table of step t: exclusive scans of (count, occupied, touched) over all grid
-// blocks, the occupied list, touched list and slot map; zeroes the step's grid slots.
+// blocks, the occupied list, touched list and slot map.
 // touched(b) = some block b - delta, delta in {0,1}^D, holds particles (a particle with
 // base in block b' touches nodes of b' and b' + delta only).
+// Three kernels: (a) per-block flags + tile sums (one block per thread), (b) one CTA scans
+// the tile sums and sets the step record, (c) tile-local scans write the tables.
 // ------------------------------------------------------------------------------------
 template <int D>
 __device__ __forceinline__ void block_flags(const KParams& P, const int* cnt, int gb, int& c,
@@ -402,7 +407,7 @@ __device__ __forceinline__ void block_flags(const KParams& P, const int* cnt, in
       nb_[a] = b[a] - ((dl >> (D - 1 - a)) & 1);
       ok &= nb_[a] >= 0;
     }
-    if (ok) any |= cnt[r * P.nb + block_lin<D>(nb_, P.nbpa)] > 0;
+    if (ok) any |= __ldg(&cnt[r * P.nb + block_lin<D>(nb_, P.nbpa)]) > 0;
   }
   tch = any;
 }
@@ -437,23 +442,20 @@ __device__ __forceinline__ int3 cta_excl_scan3(int3 v, int3* s_warp, int3& total
   return make_int3(wo.x + inc.x - v.x, wo.y + inc.y - v.y, wo.z + inc.z - v.z);
 }
 
+// flag word of a block: count | occupied << 30 | touched << 31
 template <int D>
 __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __restrict__ cnt,
+                                                     unsigned* __restrict__ bflag,
                                                      int3* __restrict__ tile_sums) {
-  constexpr int PER = kScanTile / kThreads;
   __shared__ int3 s_warp[kThreads / 32 + 1];
-  int3 sum = make_int3(0, 0, 0);
-  int g0 = blockIdx.x * kScanTile + threadIdx.x * PER;
-  for (int q = 0; q < PER; ++q) {
-    int gb = g0 + q;
-    if (gb < P.NBT) {
-      int c, o, t;
-      block_flags<D>(P, cnt, gb, c, o, t);
-      sum.x += c; sum.y += o; sum.z += t;
-    }
+  const int gb = blockIdx.x * kScanTile + threadIdx.x;
+  int c = 0, o = 0, t = 0;
+  if (gb < P.NBT) {
+    block_flags<D>(P, cnt, gb, c, o, t);
+    bflag[gb] = (unsigned)c | ((unsigned)o << 30) | ((unsigned)t << 31);
   }
   int3 tot;
-  cta_excl_scan3(sum, s_warp, tot);
+  cta_excl_scan3(make_int3(c, o, t), s_warp, tot);
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
 }
 
@@ -495,56 +497,42 @@ __global__ void k_scan_b(KParams P, int n_tiles, int3* __restrict__ tile_sums, i
   }
 }
 
-template <int D>
-__global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const int* __restrict__ cnt,
+__global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const unsigned* __restrict__ bflag,
                                                      const int3* __restrict__ tile_pre,
                                                      const int* __restrict__ info_t,
                                                      int* __restrict__ block_start,
                                                      int* __restrict__ slot_of,
                                                      int* __restrict__ occ_list,
-                                                     int* __restrict__ touched_list,
-                                                     float4* __restrict__ arena) {
-  constexpr int PER = kScanTile / kThreads;
+                                                     int* __restrict__ touched_list) {
   __shared__ int3 s_warp[kThreads / 32 + 1];
-  int ok = info_t[I_OK];
-  int base = info_t[I_BASE];
-  int c[PER], o[PER], tc[PER];
-  int3 sum = make_int3(0, 0, 0);
-  int g0 = blockIdx.x * kScanTile + threadIdx.x * PER;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    int gb = g0 + q;
-    c[q] = o[q] = tc[q] = 0;
-    if (gb < P.NBT) block_flags<D>(P, cnt, gb, c[q], o[q], tc[q]);
-    sum.x += c[q]; sum.y += o[q]; sum.z += tc[q];
-  }
+  const int ok = info_t[I_OK];
+  const int base = info_t[I_BASE];
+  const int gb = blockIdx.x * kScanTile + threadIdx.x;
+  const unsigned f = gb < P.NBT ? bflag[gb] : 0u;
+  const int c = (int)(f & 0x3fffffffu), o = (f >> 30) & 1, tc = f >> 31;
   int3 tot;
-  int3 ex = cta_excl_scan3(sum, s_warp, tot);
-  int3 tp = tile_pre[blockIdx.x];
-  ex.x += tp.x; ex.y += tp.y; ex.z += tp.z;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) {
-    int gb = g0 + q;
-    if (gb < P.NBT) {
-      block_start[gb] = ex.x;
-      if (ok && o[q]) occ_list[ex.y] = gb;
-      slot_of[gb] = (ok && tc[q]) ? base + ex.z : -1;
-      if (ok && tc[q]) touched_list[ex.z] = gb;
-    }
-    ex.x += c[q]; ex.y += o[q]; ex.z += tc[q];
+  int3 ex = cta_excl_scan3(make_int3(c, o, tc), s_warp, tot);
+  const int3 tp = tile_pre[blockIdx.x];
+  if (gb < P.NBT) {
+    block_start[gb] = ex.x + tp.x;
+    if (ok && o) occ_list[ex.y + tp.y] = gb;
+    slot_of[gb] = (ok && tc) ? base + ex.z + tp.z : -1;
+    if (ok && tc) touched_list[ex.z + tp.z] = gb;
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kThreads - 1) block_start[P.NBT] = P.NT;
-  // zero this tile's contiguous range of slots
-  if (ok) {
-    float4* z = arena + (size_t)(base + tp.z) * kCPB;
-    int n = tot.z * kCPB;
-    for (int i = threadIdx.x; i < n; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  if (gb == P.NBT - 1) block_start[P.NBT] = P.NT;
 }
 
-// counting-sort scatter by block (positions inside a block are fixed up by k_p2g)
+// counting-sort scatter by block (positions inside a block are fixed up by k_block_scatter);
+// also zeroes the grid slots of step t (the P2G flush accumulates into them)
 __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __restrict__ block_start,
-                          int* __restrict__ cnt, int* __restrict__ tmp_perm) {
+                          int* __restrict__ cnt, int* __restrict__ tmp_perm,
+                          const int* __restrict__ info_t, float4* __restrict__ arena) {
+  {
+    const int nz = info_t[I_NTOUCH] * kCPB;
+    float4* z = arena + (size_t)info_t[I_BASE] * kCPB;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += gridDim.x * blockDim.x)
+      z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = j < NT;
   int gb = valid ? key[j] / kCPB : 0;
@@ -562,13 +550,18 @@ __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __rest
 }
 
 // ------------------------------------------------------------------------------------
-// zero a run of grid slots (adjoint grid of a backward step)
+// adjoint grid of backward step t: zero its slots and reset the step's work counters.
+// Used for the first backward step; later steps are prepared by k_grid_adj of step t+1.
 // ------------------------------------------------------------------------------------
+__device__ __forceinline__ void adj_prepare(int* __restrict__ info_t, float4* __restrict__ g, int tid,
+                                            int nthreads) {
+  const int n = info_t[I_NTOUCH] * kCPB;
+  if (tid == 0) info_t[I_WORK2] = info_t[I_WORK4] = 0;
+  for (int i = tid; i < n; i += nthreads) g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 __global__ void k_zero_slots(int* __restrict__ info_t, float4* __restrict__ g) {
-  int n = info_t[I_NTOUCH] * kCPB;
-  if (blockIdx.x == 0 && threadIdx.x == 0) info_t[I_WORK2] = info_t[I_WORK4] = 0;  // adjoint work counters
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    g[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  adj_prepare(info_t, g, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 // ------------------------------------------------------------------------------------
@@ -622,7 +615,10 @@ struct StepArgs {
 };
 
 template <int D, bool ADJ>
-__global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
+constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(float); }
+
+template <int D, bool ADJ>
+__global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
   using DD = Dim<D>;
   using PY = Pay<D, ADJ>;
   constexpr int BB = DD::BB, TE = DD::TE, TN = DD::TN;
@@ -631,7 +627,8 @@ __global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KPara
   __shared__ int s_cstart[kCPB + 1];
   __shared__ int s_cursor[kCPB];
   __shared__ int s_sort[ADJ ? 1 : kSortCap];
-  __shared__ float s_pay[PY::N][kCap];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  float (*s_pay)[kCap] = reinterpret_cast<float (*)[kCap]>(s_dyn);  // [PY::N][kCap], dynamic
   __shared__ float4 s_tile[3][TN];
   __shared__ int s_blk;
   const int tid = threadIdx.x;
@@ -711,10 +708,11 @@ __global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KPara
     }
 
     // ---- chunks of kCap particles: produce payload, consume per (cell, ox), phase-write ----
+    const int ox = tid / kCPB, c = tid % kCPB;
     for (int lo = 0; lo < n; lo += kCap) {
       const int hi = min(n, lo + kCap);
-      if (tid < hi - lo) {
-        const int k = s + lo + tid;
+      for (int pi = tid; pi < hi - lo; pi += kThreads) {
+        const int k = s + lo + pi;
         const int j = A.perm[k];
         float x[D], f[D];
         Stencil<D> sc;
@@ -725,7 +723,7 @@ __global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KPara
         for (int a = 0; a < D; ++a) {
           f[a] = sc.fx[a];
 #pragma unroll
-          for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][tid] = sc.w[a][o];
+          for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][pi] = sc.w[a][o];
         }
         float Av[D], Bm[D][D];
         if (!ADJ) {
@@ -765,7 +763,7 @@ __global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KPara
             for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], f[b], acc);
             Av[a] = acc;
           }
-          if (PY::M >= 0) s_pay[PY::M < 0 ? 0 : PY::M][tid] = pr.x;
+          if (PY::M >= 0) s_pay[PY::M < 0 ? 0 : PY::M][pi] = pr.x;
         } else {
           // steps A and B: g_v = gv + dt gx ; g_C = gC + dt gF F^T
           const float* gi = A.gin;
@@ -800,9 +798,9 @@ __global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KPara
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-          s_pay[PY::A + a][tid] = Av[a];
+          s_pay[PY::A + a][pi] = Av[a];
 #pragma unroll
-          for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][tid] = Bm[a][b];
+          for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][pi] = Bm[a][b];
         }
       }
       __syncthreads();
@@ -811,7 +809,6 @@ __global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KPara
       float4 acc[NSUB];
 #pragma unroll
       for (int q = 0; q < NSUB; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      const int ox = tid / kCPB, c = tid % kCPB;
       if (tid < 3 * kCPB) {
         const int i0 = max(s_cstart[c], lo) - lo, i1 = min(s_cstart[c + 1], hi) - lo;
         for (int i = i0; i < i1; ++i) {
@@ -852,25 +849,27 @@ __global__ __launch_bounds__(kThreads, MPM_SCAT_MINB) void k_block_scatter(KPara
           }
         }
       }
-      // phase-write: in phase q all threads of copy ox write distinct nodes c + (ox, q)
-      int cc[D];
-      {
-        int t = c;
+      // phase-write: in phase q the 64 threads of copy ox write the distinct nodes c + (ox, q);
+      // only threads of the same copy can collide across phases -> 64-thread named barriers
+      if (tid < 3 * kCPB) {
+        int cc[D];
+        {
+          int t = c;
 #pragma unroll
-        for (int a = D - 1; a >= 0; --a) { cc[a] = t % BB; t /= BB; }
-      }
+          for (int a = D - 1; a >= 0; --a) { cc[a] = t % BB; t /= BB; }
+        }
 #pragma unroll
-      for (int q = 0; q < NSUB; ++q) {
-        if (tid < 3 * kCPB) {
+        for (int q = 0; q < NSUB; ++q) {
           int tl;
           if (D == 3) tl = ((cc[0] + ox) * TE + cc[1] + q / 3) * TE + cc[D - 1] + q % 3;
           else tl = (cc[0] + ox) * TE + cc[D - 1] + q;
           float4 v = s_tile[ox][tl];
           v.x += acc[q].x; v.y += acc[q].y; v.z += acc[q].z; v.w += acc[q].w;
           s_tile[ox][tl] = v;
+          if (q + 1 < NSUB) asm volatile("bar.sync %0, %1;" ::"r"(1 + ox), "r"(kCPB) : "memory");
         }
-        __syncthreads();
       }
+      __syncthreads();  // payload consumed, tile copies written
     }
 
     // ---- flush: one vector RED per non-zero tile node ----
@@ -1415,7 +1414,10 @@ __global__ __launch_bounds__(kThreads, MPM_P2GT_MINB) void k_p2g_adj(KParams P, 
 // ------------------------------------------------------------------------------------
 template <int D>
 __global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int* __restrict__ touched_list,
-                           const float4* __restrict__ arena, float4* __restrict__ ag) {
+                           const float4* __restrict__ arena, float4* __restrict__ ag,
+                           int* __restrict__ info_prev, float4* __restrict__ ag_prev) {
+  // prepare the other adjoint buffer for backward step t-1 (zero + reset its counters)
+  if (info_prev) adj_prepare(info_prev, ag_prev, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   const int n = info_t[I_NTOUCH] * kCPB;
   const float4* g = arena + (size_t)info_t[I_BASE] * kCPB;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
