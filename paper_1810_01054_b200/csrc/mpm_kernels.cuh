@@ -1106,92 +1106,91 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
 //     s_i = v_i . u(o) + dp_i . q(o) + m dm_i,  u(o) = g_v + 4 res g_C (o - fx)  (the G2P^T
 //     payload), q(o) = m v + dx G (o - fx) (the P2G payload) -- both affine in o
 //   dsigma = F^T T F (diag -> actuation); dmu = T : (F F^T - I); dlam = tr(T) ln J
-template <int D> struct AdjAcc {
-  float S[D], Sd[D];          // sum W v_i, sum W dp_i
-  float Mv[D][D], Md[D][D];   // sum W v_i o_b, sum W dp_i o_b
-  float gx[D];                // sum dW s_i
+// Two passes over the 3^D stencil keep the live set small: the v-pass (S, M_v, sum dW v.u)
+// and the dp-pass (S_d, M_d, sum dW (dp.q + m dm)).
+// Per (ox, oy) row the oz-sums sum wz f and sum oz wz f are formed, then folded.
+template <int D> struct PassAcc {
+  float S[D];      // sum W f_i
+  float M[D][D];   // sum W f_i o_b
+  float g[D];      // sum dW (f_i . c(o) + e_i)
 };
 
-template <int D> struct AdjPay {
-  float u0[D], U[D][D];       // u(o) = u0 + U o
-  float q0[D], Qm[D][D];      // q(o) = q0 + Qm o
-  float m;
-  float dw[D][3];             // res * dN
-};
-
-template <int D, int OX, int OY, int OZ>
-__device__ __forceinline__ void adj_node(const float4* s_v, const float4* s_a, const int* lb,
-                                         const Stencil<D>& sc, const AdjPay<D>& Y, const float* uxy,
-                                         const float* qxy, float wxy, float* Sxy, float* Zxy,
-                                         float* Dxy, float* Exy, float& t1, float& t2) {
-  const int ti = tile_idx<D, OX, OY, OZ>(lb);
-  const float4 g = s_v[ti];
-  const float4 ad = s_a[ti];
-  float vi[3] = {g.x, g.y, g.z}, dp[3] = {ad.x, ad.y, ad.z};
-  float s = Y.m * ad.w;
+// one pass; F4 = tile of float4 (f = .xyz, e = em * .w), c(o) = c0 + Cm o
+template <int D, int OX, int OY>
+__device__ __forceinline__ void pass_row(const float4* tile, const int* lb, const float (&w)[D][3],
+                                         const float (&dw)[D][3], const float* c0, const float (&Cm)[D][D],
+                                         float em, PassAcc<D>& R) {
+  float cxy[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    float u = uxy[a], q = qxy[a];
-    if constexpr (D == 3) {
-      if (OZ) {
-        u = fmaf((float)OZ, Y.U[a][2], u);
-        q = fmaf((float)OZ, Y.Qm[a][2], q);
-      }
-    }
-    s = fmaf(vi[a], u, s);
-    s = fmaf(dp[a], q, s);
+    cxy[a] = c0[a];
+    if (OX) cxy[a] = fmaf((float)OX, Cm[a][0], cxy[a]);
+    if (OY) cxy[a] = fmaf((float)OY, Cm[a][1], cxy[a]);
   }
-  const float wz = (D == 3) ? sc.w[D - 1][OZ] : 1.f;
-  const float W = wxy * wz;
-  t1 = fmaf(wz, s, t1);
-  if constexpr (D == 3) t2 = fmaf(Y.dw[2][OZ], s, t2);
+  float A0[D], A1[D], t1 = 0.f, t2 = 0.f;
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    const float wv = W * vi[a], wd = W * dp[a];
-    Sxy[a] += wv;
-    Dxy[a] += wd;
-    if (OZ == 1) { Zxy[a] += wv; Exy[a] += wd; }
-    if (OZ == 2) { Zxy[a] = fmaf(2.f, wv, Zxy[a]); Exy[a] = fmaf(2.f, wd, Exy[a]); }
+  for (int a = 0; a < D; ++a) A0[a] = A1[a] = 0.f;
+  if constexpr (D == 3) {
+#pragma unroll
+    for (int oz = 0; oz < 3; ++oz) {
+      const float4 q = tile[tile_idx<D, OX, OY, 0>(lb) + oz];
+      const float f[3] = {q.x, q.y, q.z};
+      float sv = em * q.w;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) sv = fmaf(f[a], oz == 0 ? cxy[a] : fmaf((float)oz, Cm[a][2], cxy[a]), sv);
+      const float wz = w[2][oz];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        A0[a] = fmaf(wz, f[a], A0[a]);
+        if (oz) A1[a] = fmaf((float)oz * wz, f[a], A1[a]);
+      }
+      t1 = fmaf(wz, sv, t1);
+      t2 = fmaf(dw[2][oz], sv, t2);
+    }
+    const float wx = w[0][OX], wy = w[1][OY], wxy = wx * wy;
+    R.g[0] = fmaf(dw[0][OX] * wy, t1, R.g[0]);
+    R.g[1] = fmaf(wx * dw[1][OY], t1, R.g[1]);
+    R.g[2] = fmaf(wxy, t2, R.g[2]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      R.S[a] = fmaf(wxy, A0[a], R.S[a]);
+      if (OX) R.M[a][0] = fmaf((float)OX * wxy, A0[a], R.M[a][0]);
+      if (OY) R.M[a][1] = fmaf((float)OY * wxy, A0[a], R.M[a][1]);
+      R.M[a][2] = fmaf(wxy, A1[a], R.M[a][2]);
+    }
+  } else {
+    const float4 q = tile[tile_idx<D, OX, OY, 0>(lb)];
+    const float f[2] = {q.x, q.y};
+    float sv = em * q.w;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) sv = fmaf(f[a], cxy[a], sv);
+    const float wx = w[0][OX], wy = w[1][OY], wxy = wx * wy;
+    R.g[0] = fmaf(dw[0][OX] * wy, sv, R.g[0]);
+    R.g[1] = fmaf(wx * dw[1][OY], sv, R.g[1]);
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      R.S[a] = fmaf(wxy, f[a], R.S[a]);
+      if (OX) R.M[a][0] = fmaf((float)OX * wxy, f[a], R.M[a][0]);
+      if (OY) R.M[a][1] = fmaf((float)OY * wxy, f[a], R.M[a][1]);
+    }
   }
 }
 
-template <int D, int OX, int OY>
-__device__ __forceinline__ void adj_row(const float4* s_v, const float4* s_a, const int* lb,
-                                        const Stencil<D>& sc, const AdjPay<D>& Y, AdjAcc<D>& R) {
-  float uxy[D], qxy[D];
+template <int D>
+__device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, const float (&w)[D][3],
+                                             const float (&dw)[D][3], const float* c0,
+                                             const float (&Cm)[D][D], float em, PassAcc<D>& R) {
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    uxy[a] = Y.u0[a];
-    qxy[a] = Y.q0[a];
-    if (OX) { uxy[a] = fmaf((float)OX, Y.U[a][0], uxy[a]); qxy[a] = fmaf((float)OX, Y.Qm[a][0], qxy[a]); }
-    if (OY) { uxy[a] = fmaf((float)OY, Y.U[a][1], uxy[a]); qxy[a] = fmaf((float)OY, Y.Qm[a][1], qxy[a]); }
-  }
-  const float wx = sc.w[0][OX], wy = sc.w[1][OY];
-  const float wxy = wx * wy;
-  float Sxy[D], Zxy[D], Dxy[D], Exy[D];
+    R.S[a] = R.g[a] = 0.f;
 #pragma unroll
-  for (int a = 0; a < D; ++a) Sxy[a] = Zxy[a] = Dxy[a] = Exy[a] = 0.f;
-  float t1 = 0.f, t2 = 0.f;
-  if constexpr (D == 3) {
-    adj_node<D, OX, OY, 0>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
-    adj_node<D, OX, OY, 1>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
-    adj_node<D, OX, OY, 2>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
-    R.gx[0] = fmaf(Y.dw[0][OX] * wy, t1, R.gx[0]);
-    R.gx[1] = fmaf(wx * Y.dw[1][OY], t1, R.gx[1]);
-    R.gx[2] = fmaf(wxy, t2, R.gx[2]);
-  } else {
-    adj_node<D, OX, OY, 0>(s_v, s_a, lb, sc, Y, uxy, qxy, wxy, Sxy, Zxy, Dxy, Exy, t1, t2);
-    R.gx[0] = fmaf(Y.dw[0][OX] * wy, t1, R.gx[0]);
-    R.gx[1] = fmaf(wx * Y.dw[1][OY], t1, R.gx[1]);
+    for (int b = 0; b < D; ++b) R.M[a][b] = 0.f;
   }
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    R.S[a] += Sxy[a];
-    R.Sd[a] += Dxy[a];
-    if (OX) { R.Mv[a][0] = fmaf((float)OX, Sxy[a], R.Mv[a][0]); R.Md[a][0] = fmaf((float)OX, Dxy[a], R.Md[a][0]); }
-    if (OY) { R.Mv[a][1] = fmaf((float)OY, Sxy[a], R.Mv[a][1]); R.Md[a][1] = fmaf((float)OY, Dxy[a], R.Md[a][1]); }
-    if constexpr (D == 3) { R.Mv[a][2] += Zxy[a]; R.Md[a][2] += Exy[a]; }
-  }
+  pass_row<D, 0, 0>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 0, 1>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row<D, 0, 2>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 1, 0>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row<D, 1, 1>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 1, 2>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row<D, 2, 0>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 2, 1>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row<D, 2, 2>(tile, lb, w, dw, c0, Cm, em, R);
 }
 
 template <int D>
@@ -1199,108 +1198,103 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
                                                  const float4* s_a, const int* bc, int r, int k,
                                                  int& aid_out, float* dsig_out) {
   const size_t NT = P.NT;
-  const int j = __ldg(&A.perm[k]);
-  const int u = __ldg(&A.orig[j]);
-  const float4 pr = __ldg(&A.prm[u]);
   const float* gi = A.gin;
+  const int j = __ldg(&A.perm[k]);
+  const int u = __ldg(&A.orig_next[k]);  // = orig_t[perm[k]] (written by G2P of this step)
+  const float4 pr = __ldg(&A.prm[u]);
+  const int ai = __ldg(&A.aid[u]);
+  const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
   float x[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
   Stencil<D> sc;
   make_stencil<D>(x, P.fres, sc);
-  const int ai = __ldg(&A.aid[u]);
-  float sig[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a)
-    sig[a] = ai >= 0 ? P.act_s * __ldg(&A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a]) : 0.f;
-  const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
-  AdjPay<D> Y;
-  Y.m = pr.x;
-  {
-    float F[D][D], tau[D][D];
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
-    const float lnJ = logf(det<D>(F));
-    kirchhoff<D>(F, pr.z, pr.w, sig, tau, lnJ);
-    // q(o) = m v + dx G (o - fx), G = -kk tau + m C  (Eq. 4-5)
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      float q0 = pr.x * __ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]);
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        const float Gab = fmaf(-kk, tau[a][b], pr.x * __ldg(&A.st[(size_t)comp_C<D>(a, b) * NT + j]));
-        Y.Qm[a][b] = P.dx * Gab;
-        q0 = fmaf(-Y.Qm[a][b], sc.fx[b], q0);
-      }
-      Y.q0[a] = q0;
-    }
-    // u(o) = g_v + 4 res g_C (o - fx); g_v = gv + dt gx (step A), g_C = gC + dt gF F^T (step B)
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      float u0 = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
-      float gF[D];
-#pragma unroll
-      for (int c = 0; c < D; ++c) gF[c] = gi[(size_t)comp_F<D>(a, c) * NT + k];
-#pragma unroll
-      for (int b = 0; b < D; ++b) {
-        float gc = gi[(size_t)comp_C<D>(a, b) * NT + k];
-#pragma unroll
-        for (int c = 0; c < D; ++c) gc = fmaf(P.dt * gF[c], F[b][c], gc);
-        Y.U[a][b] = 4.f * P.fres * gc;
-        u0 = fmaf(-Y.U[a][b], sc.fx[b], u0);
-      }
-      Y.u0[a] = u0;
-    }
-  }
+  float dw[D][3];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    float dw[3];
-    stencil_dw(sc.fx[a], dw);
+    stencil_dw(sc.fx[a], dw[a]);
 #pragma unroll
-    for (int o = 0; o < 3; ++o) Y.dw[a][o] = P.fres * dw[o];
+    for (int o = 0; o < 3; ++o) dw[a][o] *= P.fres;
   }
   int lb[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) lb[a] = sc.base[a] - bc[a] * Dim<D>::BB;
-  AdjAcc<D> R;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    R.S[a] = R.Sd[a] = R.gx[a] = 0.f;
-#pragma unroll
-    for (int b = 0; b < D; ++b) R.Mv[a][b] = R.Md[a][b] = 0.f;
-  }
-  adj_row<D, 0, 0>(s_v, s_a, lb, sc, Y, R); adj_row<D, 0, 1>(s_v, s_a, lb, sc, Y, R); adj_row<D, 0, 2>(s_v, s_a, lb, sc, Y, R);
-  adj_row<D, 1, 0>(s_v, s_a, lb, sc, Y, R); adj_row<D, 1, 1>(s_v, s_a, lb, sc, Y, R); adj_row<D, 1, 2>(s_v, s_a, lb, sc, Y, R);
-  adj_row<D, 2, 0>(s_v, s_a, lb, sc, Y, R); adj_row<D, 2, 1>(s_v, s_a, lb, sc, Y, R); adj_row<D, 2, 2>(s_v, s_a, lb, sc, Y, R);
 
-  float Q[D][D], Cn[D][D], T[D][D];
+  // ---- v-pass: c(o) = u(o) = g_v + 4 res g_C (o - fx)   (steps A, B) ----
+  PassAcc<D> Rv;
+  float Cn[D][D];  // C^{t+1} (Eq. 8 recomputed)
+  float gxv[D];
+  {
+    float u0[D], U[D][D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      u0[a] = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float gc = gi[(size_t)comp_C<D>(a, b) * NT + k];
+#pragma unroll
+        for (int c = 0; c < D; ++c)
+          gc = fmaf(P.dt * gi[(size_t)comp_F<D>(a, c) * NT + k], __ldg(&A.st[(size_t)comp_F<D>(b, c) * NT + j]), gc);
+        U[a][b] = 4.f * P.fres * gc;
+        u0[a] = fmaf(-U[a][b], sc.fx[b], u0[a]);
+      }
+    }
+    stencil_pass<D>(s_v, lb, sc.w, dw, u0, U, 0.f, Rv);
+    // dx term -4 res^2 g_C^T v^{t+1} = -res U^T S_v
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float acc = Rv.g[a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) acc = fmaf(-P.fres * U[b][a], Rv.S[b], acc);
+      gxv[a] = acc;
+#pragma unroll
+      for (int b = 0; b < D; ++b) Cn[a][b] = 4.f * P.fres * fmaf(-Rv.S[a], sc.fx[b], Rv.M[a][b]);
+    }
+  }
+  // ---- dp-pass: c(o) = q(o) = m v + dx G (o - fx), e_i = m dm_i   (Eqs. 4-5) ----
+  float sig[D];
 #pragma unroll
   for (int a = 0; a < D; ++a)
+    sig[a] = ai >= 0 ? P.act_s * __ldg(&A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a]) : 0.f;
+  PassAcc<D> Rd;
+  float Gm[D][D];  // dx G
+  {
+    float F[D][D], tau[D][D], q0[D];
 #pragma unroll
-    for (int b = 0; b < D; ++b) {
-      Q[a][b] = P.dx * fmaf(-R.Sd[a], sc.fx[b], R.Md[a][b]);
-      Cn[a][b] = 4.f * P.fres * fmaf(-R.S[a], sc.fx[b], R.Mv[a][b]);  // C^{t+1}, Eq. 8
-      T[a][b] = -kk * Q[a][b];
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
+    kirchhoff<D>(F, pr.z, pr.w, sig, tau, logf(det<D>(F)));
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      q0[a] = pr.x * __ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]);
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        Gm[a][b] = P.dx * fmaf(-kk, tau[a][b], pr.x * __ldg(&A.st[(size_t)comp_C<D>(a, b) * NT + j]));
+        q0[a] = fmaf(-Gm[a][b], sc.fx[b], q0[a]);
+      }
     }
-  float* go = A.gout;
-  const float m = pr.x;
-#pragma unroll
-  for (int a = 0; a < D; ++a) {
-    go[(size_t)comp_v<D>(a) * NT + j] = m * R.Sd[a];  // (F)
-#pragma unroll
-    for (int b = 0; b < D; ++b) go[(size_t)comp_C<D>(a, b) * NT + j] = m * Q[a][b];  // (I)
+    stencil_pass<D>(s_a, lb, sc.w, dw, q0, Gm, pr.x, Rd);
   }
-  // (J): G^T = Qm^T / dx, g_C = U / (4 res)
+  const float m = pr.x;
+  float* go = A.gout;
+  float Q[D][D], T[D][D];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    float acc = gi[(size_t)comp_x<D>(a) * NT + k] + R.gx[a];
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      acc = fmaf(-P.fres * Y.U[b][a], R.S[b], acc);
-      acc = fmaf(-P.fres * Y.Qm[b][a], R.Sd[b], acc);
+      Q[a][b] = P.dx * fmaf(-Rd.S[a], sc.fx[b], Rd.M[a][b]);
+      T[a][b] = -kk * Q[a][b];
+      go[(size_t)comp_C<D>(a, b) * NT + j] = m * Q[a][b];  // (I)
     }
+    go[(size_t)comp_v<D>(a) * NT + j] = m * Rd.S[a];  // (F)
+  }
+  // (J): dx = gx + sum dW s - 4res^2 g_C^T S_v - G^T S_d
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float acc = gi[(size_t)comp_x<D>(a) * NT + k] + gxv[a] + Rd.g[a];
+#pragma unroll
+    for (int b = 0; b < D; ++b) acc = fmaf(-P.fres * Gm[b][a], Rd.S[b], acc);
     go[(size_t)comp_x<D>(a) * NT + j] = acc;
   }
   // (H), (K), material parameters
@@ -1331,7 +1325,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
       acc = fmaf(pr.w * trT, FiT[a][b], acc);
       go[(size_t)comp_F<D>(a, b) * NT + j] = acc;
     }
-  float dmu = 0.f, dsig[D];
+  float dmu = 0.f;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     float ds = 0.f;
@@ -1346,13 +1340,11 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
       ds = fmaf(F[b][a], tf, ds);
       dmu = fmaf(T[a][b], ff - (a == b ? 1.f : 0.f), dmu);
     }
-    dsig[a] = P.act_s * ds;
+    dsig_out[a] = P.act_s * ds;
   }
   A.dmu[u] += dmu;
   A.dlam[u] += trT * lnJ;
   aid_out = ai;
-#pragma unroll
-  for (int a = 0; a < D; ++a) dsig_out[a] = dsig[a];
 }
 
 // Segmented warp reduction of the actuation gradient (step K -> dL/da[r][t][k]): one
