@@ -937,43 +937,64 @@ __device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, i
   for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
 }
 
-// stage tile nodes: velocity (projected) into s_v; optional second grid (adjoint) into s_a
+// fetch one node of step t: velocity after the wall projection (v.w = m) and, optionally,
+// the adjoint node (dL/dp_i, dL/dm_i); zero outside the domain / untouched blocks
+template <int D, bool TWO>
+__device__ __forceinline__ void fetch_node(const KParams& P, const StepArgs& A, int r, const int* node,
+                                           size_t abase, float4& v, float4& ad) {
+  using DD = Dim<D>;
+  int nb_[D], loc[D];
+  bool inside = true;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    inside &= node[a] < P.res;
+    nb_[a] = node[a] >> DD::LOG_BB;
+    loc[a] = node[a] & (DD::BB - 1);
+  }
+  v = make_float4(0.f, 0.f, 0.f, 0.f);
+  ad = v;
+  if (!inside) return;
+  const int slot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+  if (slot < 0) return;
+  const size_t addr = (size_t)slot * kCPB + cell_lin<D>(loc);
+  v = A.tgrid[addr];
+  if (v.w > 0.f && in_band<D>(node, P.res, P.bound)) {
+    float vv[D];
+    vv[0] = v.x; vv[1] = v.y;
+    if constexpr (D == 3) vv[2] = v.z;
+    project_node<D>(vv, node, P);
+    v.x = vv[0]; v.y = vv[1];
+    if constexpr (D == 3) v.z = vv[2];
+  }
+  if (TWO) ad = A.grid[addr - abase];
+}
+
+// Stage the block's node tile: s_v = v_i - vref, s_a = a_i - aref, with (vref, aref) the
+// values of the block-centre node.  Every stencil sum the gathers form is invariant under
+// such a constant shift (sum W = 1, sum W o = fx, sum dW = 0, sum dW (o - fx)^T = res I for
+// the quadratic B-spline); the shift removes the common-mode velocity / adjoint so the fp32
+// cancellations in C' (Eq. 8) and in step J shrink to |v_i - vref|.  Callers add the
+// references back where an unshifted sum is needed (v' = S + vref, sum W dp = S_d + aref).
 template <int D, bool TWO>
 __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, int r, const int* bc,
-                                           float4* s_v, float4* s_a, size_t abase) {
+                                           float4* s_v, float4* s_a, size_t abase, float4& vref,
+                                           float4& aref) {
   using DD = Dim<D>;
+  {
+    int node[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) node[a] = bc[a] * DD::BB + DD::BB / 2;
+    fetch_node<D, TWO>(P, A, r, node, abase, vref, aref);
+  }
   for (int tn = threadIdx.x; tn < DD::TN; tn += kThreads) {
-    int tl[D], node[D], nb_[D], loc[D];
+    int node[D];
     int t = tn;
 #pragma unroll
-    for (int a = D - 1; a >= 0; --a) { tl[a] = t % DD::TE; t /= DD::TE; }
-    bool inside = true;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      node[a] = bc[a] * DD::BB + tl[a];
-      inside &= node[a] < P.res;
-      nb_[a] = node[a] >> DD::LOG_BB;
-      loc[a] = node[a] & (DD::BB - 1);
-    }
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f), ad = v;
-    if (inside) {
-      const int slot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
-      if (slot >= 0) {
-        const size_t addr = (size_t)slot * kCPB + cell_lin<D>(loc);
-        v = A.tgrid[addr];
-        if (v.w > 0.f && in_band<D>(node, P.res, P.bound)) {
-          float vv[D];
-          vv[0] = v.x; vv[1] = v.y;
-          if constexpr (D == 3) vv[2] = v.z;
-          project_node<D>(vv, node, P);
-          v.x = vv[0]; v.y = vv[1];
-          if constexpr (D == 3) v.z = vv[2];
-        }
-        if (TWO) ad = A.grid[addr - abase];
-      }
-    }
-    s_v[tn] = v;
-    if (TWO) s_a[tn] = ad;
+    for (int a = D - 1; a >= 0; --a) { node[a] = bc[a] * DD::BB + t % DD::TE; t /= DD::TE; }
+    float4 v, ad;
+    fetch_node<D, TWO>(P, A, r, node, abase, v, ad);
+    s_v[tn] = make_float4(v.x - vref.x, v.y - vref.y, v.z - vref.z, v.w);
+    if (TWO) s_a[tn] = make_float4(ad.x - aref.x, ad.y - aref.y, ad.z - aref.z, ad.w - aref.w);
   }
 }
 
@@ -988,7 +1009,7 @@ __device__ __forceinline__ int tile_idx(const int* lb) {
 //      x' = x + dt v'; writes state t+1 in sorted order + keys/histogram of step t+1 ----
 template <int D, int OX, int OY, int OZ>
 __device__ __forceinline__ void g2p_node(const float4* s_v, const int* lb, const Stencil<D>& sc,
-                                         float wxy, float* Sxy, float* Zxy) {
+                                         const float4& vref, float wxy, float* Sxy, float* Zxy) {
   const float4 g = s_v[tile_idx<D, OX, OY, OZ>(lb)];
   float vi[3] = {g.x, g.y, g.z};
   const float W = (D == 3) ? wxy * sc.w[D - 1][OZ] : wxy;
@@ -1003,17 +1024,17 @@ __device__ __forceinline__ void g2p_node(const float4* s_v, const int* lb, const
 
 template <int D, int OX, int OY>
 __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const Stencil<D>& sc,
-                                        float* S, float (&M)[D][D]) {
+                                        const float4& vref, float* S, float (&M)[D][D]) {
   const float wxy = sc.w[0][OX] * sc.w[1][OY];
   float Sxy[D], Zxy[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) Sxy[a] = Zxy[a] = 0.f;
   if constexpr (D == 3) {
-    g2p_node<D, OX, OY, 0>(s_v, lb, sc, wxy, Sxy, Zxy);
-    g2p_node<D, OX, OY, 1>(s_v, lb, sc, wxy, Sxy, Zxy);
-    g2p_node<D, OX, OY, 2>(s_v, lb, sc, wxy, Sxy, Zxy);
+    g2p_node<D, OX, OY, 0>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
+    g2p_node<D, OX, OY, 1>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
+    g2p_node<D, OX, OY, 2>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
   } else {
-    g2p_node<D, OX, OY, 0>(s_v, lb, sc, wxy, Sxy, Zxy);
+    g2p_node<D, OX, OY, 0>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
   }
 #pragma unroll
   for (int a = 0; a < D; ++a) {
@@ -1039,7 +1060,8 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
     const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
-    stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0);
+    float4 vref, aref_unused;
+    stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += kThreads) {
       const int k = s + i;
@@ -1064,9 +1086,9 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
 #pragma unroll
         for (int b = 0; b < D; ++b) M[a][b] = 0.f;
       }
-      g2p_row<D, 0, 0>(s_v, lb, sc, S, M); g2p_row<D, 0, 1>(s_v, lb, sc, S, M); g2p_row<D, 0, 2>(s_v, lb, sc, S, M);
-      g2p_row<D, 1, 0>(s_v, lb, sc, S, M); g2p_row<D, 1, 1>(s_v, lb, sc, S, M); g2p_row<D, 1, 2>(s_v, lb, sc, S, M);
-      g2p_row<D, 2, 0>(s_v, lb, sc, S, M); g2p_row<D, 2, 1>(s_v, lb, sc, S, M); g2p_row<D, 2, 2>(s_v, lb, sc, S, M);
+      g2p_row<D, 0, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 0, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 0, 2>(s_v, lb, sc, vref, S, M);
+      g2p_row<D, 1, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 1, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 1, 2>(s_v, lb, sc, vref, S, M);
+      g2p_row<D, 2, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 2, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 2, 2>(s_v, lb, sc, vref, S, M);
       float* out = A.st_next;
 #pragma unroll
       for (int a = 0; a < D; ++a) {
@@ -1081,8 +1103,9 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
           out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
           out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[b];
         }
-        out[(size_t)comp_v<D>(a) * NT + k] = S[a];
-        x[a] = fmaf(P.dt, S[a], x[a]);
+        const float vn = S[a] + (&vref.x)[a];
+        out[(size_t)comp_v<D>(a) * NT + k] = vn;
+        x[a] = fmaf(P.dt, vn, x[a]);
         out[(size_t)comp_x<D>(a) * NT + k] = x[a];
       }
       A.orig_next[k] = u;
@@ -1119,7 +1142,7 @@ template <int D> struct PassAcc {
 template <int D, int OX, int OY>
 __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, const float (&w)[D][3],
                                          const float (&dw)[D][3], const float* c0, const float (&Cm)[D][D],
-                                         float em, PassAcc<D>& R) {
+                                         float em, const float4& ref, PassAcc<D>& R) {
   float cxy[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) {
@@ -1134,8 +1157,8 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
 #pragma unroll
     for (int oz = 0; oz < 3; ++oz) {
       const float4 q = tile[tile_idx<D, OX, OY, 0>(lb) + oz];
-      const float f[3] = {q.x, q.y, q.z};
-      float sv = em * q.w;
+      const float f[3] = {q.x - ref.x, q.y - ref.y, q.z - ref.z};
+      float sv = em * (q.w - ref.w);
 #pragma unroll
       for (int a = 0; a < 3; ++a) sv = fmaf(f[a], oz == 0 ? cxy[a] : fmaf((float)oz, Cm[a][2], cxy[a]), sv);
       const float wz = w[2][oz];
@@ -1160,8 +1183,8 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
     }
   } else {
     const float4 q = tile[tile_idx<D, OX, OY, 0>(lb)];
-    const float f[2] = {q.x, q.y};
-    float sv = em * q.w;
+    const float f[2] = {q.x - ref.x, q.y - ref.y};
+    float sv = em * (q.w - ref.w);
 #pragma unroll
     for (int a = 0; a < 2; ++a) sv = fmaf(f[a], cxy[a], sv);
     const float wx = w[0][OX], wy = w[1][OY], wxy = wx * wy;
@@ -1179,24 +1202,25 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
 template <int D>
 __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, const float (&w)[D][3],
                                              const float (&dw)[D][3], const float* c0,
-                                             const float (&Cm)[D][D], float em, PassAcc<D>& R) {
+                                             const float (&Cm)[D][D], float em, const float4& ref,
+                                             PassAcc<D>& R) {
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     R.S[a] = R.g[a] = 0.f;
 #pragma unroll
     for (int b = 0; b < D; ++b) R.M[a][b] = 0.f;
   }
-  pass_row<D, 0, 0>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 0, 1>(tile, lb, w, dw, c0, Cm, em, R);
-  pass_row<D, 0, 2>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 1, 0>(tile, lb, w, dw, c0, Cm, em, R);
-  pass_row<D, 1, 1>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 1, 2>(tile, lb, w, dw, c0, Cm, em, R);
-  pass_row<D, 2, 0>(tile, lb, w, dw, c0, Cm, em, R); pass_row<D, 2, 1>(tile, lb, w, dw, c0, Cm, em, R);
-  pass_row<D, 2, 2>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row<D, 0, 0>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 0, 1>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 0, 2>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 0>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 1, 1>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 2>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 2, 0>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 2, 1>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 2, 2>(tile, lb, w, dw, c0, Cm, em, ref, R);
 }
 
 template <int D>
 __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArgs& A, const float4* s_v,
-                                                 const float4* s_a, const int* bc, int r, int k,
-                                                 int& aid_out, float* dsig_out) {
+                                                 const float4* s_a, const float4& aref, const int* bc,
+                                                 int r, int k, int& aid_out, float* dsig_out) {
   const size_t NT = P.NT;
   const float* gi = A.gin;
   const int j = __ldg(&A.perm[k]);
@@ -1239,7 +1263,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         u0[a] = fmaf(-U[a][b], sc.fx[b], u0[a]);
       }
     }
-    stencil_pass<D>(s_v, lb, sc.w, dw, u0, U, 0.f, Rv);
+    stencil_pass<D>(s_v, lb, sc.w, dw, u0, U, 0.f, make_float4(0.f, 0.f, 0.f, 0.f), Rv);
     // dx term -4 res^2 g_C^T v^{t+1} = -res U^T S_v
 #pragma unroll
     for (int a = 0; a < D; ++a) {
@@ -1274,7 +1298,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         q0[a] = fmaf(-Gm[a][b], sc.fx[b], q0[a]);
       }
     }
-    stencil_pass<D>(s_a, lb, sc.w, dw, q0, Gm, pr.x, Rd);
+    stencil_pass<D>(s_a, lb, sc.w, dw, q0, Gm, pr.x, make_float4(0.f, 0.f, 0.f, 0.f), Rd);
   }
   const float m = pr.x;
   float* go = A.gout;
@@ -1287,7 +1311,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
       T[a][b] = -kk * Q[a][b];
       go[(size_t)comp_C<D>(a, b) * NT + j] = m * Q[a][b];  // (I)
     }
-    go[(size_t)comp_v<D>(a) * NT + j] = m * Rd.S[a];  // (F)
+    go[(size_t)comp_v<D>(a) * NT + j] = m * (Rd.S[a] + (&aref.x)[a]);  // (F): sum W dp = S' + dp_ref
   }
   // (J): dx = gx + sum dW s - 4res^2 g_C^T S_v - G^T S_d
 #pragma unroll
@@ -1386,13 +1410,14 @@ __global__ __launch_bounds__(kThreads, MPM_P2GT_MINB) void k_p2g_adj(KParams P, 
     const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
-    stage_tile<D, true>(P, A, r, bc, s_v, s_a, abase);
+    float4 vref, aref;  // block-centre shifts (see stage_tile)
+    stage_tile<D, true>(P, A, r, bc, s_v, s_a, abase, vref, aref);
     __syncthreads();
     for (int i0 = 0; i0 < n; i0 += kThreads) {  // uniform trip count: whole warps reach the reduction
       const int i = i0 + threadIdx.x;
       int ai = -1;
       float dsig[D] = {};
-      if (i < n) p2g_adj_particle<D>(P, A, s_v, s_a, bc, r, s + i, ai, dsig);
+      if (i < n) p2g_adj_particle<D>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
       __syncwarp();
       if (P.K > 0) reduce_actuation<D>(P, A, r, ai, dsig);
     }
