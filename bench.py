@@ -29,20 +29,33 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from paper_1810_01054_b200 import scenes  # noqa: E402
+from paper_1810_01054_b200 import parallel, scenes  # noqa: E402
 
 METRIC = "particle-steps/sec fwd and fwd+bwd (3D, 1/2/4/8 B200); HBM GB/s % peak"
 UNIT = "particle-steps/s"
-WORKLOAD = ("C4 (configs[3]): 3D 128^3 grid, 1,048,576-particle neo-Hookean slab, "
-            "forward+backward, loss = final CoM x")
+WORKLOADS = {
+    "C4": ("C4 (configs[3]): 3D 128^3 grid, 1,048,576-particle neo-Hookean slab, "
+           "forward+backward, loss = final CoM x; one rollout per rank"),
+    "C5b": ("C5b (configs[4] batch part): 64 independent 3D 64^3 quadruped rollouts "
+            "(29,952 particles each, per-rollout actuation phase and E scale), sharded over ranks"),
+}
 SEG = 200  # max steps per tape segment (tape memory ~ 100 MB per step at C4)
 
 
-def _cfg_dict(K, W, n_gpus, sc):
-    return {"workload": WORKLOAD, "particles_per_rank": int(sc.batch * sc.n), "grid": f"{sc.res}^3",
-            "dim": 3, "dt": sc.dt, "steps_per_pass": K, "warmup": W,
-            "parallelism": f"batch-sharded x{n_gpus} (independent rollouts)" if n_gpus > 1 else "single GPU",
-            "l2": "inputs larger than L2: per-step state 96 MiB read + 96 MiB written, tape of K states"}
+def _cfg_dict(K, W, n_gpus, sc, workload="C4"):
+    return {"workload": WORKLOADS[workload], "particles_per_rank": int(sc.batch * sc.n),
+            "rollouts_per_rank": int(sc.batch), "grid": f"{sc.res}^3", "dim": 3, "dt": sc.dt,
+            "steps_per_pass": K, "warmup": W,
+            "parallelism": f"rollout-sharded x{n_gpus} (no data-path collective)" if n_gpus > 1 else "single GPU",
+            "l2": (f"inputs larger than L2: per-step state {sc.batch * sc.n * 96 / 2**20:.0f} MiB read + written, "
+                   f"tape of K states")}
+
+
+def make_scene(workload, rank, world, tape):
+    if workload == "C4":
+        return scenes.slab_3d(seed=rank, steps=tape)
+    full = scenes.quadruped_3d(seed=0, batch=64, steps=tape, e_scale=True)
+    return parallel.shard_scene(full, parallel.Dist(rank, world))
 
 
 # ---------------------------------------------------------------------------------------
@@ -129,33 +142,28 @@ def _traffic(kernel):
 # ---------------------------------------------------------------------------------------
 def run_ours(args):
     import torch
-    import torch.distributed as dist
 
     from paper_1810_01054_b200 import mpm
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    D = parallel.init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else None)
+    world, rank, local = D.world, D.rank, D.local_rank
     dev = torch.device("cuda", local if world > 1 else 0)
     torch.cuda.set_device(dev)
     K, W = args.steps, args.warmup
     seg = min(K, SEG)
     tape = max(seg, min(W, SEG), 1)
-    sc = scenes.slab_3d(seed=rank, steps=tape)
+    sc = make_scene(args.workload, rank, world, tape)
     stream = torch.cuda.current_stream(dev)
     sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=tape, device=dev.index, stream=stream.cuda_stream))
     NT = sc.batch * sc.n
-    m = torch.tensor(sc.mass.reshape(-1), device=dev, dtype=torch.float64)
+    m = torch.tensor(sc.mass, device=dev, dtype=torch.float64)  # [B][N]
     seed = torch.zeros((NT, 3), device=dev, dtype=torch.float32)
-    seed[:, 0] = (m / m.sum()).float()
+    seed[:, 0] = (m / m.sum(dim=1, keepdim=True)).reshape(-1).float()  # CoM_x of each rollout
     sim.set_scene(sc)
 
     def barrier():
         if world > 1:
-            dist.barrier()
+            torch.distributed.barrier()
         torch.cuda.synchronize(dev)
 
     def passes(n_steps, fwd_events=None):
@@ -186,11 +194,10 @@ def run_ours(args):
     launches = sim.launches - n0
     ms = e0.elapsed_time(e1)
     fwd_ms = e0.elapsed_time(fwd_ev[0]) if len(fwd_ev) == 1 else None
-    t = torch.tensor([ms, fwd_ms or 0.0], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, fwd_ms = float(t[0]), (float(t[1]) if fwd_ms is not None else None)
-    value = NT * K * world / (ms / 1e3)
+    ms = parallel.max_over_ranks(ms, D, dev)
+    fwd_ms = parallel.max_over_ranks(fwd_ms, D, dev) if fwd_ms is not None else None
+    total_particles = NT * world if args.workload == "C4" else 64 * sc.n
+    value = total_particles * K / (ms / 1e3)
 
     # roofline: per-kernel CUDA-event times of a second, profiled pass of the same K steps
     sim.set_profiling(True)
@@ -224,13 +231,13 @@ def run_ours(args):
     # backward (seed H2D), grad (D2H), every pass
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
     h_in = [pin(a.reshape(NT, *a.shape[2:])) for a in (sc.x, sc.v, sc.F, sc.C, sc.mass, sc.vol, sc.E, sc.nu, sc.actuator_id)]
-    act = np.zeros((1, tape, sc.n_act, 3), np.float32)
+    act = np.zeros((sc.batch, tape, sc.n_act, 3), np.float32)
     act[:, :min(tape, sc.act.shape[1])] = sc.act[:, :tape]
     h_act = pin(act)
     h_seed = pin(seed.cpu().numpy())
     h_out = {k: torch.empty(s, dtype=torch.float32).pin_memory() for k, s in
              (("dx0", (NT, 3)), ("dv0", (NT, 3)), ("dF0", (NT, 3, 3)), ("dC0", (NT, 3, 3)),
-              ("dE", (NT,)), ("dnu", (NT,)), ("da", (1, tape, sc.n_act, 3)))}
+              ("dE", (NT,)), ("dnu", (NT,)), ("da", (sc.batch, tape, sc.n_act, 3)))}
     h2d = sum(a.numel() * a.element_size() for a in h_in) + h_act.numel() * 4
     d2h = sum(a.numel() * a.element_size() for a in h_out.values())
     barrier()
@@ -251,29 +258,28 @@ def run_ours(args):
     e3.record(stream)
     barrier()
     e2e_ms = e2.elapsed_time(e3)
-    t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t[0])
-    e2e = {"value": NT * K * world / (e2e_ms / 1e3), "unit": UNIT,
+    e2e_ms = parallel.max_over_ranks(e2e_ms, D, dev)
+    e2e = {"value": total_particles * K / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int((h2d + h_seed.numel() * 4) * nseg / K),
            "d2h_bytes_per_step": int(d2h * nseg / K)}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "weak" if args.workload == "C4" else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded jittered-lattice slab)",
-            "config": _cfg_dict(K, W, world, sc),
-            "fwd": {"value": (NT * K * world / (fwd_ms / 1e3)) if fwd_ms else None,
+            "config": _cfg_dict(K, W, world, sc, args.workload),
+            "fwd": {"value": (total_particles * K / (fwd_ms / 1e3)) if fwd_ms else None,
                     "ms_per_step": (fwd_ms / K) if fwd_ms else None},
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_full(sc)
+        line["cpu_baseline"] = cpu_baseline_full(sc if args.workload == "C4" else scenes.quadruped_3d(steps=1))
     sim.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------------------
@@ -329,7 +335,7 @@ def run_reference(args):
             "steps": K, "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded jittered-lattice slab)",
-            "config": _cfg_dict(K, W, args.gpus, full),
+            "config": _cfg_dict(K, W, args.gpus, full, "C4"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -342,6 +348,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -174,3 +174,33 @@ def test_c4_com_gradient_closed_form(c4):
     assert np.abs(g["dF0"]).max() < 1e-3 * scale
     assert np.abs(g["dC0"]).max() < 1e-3 * scale * sc.dt
     assert np.abs(g["da"]).max() < 1e-6
+
+
+def test_batched_quadrupeds_per_rollout():
+    """C5b-style batch: 3 quadruped rollouts (own actuation phase and E scale) in one
+    context -- the batch dimension folded into the launch grid; each rollout vs the oracle."""
+    T = 20
+    sc = scenes.quadruped_3d(batch=3, steps=T, e_scale=True)
+    sim = _sim(sc, T)
+    sim.forward(T)
+    x, v, F, Cm = sim.get_state(T)
+    rng = np.random.default_rng(9)
+    S = oracle.S_of(3)
+    w = rng.standard_normal((sc.batch, sc.n, S))
+    wx, wv, wC, wF = oracle.unpack(w.reshape(-1, S), 3)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    cfg = oracle_cfg(sc)
+    for r in range(sc.batch):
+        st, prm, aid, act = _orc_inputs(sc, r)
+        traj = oracle.forward(cfg, st, *prm, aid, act[:T], T)
+        ox, ov, oC, oF = oracle.unpack(traj[T], 3)
+        sl = slice(r * sc.n, (r + 1) * sc.n)
+        for k, a, b in (("x", x[sl], ox), ("v", v[sl], ov), ("F", F[sl], oF), ("C", Cm[sl], oC)):
+            assert rel_err(a, b) < 1e-4, (r, k, rel_err(a, b))
+        g0, gE, gnu, ga = oracle.backward(cfg, traj, *prm, aid, act[:T], w[r])
+        gx, gv, gC, gF = oracle.unpack(g0, 3)
+        for k, a, b in (("dx0", g["dx0"][sl], gx), ("dv0", g["dv0"][sl], gv), ("dF0", g["dF0"][sl], gF),
+                        ("dE", g["dE"][sl], gE), ("da", g["da"][r, :T], ga)):
+            assert rel_err(a, b) < 1e-3, (r, k, rel_err(a, b))
