@@ -6,9 +6,9 @@ import subprocess
 import sys
 
 KEYS = [
-    ("time_us", "gpu__time_duration.sum", 1e-3),
-    ("dram_rd_MB", "dram__bytes_read.sum", 1e-6),
-    ("dram_wr_MB", "dram__bytes_write.sum", 1e-6),
+    ("time_us", "gpu__time_duration.sum", "us"),
+    ("dram_rd_MB", "dram__bytes_read.sum", "MB"),
+    ("dram_wr_MB", "dram__bytes_write.sum", "MB"),
     ("dram_pct", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
     ("sm_pct", "sm__throughput.avg.pct_of_peak_sustained_elapsed", 1),
     ("l1_pct", "l1tex__throughput.avg.pct_of_peak_sustained_active", 1),
@@ -25,6 +25,18 @@ KEYS = [
 ]
 
 
+TO_US = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}
+TO_MB = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "KB": 1e-3, "MB": 1.0, "GB": 1e3}
+
+
+def _scale(sc, unit):
+    if sc == "us":
+        return TO_US.get(unit, 1.0)
+    if sc == "MB":
+        return TO_MB.get(unit, 1.0)
+    return sc
+
+
 def main(rep):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -36,7 +48,8 @@ def main(rep):
         out = []
         for short, key, sc in KEYS:
             if key in hdr and r[hdr.index(key)] not in ("", "n/a"):
-                out.append(f"{short}={float(r[hdr.index(key)].replace(',', '')) * sc:.4g}")
+                i = hdr.index(key)
+                out.append(f"{short}={float(r[i].replace(',', '')) * _scale(sc, units[i]):.4g}")
         st = sorted(((hdr[i][34:-27], float(r[i] or 0)) for i in stall), key=lambda x: -x[1])[:5]
         print(name)
         print("   " + " ".join(out))
