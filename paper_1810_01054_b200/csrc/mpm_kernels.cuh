@@ -651,44 +651,38 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 #pragma unroll
       for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
     }
-    if (tid < kCPB) s_hist[tid] = 0;
+    if (tid < kCPB) {
+      s_hist[tid] = 0;
+      if (ADJ) { s_cstart[tid] = 0x7fffffff; s_cursor[tid] = -1; }  // per-chunk [first, last] of a cell
+    }
     for (int i = tid; i < 3 * TN; i += kThreads) (&s_tile[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
 
-    // ---- cell ranges (and, forward, the stable in-block sort by (cell, index)) ----
+    // ---- forward: cell ranges + the stable in-block sort by (cell, index).  The adjoint
+    //      (perm already sorted) finds each cell's sub-range per chunk in the producer. ----
     if (!ADJ) {
       for (int i = tid; i < n; i += kThreads) {
         int j = A.tmp_perm[s + i];
         atomicAdd(&s_hist[A.key[j] & (kCPB - 1)], 1);
       }
-    } else {
-      for (int i = tid; i < n; i += kThreads) {
-        int j = A.perm[s + i];
-        int cl[D];
+      __syncthreads();
+      if (tid < 32) {
+        int v0 = s_hist[tid], v1 = s_hist[tid + 32];
+        int i0 = v0, i1 = v1;
 #pragma unroll
-        for (int a = 0; a < D; ++a) cl[a] = base_of(A.st[(size_t)comp_x<D>(a) * NT + j], P.fres) & (BB - 1);
-        atomicAdd(&s_hist[cell_lin<D>(cl)], 1);
+        for (int o = 1; o < 32; o <<= 1) {
+          int a = __shfl_up_sync(0xffffffffu, i0, o);
+          int b = __shfl_up_sync(0xffffffffu, i1, o);
+          if (tid >= o) { i0 += a; i1 += b; }
+        }
+        int tot0 = __shfl_sync(0xffffffffu, i0, 31);
+        s_cstart[tid] = i0 - v0;
+        s_cstart[tid + 32] = tot0 + i1 - v1;
+        s_cursor[tid] = i0 - v0;
+        s_cursor[tid + 32] = tot0 + i1 - v1;
+        if (tid == 31) s_cstart[kCPB] = tot0 + i1;
       }
-    }
-    __syncthreads();
-    if (tid < 32) {
-      int v0 = s_hist[tid], v1 = s_hist[tid + 32];
-      int i0 = v0, i1 = v1;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int a = __shfl_up_sync(0xffffffffu, i0, o);
-        int b = __shfl_up_sync(0xffffffffu, i1, o);
-        if (tid >= o) { i0 += a; i1 += b; }
-      }
-      int tot0 = __shfl_sync(0xffffffffu, i0, 31);
-      s_cstart[tid] = i0 - v0;
-      s_cstart[tid + 32] = tot0 + i1 - v1;
-      s_cursor[tid] = i0 - v0;
-      s_cursor[tid + 32] = tot0 + i1 - v1;
-      if (tid == 31) s_cstart[kCPB] = tot0 + i1;
-    }
-    __syncthreads();
-    if (!ADJ) {
+      __syncthreads();
       int* buf = (n <= kSortCap) ? s_sort : (A.scratch + s);
       for (int i = tid; i < n; i += kThreads) {
         int j = A.tmp_perm[s + i];
@@ -711,6 +705,10 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
     const int ox = tid / kCPB, c = tid % kCPB;
     for (int lo = 0; lo < n; lo += kCap) {
       const int hi = min(n, lo + kCap);
+      if (ADJ && lo > 0) {  // later chunks of an oversize block: reset the cell sub-ranges
+        if (tid < kCPB) { s_cstart[tid] = 0x7fffffff; s_cursor[tid] = -1; }
+        __syncthreads();
+      }
       for (int pi = tid; pi < hi - lo; pi += kThreads) {
         const int k = s + lo + pi;
         const int j = A.perm[k];
@@ -724,6 +722,13 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
           f[a] = sc.fx[a];
 #pragma unroll
           for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][pi] = sc.w[a][o];
+        }
+        if (ADJ) {
+          int cl[D];
+#pragma unroll
+          for (int a = 0; a < D; ++a) cl[a] = sc.base[a] & (BB - 1);
+          atomicMin(&s_cstart[cell_lin<D>(cl)], pi);
+          atomicMax(&s_cursor[cell_lin<D>(cl)], pi);
         }
         float Av[D], Bm[D][D];
         if (!ADJ) {
@@ -810,7 +815,8 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 #pragma unroll
       for (int q = 0; q < NSUB; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (tid < 3 * kCPB) {
-        const int i0 = max(s_cstart[c], lo) - lo, i1 = min(s_cstart[c + 1], hi) - lo;
+        const int i0 = ADJ ? s_cstart[c] : max(s_cstart[c], lo) - lo;
+        const int i1 = ADJ ? s_cursor[c] + 1 : min(s_cstart[c + 1], hi) - lo;
         for (int i = i0; i < i1; ++i) {
           const float wx = s_pay[PY::W + ox][i];
           float Ax[3];
@@ -1366,7 +1372,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     }
     dsig_out[a] = P.act_s * ds;
   }
-  A.dmu[u] += dmu;
+  A.dmu[u] += dmu;  // plain RMW: measured 36 us faster than a fp32 RED at C4
   A.dlam[u] += trT * lnJ;
   aid_out = ai;
 }

@@ -1,0 +1,33 @@
+"""Per-source-line stall samples and executed instructions for one kernel of an ncu report:
+  python tools/ncu_lines.py report.ncu-rep <kernel-regex> [top]"""
+import csv
+import io
+import subprocess
+import sys
+
+
+def main(rep, kern, top=30):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
+                          "--launch-skip", "0", "--launch-count", "1", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hi = [i for i, r in enumerate(rows) if "Warp Stall Sampling (All Samples)" in r][0]
+    h = rows[hi]
+    ism, iex = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
+    lines = []
+    for r in rows[hi + 1:]:
+        if len(r) < len(h) or r[0] == "":
+            continue
+        try:
+            lines.append((int(r[0]), r[1].strip()[:100], int(r[ism] or 0), int(r[iex] or 0)))
+        except ValueError:
+            continue
+    tot_s = sum(l[2] for l in lines) or 1
+    tot_i = sum(l[3] for l in lines) or 1
+    print(f"samples {tot_s}  warp-instructions {tot_i}")
+    for ln, src, s, i in sorted(lines, key=lambda l: -l[2])[:top]:
+        print(f"{ln:5d} stall {s / tot_s:6.3f} inst {i / tot_i:6.3f}  {src}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30)
