@@ -291,7 +291,7 @@ void launch_backward_step(mpm_ctx c, int t, const float* gin, float* gout) {
                                                        t > 0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
-  launch(c, KI_P2GT, [&] { k_p2g_adj<D><<<na, kThreads, 0, c->stream>>>(P, A); });
+  launch(c, KI_P2GT, [&] { k_p2g_adj<D><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
 }
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
@@ -536,12 +536,12 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<3>, kThreads, 0);
     c->occ_g2p = std::max(1, occ);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<3>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<3>, MPM_P2GT_THREADS, 0);
     c->occ_p2gT = std::max(1, occ);
   } else {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<2>, kThreads, 0);
     c->occ_g2p = std::max(1, occ);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<2>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<2>, MPM_P2GT_THREADS, 0);
     c->occ_p2gT = std::max(1, occ);
   }
 

@@ -20,7 +20,10 @@
 #define MPM_G2P_MINB 4
 #endif
 #ifndef MPM_P2GT_MINB
-#define MPM_P2GT_MINB 2
+#define MPM_P2GT_MINB 4
+#endif
+#ifndef MPM_P2GT_THREADS
+#define MPM_P2GT_THREADS 128
 #endif
 #ifndef MPM_SCAT_MINB
 #define MPM_SCAT_MINB 3
@@ -926,6 +929,15 @@ __global__ void k_grid_update(KParams P, const int* __restrict__ info_t, float4*
   }
 }
 
+// L2 prefetch of one particle's SoA record (ncomp components at index j) -- issued for a
+// block's particles before its tile is staged, so the particle loop's loads hit L2
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_record(const float* base, size_t NT, int j, int c0, int ncomp) {
+  for (int c = c0; c < c0 + ncomp; ++c) prefetch_l2(base + (size_t)c * NT + j);
+}
+
 // ------------------------------------------------------------------------------------
 // Block-tile gathers (G2P, P2G^T).  One CTA per occupied grid block (dynamic work
 // counter).  The block's (Bb+2)^D node tile is staged once in shared memory -- node
@@ -981,7 +993,7 @@ __device__ __forceinline__ void fetch_node(const KParams& P, const StepArgs& A, 
 // the quadratic B-spline); the shift removes the common-mode velocity / adjoint so the fp32
 // cancellations in C' (Eq. 8) and in step J shrink to |v_i - vref|.  Callers add the
 // references back where an unshifted sum is needed (v' = S + vref, sum W dp = S_d + aref).
-template <int D, bool TWO>
+template <int D, bool TWO, int NTH = kThreads>
 __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, int r, const int* bc,
                                            float4* s_v, float4* s_a, size_t abase, float4& vref,
                                            float4& aref) {
@@ -992,7 +1004,7 @@ __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, 
     for (int a = 0; a < D; ++a) node[a] = bc[a] * DD::BB + DD::BB / 2;
     fetch_node<D, TWO>(P, A, r, node, abase, vref, aref);
   }
-  for (int tn = threadIdx.x; tn < DD::TN; tn += kThreads) {
+  for (int tn = threadIdx.x; tn < DD::TN; tn += NTH) {
     int node[D];
     int t = tn;
 #pragma unroll
@@ -1067,6 +1079,11 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
     float4 vref, aref_unused;
+    for (int i = threadIdx.x; i < n; i += kThreads) {  // this block's x, F -> L2
+      const int j = __ldg(&A.perm[s + i]);
+      prefetch_record(A.st, NT, j, 0, D);
+      prefetch_record(A.st, NT, j, comp_F<D>(0, 0), D * D);
+    }
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += kThreads) {
@@ -1401,12 +1418,13 @@ __device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArg
 }
 
 template <int D>
-__global__ __launch_bounds__(kThreads, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
+__global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
   __shared__ float4 s_v[Dim<D>::TN];
   __shared__ float4 s_a[Dim<D>::TN];
   __shared__ int s_blk;
   const int n_occ = A.info_t[I_NOCC];
   const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
+  const size_t NT = P.NT;
   for (;;) {
     if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
     __syncthreads();
@@ -1417,9 +1435,15 @@ __global__ __launch_bounds__(kThreads, MPM_P2GT_MINB) void k_p2g_adj(KParams P, 
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
     float4 vref, aref;  // block-centre shifts (see stage_tile)
-    stage_tile<D, true>(P, A, r, bc, s_v, s_a, abase, vref, aref);
+    for (int i = threadIdx.x; i < n; i += MPM_P2GT_THREADS) {  // this block's particle records -> L2
+      const int k = s + i, j = __ldg(&A.perm[k]), u = __ldg(&A.orig_next[k]);
+      prefetch_record(A.st, NT, j, 0, Dim<D>::S);
+      prefetch_record(A.gin, NT, k, 0, Dim<D>::S);
+      prefetch_l2(&A.prm[u]);
+    }
+    stage_tile<D, true, MPM_P2GT_THREADS>(P, A, r, bc, s_v, s_a, abase, vref, aref);
     __syncthreads();
-    for (int i0 = 0; i0 < n; i0 += kThreads) {  // uniform trip count: whole warps reach the reduction
+    for (int i0 = 0; i0 < n; i0 += MPM_P2GT_THREADS) {  // uniform trip count: whole warps reach the reduction
       const int i = i0 + threadIdx.x;
       int ai = -1;
       float dsig[D] = {};
