@@ -55,7 +55,7 @@ struct mpm_ctx_s {
   // work buffers
   int* key = nullptr;
   int* cnt = nullptr;
-  int* tmp_perm = nullptr;
+  int2* tmp_pk = nullptr;
   int* scratch = nullptr;
   int* hist2 = nullptr;
   int3* tile_sums = nullptr;
@@ -218,7 +218,7 @@ StepArgs step_args(mpm_ctx c, int t) {
   StepArgs A{};
   A.st = state_at(c, t);
   A.perm = perm_at(c, t);
-  A.tmp_perm = c->tmp_perm;
+  A.tmp_pk = c->tmp_pk;
   A.key = c->key;
   A.scratch = c->scratch;
   A.orig = orig_at(c, t);
@@ -255,7 +255,7 @@ void launch_bin(mpm_ctx c, int t) {
                                                       slot_at(c, t), occ_at(c, t), touch_at(c, t));
   });
   launch(c, KI_SCATTER, [&] {
-    k_scatter<<<grid1d(P.NT), 256, 0, c->stream>>>(P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_perm, info_at(c, t), c->arena);
+    k_scatter<<<grid1d(P.NT), 256, 0, c->stream>>>(P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_pk, info_at(c, t), c->arena);
   });
 }
 
@@ -559,7 +559,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   AL(info, (T + 1) * kInfo);
   AL(key, NT);
   AL(cnt, (size_t)P.NBT);
-  AL(tmp_perm, NT);
+  AL(tmp_pk, NT);
   AL(scratch, NT);
   AL(hist2, (size_t)P.NBT);
   AL(tile_sums, (size_t)c->n_tiles);
@@ -700,9 +700,9 @@ mpm_status mpm_get_binning(mpm_ctx c, int32_t t, float* x_store, int32_t* orig, 
     // keys of storage order t: recompute from the stored positions (same device code as the step)
     int* tmp = c->scratch;
     if (D == 3)
-      k_init_keys<3><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, c->tmp_perm, c->err);
+      k_init_keys<3><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, reinterpret_cast<int*>(c->tmp_pk), c->err);
     else
-      k_init_keys<2><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, c->tmp_perm, c->err);
+      k_init_keys<2><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, reinterpret_cast<int*>(c->tmp_pk), c->err);
     CK(cudaMemcpyAsync(keyo, tmp, NT * sizeof(int), cudaMemcpyDefault, c->stream));
   }
   return sync_and_check(c, "get_binning");

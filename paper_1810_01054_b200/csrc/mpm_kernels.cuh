@@ -528,7 +528,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const unsigned* 
 // counting-sort scatter by block (positions inside a block are fixed up by k_block_scatter);
 // also zeroes the grid slots of step t (the P2G flush accumulates into them)
 __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __restrict__ block_start,
-                          int* __restrict__ cnt, int* __restrict__ tmp_perm,
+                          int* __restrict__ cnt, int2* __restrict__ tmp_pk,
                           const int* __restrict__ info_t, float4* __restrict__ arena) {
   {
     const int nz = info_t[I_NTOUCH] * kCPB;
@@ -538,7 +538,8 @@ __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __rest
   }
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = j < NT;
-  int gb = valid ? key[j] / kCPB : 0;
+  const int kj = valid ? key[j] : 0;
+  int gb = kj / kCPB;
   unsigned vm = __ballot_sync(0xffffffffu, valid);
   if (!valid) return;
   unsigned peers = __match_any_sync(vm, gb);
@@ -549,7 +550,7 @@ __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __rest
   if (lane == leader) old = atomicSub(&cnt[gb], n);
   old = __shfl_sync(peers, old, leader);
   int rank = __popc(peers & ((1u << lane) - 1));
-  tmp_perm[block_start[gb] + old - n + rank] = j;
+  tmp_pk[block_start[gb] + old - n + rank] = make_int2(j, kj);  // (storage index, key)
 }
 
 // ------------------------------------------------------------------------------------
@@ -590,7 +591,7 @@ struct StepArgs {
   // forward and adjoint
   const float* st;        // state t (SoA)
   int* perm;              // sorted slot -> storage index (written by forward k_p2g)
-  const int* tmp_perm;    // block-grouped, unsorted (forward)
+  const int2* tmp_pk;     // block-grouped, unsorted (storage index, key) (forward)
   const int* key;         // storage-order keys of step t (forward)
   int* scratch;           // sort scratch for oversize blocks
   const int* orig;        // storage index -> user index, step t
@@ -664,10 +665,19 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
     // ---- forward: cell ranges + the stable in-block sort by (cell, index).  The adjoint
     //      (perm already sorted) finds each cell's sub-range per chunk in the producer. ----
     if (!ADJ) {
-      for (int i = tid; i < n; i += kThreads) {
-        int j = A.tmp_perm[s + i];
-        atomicAdd(&s_hist[A.key[j] & (kCPB - 1)], 1);
+      // (storage index, cell) of this thread's first two particles stay in registers
+      int pj[2] = {0, 0}, pc[2] = {0, 0};
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int i = tid + q * kThreads;
+        if (i < n) {
+          const int2 e = A.tmp_pk[s + i];
+          pj[q] = e.x;
+          pc[q] = e.y & (kCPB - 1);
+          atomicAdd(&s_hist[pc[q]], 1);
+        }
       }
+      for (int i = tid + 2 * kThreads; i < n; i += kThreads) atomicAdd(&s_hist[A.tmp_pk[s + i].y & (kCPB - 1)], 1);
       __syncthreads();
       if (tid < 32) {
         int v0 = s_hist[tid], v1 = s_hist[tid + 32];
@@ -687,16 +697,21 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
       }
       __syncthreads();
       int* buf = (n <= kSortCap) ? s_sort : (A.scratch + s);
-      for (int i = tid; i < n; i += kThreads) {
-        int j = A.tmp_perm[s + i];
-        int pos = atomicAdd(&s_cursor[A.key[j] & (kCPB - 1)], 1);
-        buf[pos] = j;
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (tid + q * kThreads < n) buf[atomicAdd(&s_cursor[pc[q]], 1)] = pj[q];
+      for (int i = tid + 2 * kThreads; i < n; i += kThreads) {
+        const int2 e = A.tmp_pk[s + i];
+        buf[atomicAdd(&s_cursor[e.y & (kCPB - 1)], 1)] = e.x;
       }
       __syncthreads();
       for (int i = tid; i < n; i += kThreads) {
-        int j = buf[i];
-        int c = A.key[j] & (kCPB - 1);
-        int lo = s_cstart[c], hi = s_cstart[c + 1];
+        const int j = buf[i];
+        int c = 0;  // cell of position i: the last c with cstart[c] <= i (binary search)
+#pragma unroll
+        for (int step = kCPB / 2; step > 0; step >>= 1)
+          if (s_cstart[c + step] <= i) c += step;
+        const int lo = s_cstart[c], hi = s_cstart[c + 1];
         int rank = 0;
         for (int q = lo; q < hi; ++q) rank += buf[q] < j;
         A.perm[s + lo + rank] = j;  // stable: ties by storage index (R18)
