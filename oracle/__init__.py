@@ -81,6 +81,9 @@ def lib():
         L.orc_backward.restype = C.c_int
         L.orc_backward.argtypes = [C.POINTER(_Cfg), C.c_int, dp, dp, dp, dp, dp, ip, dp, dp,
                                    dp, dp, dp, dp]
+        L.orc_backward_ex.restype = C.c_int
+        L.orc_backward_ex.argtypes = [C.POINTER(_Cfg), C.c_int, dp, dp, dp, dp, dp, ip, dp, dp,
+                                      dp, dp, dp, dp, dp]
         L.orc_bin.restype = C.c_int
         L.orc_bin.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, fp, ip, ip, ip]
         _lib = L
@@ -217,6 +220,34 @@ def backward(cfg: Config, traj: np.ndarray, mass, vol, E, nu, act_id=None, act=N
     if rc:
         raise OracleError(rc)
     return g0, gE, gnu, ga[:n_steps, :cfg.n_act]
+
+
+def backward_ex(cfg: Config, traj: np.ndarray, mass, vol, E, nu, act_id=None, act=None,
+                seeds=None):
+    """Reverse-mode with a seed for every state (seeds [(T+1)][n][S]; a running loss) and the
+    mass gradient.  Returns (dL/dstate_0, dL/dE, dL/dnu, dL/da, dL/dm)."""
+    traj = np.ascontiguousarray(traj, np.float64)
+    n_steps = traj.shape[0] - 1
+    n, S = traj.shape[1], traj.shape[2]
+    mass, vol, E, nu = (_dv(a) for a in (mass, vol, E, nu))
+    aid = np.ascontiguousarray(np.full(n, -1, np.int32) if act_id is None else np.asarray(act_id, np.int32))
+    K = max(cfg.n_act, 1)
+    if act is None:
+        act = np.zeros((max(n_steps, 1), K, cfg.dim))
+    act = _dv(act)
+    seeds = _dv(seeds)
+    assert seeds.shape == traj.shape
+    g0 = np.zeros((n, S))
+    gE = np.zeros(n)
+    gnu = np.zeros(n)
+    gm = np.zeros(n)
+    ga = np.zeros((max(n_steps, 1), K, cfg.dim))
+    cc = cfg.c(n)
+    rc = lib().orc_backward_ex(C.byref(cc), n_steps, _d(traj), _d(mass), _d(vol), _d(E), _d(nu),
+                               _i(aid), _d(act), _d(seeds), _d(g0), _d(gE), _d(gnu), _d(ga), _d(gm))
+    if rc:
+        raise OracleError(rc)
+    return g0, gE, gnu, ga[:n_steps, :cfg.n_act], gm
 
 
 def bin_particles(dim: int, res: int, x32: np.ndarray):

@@ -526,7 +526,7 @@ static int step_backward(const orc_cfg* cfg, const double* st, const double* st_
                          const double* mass, const double* vol, const double* E,
                          const double* nu, const int* act_id, const double* act_t,
                          const double* gin, double* gout, double* gE, double* gnu,
-                         double* ga_t, grid_t* g, pq_t* pq, double* dvi, double* dpi,
+                         double* ga_t, double* gm, grid_t* g, pq_t* pq, double* dvi, double* dpi,
                          double* dmi) {
   int d = cfg->dim, S = S_of(d), nn = nodes_of(cfg), ns = n_stencil(d);
   double dx = 1.0 / (double)cfg->res, res = (double)cfg->res;
@@ -648,6 +648,18 @@ static int step_backward(const orc_cfg* cfg, const double* st, const double* st_
         double t5 = m * dm * dW[a];
         dx_o[a] += t2 + t3 + t4 + t5;
       }
+      /* NEXT N3: dL/dm_p = sum_i N dL/dm_i + sum_i N dL/dp_i . (v_p + C_p (x_i - x_p))
+       * (chain rule through Eqs. 3-5; formula as restated in SPEC.md:324) */
+      if (gm) {
+        const double* Cp = rec + 2 * d;
+        double sm = dm;
+        for (int a = 0; a < d; ++a) {
+          double cd = 0.0;
+          for (int b = 0; b < d; ++b) cd += Cp[a * d + b] * dpos[b];
+          sm += dp[a] * (v[a] + cd);
+        }
+        gm[pi] += W * sm;
+      }
     }
     /* (H) P:561-568: first three terms */
     double H[81];
@@ -694,10 +706,10 @@ static int step_backward(const orc_cfg* cfg, const double* st, const double* st_
   return ORC_OK;
 }
 
-int orc_backward(const orc_cfg* cfg, int n_steps, const double* traj, const double* mass,
-                 const double* vol, const double* E, const double* nu, const int* act_id,
-                 const double* act, const double* seed, double* grad0, double* gE, double* gnu,
-                 double* ga) {
+int orc_backward_ex(const orc_cfg* cfg, int n_steps, const double* traj, const double* mass,
+                    const double* vol, const double* E, const double* nu, const int* act_id,
+                    const double* act, const double* seeds, double* grad0, double* gE,
+                    double* gnu, double* ga, double* gm) {
   if (check_cfg(cfg) || n_steps < 0) return ORC_ERR_ARG;
   int d = cfg->dim, S = S_of(d), nn = nodes_of(cfg);
   size_t rec = (size_t)cfg->n * S;
@@ -709,21 +721,38 @@ int orc_backward(const orc_cfg* cfg, int n_steps, const double* traj, const doub
   double* dmi = (double*)calloc((size_t)nn, sizeof(double));
   double* a = (double*)malloc(sizeof(double) * (rec > 0 ? rec : 1));
   double* b = (double*)malloc(sizeof(double) * (rec > 0 ? rec : 1));
-  memcpy(a, seed, sizeof(double) * rec);
-  for (int pi = 0; pi < cfg->n; ++pi) { gE[pi] = 0.0; gnu[pi] = 0.0; }
+  /* the adjoint of state T is its own seed; every earlier state t adds seeds[t] (NEXT N4:
+   * a running loss sum_t L_t(state_t) -- chain rule of P:165 with per-step terms) */
+  memcpy(a, seeds + (size_t)n_steps * rec, sizeof(double) * rec);
+  for (int pi = 0; pi < cfg->n; ++pi) { gE[pi] = 0.0; gnu[pi] = 0.0; if (gm) gm[pi] = 0.0; }
   if (ga) memset(ga, 0, sizeof(double) * (size_t)n_steps * cfg->n_act * d);
   int err = ORC_OK;
   for (int t = n_steps - 1; t >= 0; --t) {
     const double* act_t = act ? act + (size_t)t * cfg->n_act * d : NULL;
     double* ga_t = ga ? ga + (size_t)t * cfg->n_act * d : NULL;
     err = step_backward(cfg, traj + (size_t)t * rec, traj + (size_t)(t + 1) * rec, mass, vol, E,
-                        nu, act_id, act_t, a, b, gE, gnu, ga_t, &g, pq, dvi, dpi, dmi);
+                        nu, act_id, act_t, a, b, gE, gnu, ga_t, gm, &g, pq, dvi, dpi, dmi);
     if (err) break;
+    for (size_t q = 0; q < rec; ++q) b[q] += seeds[(size_t)t * rec + q];
     double* tmp = a; a = b; b = tmp;
   }
   if (!err) memcpy(grad0, a, sizeof(double) * rec);
   free(a); free(b); free(dvi); free(dpi); free(dmi); free(pq);
   free_grid(&g);
+  return err;
+}
+
+int orc_backward(const orc_cfg* cfg, int n_steps, const double* traj, const double* mass,
+                 const double* vol, const double* E, const double* nu, const int* act_id,
+                 const double* act, const double* seed, double* grad0, double* gE, double* gnu,
+                 double* ga) {
+  if (check_cfg(cfg) || n_steps < 0) return ORC_ERR_ARG;
+  size_t rec = (size_t)cfg->n * S_of(cfg->dim);
+  double* seeds = (double*)calloc((size_t)(n_steps + 1) * (rec > 0 ? rec : 1), sizeof(double));
+  memcpy(seeds + (size_t)n_steps * rec, seed, sizeof(double) * rec);
+  int err = orc_backward_ex(cfg, n_steps, traj, mass, vol, E, nu, act_id, act, seeds, grad0, gE,
+                            gnu, ga, NULL);
+  free(seeds);
   return err;
 }
 

@@ -80,6 +80,13 @@ int orc_backward(const orc_cfg* cfg, int n_steps, const double* traj,
                  const int* act_id, const double* act, const double* seed,
                  double* grad0, double* gE, double* gnu, double* ga);
 
+/* As orc_backward, with a seed for EVERY state (seeds [(n_steps+1)][n][S]: a running loss
+ * sum_t L_t(state_t), NEXT N4) and the mass gradient gm [n] (NEXT N3; NULL = skip).      */
+int orc_backward_ex(const orc_cfg* cfg, int n_steps, const double* traj,
+                    const double* mass, const double* vol, const double* E, const double* nu,
+                    const int* act_id, const double* act, const double* seeds,
+                    double* grad0, double* gE, double* gnu, double* ga, double* gm);
+
 /* Binning (north_star item 1), decided on fp32 positions.
  * x: [batch][n][dim] fp32.  key: [batch*n].  perm: [batch*n] (sorted slot -> index).
  * block_start: [batch*nb + 1], nb = (res/Bb)^dim, Bb = 4 (3D) / 8 (2D).              */

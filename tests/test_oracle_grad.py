@@ -174,3 +174,41 @@ def test_frictionless_wall_tangential_gradient():
     g0, gE, gnu, ga = oracle.backward(cfg, traj, m, vol, E, nu, aid, act, seed)
     np.testing.assert_allclose(g0[:, 1 + d], T * cfg.dt * m / M, rtol=1e-9, atol=1e-15)
     np.testing.assert_allclose(g0[:, 1], m / M, rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_mass_gradient_and_running_loss_vs_fd(d):
+    """NEXT N3 (dL/dm_p, the gradient behind the paper's density inference) and N4
+    (a running loss L = sum_t <w_t, state_t>): oracle reverse mode vs central differences on
+    sampled masses and along a random direction of the initial state."""
+    T = 8
+    sc, cfg = _fd_scene(d, 90 + d, T)
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    st = oracle_state(sc)
+    rng = np.random.default_rng(91 + d)
+    W = rng.standard_normal((T + 1,) + st.shape)
+
+    def L(st_, m_):
+        traj = oracle.forward(cfg, st_, m_, vol, E, nu, aid, act, T)
+        return float(np.sum(traj * W)), traj
+
+    L0, traj = L(st, m)
+    g0, gE, gnu, ga, gm = oracle.backward_ex(cfg, traj, m, vol, E, nu, aid, act, W)
+    for p in rng.choice(sc.n, 8, replace=False):
+        h = 1e-6 * m[p]
+        mp, mm = m.copy(), m.copy()
+        mp[p] += h
+        mm[p] -= h
+        fd = (L(st, mp)[0] - L(st, mm)[0]) / (2 * h)
+        assert abs(fd - gm[p]) < 1e-5 * max(abs(fd), 1e-3 * np.abs(gm).max()), (p, fd, gm[p])
+    ds = rng.standard_normal(st.shape) * np.concatenate([np.full(d, 1e-3), np.full(st.shape[1] - d, 1e-2)])
+    pred = float(np.sum(g0 * ds))
+    h = 1e-4
+    fd = (L(st + h * ds, m)[0] - L(st - h * ds, m)[0]) / (2 * h)
+    assert abs(fd - pred) < 1e-6 * abs(pred), (fd, pred)
+    # the running loss reduces to orc_backward when only the last seed is non-zero
+    W2 = np.zeros_like(W)
+    W2[-1] = W[-1]
+    a = oracle.backward_ex(cfg, traj, m, vol, E, nu, aid, act, W2)
+    b = oracle.backward(cfg, traj, m, vol, E, nu, aid, act, W[-1])
+    np.testing.assert_array_equal(a[0], b[0])
