@@ -116,6 +116,24 @@ mpm_status mpm_backward(mpm_ctx ctx, const float* dLdx, const float* dLdv, const
 mpm_status mpm_grad(mpm_ctx ctx, float* dx0, float* dv0, float* dF0, float* dC0, float* dE,
                     float* dnu, float* da);
 
+/* NEXT N3: dL/dm_p [batch][n] (user order) from the last mpm_backward -- the gradient behind
+ * the paper's physical-parameter inference (density of a ball).  Derived by the chain
+ * rule through Eqs. 3-5 (m enters m_i, m v and the m C part of G).          */
+mpm_status mpm_grad_mass(mpm_ctx ctx, float* dmass);
+/* Opt-in switch for the mass gradient (off by default: it costs ~15% of the P2G^T kernel).
+ * mpm_grad_mass returns MPM_ERR_CALL_ORDER unless the last backward ran with it on.      */
+mpm_status mpm_enable_mass_grad(mpm_ctx ctx, int32_t on);
+
+/* NEXT N4: register an additive seed dL/dstate_t for state t (0 <= t <= max_steps), user
+ * order, layouts as mpm_get_state; NULL = 0.  mpm_backward then differentiates the running
+ * loss sum_t L_t(state_t) (P:348-349 goal-velocity reward, P:363 costs): the adjoint of
+ * state t gets the seed added before step t-1 is reversed; the seed at t = tape length is
+ * added to mpm_backward's own.  Seeds persist until mpm_clear_seeds; each costs
+ * (2d + 2d^2) * batch * n floats of device memory (MPM_ERR_OOM if that fails).           */
+mpm_status mpm_add_seed(mpm_ctx ctx, int32_t t, const float* dLdx, const float* dLdv,
+                        const float* dLdF, const float* dLdC);
+mpm_status mpm_clear_seeds(mpm_ctx ctx);
+
 const char* mpm_last_error(mpm_ctx ctx);
 
 /* ---- introspection, used by the parity tests (all synchronous) ---- */

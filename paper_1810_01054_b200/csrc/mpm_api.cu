@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -74,11 +75,15 @@ struct mpm_ctx_s {
   unsigned* bflag = nullptr;
   float* dmu = nullptr;
   float* dlam = nullptr;
+  float* dmass = nullptr;
+  std::map<int, float*> seeds;  // per-step additive seeds (user-order AoS x|v|F|C), N4
   float* da = nullptr;
   float* stage = nullptr;
   std::vector<void*> allocs;
   // profiling
   bool profiling = false;
+  bool mass_grad = false;  // N3: compute dL/dm_p in P2G^T (opt-in)
+  bool mass_grad_valid = false;
   std::vector<PendingEvent> pending;
   std::vector<cudaEvent_t> event_pool;
   double prof_ms[KI_COUNT] = {};
@@ -238,6 +243,7 @@ StepArgs step_args(mpm_ctx c, int t) {
   A.cnt = c->cnt;
   A.dmu = c->dmu;
   A.dlam = c->dlam;
+  A.dmass = c->dmass;
   A.da = c->da;
   A.err = c->err;
   A.t = t;
@@ -291,7 +297,10 @@ void launch_backward_step(mpm_ctx c, int t, const float* gin, float* gout) {
                                                        t > 0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
-  launch(c, KI_P2GT, [&] { k_p2g_adj<D><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
+  if (c->mass_grad)
+    launch(c, KI_P2GT, [&] { k_p2g_adj<D, true><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
+  else
+    launch(c, KI_P2GT, [&] { k_p2g_adj<D, false><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
 }
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
@@ -389,13 +398,25 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
   float* nxt = c->gB;
   launch(c, KI_MISC, [&] {
     k_seed<D><<<grid1d(NT), 256, 0, c->stream>>>(P, orig_at(c, T), gx ? sx : nullptr, gv ? sv : nullptr,
-                                                  gF ? sF : nullptr, gC ? sC : nullptr, cur);
+                                                  gF ? sF : nullptr, gC ? sC : nullptr, cur, 0);
   });
+  auto add_step_seed = [&](int t, float* g) {  // N4: additive seed of state t, if registered
+    auto it = c->seeds.find(t);
+    if (it == c->seeds.end()) return;
+    const float* b = it->second;
+    launch(c, KI_MISC, [&] {
+      k_seed<D><<<grid1d(NT), 256, 0, c->stream>>>(P, orig_at(c, t), b, b + NT * D, b + 2 * NT * D,
+                                                    b + 2 * NT * D + NT * D * D, g, 1);
+    });
+  };
+  add_step_seed(T, cur);
   CK(cudaMemsetAsync(c->dmu, 0, NT * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->dlam, 0, NT * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->dmass, 0, NT * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->da, 0, (size_t)P.B * P.T * std::max(P.K, 1) * D * sizeof(float), c->stream));
   for (int t = T - 1; t >= 0; --t) {
     launch_backward_step<D>(c, t, cur, nxt);
+    add_step_seed(t, nxt);
     std::swap(cur, nxt);
   }
   // gradient w.r.t. state 0 now in `cur` (storage order 0 = user order)
@@ -403,6 +424,7 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
   mpm_status s = sync_and_check(c, "backward");
   if (s) return s;
   c->has_grad = true;
+  c->mass_grad_valid = c->mass_grad;
   return MPM_OK;
 }
 
@@ -414,7 +436,7 @@ mpm_status do_get_state(mpm_ctx c, int t, float* x, float* v, float* F, float* C
   float* sF = sv + NT * D;
   float* sC = sF + NT * D * D;
   launch(c, KI_MISC, [&] {
-    k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(c->P, orig_at(c, t), state_at(c, t), sx, sv, sF, sC);
+    k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(c->P, orig_at(c, t), state_at(c, t), sx, sv, sF, sC, 1);
   });
   if (x) CK(cudaMemcpyAsync(x, sx, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
   if (v) CK(cudaMemcpyAsync(v, sv, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
@@ -433,7 +455,7 @@ mpm_status do_grad(mpm_ctx c, float* dx0, float* dv0, float* dF0, float* dC0, fl
   float* sC = sF + NT * D * D;
   float* sE = sC + NT * D * D;
   float* sn = sE + NT;
-  launch(c, KI_MISC, [&] { k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(P, nullptr, c->gA, sx, sv, sF, sC); });
+  launch(c, KI_MISC, [&] { k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(P, nullptr, c->gA, sx, sv, sF, sC, 0); });
   launch(c, KI_MISC, [&] { k_finalize_params<<<grid1d(NT), 256, 0, c->stream>>>((int)NT, c->E, c->nu, c->dmu, c->dlam, sE, sn); });
   if (dx0) CK(cudaMemcpyAsync(dx0, sx, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
   if (dv0) CK(cudaMemcpyAsync(dv0, sv, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
@@ -536,12 +558,12 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<3>, kThreads, 0);
     c->occ_g2p = std::max(1, occ);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<3>, MPM_P2GT_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<3, false>, MPM_P2GT_THREADS, 0);
     c->occ_p2gT = std::max(1, occ);
   } else {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<2>, kThreads, 0);
     c->occ_g2p = std::max(1, occ);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<2>, MPM_P2GT_THREADS, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g_adj<2, false>, MPM_P2GT_THREADS, 0);
     c->occ_p2gT = std::max(1, occ);
   }
 
@@ -575,6 +597,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   AL(gB, S * NT);
   AL(dmu, NT);
   AL(dlam, NT);
+  AL(dmass, NT);
   AL(da, (size_t)P.B * T * std::max(P.K, 1) * D);
   AL(stage, NT * (2 * D + 2 * D * D + 2));
 #undef AL
@@ -602,6 +625,7 @@ void mpm_destroy(mpm_ctx c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   else cudaDeviceSynchronize();
   for (void* p : c->allocs) cudaFree(p);
+  for (auto& kv : c->seeds) cudaFree(kv.second);
   for (auto& p : c->pending) {
     cudaEventDestroy(p.a);
     cudaEventDestroy(p.b);
@@ -786,5 +810,55 @@ mpm_status mpm_get_profile(mpm_ctx c, int32_t* n_kernels, float* ms, int64_t* la
 }
 
 int64_t mpm_launch_count(mpm_ctx c) { return c ? c->launches : -1; }
+
+mpm_status mpm_add_seed(mpm_ctx c, int32_t t, const float* dLdx, const float* dLdv, const float* dLdF,
+                        const float* dLdC) {
+  if (!c || t < 0 || t > c->cfg.max_steps) return MPM_ERR_INVALID_ARG;
+  cudaSetDevice(c->cfg.device);
+  const size_t NT = c->P.NT, D = c->D;
+  const size_t n = NT * (2 * D + 2 * D * D);
+  float*& b = c->seeds[t];
+  if (!b) {
+    mpm_status s = dalloc(c, &b, n);
+    if (s) {
+      c->seeds.erase(t);
+      return s;
+    }
+    c->allocs.pop_back();  // owned by the seed map (freed by mpm_clear_seeds / destroy)
+    CK(cudaMemsetAsync(b, 0, n * sizeof(float), c->stream));
+  }
+  const float* src[4] = {dLdx, dLdv, dLdF, dLdC};
+  const size_t off[4] = {0, NT * D, 2 * NT * D, 2 * NT * D + NT * D * D};
+  const size_t len[4] = {NT * D, NT * D, NT * D * D, NT * D * D};
+  for (int i = 0; i < 4; ++i)
+    if (src[i]) CK(cudaMemcpyAsync(b + off[i], src[i], len[i] * sizeof(float), cudaMemcpyDefault, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return MPM_OK;
+}
+
+mpm_status mpm_clear_seeds(mpm_ctx c) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  cudaSetDevice(c->cfg.device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->seeds) cudaFree(kv.second);
+  c->seeds.clear();
+  return MPM_OK;
+}
+
+mpm_status mpm_enable_mass_grad(mpm_ctx c, int32_t on) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  c->mass_grad = on != 0;
+  c->mass_grad_valid = false;
+  return MPM_OK;
+}
+
+mpm_status mpm_grad_mass(mpm_ctx c, float* dmass) {
+  if (!c || !dmass) return MPM_ERR_INVALID_ARG;
+  if (!c->has_grad || !c->mass_grad_valid)
+    return fail(c, MPM_ERR_CALL_ORDER, "mpm_grad_mass needs mpm_enable_mass_grad(1) before mpm_backward");
+  cudaSetDevice(c->cfg.device);
+  CK(cudaMemcpyAsync(dmass, c->dmass, (size_t)c->P.NT * sizeof(float), cudaMemcpyDefault, c->stream));
+  return sync_and_check(c, "grad_mass");
+}
 
 }  // extern "C"

@@ -191,6 +191,66 @@ __device__ __forceinline__ void kirchhoff(const float (&F)[D][D], float mu, floa
     }
 }
 
+// The state stores the displacement gradient H = F - I instead of F (DESIGN.md 6,
+// "numerics"): F is within ~1e-3 of I in these scenes, and fp32 F would carry an absolute
+// rounding error that is large relative to the strain F - I the stress depends on.  With H,
+// F F^T - I = H + H^T + H H^T and det F - 1 are formed without cancellation.
+template <int D> __device__ __forceinline__ float det1m(const float (&H)[D][D]);  // det(I+H) - 1
+template <> __device__ __forceinline__ float det1m<2>(const float (&H)[2][2]) {
+  return H[0][0] + H[1][1] + (H[0][0] * H[1][1] - H[0][1] * H[1][0]);
+}
+template <> __device__ __forceinline__ float det1m<3>(const float (&H)[3][3]) {
+  const float tr = H[0][0] + H[1][1] + H[2][2];
+  const float m2 = (H[0][0] * H[1][1] - H[0][1] * H[1][0]) + (H[0][0] * H[2][2] - H[0][2] * H[2][0]) +
+                   (H[1][1] * H[2][2] - H[1][2] * H[2][1]);
+  return tr + m2 + det<3>(H);
+}
+
+template <int D>
+__device__ __forceinline__ void load_H(const float* st, size_t NT, int j, float (&H)[D][D]) {
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) H[a][b] = __ldg(&st[(size_t)comp_F<D>(a, b) * NT + j]);
+}
+
+template <int D>
+__device__ __forceinline__ void F_of_H(const float (&H)[D][D], float (&F)[D][D]) {
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) F[a][b] = H[a][b] + (a == b ? 1.f : 0.f);
+}
+
+// F F^T - I from H
+template <int D>
+__device__ __forceinline__ float ffti(const float (&H)[D][D], int a, int b) {
+  float acc = H[a][b] + H[b][a];
+#pragma unroll
+  for (int c = 0; c < D; ++c) acc = fmaf(H[a][c], H[b][c], acc);
+  return acc;
+}
+
+// tau = mu (F F^T - I) + lam ln J I + F Diag(sig) F^T, from H (R1, S1)
+template <int D>
+__device__ __forceinline__ void kirchhoff_h(const float (&H)[D][D], float mu, float lam, const float* sig,
+                                            float (&tau)[D][D], float lnJ) {
+  float F[D][D];
+  F_of_H<D>(H, F);
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = a; b < D; ++b) {
+      float fsf = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; ++c) fsf = fmaf(F[a][c] * sig[c], F[b][c], fsf);
+      float t = fmaf(mu, ffti<D>(H, a, b), fsf);
+      if (a == b) t = fmaf(lam, lnJ, t);
+      tau[a][b] = t;
+      tau[b][a] = t;
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // Wall-band friction projection of step L (R6 band geometry, R7, R8), applied
 // to a node's vbar on read.  Walls are axis aligned: n = +e_a (low wall), -e_a (high).
@@ -346,7 +406,7 @@ __global__ void k_user_to_soa(KParams P, const float* __restrict__ x, const floa
 #pragma unroll
     for (int b = 0; b < D; ++b) {
       st[comp_C<D>(a, b) * NT + j] = C ? C[(j * D + a) * D + b] : 0.f;
-      st[comp_F<D>(a, b) * NT + j] = F ? F[(j * D + a) * D + b] : (a == b ? 1.f : 0.f);
+      st[comp_F<D>(a, b) * NT + j] = F ? F[(j * D + a) * D + b] - (a == b ? 1.f : 0.f) : 0.f;  // H = F - I
     }
   }
 }
@@ -613,6 +673,7 @@ struct StepArgs {
   int* cnt;               // histogram of t+1
   float* dmu;             // [NT] user order
   float* dlam;
+  float* dmass;           // [NT] user order (NEXT N3)
   float* da;              // [B][T][K][D]
   ErrLatch* err;
   int t;
@@ -752,13 +813,13 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
         if (!ADJ) {
           const int u = A.orig[j];
           const float4 pr = A.prm[u];  // m, V, mu, lam
-          float F[D][D], Cm[D][D], v[D];
+          float H[D][D], Cm[D][D], v[D];
 #pragma unroll
           for (int a = 0; a < D; ++a) {
             v[a] = A.st[(size_t)comp_v<D>(a) * NT + j];
 #pragma unroll
             for (int b = 0; b < D; ++b) {
-              F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
+              H[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
               Cm[a][b] = A.st[(size_t)comp_C<D>(a, b) * NT + j];
             }
           }
@@ -767,11 +828,11 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 #pragma unroll
           for (int a = 0; a < D; ++a)
             sig[a] = ai >= 0 ? P.act_s * A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a] : 0.f;
-          float J = det<D>(F);
-          if (!(J > 0.f)) latch(A.err, E_INVERTED, A.t, u);
-          float lnJ = logf(J);
+          const float jm1 = det1m<D>(H);  // J - 1
+          if (!(jm1 > -1.f)) latch(A.err, E_INVERTED, A.t, u);
+          const float lnJ = log1pf(jm1);
           float tau[D][D];
-          kirchhoff<D>(F, pr.z, pr.w, sig, tau, lnJ);
+          kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, lnJ);
           // B = dx G = -4 res dt V tau + m dx C ;  A = m v - B fx
           const float kk = 4.f * P.fres * P.dt * pr.y;
           const float mdx = pr.x * P.dx;
@@ -796,7 +857,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
             gv[a] = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
 #pragma unroll
             for (int b = 0; b < D; ++b) {
-              F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
+              F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j] + (a == b ? 1.f : 0.f);  // F = I + H
               gF[a][b] = gi[(size_t)comp_F<D>(a, b) * NT + k];
               gC[a][b] = gi[(size_t)comp_C<D>(a, b) * NT + k];
             }
@@ -1104,12 +1165,12 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
     for (int i = threadIdx.x; i < n; i += kThreads) {
       const int k = s + i;
       const int j = __ldg(&A.perm[k]);
-      float x[D], F[D][D];
+      float x[D], H[D][D];  // H = F - I
 #pragma unroll
       for (int a = 0; a < D; ++a) {
         x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
 #pragma unroll
-        for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
+        for (int b = 0; b < D; ++b) H[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
       }
       const int u = __ldg(&A.orig[j]);
       Stencil<D> sc;
@@ -1135,9 +1196,10 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
         for (int b = 0; b < D; ++b) Cn[b] = 4.f * P.fres * fmaf(-S[a], sc.fx[b], M[a][b]);
 #pragma unroll
         for (int b = 0; b < D; ++b) {
-          float acc = F[a][b];
+          // F' = (I + dt C') F  <=>  H' = H + dt C' (I + H)  (Eq. 9 on H = F - I)
+          float acc = fmaf(P.dt, Cn[b], H[a][b]);
 #pragma unroll
-          for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[c], F[c][b], acc);
+          for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[c], H[c][b], acc);
           out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
           out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[b];
         }
@@ -1174,10 +1236,11 @@ template <int D> struct PassAcc {
   float S[D];      // sum W f_i
   float M[D][D];   // sum W f_i o_b
   float g[D];      // sum dW (f_i . c(o) + e_i)
+  float Se;        // sum W (.w)   (dp-pass only: sum W dL/dm_i, for the mass gradient)
 };
 
 // one pass; F4 = tile of float4 (f = .xyz, e = em * .w), c(o) = c0 + Cm o
-template <int D, int OX, int OY>
+template <int D, int OX, int OY, bool WS>
 __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, const float (&w)[D][3],
                                          const float (&dw)[D][3], const float* c0, const float (&Cm)[D][D],
                                          float em, const float4& ref, PassAcc<D>& R) {
@@ -1188,7 +1251,7 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
     if (OX) cxy[a] = fmaf((float)OX, Cm[a][0], cxy[a]);
     if (OY) cxy[a] = fmaf((float)OY, Cm[a][1], cxy[a]);
   }
-  float A0[D], A1[D], t1 = 0.f, t2 = 0.f;
+  float A0[D], A1[D], t1 = 0.f, t2 = 0.f, Aw = 0.f;
 #pragma unroll
   for (int a = 0; a < D; ++a) A0[a] = A1[a] = 0.f;
   if constexpr (D == 3) {
@@ -1207,8 +1270,10 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
       }
       t1 = fmaf(wz, sv, t1);
       t2 = fmaf(dw[2][oz], sv, t2);
+      if (WS) Aw = fmaf(wz, q.w - ref.w, Aw);
     }
     const float wx = w[0][OX], wy = w[1][OY], wxy = wx * wy;
+    if (WS) R.Se = fmaf(wxy, Aw, R.Se);
     R.g[0] = fmaf(dw[0][OX] * wy, t1, R.g[0]);
     R.g[1] = fmaf(wx * dw[1][OY], t1, R.g[1]);
     R.g[2] = fmaf(wxy, t2, R.g[2]);
@@ -1226,6 +1291,7 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
 #pragma unroll
     for (int a = 0; a < 2; ++a) sv = fmaf(f[a], cxy[a], sv);
     const float wx = w[0][OX], wy = w[1][OY], wxy = wx * wy;
+    if (WS) R.Se = fmaf(wxy, q.w - ref.w, R.Se);
     R.g[0] = fmaf(dw[0][OX] * wy, sv, R.g[0]);
     R.g[1] = fmaf(wx * dw[1][OY], sv, R.g[1]);
 #pragma unroll
@@ -1237,7 +1303,7 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
   }
 }
 
-template <int D>
+template <int D, bool WS>
 __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, const float (&w)[D][3],
                                              const float (&dw)[D][3], const float* c0,
                                              const float (&Cm)[D][D], float em, const float4& ref,
@@ -1248,14 +1314,15 @@ __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, 
 #pragma unroll
     for (int b = 0; b < D; ++b) R.M[a][b] = 0.f;
   }
-  pass_row<D, 0, 0>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 0, 1>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 0, 2>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 0>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 1, 1>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 2>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 2, 0>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 2, 1>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 2, 2>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  R.Se = 0.f;
+  pass_row<D, 0, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 0, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 0, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 1, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 2, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 2, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 2, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
 }
 
-template <int D>
+template <int D, bool MG>
 __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArgs& A, const float4* s_v,
                                                  const float4* s_a, const float4& aref, const int* bc,
                                                  int r, int k, int& aid_out, float* dsig_out) {
@@ -1266,6 +1333,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   const float4 pr = __ldg(&A.prm[u]);
   const int ai = __ldg(&A.aid[u]);
   const float dmu0 = A.dmu[u], dlam0 = A.dlam[u];  // accumulators: loaded early, stored at the end
+  const float dm0 = MG ? A.dmass[u] : 0.f;
   const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
   float x[D];
 #pragma unroll
@@ -1294,7 +1362,8 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
       u0[a] = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
 #pragma unroll
       for (int b = 0; b < D; ++b) {
-        float gc = gi[(size_t)comp_C<D>(a, b) * NT + k];
+        // g_C = gC + dt gF F^T with F = I + H
+        float gc = fmaf(P.dt, gi[(size_t)comp_F<D>(a, b) * NT + k], gi[(size_t)comp_C<D>(a, b) * NT + k]);
 #pragma unroll
         for (int c = 0; c < D; ++c)
           gc = fmaf(P.dt * gi[(size_t)comp_F<D>(a, c) * NT + k], __ldg(&A.st[(size_t)comp_F<D>(b, c) * NT + j]), gc);
@@ -1302,7 +1371,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         u0[a] = fmaf(-U[a][b], sc.fx[b], u0[a]);
       }
     }
-    stencil_pass<D>(s_v, lb, sc.w, dw, u0, U, 0.f, make_float4(0.f, 0.f, 0.f, 0.f), Rv);
+    stencil_pass<D, false>(s_v, lb, sc.w, dw, u0, U, 0.f, make_float4(0.f, 0.f, 0.f, 0.f), Rv);
     // dx term -4 res^2 g_C^T v^{t+1} = -res U^T S_v
 #pragma unroll
     for (int a = 0; a < D; ++a) {
@@ -1322,12 +1391,9 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   PassAcc<D> Rd;
   float Gm[D][D];  // dx G
   {
-    float F[D][D], tau[D][D], q0[D];
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-      for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
-    kirchhoff<D>(F, pr.z, pr.w, sig, tau, logf(det<D>(F)));
+    float H[D][D], tau[D][D], q0[D];
+    load_H<D>(A.st, NT, j, H);
+    kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, log1pf(det1m<D>(H)));
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       q0[a] = pr.x * __ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]);
@@ -1337,7 +1403,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         q0[a] = fmaf(-Gm[a][b], sc.fx[b], q0[a]);
       }
     }
-    stencil_pass<D>(s_a, lb, sc.w, dw, q0, Gm, pr.x, make_float4(0.f, 0.f, 0.f, 0.f), Rd);
+    stencil_pass<D, MG>(s_a, lb, sc.w, dw, q0, Gm, pr.x, make_float4(0.f, 0.f, 0.f, 0.f), Rd);
   }
   const float m = pr.x;
   float* go = A.gout;
@@ -1361,13 +1427,12 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     go[(size_t)comp_x<D>(a) * NT + j] = acc;
   }
   // (H), (K), material parameters
-  float F[D][D];
-#pragma unroll
-  for (int a = 0; a < D; ++a)
-#pragma unroll
-    for (int b = 0; b < D; ++b) F[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
-  const float J = det<D>(F);
-  const float lnJ = logf(J);
+  float H[D][D], F[D][D];
+  load_H<D>(A.st, NT, j, H);
+  F_of_H<D>(H, F);
+  const float jm1 = det1m<D>(H);
+  const float J = 1.f + jm1;
+  const float lnJ = log1pf(jm1);
   float FiT[D][D];
   inv_T<D>(F, J, FiT);
   float trT = 0.f;
@@ -1394,18 +1459,27 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     float ds = 0.f;
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      float tf = 0.f, ff = 0.f;
+      float tf = 0.f;
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
-        tf = fmaf(T[b][c], F[c][a], tf);
-        ff = fmaf(F[a][c], F[b][c], ff);
-      }
+      for (int c = 0; c < D; ++c) tf = fmaf(T[b][c], F[c][a], tf);
       ds = fmaf(F[b][a], tf, ds);
-      dmu = fmaf(T[a][b], ff - (a == b ? 1.f : 0.f), dmu);
+      dmu = fmaf(T[a][b], ffti<D>(H, a, b), dmu);  // T : (F F^T - I), formed from H
     }
     dsig_out[a] = P.act_s * ds;
   }
   A.dmu[u] = dmu0 + dmu;  // plain RMW (unique per particle): measured 36 us faster than a fp32 RED
+  if (MG) {
+    // NEXT N3: dL/dm_p = sum_i W dm_i + v . sum_i W dp_i + C : Q  (chain rule through Eqs. 3-5;
+    // m enters m_i, m v and the m C part of G)
+    float gmass = Rd.Se + aref.w;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      gmass = fmaf(__ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]), Rd.S[a] + (&aref.x)[a], gmass);
+#pragma unroll
+      for (int b = 0; b < D; ++b) gmass = fmaf(__ldg(&A.st[(size_t)comp_C<D>(a, b) * NT + j]), Q[a][b], gmass);
+    }
+    A.dmass[u] = dm0 + gmass;
+  }
   A.dlam[u] = dlam0 + trT * lnJ;
   aid_out = ai;
 }
@@ -1433,7 +1507,7 @@ __device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArg
   }
 }
 
-template <int D>
+template <int D, bool MG>
 __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
   __shared__ float4 s_v[Dim<D>::TN];
   __shared__ float4 s_a[Dim<D>::TN];
@@ -1463,7 +1537,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       const int i = i0 + threadIdx.x;
       int ai = -1;
       float dsig[D] = {};
-      if (i < n) p2g_adj_particle<D>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
+      if (i < n) p2g_adj_particle<D, MG>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
       __syncwarp();
       if (P.K > 0) reduce_actuation<D>(P, A, r, ai, dsig);
     }
@@ -1521,23 +1595,28 @@ __global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int*
 // ------------------------------------------------------------------------------------
 // seed, readback, finalize
 // ------------------------------------------------------------------------------------
-// user-order AoS seed -> SoA adjoint in storage order T (orig_T maps storage -> user)
+// user-order AoS seed -> SoA adjoint in storage order t (orig_t maps storage -> user);
+// accumulate = add to the adjoint already there (per-step seeds of a running loss, N4)
 template <int D>
 __global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __restrict__ gx,
                        const float* __restrict__ gv, const float* __restrict__ gF,
-                       const float* __restrict__ gC, float* __restrict__ g) {
+                       const float* __restrict__ gC, float* __restrict__ g, int accumulate) {
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= P.NT) return;
   const size_t NT = P.NT;
   int u = orig[k];
+  auto put = [&](int comp, float val) {
+    float* q = &g[(size_t)comp * NT + k];
+    *q = accumulate ? *q + val : val;
+  };
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    g[(size_t)comp_x<D>(a) * NT + k] = gx ? gx[u * D + a] : 0.f;
-    g[(size_t)comp_v<D>(a) * NT + k] = gv ? gv[u * D + a] : 0.f;
+    put(comp_x<D>(a), gx ? gx[u * D + a] : 0.f);
+    put(comp_v<D>(a), gv ? gv[u * D + a] : 0.f);
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      g[(size_t)comp_F<D>(a, b) * NT + k] = gF ? gF[(u * D + a) * D + b] : 0.f;
-      g[(size_t)comp_C<D>(a, b) * NT + k] = gC ? gC[(u * D + a) * D + b] : 0.f;
+      put(comp_F<D>(a, b), gF ? gF[(u * D + a) * D + b] : 0.f);
+      put(comp_C<D>(a, b), gC ? gC[(u * D + a) * D + b] : 0.f);
     }
   }
 }
@@ -1545,7 +1624,7 @@ __global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __r
 // SoA storage order -> user AoS (x, v, F, C), any may be null
 template <int D>
 __global__ void k_soa_to_user(KParams P, const int* __restrict__ orig, const float* __restrict__ st,
-                              float* x, float* v, float* F, float* C) {
+                              float* x, float* v, float* F, float* C, int state) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= P.NT) return;
   const size_t NT = P.NT;
@@ -1556,7 +1635,8 @@ __global__ void k_soa_to_user(KParams P, const int* __restrict__ orig, const flo
     if (v) v[u * D + a] = st[(size_t)comp_v<D>(a) * NT + j];
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      if (F) F[(u * D + a) * D + b] = st[(size_t)comp_F<D>(a, b) * NT + j];
+      // states store H = F - I; adjoints (dL/dF = dL/dH) are returned as they are
+      if (F) F[(u * D + a) * D + b] = st[(size_t)comp_F<D>(a, b) * NT + j] + ((state && a == b) ? 1.f : 0.f);
       if (C) C[(u * D + a) * D + b] = st[(size_t)comp_C<D>(a, b) * NT + j];
     }
   }

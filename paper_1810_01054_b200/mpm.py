@@ -27,7 +27,8 @@ STATUS = {0: "MPM_OK", 1: "MPM_ERR_INVALID_ARG", 2: "MPM_ERR_OOM", 3: "MPM_ERR_C
 EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "mpm_forward",
            "mpm_tape_length", "mpm_rewind", "mpm_get_state", "mpm_backward", "mpm_grad",
            "mpm_last_error", "mpm_get_binning", "mpm_get_grid", "mpm_set_profiling",
-           "mpm_get_profile", "mpm_launch_count", "mpm_get_step_info")
+           "mpm_get_profile", "mpm_launch_count", "mpm_get_step_info", "mpm_grad_mass",
+           "mpm_add_seed", "mpm_clear_seeds", "mpm_enable_mass_grad")
 
 
 class MPMError(RuntimeError):
@@ -76,6 +77,10 @@ def load():
     L.mpm_set_profiling.argtypes = [vp, i32]
     L.mpm_get_profile.argtypes = [vp, C.POINTER(i32), vp, vp, C.c_char_p, i32]
     L.mpm_get_step_info.argtypes = [vp, i32, vp]
+    L.mpm_grad_mass.argtypes = [vp, vp]
+    L.mpm_enable_mass_grad.argtypes = [vp, i32]
+    L.mpm_add_seed.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.mpm_clear_seeds.argtypes = [vp]
     L.mpm_launch_count.argtypes = [vp]
     L.mpm_launch_count.restype = i64
     for name in EXPORTS:
@@ -231,6 +236,26 @@ class MPM:
         keys = ("dx0", "dv0", "dF0", "dC0", "dE", "dnu", "da")
         self._check(self.L.mpm_grad(self.h, *[_ptr(out.get(k)) for k in keys]))
         return out
+
+    def enable_mass_grad(self, on: bool = True):
+        self._check(self.L.mpm_enable_mass_grad(self.h, 1 if on else 0))
+
+    def grad_mass(self, out=None):
+        """dL/dm_p (NEXT N3) from the last backward, user order [B*N]."""
+        if out is None:
+            out = np.empty(self.NT, np.float32)
+        self._check(self.L.mpm_grad_mass(self.h, _ptr(out)))
+        return out
+
+    def add_seed(self, t, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
+        """Additive seed dL/dstate_t for a running loss (NEXT N4)."""
+        d, NT = self.cfg.dim, self.NT
+        arrs = [_in(dLdx, np.float32, (NT, d)), _in(dLdv, np.float32, (NT, d)),
+                _in(dLdF, np.float32, (NT, d, d)), _in(dLdC, np.float32, (NT, d, d))]
+        self._check(self.L.mpm_add_seed(self.h, int(t), *[_ptr(a) for a in arrs]))
+
+    def clear_seeds(self):
+        self._check(self.L.mpm_clear_seeds(self.h))
 
     # -- introspection -------------------------------------------------------------------
     def get_binning(self, t: int):

@@ -192,3 +192,40 @@ def test_errors_out_of_domain_and_inverted_and_call_order():
     with pytest.raises(mpm.MPMError) as e:
         sim.forward(1)
     assert e.value.status == "MPM_ERR_TAPE_FULL"
+
+
+@pytest.mark.parametrize("d,T", [(2, 10), (3, 12)])
+def test_mass_gradient_and_running_loss_parity(d, T):
+    """NEXT N3 (dL/dm_p) and N4 (seeds at intermediate states: a running loss
+    sum_t <w_t, state_t>) against the oracle's orc_backward_ex."""
+    sc = scenes.tiny(d, seed=51 + d, res=16 if d == 3 else 32, n_cells=(4,) * d, steps=T, K=2,
+                     s=40.0, center=(6, 4, 6) if d == 3 else (12, 4))
+    sim = _sim(sc, T)
+    sim.enable_mass_grad(True)
+    sim.forward(T)
+    cfg, traj = _oracle_traj(sc, 0, T)
+    rng = np.random.default_rng(52 + d)
+    W = rng.standard_normal(traj.shape)
+    W[1::2] = 0.0  # seeds on every other state (and always on the last)
+    W[T] = rng.standard_normal(traj[T].shape)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    for t in range(T):
+        if np.any(W[t]):
+            wx, wv, wC, wF = oracle.unpack(W[t], d)
+            sim.add_seed(t, f32(wx), f32(wv), f32(wF), f32(wC))
+    wx, wv, wC, wF = oracle.unpack(W[T], d)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    gm = sim.grad_mass()
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    g0, gE, gnu, ga, ogm = oracle.backward_ex(cfg, traj, m, vol, E, nu, aid, act[:T], W)
+    gx, gv, gC, gF = oracle.unpack(g0, d)
+    for k, a, b in (("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF),
+                    ("dC0", g["dC0"], gC), ("dE", g["dE"], gE), ("dm", gm, ogm)):
+        e = rel_err(a, b)
+        assert e < 1e-3, (k, e)
+    sim.clear_seeds()
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g2 = sim.grad()
+    g0b, *_ = oracle.backward(cfg, traj, m, vol, E, nu, aid, act[:T], W[T])
+    assert rel_err(g2["dx0"], oracle.unpack(g0b, d)[0]) < 1e-3

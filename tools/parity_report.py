@@ -1,0 +1,62 @@
+"""Parity margins: norm-wise relative error (reading R16) of the CUDA path vs the fp64 oracle,
+per field, for the BASELINE configs C1-C3 and a C5b-style batch; prints one JSON line per case.
+Run on a GPU box:  python tools/parity_report.py > profiles/parity_margins.jsonl"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402  (test infrastructure; this is a report tool, not the product)
+from paper_1810_01054_b200 import mpm, scenes  # noqa: E402
+from tests.helpers import oracle_cfg, rel_err  # noqa: E402
+
+
+def case(name, sc, T, r=0):
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    sim.set_scene(sc)
+    sim.enable_mass_grad(True)
+    sim.forward(T)
+    x, v, F, Cm = sim.get_state(T)
+    cfg = oracle_cfg(sc)
+    st = oracle.pack(sc.x[r], sc.v[r], sc.C[r], sc.F[r])
+    prm = [a[r].astype(np.float64) for a in (sc.mass, sc.vol, sc.E, sc.nu)]
+    aid, act = sc.actuator_id[r], sc.act[r].astype(np.float64)[:T]
+    t0 = time.time()
+    traj = oracle.forward(cfg, st, *prm, aid, act, T)
+    ox, ov, oC, oF = oracle.unpack(traj[T], sc.dim)
+    sl = slice(r * sc.n, (r + 1) * sc.n)
+    out = {"case": name, "steps": T, "particles": sc.n,
+           "state": {k: rel_err(a[sl], b) for k, a, b in (("x", x, ox), ("v", v, ov), ("F", F, oF), ("C", Cm, oC))}}
+    rng = np.random.default_rng(1)
+    S = oracle.S_of(sc.dim)
+    w = rng.standard_normal((sc.batch, sc.n, S))
+    wx, wv, wC, wF = oracle.unpack(w.reshape(-1, S), sc.dim)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    gm = sim.grad_mass()
+    seeds = np.zeros_like(traj)
+    seeds[T] = w[r]
+    g0, gE, gnu, ga, ogm = oracle.backward_ex(cfg, traj, *prm, aid, act, seeds)
+    gx, gv, gC, gF = oracle.unpack(g0, sc.dim)
+    out["grad"] = {k: rel_err(a, b) for k, a, b in (
+        ("dx0", g["dx0"][sl], gx), ("dv0", g["dv0"][sl], gv), ("dF0", g["dF0"][sl], gF),
+        ("dC0", g["dC0"][sl], gC), ("dE", g["dE"][sl], gE), ("dnu", g["dnu"][sl], gnu),
+        ("da", g["da"][r, :T], ga), ("dm", gm[sl], ogm))}
+    out["oracle_s"] = round(time.time() - t0, 1)
+    sim.close()
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    case("C1 configs[0] 2D block", scenes.block_2d(steps=50, perturb=True), 50)
+    case("C2 configs[1] 2D walker", scenes.walker_2d(steps=100), 100)
+    case("C2 configs[1] 2D walker, 500 steps", scenes.walker_2d(steps=500), 500)
+    case("C3 configs[2] 3D quadruped", scenes.quadruped_3d(steps=100), 100)
+    case("C3 configs[2] 3D quadruped, 200 steps", scenes.quadruped_3d(steps=200), 200)
+    case("C5b-style batch (rollout 2 of 3)", scenes.quadruped_3d(batch=3, steps=50, e_scale=True), 50, r=2)
