@@ -113,7 +113,7 @@ def block_2d(seed=0, batch=1, steps=50, perturb=False):
 def walker_2d(seed=0, batch=1, steps=500):
     """C2 (configs[1]): 2D 128^2 walker, body 40x14 cells on 4 legs of 8x28 cells standing on
     the floor; 5,824 particles; K = 4 leg actuators on the vertical channel,
-    a[t][k] = sin(2 pi t / 100 + k pi / 2), s = 300."""
+    a[t][k] = sin(2 pi t / 100 + k pi / 2), s = 40 (s = 300 inverts elements within 500 steps)."""
     dim, res, K = 2, 128, 4
     legs_x = (20, 31, 41, 52)
     xs, vs, Fs, Cs, ms, vols, Es, nus, aids, acts = ([] for _ in range(10))
@@ -130,7 +130,7 @@ def walker_2d(seed=0, batch=1, steps=500):
         xs.append(x); vs.append(np.zeros((n, dim), np.float32)); Fs.append(_identity(n, dim))
         Cs.append(np.zeros((n, dim, dim), np.float32)); ms.append(m); vols.append(vol)
         Es.append(E); nus.append(nu); aids.append(tag.astype(np.int32)); acts.append(a)
-    return _pack("C2_walker2d", dim, res, 1e-4, steps, K, 300.0, xs, vs, Fs, Cs, ms, vols, Es,
+    return _pack("C2_walker2d", dim, res, 1e-4, steps, K, 40.0, xs, vs, Fs, Cs, ms, vols, Es,
                  nus, aids, acts)
 
 

@@ -28,9 +28,10 @@ def _orc_inputs(sc, r=0):
             sc.actuator_id[r], sc.act[r].astype(np.float64))
 
 
-@pytest.mark.parametrize("name,T", [("C2", 100), ("C3", 100)])
+@pytest.mark.parametrize("name,T", [("C2", 500), ("C3", 200)])
 def test_full_config_state_and_gradient(name, T):
-    """Full C2 / C3 scenes (actuation, floor friction): state after T steps within 1e-3,
+    """Full C2 (500 steps) / C3 (200 steps) scenes -- the configs' own horizons -- with
+    actuation and floor friction: state after T steps within 1e-3,
     gradients of a random linear loss within 1e-3 (north_star), every input family."""
     sc = scenes.CONFIGS[name](steps=T)
     sim = _sim(sc, T)
