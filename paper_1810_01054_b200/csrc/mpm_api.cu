@@ -272,7 +272,6 @@ void launch_forward_step(mpm_ctx c, int t) {
   StepArgs A = step_args(c, t);
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
   launch(c, KI_P2G, [&] { k_block_scatter<D, false><<<nblk, kThreads, scatter_dyn_smem<D, false>(), c->stream>>>(P, A); });
-  launch(c, KI_GRID, [&] { k_grid_update<<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), c->arena); });
   const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
   launch(c, KI_G2P, [&] { k_g2p<D><<<ng, kThreads, 0, c->stream>>>(P, A); });
 }
@@ -287,6 +286,7 @@ void launch_backward_step(mpm_ctx c, int t, const float* gin, float* gout) {
   A.grid = agrid_of(c, t);
   A.gin = gin;
   A.gout = gout;
+
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
   if (t == c->tape_len - 1)  // first backward step: prepare its buffer (later steps: by grid_T)
     launch(c, KI_ZERO, [&] { k_zero_slots<<<c->n_sm * 4, 256, 0, c->stream>>>(info_at(c, t), A.grid); });

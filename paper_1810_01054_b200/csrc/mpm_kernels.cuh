@@ -671,6 +671,8 @@ struct StepArgs {
   int* orig_next;
   int* key_next;          // keys of t+1 (in the single key buffer)
   int* cnt;               // histogram of t+1
+  int* info_prev;         // backward: step record of t-1 (its adjoint buffer is prepared)
+  float4* agrid_prev;
   float* dmu;             // [NT] user order
   float* dlam;
   float* dmass;           // [NT] user order (NEXT N3)
@@ -988,22 +990,10 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 }
 
 // ------------------------------------------------------------------------------------
-// Grid update (Eq. 6; gravity R5): (p, m) -> (vbar = p/m + dt g, m) in place.
-// The wall projection (R6) is applied when a node is read.
+// The grid operation (Eq. 6; gravity R5; wall projection R6) has no kernel of its
+// own: the memo keeps the (p, m) P2G accumulated, and every gather computes
+// vbar = p / m + dt g and the projection per node while staging its tile (fetch_node).
 // ------------------------------------------------------------------------------------
-__global__ void k_grid_update(KParams P, const int* __restrict__ info_t, float4* __restrict__ arena) {
-  const int n = info_t[I_NTOUCH] * kCPB;
-  float4* g = arena + (size_t)info_t[I_BASE] * kCPB;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    float4 q = g[i];
-    if (q.w > 0.f) {
-      q.x = q.x / q.w + P.dt * P.g[0];
-      q.y = q.y / q.w + P.dt * P.g[1];
-      q.z = q.z / q.w + P.dt * P.g[2];
-      g[i] = q;
-    }
-  }
-}
 
 // L2 prefetch of one particle's SoA record (ncomp components at index j) -- issued for a
 // block's particles before its tile is staged, so the particle loop's loads hit L2
@@ -1051,16 +1041,18 @@ __device__ __forceinline__ void fetch_node(const KParams& P, const StepArgs& A, 
   const int slot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
   if (slot < 0) return;
   const size_t addr = (size_t)slot * kCPB + cell_lin<D>(loc);
-  v = A.tgrid[addr];
-  if (v.w > 0.f && in_band<D>(node, P.res, P.bound)) {
-    float vv[D];
-    vv[0] = v.x; vv[1] = v.y;
-    if constexpr (D == 3) vv[2] = v.z;
-    project_node<D>(vv, node, P);
-    v.x = vv[0]; v.y = vv[1];
-    if constexpr (D == 3) v.z = vv[2];
-  }
-  if (TWO) ad = A.grid[addr - abase];
+  const float4 pm = A.tgrid[addr];  // (p, m) as accumulated by P2G -- the memo's grid
+  if (!(pm.w > 0.f)) return;        // empty node: v = 0 (R13), no adjoint
+  // grid operation (Eq. 6 + gravity, R5): vbar = p / m + dt g, then the wall projection (R6)
+  float vb[D], vv[D];
+  vb[0] = pm.x / pm.w + P.dt * P.g[0];
+  vb[1] = pm.y / pm.w + P.dt * P.g[1];
+  if constexpr (D == 3) vb[2] = pm.z / pm.w + P.dt * P.g[2];
+#pragma unroll
+  for (int a = 0; a < D; ++a) vv[a] = vb[a];
+  if (in_band<D>(node, P.res, P.bound)) project_node<D>(vv, node, P);
+  v = make_float4(vv[0], vv[1], D == 3 ? vv[D - 1] : 0.f, pm.w);
+  if (TWO) ad = A.grid[addr - abase];  // (dL/dp_i, dL/dm_i) from k_grid_adj
 }
 
 // Stage the block's node tile: s_v = v_i - vref, s_a = a_i - aref, with (vref, aref) the
@@ -1547,19 +1539,19 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
 
 // ------------------------------------------------------------------------------------
 // grid^T: steps L (reverse wall order R6), D, E (R9).
-// adjoint node (dL/dv_i) -> (dL/dp_i, dL/dm_i) in place.
+// adjoint node (dL/dv_i) -> (dL/dp_i, dL/dm_i) in place, from the memo's (p, m).  Also
+// prepares the other adjoint buffer for backward step t-1 (zero + reset its counters).
 // ------------------------------------------------------------------------------------
 template <int D>
 __global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int* __restrict__ touched_list,
                            const float4* __restrict__ arena, float4* __restrict__ ag,
                            int* __restrict__ info_prev, float4* __restrict__ ag_prev) {
-  // prepare the other adjoint buffer for backward step t-1 (zero + reset its counters)
   if (info_prev) adj_prepare(info_prev, ag_prev, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   const int n = info_t[I_NTOUCH] * kCPB;
   const float4* g = arena + (size_t)info_t[I_BASE] * kCPB;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    float4 q = g[i];
-    float4 a = ag[i];
+    const float4 q = g[i];  // (p, m)
+    const float4 a = ag[i];
     float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
     if (q.w > 0.f) {
       const int gb = touched_list[i / kCPB];
@@ -1574,12 +1566,13 @@ __global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int*
           l /= Dim<D>::BB;
         }
       }
-      float vb[D] = {}, gv[D] = {};
-      vb[0] = q.x; vb[1] = q.y; gv[0] = a.x; gv[1] = a.y;
-      if (D == 3) { vb[D - 1] = q.z; gv[D - 1] = a.z; }
-      if (in_band<D>(node, P.res, P.bound)) project_node_adj<D>(vb, gv, node, P);
-      // gravity adjoint = identity (R5); v = p/m + dt g -> dp = gv/m, dm = -(p . gv)/m^2
       const float im = 1.f / q.w;
+      float vb[D] = {}, gv[D] = {};
+      vb[0] = fmaf(q.x, im, P.dt * P.g[0]); vb[1] = fmaf(q.y, im, P.dt * P.g[1]);
+      gv[0] = a.x; gv[1] = a.y;
+      if (D == 3) { vb[D - 1] = fmaf(q.z, im, P.dt * P.g[2]); gv[D - 1] = a.z; }
+      if (in_band<D>(node, P.res, P.bound)) project_node_adj<D>(vb, gv, node, P);
+      // gravity adjoint = identity (R5); vbar = p/m + dt g -> dp = gv/m, dm = -(p . gv)/m^2
       float pg = 0.f;
 #pragma unroll
       for (int d = 0; d < D; ++d) pg = fmaf(vb[d] - P.dt * P.g[d], gv[d], pg);
@@ -1678,12 +1671,12 @@ __global__ void k_dense_grid(KParams P, const int* __restrict__ info_t, const in
 #pragma unroll
     for (int d = 0; d < D; ++d) nn *= P.res;
     size_t o = (size_t)r * nn + lin;
-    float4 q = g[i];
+    float4 q = g[i];  // (p, m)
     if (m) m[o] = q.w;
-    if (vbar) {
-      vbar[o * D + 0] = q.x;
-      vbar[o * D + 1] = q.y;
-      if (D == 3) vbar[o * D + D - 1] = q.z;
+    if (vbar && q.w > 0.f) {
+      vbar[o * D + 0] = q.x / q.w + P.dt * P.g[0];
+      vbar[o * D + 1] = q.y / q.w + P.dt * P.g[1];
+      if (D == 3) vbar[o * D + D - 1] = q.z / q.w + P.dt * P.g[2];
     }
   }
 }
