@@ -56,7 +56,8 @@ typedef enum {
   MPM_ERR_INVERTED = 5,      /* det F <= 0, ln J undefined (DESIGN R14)             */
   MPM_ERR_TAPE_FULL = 6,     /* forward beyond max_steps, or grid-slot arena full    */
   MPM_ERR_CALL_ORDER = 7,    /* e.g. backward before forward, grad before backward   */
-  MPM_ERR_COMM = 8
+  MPM_ERR_COMM = 8,          /* NCCL failure (slab mode)                             */
+  MPM_ERR_OUT_OF_SLAB = 9    /* particle left its slab's halo (slab mode, see below) */
 } mpm_status;
 
 typedef struct {
@@ -135,6 +136,39 @@ mpm_status mpm_add_seed(mpm_ctx ctx, int32_t t, const float* dLdx, const float* 
 mpm_status mpm_clear_seeds(mpm_ctx ctx);
 
 const char* mpm_last_error(mpm_ctx ctx);
+
+/* ---- slab mode: one large rollout sharded by x-slab (configs[4] "8M particles
+ * slab-sharded") ----
+ * A context simulates the particles of one x-slab [x_lo, x_hi) of node planes (ownership
+ * by base_x at t = 0, fixed for the rollout).  Nodes that two slabs can both touch lie in a
+ * window of 2*halo_blocks block-planes (block = 4 nodes in 3D, 8 in 2D) centred on each
+ * slab boundary; the exchange is the symmetric sum of those windows after P2G (Eq. 3-5 are
+ * sums over ALL particles) and after G2P^T (the adjoint of that sum), so every node a rank
+ * reads holds the whole-body value.  A particle may drift at most halo_blocks*block - 2
+ * nodes past the slab (base_x in [x_lo - h, x_hi + h - 3], h = halo_blocks*block, on a side
+ * that has a neighbour); beyond that forward latches MPM_ERR_OUT_OF_SLAB.  The actuation is
+ * shared: after mpm_backward / mpm_group_backward, mpm_grad's da is summed over all slabs.
+ *
+ * mpm_set_slab: before mpm_set_state; batch must be 1; x_lo, x_hi multiples of the block
+ *   size, 0 <= x_lo < x_hi <= res; a side with a neighbour (x_lo > 0, x_hi < res) needs
+ *   x_hi - x_lo >= 2h and its window inside the domain.  Allocates 4 window buffers of
+ *   2*halo_blocks*(res/block)^(dim-1)*64 float4 each.
+ * mpm_comm_unique_id / mpm_comm_init: one context per GPU, one process per GPU; rank r's
+ *   left neighbour is rank r-1 (ranks ordered by slab).  The exchange is a grouped NCCL
+ *   send/recv with the two neighbours on config.stream; the da sum an NCCL all-reduce.
+ *   mpm_comm_init is collective over the world (blocks until all ranks call it).
+ * mpm_group_forward / mpm_group_backward: the same exchange between n contexts of ONE
+ *   process (adjacent slabs in x order, one device, one stream), done as device-to-device
+ *   copies between the phases of every step -- a single-GPU emulation of the sharded run
+ *   used by the parity tests; no kernel waits on another.  Seeds: arrays of n pointers
+ *   (user order of each context) or NULL.                                                 */
+mpm_status mpm_set_slab(mpm_ctx ctx, int32_t x_lo, int32_t x_hi, int32_t halo_blocks);
+mpm_status mpm_comm_unique_id(char out[128]);
+mpm_status mpm_comm_init(mpm_ctx ctx, int32_t rank, int32_t world, const char id[128]);
+mpm_status mpm_group_forward(mpm_ctx* ctxs, int32_t n_ctx, int32_t n_steps);
+mpm_status mpm_group_backward(mpm_ctx* ctxs, int32_t n_ctx, const float* const* dLdx,
+                              const float* const* dLdv, const float* const* dLdF,
+                              const float* const* dLdC);
 
 /* ---- introspection, used by the parity tests (all synchronous) ---- */
 

@@ -2,6 +2,8 @@
 // Declared in include/mpm.h.  Owns device memory, the tape (the paper's memo),
 // the per-step launch schedule, the device error latch and per-kernel profiling.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is resolved at run time (see nccl_api)
 
 #include <algorithm>
 #include <cstdio>
@@ -19,15 +21,51 @@ namespace {
 
 enum KernelId {
   KI_SCAN_A, KI_SCAN_B, KI_SCAN_C, KI_SCATTER, KI_P2G, KI_GRID, KI_G2P,
-  KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC, KI_COUNT
+  KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC, KI_BANDP, KI_BANDU, KI_COUNT
 };
 const char* kKernelNames[KI_COUNT] = {"scan_a", "scan_b", "scan_c",  "scatter", "p2g",  "grid_update",
-                                      "g2p",    "zero_adj", "g2p_T", "grid_T", "p2g_T", "misc"};
+                                      "g2p",    "zero_adj", "g2p_T", "grid_T", "p2g_T", "misc",
+                                      "band_pack", "band_unpack"};
 
 struct PendingEvent {
   cudaEvent_t a, b;
   int kid;
 };
+
+// NCCL entry points, resolved on first use (slab mode only).  No link-time dependency: a
+// process that loads libmpm before torch must not bind libnccl.so.2 to a different copy than
+// the one torch needs; an already-loaded libnccl (torch's) is preferred.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char* (*GetErrorString)(ncclResult_t);
+};
+
+const NcclApi* nccl_api() {
+  static NcclApi api{};
+  static int state = 0;  // 0 = not tried, 1 = ok, -1 = unavailable
+  if (state) return state > 0 ? &api : nullptr;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  bool ok = h != nullptr;
+#define NCCL_SYM(f)                                                    \
+  if (ok) {                                                            \
+    *reinterpret_cast<void**>(&api.f) = dlsym(h, "nccl" #f);            \
+    ok = api.f != nullptr;                                             \
+  }
+  NCCL_SYM(GetUniqueId) NCCL_SYM(CommInitRank) NCCL_SYM(CommDestroy) NCCL_SYM(Send) NCCL_SYM(Recv)
+  NCCL_SYM(AllReduce) NCCL_SYM(GroupStart) NCCL_SYM(GroupEnd) NCCL_SYM(GetErrorString)
+#undef NCCL_SYM
+  state = ok ? 1 : -1;
+  return ok ? &api : nullptr;
+}
 
 }  // namespace
 
@@ -80,6 +118,15 @@ struct mpm_ctx_s {
   float* da = nullptr;
   float* stage = nullptr;
   std::vector<void*> allocs;
+  // slab mode: x-slab [x_lo, x_hi), boundary windows of 2*halo block-planes
+  bool slab = false, left = false, right = false;
+  int x_lo = 0, x_hi = 0, halo = 0;
+  int band_blocks = 0, gb_lo = 0, gb_hi = 0;  // blocks per window, first block of each window
+  float4 *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  float* bcur = nullptr;  // backward: adjoint of the current step (storage order)
+  float* bnxt = nullptr;
   // profiling
   bool profiling = false;
   bool mass_grad = false;  // N3: compute dL/dm_p in P2G^T (opt-in)
@@ -197,6 +244,12 @@ mpm_status check_latch(mpm_ctx c) {
     c->poisoned = true;
     return fail(c, MPM_ERR_TAPE_FULL, buf);
   }
+  if (h.code == E_SLAB) {
+    snprintf(buf, sizeof buf, "particle %d left its slab's halo (base x outside [%d, %d]) at step %d", h.particle,
+             c->P.slab_lo, c->P.slab_hi, h.step);
+    c->poisoned = true;
+    return fail(c, MPM_ERR_OUT_OF_SLAB, buf);
+  }
   snprintf(buf, sizeof buf, "device error code %d", h.code);
   return fail(c, MPM_ERR_CUDA, buf);
 }
@@ -265,13 +318,69 @@ void launch_bin(mpm_ctx c, int t) {
   });
 }
 
+bool has_nbr(mpm_ctx c) { return c->slab && (c->left || c->right); }
+
+// slab mode: boundary windows of step t's grid -> send buffers (forward: tape arena; adjoint:
+// the step's adjoint buffer)
+void launch_band_pack(mpm_ctx c, int t, bool adj, const float4* g) {
+  launch(c, KI_BANDP, [&] {
+    k_band_pack<<<c->n_sm * 4, 256, 0, c->stream>>>(c->band_blocks, c->gb_lo, c->gb_hi, slot_at(c, t), info_at(c, t),
+                                                    adj, g, c->left ? c->send_lo : nullptr,
+                                                    c->right ? c->send_hi : nullptr);
+  });
+}
+void launch_band_unpack(mpm_ctx c, int t, bool adj, float4* g) {
+  launch(c, KI_BANDU, [&] {
+    k_band_unpack<<<c->n_sm * 4, 256, 0, c->stream>>>(c->band_blocks, c->gb_lo, c->gb_hi, slot_at(c, t), info_at(c, t),
+                                                      adj, g, c->left ? c->recv_lo : nullptr,
+                                                      c->right ? c->recv_hi : nullptr);
+  });
+}
+size_t band_floats(mpm_ctx c) { return (size_t)c->band_blocks * kCPB * 4; }
+
+// NCCL transport: grouped send/recv with the x-neighbours (ranks ordered by slab)
+mpm_status exchange_nccl(mpm_ctx c) {
+  const size_t n = band_floats(c);
+  const NcclApi* N = nccl_api();  // non-null: the communicator exists
+  ncclResult_t r = N->GroupStart();
+  if (r == ncclSuccess && c->left) r = N->Send(c->send_lo, n, ncclFloat, c->rank - 1, c->comm, c->stream);
+  if (r == ncclSuccess && c->left) r = N->Recv(c->recv_lo, n, ncclFloat, c->rank - 1, c->comm, c->stream);
+  if (r == ncclSuccess && c->right) r = N->Send(c->send_hi, n, ncclFloat, c->rank + 1, c->comm, c->stream);
+  if (r == ncclSuccess && c->right) r = N->Recv(c->recv_hi, n, ncclFloat, c->rank + 1, c->comm, c->stream);
+  ncclResult_t r2 = N->GroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) return fail(c, MPM_ERR_COMM, std::string("halo exchange: ") + N->GetErrorString(r));
+  return MPM_OK;
+}
+
+// in-process transport (mpm_group_*): contexts in slab order on one stream
+mpm_status exchange_local(mpm_ctx* cs, int n) {
+  for (int i = 0; i + 1 < n; ++i) {
+    mpm_ctx a = cs[i], b = cs[i + 1];
+    mpm_ctx c = a;
+    const size_t bytes = band_floats(a) * sizeof(float);
+    CK(cudaMemcpyAsync(b->recv_lo, a->send_hi, bytes, cudaMemcpyDeviceToDevice, a->stream));
+    CK(cudaMemcpyAsync(a->recv_hi, b->send_lo, bytes, cudaMemcpyDeviceToDevice, a->stream));
+  }
+  return MPM_OK;
+}
+
+// forward step t = phase A (binning, P2G [, window pack]) | exchange | phase B ([unpack,] G2P)
 template <int D>
-void launch_forward_step(mpm_ctx c, int t) {
+void forward_phase_a(mpm_ctx c, int t) {
   const KParams& P = c->P;
   launch_bin<D>(c, t);
   StepArgs A = step_args(c, t);
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
   launch(c, KI_P2G, [&] { k_block_scatter<D, false><<<nblk, kThreads, scatter_dyn_smem<D, false>(), c->stream>>>(P, A); });
+  if (has_nbr(c)) launch_band_pack(c, t, false, c->arena);
+}
+
+template <int D>
+void forward_phase_b(mpm_ctx c, int t) {
+  const KParams& P = c->P;
+  if (has_nbr(c)) launch_band_unpack(c, t, false, c->arena);
+  StepArgs A = step_args(c, t);
   const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
   launch(c, KI_G2P, [&] { k_g2p<D><<<ng, kThreads, 0, c->stream>>>(P, A); });
 }
@@ -279,19 +388,30 @@ void launch_forward_step(mpm_ctx c, int t) {
 // adjoint grid buffer of backward step t (double-buffered by step parity)
 float4* agrid_of(mpm_ctx c, int t) { return (t & 1) ? c->agrid1 : c->agrid; }
 
+// backward step t = phase A ([zero,] G2P^T [, window pack]) | exchange | phase B ([unpack,]
+// grid^T, P2G^T); the particle adjoint flows c->bcur -> c->bnxt
 template <int D>
-void launch_backward_step(mpm_ctx c, int t, const float* gin, float* gout) {
+void backward_phase_a(mpm_ctx c, int t) {
   const KParams& P = c->P;
   StepArgs A = step_args(c, t);
   A.grid = agrid_of(c, t);
-  A.gin = gin;
-  A.gout = gout;
-
-  const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
+  A.gin = c->bcur;
+  A.gout = c->bnxt;
   if (t == c->tape_len - 1)  // first backward step: prepare its buffer (later steps: by grid_T)
     launch(c, KI_ZERO, [&] { k_zero_slots<<<c->n_sm * 4, 256, 0, c->stream>>>(info_at(c, t), A.grid); });
   const int nbla = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter_adj));
   launch(c, KI_G2PT, [&] { k_block_scatter<D, true><<<nbla, kThreads, scatter_dyn_smem<D, true>(), c->stream>>>(P, A); });
+  if (has_nbr(c)) launch_band_pack(c, t, true, A.grid);
+}
+
+template <int D>
+void backward_phase_b(mpm_ctx c, int t) {
+  const KParams& P = c->P;
+  StepArgs A = step_args(c, t);
+  A.grid = agrid_of(c, t);
+  A.gin = c->bcur;
+  A.gout = c->bnxt;
+  if (has_nbr(c)) launch_band_unpack(c, t, true, A.grid);
   launch(c, KI_GRIDT, [&] {
     k_grid_adj<D><<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
                                                        t > 0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
@@ -373,19 +493,40 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
 
 template <int D>
 mpm_status do_forward(mpm_ctx c, int n) {
-  for (int i = 0; i < n; ++i) launch_forward_step<D>(c, c->tape_len + i);
+  for (int i = 0; i < n; ++i) {
+    const int t = c->tape_len + i;
+    forward_phase_a<D>(c, t);
+    if (has_nbr(c)) {
+      mpm_status s = exchange_nccl(c);
+      if (s) return s;
+    }
+    forward_phase_b<D>(c, t);
+  }
   mpm_status s = sync_and_check(c, "forward");
   if (s) return s;
   c->tape_len += n;
   return MPM_OK;
 }
 
+// N4: additive seed of state t into the adjoint buffer g, if registered
 template <int D>
-mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float* gF, const float* gC) {
+void add_step_seed(mpm_ctx c, int t, float* g) {
+  auto it = c->seeds.find(t);
+  if (it == c->seeds.end()) return;
+  const size_t NT = c->P.NT;
+  const float* b = it->second;
+  launch(c, KI_MISC, [&] {
+    k_seed<D><<<grid1d(NT), 256, 0, c->stream>>>(c->P, orig_at(c, t), b, b + NT * D, b + 2 * NT * D,
+                                                  b + 2 * NT * D + NT * D * D, g, 1);
+  });
+}
+
+// stage the terminal seed (user order AoS -> storage order T) and clear the accumulators
+template <int D>
+mpm_status backward_begin(mpm_ctx c, const float* gx, const float* gv, const float* gF, const float* gC) {
   const KParams& P = c->P;
   const size_t NT = P.NT;
   const int T = c->tape_len;
-  // stage seeds (user order AoS) then permute into storage order T
   float* sx = c->stage;
   float* sv = sx + NT * D;
   float* sF = sv + NT * D;
@@ -394,34 +535,56 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
   if (gv) CK(cudaMemcpyAsync(sv, gv, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
   if (gF) CK(cudaMemcpyAsync(sF, gF, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
   if (gC) CK(cudaMemcpyAsync(sC, gC, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  float* cur = c->gA;
-  float* nxt = c->gB;
+  c->bcur = c->gA;
+  c->bnxt = c->gB;
   launch(c, KI_MISC, [&] {
     k_seed<D><<<grid1d(NT), 256, 0, c->stream>>>(P, orig_at(c, T), gx ? sx : nullptr, gv ? sv : nullptr,
-                                                  gF ? sF : nullptr, gC ? sC : nullptr, cur, 0);
+                                                  gF ? sF : nullptr, gC ? sC : nullptr, c->bcur, 0);
   });
-  auto add_step_seed = [&](int t, float* g) {  // N4: additive seed of state t, if registered
-    auto it = c->seeds.find(t);
-    if (it == c->seeds.end()) return;
-    const float* b = it->second;
-    launch(c, KI_MISC, [&] {
-      k_seed<D><<<grid1d(NT), 256, 0, c->stream>>>(P, orig_at(c, t), b, b + NT * D, b + 2 * NT * D,
-                                                    b + 2 * NT * D + NT * D * D, g, 1);
-    });
-  };
-  add_step_seed(T, cur);
+  add_step_seed<D>(c, T, c->bcur);
   CK(cudaMemsetAsync(c->dmu, 0, NT * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->dlam, 0, NT * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->dmass, 0, NT * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->da, 0, (size_t)P.B * P.T * std::max(P.K, 1) * D * sizeof(float), c->stream));
-  for (int t = T - 1; t >= 0; --t) {
-    launch_backward_step<D>(c, t, cur, nxt);
-    add_step_seed(t, nxt);
-    std::swap(cur, nxt);
+  return MPM_OK;
+}
+
+template <int D>
+void backward_step_end(mpm_ctx c, int t) {
+  add_step_seed<D>(c, t, c->bnxt);
+  std::swap(c->bcur, c->bnxt);
+}
+
+// gradient w.r.t. state 0 is in bcur (storage order 0 = user order)
+mpm_status backward_finish(mpm_ctx c) {
+  if (c->bcur != c->gA)
+    CK(cudaMemcpyAsync(c->gA, c->bcur, (size_t)c->S * c->P.NT * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  return MPM_OK;
+}
+
+size_t da_count(mpm_ctx c) { return (size_t)c->P.B * c->P.T * std::max(c->P.K, 1) * c->D; }
+
+template <int D>
+mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float* gF, const float* gC) {
+  mpm_status s = backward_begin<D>(c, gx, gv, gF, gC);
+  if (s) return s;
+  for (int t = c->tape_len - 1; t >= 0; --t) {
+    backward_phase_a<D>(c, t);
+    if (has_nbr(c)) {
+      s = exchange_nccl(c);
+      if (s) return s;
+    }
+    backward_phase_b<D>(c, t);
+    backward_step_end<D>(c, t);
   }
-  // gradient w.r.t. state 0 now in `cur` (storage order 0 = user order)
-  if (cur != c->gA) CK(cudaMemcpyAsync(c->gA, cur, (size_t)c->S * NT * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
-  mpm_status s = sync_and_check(c, "backward");
+  s = backward_finish(c);
+  if (s) return s;
+  if (c->slab && c->comm && c->P.K > 0) {  // slab mode: the actuation is shared by all slabs
+    const NcclApi* N = nccl_api();
+    ncclResult_t r = N->AllReduce(c->da, c->da, da_count(c), ncclFloat, ncclSum, c->comm, c->stream);
+    if (r != ncclSuccess) return fail(c, MPM_ERR_COMM, std::string("actuation-gradient all-reduce: ") + N->GetErrorString(r));
+  }
+  s = sync_and_check(c, "backward");
   if (s) return s;
   c->has_grad = true;
   c->mass_grad_valid = c->mass_grad;
@@ -482,6 +645,97 @@ mpm_status do_rewind(mpm_ctx c, int t) {
 
 }  // namespace
 
+namespace {
+mpm_status group_check(mpm_ctx* cs, int32_t n) {
+  if (!cs || n < 1) return MPM_ERR_INVALID_ARG;
+  for (int i = 0; i < n; ++i)
+    if (!cs[i]) return MPM_ERR_INVALID_ARG;
+  mpm_ctx c0 = cs[0];
+  for (int i = 0; i < n; ++i) {
+    mpm_ctx c = cs[i];
+    if (!c->has_state) return fail(c, MPM_ERR_CALL_ORDER, "group call before mpm_set_state");
+    if (c->poisoned) return fail(c, MPM_ERR_CALL_ORDER, "context poisoned by an earlier error; call mpm_set_state");
+    if (c->comm) return fail(c, MPM_ERR_CALL_ORDER, "context has a communicator; use mpm_forward/mpm_backward");
+    if (c->cfg.device != c0->cfg.device || c->stream != c0->stream || c->D != c0->D || c->P.res != c0->P.res ||
+        c->tape_len != c0->tape_len)
+      return fail(c, MPM_ERR_INVALID_ARG, "group contexts need one device, one stream, equal dim/res/tape length");
+    if (n > 1 && !c->slab) return fail(c, MPM_ERR_INVALID_ARG, "group contexts need mpm_set_slab");
+    if (c->slab) {
+      const bool want_left = i > 0, want_right = i + 1 < n;
+      if (c->left != want_left || c->right != want_right || (i + 1 < n && (c->x_hi != cs[i + 1]->x_lo ||
+                                                                        c->halo != cs[i + 1]->halo)))
+        return fail(c, MPM_ERR_INVALID_ARG, "group contexts must be adjacent slabs in x order with equal halo");
+    }
+  }
+  return MPM_OK;
+}
+
+template <int D>
+mpm_status group_forward(mpm_ctx* cs, int32_t n, int32_t steps) {
+  for (int k = 0; k < steps; ++k) {
+    const int t = cs[0]->tape_len + k;
+    for (int i = 0; i < n; ++i) forward_phase_a<D>(cs[i], t);
+    if (n > 1) {
+      mpm_status s = exchange_local(cs, n);
+      if (s) return s;
+    }
+    for (int i = 0; i < n; ++i) forward_phase_b<D>(cs[i], t);
+  }
+  mpm_status first = MPM_OK;
+  for (int i = 0; i < n; ++i) {
+    mpm_status s = sync_and_check(cs[i], "group forward");
+    if (s && !first) first = s;
+  }
+  if (first) return first;
+  for (int i = 0; i < n; ++i) cs[i]->tape_len += steps;
+  return MPM_OK;
+}
+
+template <int D>
+mpm_status group_backward(mpm_ctx* cs, int32_t n, const float* const* gx, const float* const* gv,
+                          const float* const* gF, const float* const* gC) {
+  for (int i = 0; i < n; ++i) {
+    mpm_status s = backward_begin<D>(cs[i], gx ? gx[i] : nullptr, gv ? gv[i] : nullptr, gF ? gF[i] : nullptr,
+                                     gC ? gC[i] : nullptr);
+    if (s) return s;
+  }
+  for (int t = cs[0]->tape_len - 1; t >= 0; --t) {
+    for (int i = 0; i < n; ++i) backward_phase_a<D>(cs[i], t);
+    if (n > 1) {
+      mpm_status s = exchange_local(cs, n);
+      if (s) return s;
+    }
+    for (int i = 0; i < n; ++i) {
+      backward_phase_b<D>(cs[i], t);
+      backward_step_end<D>(cs[i], t);
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    mpm_status s = backward_finish(cs[i]);
+    if (s) return s;
+  }
+  mpm_ctx c = cs[0];
+  if (n > 1 && c->P.K > 0) {  // the actuation is shared by all slabs: every context gets the sum
+    const size_t m = da_count(c);
+    for (int i = 1; i < n; ++i)
+      launch(c, KI_MISC, [&] { k_add_inplace<<<c->n_sm, 256, 0, c->stream>>>(m, c->da, cs[i]->da); });
+    for (int i = 1; i < n; ++i)
+      CK(cudaMemcpyAsync(cs[i]->da, c->da, m * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  mpm_status first = MPM_OK;
+  for (int i = 0; i < n; ++i) {
+    mpm_status s = sync_and_check(cs[i], "group backward");
+    if (s && !first) first = s;
+  }
+  if (first) return first;
+  for (int i = 0; i < n; ++i) {
+    cs[i]->has_grad = true;
+    cs[i]->mass_grad_valid = cs[i]->mass_grad;
+  }
+  return MPM_OK;
+}
+}  // namespace
+
 // =====================================================================================
 // ABI
 // =====================================================================================
@@ -537,6 +791,8 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   P.bound = k.bound;
   for (int a = 0; a < 6; ++a) P.fric[a] = k.friction[a];
   P.act_s = k.act_strength;
+  P.slab_lo = 0;
+  P.slab_hi = k.res - 3;
   c->n_tiles = (P.NBT + kScanTile - 1) / kScanTile;
   int occ = 0;
   // dynamic shared memory of the block-tile scatter (payload buffer) above the 48 KB default
@@ -624,6 +880,7 @@ void mpm_destroy(mpm_ctx c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   else cudaDeviceSynchronize();
+  if (c->comm) nccl_api()->CommDestroy(c->comm);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& kv : c->seeds) cudaFree(kv.second);
   for (auto& p : c->pending) {
@@ -660,6 +917,8 @@ mpm_status mpm_forward(mpm_ctx c, int32_t n) {
   if (!c->has_state) return fail(c, MPM_ERR_CALL_ORDER, "mpm_forward before mpm_set_state");
   if (c->poisoned) return fail(c, MPM_ERR_CALL_ORDER, "context poisoned by an earlier error; call mpm_set_state");
   if (c->tape_len + n > c->cfg.max_steps) return fail(c, MPM_ERR_TAPE_FULL, "forward beyond max_steps");
+  if (has_nbr(c) && !c->comm)
+    return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init, or use mpm_group_forward");
   cudaSetDevice(c->cfg.device);
   c->has_grad = false;
   return c->D == 3 ? do_forward<3>(c, n) : do_forward<2>(c, n);
@@ -686,6 +945,8 @@ mpm_status mpm_backward(mpm_ctx c, const float* gx, const float* gv, const float
   if (!c) return MPM_ERR_INVALID_ARG;
   if (!c->has_state) return fail(c, MPM_ERR_CALL_ORDER, "mpm_backward before mpm_set_state");
   if (c->poisoned) return fail(c, MPM_ERR_CALL_ORDER, "context poisoned by an earlier error; call mpm_set_state");
+  if (has_nbr(c) && !c->comm)
+    return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init, or use mpm_group_backward");
   cudaSetDevice(c->cfg.device);
   return c->D == 3 ? do_backward<3>(c, gx, gv, gF, gC) : do_backward<2>(c, gx, gv, gF, gC);
 }
@@ -859,6 +1120,102 @@ mpm_status mpm_grad_mass(mpm_ctx c, float* dmass) {
   cudaSetDevice(c->cfg.device);
   CK(cudaMemcpyAsync(dmass, c->dmass, (size_t)c->P.NT * sizeof(float), cudaMemcpyDefault, c->stream));
   return sync_and_check(c, "grad_mass");
+}
+
+// ---- slab mode ----
+
+mpm_status mpm_set_slab(mpm_ctx c, int32_t x_lo, int32_t x_hi, int32_t halo) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  if (c->has_state) return fail(c, MPM_ERR_CALL_ORDER, "mpm_set_slab must precede mpm_set_state");
+  if (c->slab) return fail(c, MPM_ERR_INVALID_ARG, "slab already set");
+  const KParams& P = c->P;
+  const int BB = c->D == 3 ? Dim<3>::BB : Dim<2>::BB, res = P.res;
+  if (P.B != 1) return fail(c, MPM_ERR_INVALID_ARG, "slab mode needs batch == 1");
+  if (halo < 1) return fail(c, MPM_ERR_INVALID_ARG, "halo_blocks >= 1 required");
+  if (x_lo < 0 || x_hi > res || x_lo >= x_hi || x_lo % BB || x_hi % BB)
+    return fail(c, MPM_ERR_INVALID_ARG, "need 0 <= x_lo < x_hi <= res, both multiples of the block size");
+  const bool left = x_lo > 0, right = x_hi < res;
+  const int hw = halo * BB;
+  if ((left || right) && x_hi - x_lo < 2 * hw)
+    return fail(c, MPM_ERR_INVALID_ARG, "slab narrower than two halo windows (2 * halo_blocks * block size)");
+  if ((left && x_lo < hw) || (right && x_hi + hw > res))
+    return fail(c, MPM_ERR_INVALID_ARG, "halo window outside the domain");
+  cudaSetDevice(c->cfg.device);
+  const int plane = P.nb / P.nbpa;  // blocks per block-plane
+  c->band_blocks = 2 * halo * plane;
+  c->gb_lo = (x_lo / BB - halo) * plane;
+  c->gb_hi = (x_hi / BB - halo) * plane;
+  if (left || right) {
+    const size_t n = (size_t)c->band_blocks * kCPB;
+    mpm_status s = dalloc(c, &c->send_lo, n);
+    if (!s) s = dalloc(c, &c->send_hi, n);
+    if (!s) s = dalloc(c, &c->recv_lo, n);
+    if (!s) s = dalloc(c, &c->recv_hi, n);
+    if (s) return s;
+  }
+  c->slab = true;
+  c->left = left;
+  c->right = right;
+  c->x_lo = x_lo;
+  c->x_hi = x_hi;
+  c->halo = halo;
+  c->P.slab_lo = left ? x_lo - hw : 0;
+  c->P.slab_hi = right ? std::min(x_hi + hw - 3, res - 3) : res - 3;
+  return MPM_OK;
+}
+
+mpm_status mpm_comm_unique_id(char out[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  if (!out) return MPM_ERR_INVALID_ARG;
+  const NcclApi* N = nccl_api();
+  if (!N) return MPM_ERR_COMM;
+  ncclUniqueId id;
+  if (N->GetUniqueId(&id) != ncclSuccess) return MPM_ERR_COMM;
+  memcpy(out, &id, sizeof id);
+  return MPM_OK;
+}
+
+mpm_status mpm_comm_init(mpm_ctx c, int32_t rank, int32_t world, const char id[128]) {
+  if (!c || !id || world < 1 || rank < 0 || rank >= world) return MPM_ERR_INVALID_ARG;
+  if (!c->slab) return fail(c, MPM_ERR_CALL_ORDER, "mpm_comm_init needs mpm_set_slab first");
+  if (c->comm) return fail(c, MPM_ERR_CALL_ORDER, "communicator already initialised");
+  if ((c->left && rank == 0) || (c->right && rank == world - 1))
+    return fail(c, MPM_ERR_INVALID_ARG, "ranks must be ordered by slab (left neighbour = rank - 1)");
+  const NcclApi* N = nccl_api();
+  if (!N) return fail(c, MPM_ERR_COMM, "libnccl.so.2 not found");
+  cudaSetDevice(c->cfg.device);
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof uid);
+  ncclResult_t r = N->CommInitRank(&c->comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    c->comm = nullptr;
+    return fail(c, MPM_ERR_COMM, std::string("ncclCommInitRank: ") + N->GetErrorString(r));
+  }
+  c->rank = rank;
+  c->world = world;
+  return MPM_OK;
+}
+
+mpm_status mpm_group_forward(mpm_ctx* cs, int32_t n, int32_t steps) {
+  mpm_status s = group_check(cs, n);
+  if (s) return s;
+  if (steps < 0) return MPM_ERR_INVALID_ARG;
+  if (cs[0]->tape_len + steps > cs[0]->cfg.max_steps)
+    return fail(cs[0], MPM_ERR_TAPE_FULL, "forward beyond max_steps");
+  for (int i = 0; i < n; ++i)
+    if (cs[i]->tape_len + steps > cs[i]->cfg.max_steps) return fail(cs[i], MPM_ERR_TAPE_FULL, "forward beyond max_steps");
+  cudaSetDevice(cs[0]->cfg.device);
+  for (int i = 0; i < n; ++i) cs[i]->has_grad = false;
+  return cs[0]->D == 3 ? group_forward<3>(cs, n, steps) : group_forward<2>(cs, n, steps);
+}
+
+mpm_status mpm_group_backward(mpm_ctx* cs, int32_t n, const float* const* dLdx, const float* const* dLdv,
+                              const float* const* dLdF, const float* const* dLdC) {
+  mpm_status s = group_check(cs, n);
+  if (s) return s;
+  cudaSetDevice(cs[0]->cfg.device);
+  return cs[0]->D == 3 ? group_backward<3>(cs, n, dLdx, dLdv, dLdF, dLdC)
+                       : group_backward<2>(cs, n, dLdx, dLdv, dLdF, dLdC);
 }
 
 }  // extern "C"

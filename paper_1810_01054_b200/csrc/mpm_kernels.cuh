@@ -41,7 +41,7 @@ constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks us
 constexpr int kScanTile = kThreads;  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
 
-enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6 };
+enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6, E_SLAB = 9 };
 
 template <int D> struct Dim;
 template <> struct Dim<3> {
@@ -61,6 +61,7 @@ struct KParams {
   float act_s;
   int slots_per_step;                       // per-step cap of touched blocks
   int arena_slots;                          // capacity of the tape grid arena
+  int slab_lo, slab_hi;                     // allowed base_x range (inclusive); slab mode
 };
 
 // Per-step bookkeeping record, info[t * kInfo + field]
@@ -372,20 +373,21 @@ __device__ __forceinline__ void warp_hist_add(int* cnt, int gb, bool valid) {
 // key of a particle from its fp32 position (north_star item 1, R17); returns false when
 // the base index is outside [0, res-3] (R14).
 template <int D>
-__device__ __forceinline__ bool key_of(const float* x, int r, const KParams& P, int& gb, int& key) {
+__device__ __forceinline__ int key_of(const float* x, int r, const KParams& P, int& gb, int& key) {
   int blk[D], cell[D];
-  bool ok = true;
+  bool ok = true, in_slab = true;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     int b = base_of(x[a], P.fres);
     ok &= (b >= 0) & (b <= P.res - 3);
+    if (a == 0) in_slab = (b >= P.slab_lo) & (b <= P.slab_hi);
     b = min(max(b, 0), P.res - 3);  // keep the bookkeeping in range; the error is latched
     blk[a] = b >> Dim<D>::LOG_BB;
     cell[a] = b & (Dim<D>::BB - 1);
   }
   gb = r * P.nb + block_lin<D>(blk, P.nbpa);
   key = gb * kCPB + cell_lin<D>(cell);
-  return ok;
+  return !ok ? E_DOMAIN : (!in_slab ? E_SLAB : E_OK);
 }
 
 // ------------------------------------------------------------------------------------
@@ -435,7 +437,7 @@ __global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __rest
     float x[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = st[(size_t)comp_x<D>(a) * P.NT + j];
-    if (!key_of<D>(x, j / P.N, P, gb, k)) latch(err, E_DOMAIN, 0, j);
+    if (const int e = key_of<D>(x, j / P.N, P, gb, k)) latch(err, e, 0, j);
     key[j] = k;
     orig[j] = j;
   }
@@ -1202,7 +1204,7 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
       }
       A.orig_next[k] = u;
       int gbn, key;
-      if (!key_of<D>(x, r, P, gbn, key)) latch(A.err, E_DOMAIN, A.t + 1, u);
+      if (const int e = key_of<D>(x, r, P, gbn, key)) latch(A.err, e, A.t + 1, u);
       A.key_next[k] = key;
       // block histogram of step t+1 (threads of a warp mostly share one block)
       const unsigned am = __activemask();
@@ -1535,6 +1537,55 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
     }
     __syncthreads();
   }
+}
+
+// ------------------------------------------------------------------------------------
+// Slab mode.  A rank owns the particles of one x-slab; the only nodes two ranks
+// can both touch lie in a window of block-planes around each slab boundary, and the only
+// exchange is the symmetric sum of those windows (after P2G in the forward, after G2P^T in
+// the backward).  Block-linear order has axis 0 slowest, so a window of block-planes
+// [bx0, bx0 + nwp) is the contiguous block range [bx0 nbpa^(D-1), (bx0 + nwp) nbpa^(D-1)).
+// pack: window blocks -> dense buffer (0 where this rank has no slot); unpack: grid += buffer
+// where this rank has a slot (a node it never reads needs no value).  Both ranks add the
+// same two partial sums, so their copies of a window node are bitwise equal.
+// grid index of slot s = (s - sub) * 64 + l, sub = 0 (tape arena) or the step base (adjoint).
+// ------------------------------------------------------------------------------------
+__global__ void k_band_pack(int nblk, int gb_lo, int gb_hi, const int* __restrict__ slot_of,
+                            const int* __restrict__ info_t, int adj, const float4* __restrict__ g,
+                            float4* __restrict__ out_lo, float4* __restrict__ out_hi) {
+  const int sub = adj ? info_t[I_BASE] : 0;
+  const int n = nblk * kCPB;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += gridDim.x * blockDim.x) {
+    const bool hi = i >= n;
+    float4* out = hi ? out_hi : out_lo;
+    if (!out) continue;
+    const int e = hi ? i - n : i;
+    const int s = __ldg(&slot_of[(hi ? gb_hi : gb_lo) + e / kCPB]);
+    out[e] = s >= 0 ? g[(size_t)(s - sub) * kCPB + e % kCPB] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+__global__ void k_band_unpack(int nblk, int gb_lo, int gb_hi, const int* __restrict__ slot_of,
+                              const int* __restrict__ info_t, int adj, float4* __restrict__ g,
+                              const float4* __restrict__ in_lo, const float4* __restrict__ in_hi) {
+  const int sub = adj ? info_t[I_BASE] : 0;
+  const int n = nblk * kCPB;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += gridDim.x * blockDim.x) {
+    const bool hi = i >= n;
+    const float4* in = hi ? in_hi : in_lo;
+    if (!in) continue;
+    const int e = hi ? i - n : i;
+    const int s = __ldg(&slot_of[(hi ? gb_hi : gb_lo) + e / kCPB]);
+    if (s < 0) continue;
+    float4& q = g[(size_t)(s - sub) * kCPB + e % kCPB];
+    const float4 r = in[e];
+    q = make_float4(q.x + r.x, q.y + r.y, q.z + r.z, q.w + r.w);
+  }
+}
+
+__global__ void k_add_inplace(size_t n, float* __restrict__ a, const float* __restrict__ b) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    a[i] += b[i];
 }
 
 // ------------------------------------------------------------------------------------

@@ -21,14 +21,15 @@ LIB_PATH = os.path.join(_HERE, "libmpm.so")
 
 STATUS = {0: "MPM_OK", 1: "MPM_ERR_INVALID_ARG", 2: "MPM_ERR_OOM", 3: "MPM_ERR_CUDA",
           4: "MPM_ERR_OUT_OF_DOMAIN", 5: "MPM_ERR_INVERTED", 6: "MPM_ERR_TAPE_FULL",
-          7: "MPM_ERR_CALL_ORDER", 8: "MPM_ERR_COMM"}
+          7: "MPM_ERR_CALL_ORDER", 8: "MPM_ERR_COMM", 9: "MPM_ERR_OUT_OF_SLAB"}
 
 # every symbol include/mpm.h declares
 EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "mpm_forward",
            "mpm_tape_length", "mpm_rewind", "mpm_get_state", "mpm_backward", "mpm_grad",
            "mpm_last_error", "mpm_get_binning", "mpm_get_grid", "mpm_set_profiling",
            "mpm_get_profile", "mpm_launch_count", "mpm_get_step_info", "mpm_grad_mass",
-           "mpm_add_seed", "mpm_clear_seeds", "mpm_enable_mass_grad")
+           "mpm_add_seed", "mpm_clear_seeds", "mpm_enable_mass_grad", "mpm_set_slab",
+           "mpm_comm_unique_id", "mpm_comm_init", "mpm_group_forward", "mpm_group_backward")
 
 
 class MPMError(RuntimeError):
@@ -83,6 +84,11 @@ def load():
     L.mpm_clear_seeds.argtypes = [vp]
     L.mpm_launch_count.argtypes = [vp]
     L.mpm_launch_count.restype = i64
+    L.mpm_set_slab.argtypes = [vp, i32, i32, i32]
+    L.mpm_comm_unique_id.argtypes = [C.c_char_p]
+    L.mpm_comm_init.argtypes = [vp, i32, i32, C.c_char_p]
+    L.mpm_group_forward.argtypes = [C.POINTER(vp), i32, i32]
+    L.mpm_group_backward.argtypes = [C.POINTER(vp), i32] + [C.POINTER(vp)] * 4
     for name in EXPORTS:
         getattr(L, name)
     _lib = L
@@ -257,6 +263,16 @@ class MPM:
     def clear_seeds(self):
         self._check(self.L.mpm_clear_seeds(self.h))
 
+    # -- slab mode -----------------------------------------------------------
+    def set_slab(self, x_lo: int, x_hi: int, halo_blocks: int = 1):
+        """This context simulates the x-slab [x_lo, x_hi) of node planes (before set_state)."""
+        self._check(self.L.mpm_set_slab(self.h, int(x_lo), int(x_hi), int(halo_blocks)))
+
+    def comm_init(self, rank: int, world: int, uid: bytes):
+        """Join the NCCL halo-exchange communicator (ranks ordered by slab; collective)."""
+        assert len(uid) == 128
+        self._check(self.L.mpm_comm_init(self.h, int(rank), int(world), uid))
+
     # -- introspection -------------------------------------------------------------------
     def get_binning(self, t: int):
         cfg = self.cfg
@@ -301,3 +317,50 @@ class MPM:
     @property
     def launches(self) -> int:
         return int(self.L.mpm_launch_count(self.h))
+
+
+def comm_unique_id() -> bytes:
+    """128-byte NCCL unique id for mpm_comm_init (create on one rank, broadcast to all)."""
+    L = load()
+    buf = C.create_string_buffer(128)
+    rc = L.mpm_comm_unique_id(buf)
+    if rc != 0:
+        raise MPMError(rc, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def _group_check(sims, rc):
+    if rc != 0:
+        msgs = [s.L.mpm_last_error(s.h).decode() for s in sims]
+        raise MPMError(rc, " | ".join(m for m in msgs if m) or "group call failed")
+
+
+def _handles(sims):
+    return (C.c_void_p * len(sims))(*[s.h.value for s in sims])
+
+
+def group_forward(sims, n_steps: int):
+    """Advance adjacent slab contexts of one process in lockstep (single-GPU slab emulation)."""
+    L = load()
+    _group_check(sims, L.mpm_group_forward(_handles(sims), len(sims), int(n_steps)))
+
+
+def group_backward(sims, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
+    """Reverse mode over adjacent slab contexts; seeds are lists (one array per context)."""
+    L = load()
+    keep = []
+
+    def arr(seeds, shape_of):
+        if seeds is None:
+            return None
+        ptrs = []
+        for s, a in zip(sims, seeds):
+            a = _in(a, np.float32, shape_of(s))
+            keep.append(a)
+            ptrs.append(_ptr(a))
+        return (C.c_void_p * len(sims))(*ptrs)
+
+    vec = lambda s: (s.NT, s.cfg.dim)
+    mat = lambda s: (s.NT, s.cfg.dim, s.cfg.dim)
+    args = [arr(dLdx, vec), arr(dLdv, vec), arr(dLdF, mat), arr(dLdC, mat)]
+    _group_check(sims, L.mpm_group_backward(_handles(sims), len(sims), *args))

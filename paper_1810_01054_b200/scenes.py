@@ -165,7 +165,7 @@ def quadruped_3d(seed=0, batch=1, steps=200, e_scale=False):
                  Es, nus, aids, acts)
 
 
-def slab_3d(seed=0, batch=1, steps=100, cells=(64, 32, 64), res=128, y0=5):
+def slab_3d(seed=0, batch=1, steps=100, cells=(64, 32, 64), res=128, y0=5, dt=1e-4, name="C4_slab3d"):
     """C4 (configs[3]): 3D 128^3 falling neo-Hookean slab of 64x32x64 cells (x, y, z),
     1,048,576 particles, v0 = (0, -1, 0); K = 8 octant actuators, sinusoidal."""
     dim, K = 3, 8
@@ -189,8 +189,15 @@ def slab_3d(seed=0, batch=1, steps=100, cells=(64, 32, 64), res=128, y0=5):
         xs.append(x); vs.append(v); Fs.append(_identity(n, dim))
         Cs.append(np.zeros((n, dim, dim), np.float32)); ms.append(m); vols.append(vol)
         Es.append(E); nus.append(nu); aids.append(oct_id); acts.append(a)
-    return _pack("C4_slab3d", dim, res, 1e-4, steps, K, 100.0, xs, vs, Fs, Cs, ms, vols, Es,
+    return _pack(name, dim, res, dt, steps, K, 100.0, xs, vs, Fs, Cs, ms, vols, Es,
                  nus, aids, acts)
+
+
+def slab_c5a(seed=0, steps=100):
+    """C5a (configs[4]): 3D 256^3 slab of 240x32x136 cells, 8,355,840 particles,
+    dt = 5e-5, the C4 recipe otherwise; sharded by x-slab across GPUs."""
+    return slab_3d(seed=seed, steps=steps, cells=(240, 32, 136), res=256, y0=10, dt=5e-5,
+                   name="C5a_slab3d")
 
 
 def tiny(dim, seed=0, n_cells=None, res=None, steps=10, perturb=True, gravity=None,

@@ -65,3 +65,80 @@ def test_gloo_world2_sharded_rollouts_and_shared_grad():
     assert t0 == t1 == 15.0
     assert m0 == m1 == 20.0
     assert e0 == 0.0 and e1 == 0.0
+
+
+# ---- slab sharding (SURVEY 8e, configs[4]) -------------------------------------------------
+
+@pytest.mark.parametrize("dim,res,G,halo", [(3, 64, 2, 1), (3, 64, 3, 1), (3, 256, 8, 1), (2, 128, 4, 1),
+                                            (3, 128, 4, 2), (2, 64, 3, 1)])
+def test_slab_partition_properties(dim, res, G, halo):
+    """Block-aligned, covering, every slab >= 2*halo blocks wide (libmpm's window rule),
+    balanced to within one block-plane of particles, membership disjoint and complete."""
+    rng = np.random.default_rng(dim * 100 + G)
+    n = 20000
+    x = rng.uniform(0.1, 0.7, (n, dim)).astype(np.float32)
+    x[:, 0] = (0.15 + 0.6 * rng.beta(2.0, 5.0, n)).astype(np.float32)  # skewed in x
+    b = parallel.slab_partition(x, res, dim, G, halo)
+    BB = parallel.block_size(dim)
+    assert b[0][0] == 0 and b[-1][1] == res and len(b) == G
+    for (lo, hi), (lo2, _) in zip(b, b[1:] + [(res, None)]):
+        assert lo % BB == 0 and hi % BB == 0 and hi == lo2
+        assert hi - lo >= 2 * halo * BB
+    idx = [parallel.slab_members(x, res, lo, hi) for lo, hi in b]
+    allidx = np.sort(np.concatenate(idx))
+    np.testing.assert_array_equal(allidx, np.arange(n))
+    bx = parallel.base_x(x, res)
+    plane = np.bincount(np.clip(bx, 0, res - 1) // BB, minlength=res // BB).max()
+    counts = [len(i) for i in idx]
+    if all(hi - lo > 2 * halo * BB for lo, hi in b):  # the width rule did not bind
+        assert max(counts) - n / G <= plane + 1, counts
+
+
+def test_slab_partition_infeasible():
+    x = np.full((10, 3), 0.5, np.float32)
+    with pytest.raises(ValueError):
+        parallel.slab_partition(x, 32, 3, 5, 1)  # 8 block-planes cannot hold 5 slabs of 2
+
+
+def _slab_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import torch
+    import torch.distributed as dist
+    d = parallel.init_from_env("gloo")
+    sc = scenes.quadruped_3d(steps=4)
+    bounds = parallel.slab_partition(sc.x[0], sc.res, sc.dim, d.world)
+    lo, hi = bounds[d.rank]
+    mine, idx = parallel.shard_slab(sc, lo, hi)
+    cnt = torch.tensor([mine.n], dtype=torch.int64)
+    dist.all_reduce(cnt)
+    # every rank derived the same partition
+    allb = [None] * world
+    dist.all_gather_object(allb, bounds)
+    owned = torch.zeros(sc.n, dtype=torch.int64)
+    owned[torch.as_tensor(idx)] = 1
+    dist.all_reduce(owned)
+    q.put((rank, lo, hi, int(cnt.item()), sc.n, all(b == bounds for b in allb),
+           int(owned.min()), int(owned.max()), float(np.abs(mine.x[0] - sc.x[0][idx]).max())))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_slab_partition_agrees():
+    """Each rank computes its slab and particles from the shared scene; the union over ranks
+    owns every particle exactly once and all ranks derived the same slab bounds."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_slab_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, lo0, hi0, c0, n0, same0, mn0, mx0, e0), (r1, lo1, hi1, c1, n1, same1, mn1, mx1, e1) = res
+    assert lo0 == 0 and hi0 == lo1 and hi1 == 64
+    assert c0 == c1 == n0 == n1
+    assert same0 and same1 and mn0 == mx0 == 1 and e0 == 0.0 and e1 == 0.0
