@@ -11,8 +11,11 @@ reverse-mode step (G2P^T, grid^T, P2G^T) -- every row of SURVEY 8(a).  K steps =
 steps onto the tape, then the backward pass over those K steps (loss: final CoM x).
 Multi-GPU: each rank runs its own independent C4 rollout (weak scaling, no data-path
 collective); the barrier / max-over-ranks timing uses torch.distributed.
+--workload C5b: 64 quadruped rollouts sharded over ranks (strong scaling, no collective).
+--workload C5a: ONE 8,355,840-particle slab at 256^3 sharded by x-slab (strong scaling; the
+grid windows at slab boundaries are summed with NCCL send/recv inside libmpm every step).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C4|C5a|C5b]
 """
 from __future__ import annotations
 
@@ -38,24 +41,38 @@ WORKLOADS = {
            "forward+backward, loss = final CoM x; one rollout per rank"),
     "C5b": ("C5b (configs[4] batch part): 64 independent 3D 64^3 quadruped rollouts "
             "(29,952 particles each, per-rollout actuation phase and E scale), sharded over ranks"),
+    "C5a": ("C5a (configs[4] slab part): one 3D 256^3 slab of 240x32x136 cells, 8,355,840 particles, "
+            "dt = 5e-5, forward+backward, loss = final CoM x; x-slab sharded over ranks with halo "
+            "window exchange"),
 }
 SEG = 200  # max steps per tape segment (tape memory ~ 100 MB per step at C4)
 
 
-def _cfg_dict(K, W, n_gpus, sc, workload="C4"):
+def _cfg_dict(K, W, n_gpus, sc, workload="C4", slabs=None):
+    par = "single GPU"
+    if n_gpus > 1:
+        par = (f"x-slab sharded x{n_gpus}, slabs {slabs}, NCCL halo-window sums" if workload == "C5a"
+               else f"rollout-sharded x{n_gpus} (no data-path collective)")
     return {"workload": WORKLOADS[workload], "particles_per_rank": int(sc.batch * sc.n),
             "rollouts_per_rank": int(sc.batch), "grid": f"{sc.res}^3", "dim": 3, "dt": sc.dt,
-            "steps_per_pass": K, "warmup": W,
-            "parallelism": f"rollout-sharded x{n_gpus} (no data-path collective)" if n_gpus > 1 else "single GPU",
+            "steps_per_pass": K, "warmup": W, "parallelism": par,
             "l2": (f"inputs larger than L2: per-step state {sc.batch * sc.n * 96 / 2**20:.0f} MiB read + written, "
                    f"tape of K states")}
 
 
 def make_scene(workload, rank, world, tape):
+    """(this rank's scene, total particles of the job, slab bounds or None, total mass per
+    rollout for the CoM seed or None)."""
     if workload == "C4":
-        return scenes.slab_3d(seed=rank, steps=tape)
+        sc = scenes.slab_3d(seed=rank, steps=tape)
+        return sc, sc.n * world, None, None
+    if workload == "C5a":
+        full = scenes.slab_c5a(seed=0, steps=tape)
+        bounds = parallel.slab_partition(full.x[0], full.res, full.dim, world)
+        sc, _ = parallel.shard_slab(full, *bounds[rank])
+        return sc, full.n, bounds, float(full.mass.astype(np.float64).sum())
     full = scenes.quadruped_3d(seed=0, batch=64, steps=tape, e_scale=True)
-    return parallel.shard_scene(full, parallel.Dist(rank, world))
+    return parallel.shard_scene(full, parallel.Dist(rank, world)), 64 * full.n, None, None
 
 
 # ---------------------------------------------------------------------------------------
@@ -152,13 +169,18 @@ def run_ours(args):
     K, W = args.steps, args.warmup
     seg = min(K, SEG)
     tape = max(seg, min(W, SEG), 1)
-    sc = make_scene(args.workload, rank, world, tape)
+    sc, total_particles, slabs, mtot = make_scene(args.workload, rank, world, tape)
     stream = torch.cuda.current_stream(dev)
     sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=tape, device=dev.index, stream=stream.cuda_stream))
+    if slabs is not None:
+        sim.set_slab(*slabs[rank], 1)
+        if world > 1:
+            parallel.init_slab_comm(sim, D)
     NT = sc.batch * sc.n
     m = torch.tensor(sc.mass, device=dev, dtype=torch.float64)  # [B][N]
     seed = torch.zeros((NT, 3), device=dev, dtype=torch.float32)
-    seed[:, 0] = (m / m.sum(dim=1, keepdim=True)).reshape(-1).float()  # CoM_x of each rollout
+    msum = m.sum(dim=1, keepdim=True) if mtot is None else mtot  # whole-body mass in slab mode
+    seed[:, 0] = (m / msum).reshape(-1).float()  # CoM_x of each rollout
     sim.set_scene(sc)
 
     def barrier():
@@ -196,7 +218,6 @@ def run_ours(args):
     fwd_ms = e0.elapsed_time(fwd_ev[0]) if len(fwd_ev) == 1 else None
     ms = parallel.max_over_ranks(ms, D, dev)
     fwd_ms = parallel.max_over_ranks(fwd_ms, D, dev) if fwd_ms is not None else None
-    total_particles = NT * world if args.workload == "C4" else 64 * sc.n
     value = total_particles * K / (ms / 1e3)
 
     # roofline: per-kernel CUDA-event times of a second, profiled pass of the same K steps
@@ -267,13 +288,19 @@ def run_ours(args):
             "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "weak" if args.workload == "C4" else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded jittered-lattice slab)",
-            "config": _cfg_dict(K, W, world, sc, args.workload),
+            "config": _cfg_dict(K, W, world, sc, args.workload, slabs),
             "fwd": {"value": (total_particles * K / (fwd_ms / 1e3)) if fwd_ms else None,
                     "ms_per_step": (fwd_ms / K) if fwd_ms else None},
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline_full(sc if args.workload == "C4" else scenes.quadruped_3d(steps=1))
+        if args.workload == "C4":
+            line["cpu_baseline"] = cpu_baseline_full(sc)
+        elif args.workload == "C5a":  # bounded sample: a 1M-particle sub-slab at the same res/density
+            line["cpu_baseline"] = cpu_baseline_full(
+                scenes.slab_3d(steps=1, cells=(64, 32, 64), res=256, y0=10, dt=5e-5), "C5a sub-slab 64x32x64 cells")
+        else:
+            line["cpu_baseline"] = cpu_baseline_full(scenes.quadruped_3d(steps=1), "one C3 quadruped rollout")
     sim.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -301,13 +328,13 @@ def _oracle_fb(sc, n_steps):
     return t1 - t0, t2 - t0
 
 
-def cpu_baseline_full(sc):
-    """The oracle as it stands (fp64, single thread) on the full C4 state: 1 forward + 1
-    backward step (~10-30 s of CPU work)."""
+def cpu_baseline_full(sc, what="full C4 state"):
+    """The oracle as it stands (fp64, single thread): 1 forward + 1 backward step of the
+    given state (~10-30 s of CPU work)."""
     f, fb = _oracle_fb(sc, 1)
     n = sc.batch * sc.n
     return {"value": n / fb, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"full C4 state ({n} particles), 1 forward + 1 backward step, fp64, 1 thread; "
+            "sample": f"{what} ({n} particles), 1 forward + 1 backward step, fp64, 1 thread; "
                       f"forward alone {n / f:.4g} particle-steps/s"}
 
 

@@ -1,9 +1,16 @@
 """Key counters per captured kernel from an ncu report (--page raw --csv):
-  python tools/ncu_summary.py gpurun_out/prof.ncu-rep"""
+  python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--traffic-json profiles/ncu_traffic.json]
+--traffic-json writes dram__bytes_read.sum + dram__bytes_write.sum per launch (mean over the
+captured launches of each kernel), keyed by bench.py's kernel names (roofline "traffic")."""
 import csv
 import io
+import json
 import subprocess
 import sys
+
+BENCH_NAME = {"k_block_scatter<3, 0>": "p2g", "k_block_scatter<3, 1>": "g2p_T", "k_g2p<3>": "g2p",
+              "k_p2g_adj<3, 0>": "p2g_T", "k_p2g_adj<3, 1>": "p2g_T_massgrad", "k_grid_adj<3>": "grid_T",
+              "k_scan_a<3>": "scan_a", "k_scan_b": "scan_b", "k_scan_c": "scan_c", "k_scatter": "scatter"}
 
 KEYS = [
     ("time_us", "gpu__time_duration.sum", "us"),
@@ -37,10 +44,11 @@ def _scale(sc, unit):
     return sc
 
 
-def main(rep):
+def main(rep, traffic_json=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
+    traffic = {}
     stall = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
              and h.endswith("_per_issue_active.ratio")]
     for r in rows[2:]:
@@ -50,11 +58,22 @@ def main(rep):
             if key in hdr and r[hdr.index(key)] not in ("", "n/a"):
                 i = hdr.index(key)
                 out.append(f"{short}={float(r[i].replace(',', '')) * _scale(sc, units[i]):.4g}")
+        try:
+            b = sum(float(r[hdr.index(k)].replace(",", "")) * TO_MB.get(units[hdr.index(k)], 1.0) * 1e6
+                    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            traffic.setdefault(BENCH_NAME.get(name, name), []).append(b)
+        except (ValueError, IndexError):
+            pass
         st = sorted(((hdr[i][34:-27], float(r[i] or 0)) for i in stall), key=lambda x: -x[1])[:5]
         print(name)
         print("   " + " ".join(out))
         print("   stalls: " + " ".join(f"{k}={v:.2f}" for k, v in st))
+    if traffic_json:
+        per = {k: round(sum(v) / len(v)) for k, v in traffic.items()}
+        json.dump({"source": rep, "per_launch_dram_bytes": per,
+                   "captured_launches": {k: len(v) for k, v in traffic.items()}}, open(traffic_json, "w"), indent=1)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    tj = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
+    main(sys.argv[1], tj)
