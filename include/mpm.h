@@ -137,6 +137,21 @@ mpm_status mpm_clear_seeds(mpm_ctx ctx);
 
 const char* mpm_last_error(mpm_ctx ctx);
 
+/* ---- NEXT N1: closed-loop controller embedded in P2G (Fig. 2 caption P:84) ----
+ * With a controller set, every forward step t first computes, per rollout,
+ *   z_t = [target (d), CoM_k (d) for k < K, V_k (d) for k < K]   (length nz = d (1 + 2K)),
+ *   CoM_k / V_k = mass-weighted mean position / velocity of the particles with actuator_id k
+ *   (the "composed soft components" of P:279, DESIGN R20), and
+ *   a_t = tanh(W z_t + b)  -> the actuation of step t ([K][d], sigma_pa = s Diag(a), R4),
+ * overwriting that step of the mpm_set_actuation buffer.  mpm_backward then adds the
+ * controller's closed-loop terms to dL/dx_p, dL/dv_p of every state and accumulates
+ * dL/dW, dL/db, dL/dtarget (summed over steps and rollouts), read by mpm_grad_controller.
+ * W: [K*d][nz] row-major, b: [K*d], target: [d]; host or device pointers, copied.
+ * Needs mpm_set_state first (group masses), n_actuators >= 1, every group non-empty in
+ * every rollout (MPM_ERR_INVALID_ARG), no slab neighbours.  W = NULL switches it off.      */
+mpm_status mpm_set_controller(mpm_ctx ctx, const float* W, const float* b, const float* target);
+mpm_status mpm_grad_controller(mpm_ctx ctx, float* dW, float* db, float* dtarget);
+
 /* ---- slab mode: one large rollout sharded by x-slab (configs[4] "8M particles
  * slab-sharded") ----
  * A context simulates the particles of one x-slab [x_lo, x_hi) of node planes (ownership

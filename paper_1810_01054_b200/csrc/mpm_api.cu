@@ -21,11 +21,11 @@ namespace {
 
 enum KernelId {
   KI_SCAN_A, KI_SCAN_B, KI_SCAN_C, KI_SCATTER, KI_P2G, KI_GRID, KI_G2P,
-  KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC, KI_BANDP, KI_BANDU, KI_COUNT
+  KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC, KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_COUNT
 };
 const char* kKernelNames[KI_COUNT] = {"scan_a", "scan_b", "scan_c",  "scatter", "p2g",  "grid_update",
                                       "g2p",    "zero_adj", "g2p_T", "grid_T", "p2g_T", "misc",
-                                      "band_pack", "band_unpack"};
+                                      "band_pack", "band_unpack", "ctrl", "ctrl_T"};
 
 struct PendingEvent {
   cudaEvent_t a, b;
@@ -125,6 +125,13 @@ struct mpm_ctx_s {
   float4 *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  // NEXT N1 controller: a_t = tanh(W z_t + b)
+  bool ctrl = false, ctrl_grad_valid = false;
+  float *ctrl_W = nullptr, *ctrl_b = nullptr, *ctrl_target = nullptr, *ctrl_Minv = nullptr, *ctrl_acc = nullptr;
+  int* ctrl_cnt = nullptr;
+  float *ctrl_M = nullptr, *ztape = nullptr, *gpre_tape = nullptr, *ctrl_gz = nullptr;
+  int* ctrl_n = nullptr;
+  float *ctrl_gW = nullptr, *ctrl_gb = nullptr, *ctrl_gt = nullptr;
   float* bcur = nullptr;  // backward: adjoint of the current step (storage order)
   float* bnxt = nullptr;
   // profiling
@@ -369,6 +376,13 @@ mpm_status exchange_local(mpm_ctx* cs, int n) {
 template <int D>
 void forward_phase_a(mpm_ctx c, int t) {
   const KParams& P = c->P;
+  if (c->ctrl)  // N1: a_t = tanh(W z_t + b) from state t, before P2G reads act[t]
+    launch(c, KI_CTRL, [&] {
+      k_ctrl_observe<D><<<c->n_sm * 4, 256, 0, c->stream>>>(P, state_at(c, t), orig_at(c, t), c->prm, c->aid,
+                                                             c->ctrl_acc, c->ctrl_cnt, c->ctrl_W, c->ctrl_b,
+                                                             c->ctrl_target, c->ctrl_Minv, c->act,
+                                                             c->ztape + (size_t)t * P.B * P.nz, t);
+    });
   launch_bin<D>(c, t);
   StepArgs A = step_args(c, t);
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
@@ -421,9 +435,46 @@ void backward_phase_b(mpm_ctx c, int t) {
     launch(c, KI_P2GT, [&] { k_p2g_adj<D, true><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
   else
     launch(c, KI_P2GT, [&] { k_p2g_adj<D, false><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
+  if (c->ctrl) {  // N1: controller adjoint of step t (needs this step's complete dL/da)
+    const int KD = P.K * D;
+    launch(c, KI_CTRLT, [&] {
+      k_ctrl_adj_param<D><<<P.B, 256, KD * sizeof(float), c->stream>>>(P, c->da, c->act, c->ctrl_W,
+                                                                       c->gpre_tape + (size_t)t * P.B * KD,
+                                                                       c->ctrl_gz, t);
+    });
+    launch(c, KI_CTRLT, [&] {
+      k_ctrl_adj_state<D><<<c->n_sm * 4, 256, 0, c->stream>>>(P, c->ctrl_gz, orig_at(c, t), c->prm, c->aid,
+                                                              c->ctrl_Minv, c->bnxt);
+    });
+  }
 }
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+// N1: group masses M[r][k] of the current particles -> 1/M (every group must be non-empty)
+mpm_status ctrl_masses(mpm_ctx c) {
+  const KParams& P = c->P;
+  const int BK = P.B * P.K;
+  CK(cudaMemsetAsync(c->ctrl_M, 0, BK * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->ctrl_n, 0, BK * sizeof(int), c->stream));
+  launch(c, KI_MISC, [&] { k_ctrl_mass<<<c->n_sm * 2, 256, 0, c->stream>>>(P.NT, P.N, P.K, c->prm, c->aid, c->ctrl_M, c->ctrl_n); });
+  std::vector<float> M(BK);
+  std::vector<int> n(BK);
+  CK(cudaMemcpyAsync(M.data(), c->ctrl_M, BK * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(n.data(), c->ctrl_n, BK * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < BK; ++i) {
+    if (n[i] == 0 || !(M[i] > 0.f))
+      return fail(c, MPM_ERR_INVALID_ARG, "controller: actuator group " + std::to_string(i % P.K) + " of rollout " +
+                                              std::to_string(i / P.K) + " is empty");
+    M[i] = 1.f / M[i];
+  }
+  CK(cudaMemcpyAsync(c->ctrl_Minv, M.data(), BK * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->ctrl_acc, 0, (size_t)BK * 2 * c->D * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->ctrl_cnt, 0, sizeof(int), c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return MPM_OK;
+}
 
 template <int D>
 mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* F, const float* C,
@@ -484,6 +535,13 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   CK(cudaMemcpy(&bad, c->dbad, sizeof(int), cudaMemcpyDeviceToHost));
   if (s) return s;
   if (bad) return fail(c, MPM_ERR_INVALID_ARG, "parameters out of range (need mass > 0, vol > 0, E > 0, 0 <= nu < 0.5)");
+  if (c->ctrl) {  // new particles: new group masses
+    s = ctrl_masses(c);
+    if (s) {
+      c->ctrl = false;
+      return s;
+    }
+  }
   c->tape_len = 0;
   c->has_state = true;
   c->has_grad = false;
@@ -555,10 +613,22 @@ void backward_step_end(mpm_ctx c, int t) {
   std::swap(c->bcur, c->bnxt);
 }
 
-// gradient w.r.t. state 0 is in bcur (storage order 0 = user order)
+// gradient w.r.t. state 0 is in bcur (storage order 0 = user order); controller parameter
+// gradients reduced over steps and rollouts
 mpm_status backward_finish(mpm_ctx c) {
   if (c->bcur != c->gA)
     CK(cudaMemcpyAsync(c->gA, c->bcur, (size_t)c->S * c->P.NT * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+  if (c->ctrl) {
+    const int T = c->tape_len;
+    launch(c, KI_CTRLT, [&] {
+      if (c->D == 3)
+        k_ctrl_adj_reduce<3><<<c->n_sm, 128, 0, c->stream>>>(c->P, T, c->gpre_tape, c->ztape, c->ctrl_W, c->ctrl_gW,
+                                                            c->ctrl_gb, c->ctrl_gt);
+      else
+        k_ctrl_adj_reduce<2><<<c->n_sm, 128, 0, c->stream>>>(c->P, T, c->gpre_tape, c->ztape, c->ctrl_W, c->ctrl_gW,
+                                                            c->ctrl_gb, c->ctrl_gt);
+    });
+  }
   return MPM_OK;
 }
 
@@ -588,6 +658,7 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
   if (s) return s;
   c->has_grad = true;
   c->mass_grad_valid = c->mass_grad;
+  c->ctrl_grad_valid = c->ctrl;
   return MPM_OK;
 }
 
@@ -731,6 +802,7 @@ mpm_status group_backward(mpm_ctx* cs, int32_t n, const float* const* gx, const 
   for (int i = 0; i < n; ++i) {
     cs[i]->has_grad = true;
     cs[i]->mass_grad_valid = cs[i]->mass_grad;
+    cs[i]->ctrl_grad_valid = cs[i]->ctrl;
   }
   return MPM_OK;
 }
@@ -1216,6 +1288,67 @@ mpm_status mpm_group_backward(mpm_ctx* cs, int32_t n, const float* const* dLdx, 
   cudaSetDevice(cs[0]->cfg.device);
   return cs[0]->D == 3 ? group_backward<3>(cs, n, dLdx, dLdv, dLdF, dLdC)
                        : group_backward<2>(cs, n, dLdx, dLdv, dLdF, dLdC);
+}
+
+// ---- NEXT N1: closed-loop controller ----
+
+mpm_status mpm_set_controller(mpm_ctx c, const float* W, const float* b, const float* target) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  cudaSetDevice(c->cfg.device);
+  if (!W) {
+    c->ctrl = false;
+    return MPM_OK;
+  }
+  if (!b || !target) return fail(c, MPM_ERR_INVALID_ARG, "W, b and target are required");
+  if (!c->has_state) return fail(c, MPM_ERR_CALL_ORDER, "mpm_set_controller needs mpm_set_state first");
+  KParams& P = c->P;
+  const int D = c->D;
+  if (P.K < 1) return fail(c, MPM_ERR_INVALID_ARG, "the controller needs n_actuators >= 1");
+  if (has_nbr(c)) return fail(c, MPM_ERR_INVALID_ARG, "the controller is not supported across slabs");
+  const int KD = P.K * D, nz = D * (1 + 2 * P.K);
+  const size_t T = c->cfg.max_steps;
+  if (!c->ctrl_W) {
+    mpm_status s = MPM_OK;
+#define AL(ptr, n) \
+  if (!s) s = dalloc(c, &c->ptr, (n))
+    AL(ctrl_W, (size_t)KD * nz);
+    AL(ctrl_b, KD);
+    AL(ctrl_target, D);
+    AL(ctrl_Minv, (size_t)P.B * P.K);
+    AL(ctrl_M, (size_t)P.B * P.K);
+    AL(ctrl_n, (size_t)P.B * P.K);
+    AL(ctrl_acc, (size_t)P.B * P.K * 2 * D);
+    AL(ctrl_cnt, 1);
+    AL(ztape, T * P.B * nz);
+    AL(gpre_tape, T * P.B * KD);
+    AL(ctrl_gz, (size_t)P.B * nz);
+    AL(ctrl_gW, (size_t)KD * nz);
+    AL(ctrl_gb, KD);
+    AL(ctrl_gt, D);
+#undef AL
+    if (s) return s;
+  }
+  P.nz = nz;
+  CK(cudaMemcpyAsync(c->ctrl_W, W, (size_t)KD * nz * sizeof(float), cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpyAsync(c->ctrl_b, b, KD * sizeof(float), cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpyAsync(c->ctrl_target, target, D * sizeof(float), cudaMemcpyDefault, c->stream));
+  mpm_status s = ctrl_masses(c);
+  if (s) return s;
+  c->ctrl = true;
+  c->has_grad = false;
+  return MPM_OK;
+}
+
+mpm_status mpm_grad_controller(mpm_ctx c, float* dW, float* db, float* dtarget) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  if (!c->has_grad || !c->ctrl_grad_valid)
+    return fail(c, MPM_ERR_CALL_ORDER, "mpm_grad_controller needs a backward run with the controller on");
+  cudaSetDevice(c->cfg.device);
+  const int KD = c->P.K * c->D;
+  if (dW) CK(cudaMemcpyAsync(dW, c->ctrl_gW, (size_t)KD * c->P.nz * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (db) CK(cudaMemcpyAsync(db, c->ctrl_gb, KD * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (dtarget) CK(cudaMemcpyAsync(dtarget, c->ctrl_gt, c->D * sizeof(float), cudaMemcpyDefault, c->stream));
+  return sync_and_check(c, "grad_controller");
 }
 
 }  // extern "C"

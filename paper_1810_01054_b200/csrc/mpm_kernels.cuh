@@ -62,6 +62,7 @@ struct KParams {
   int slots_per_step;                       // per-step cap of touched blocks
   int arena_slots;                          // capacity of the tape grid arena
   int slab_lo, slab_hi;                     // allowed base_x range (inclusive); slab mode
+  int nz;                                   // controller observation length d (1 + 2K) (NEXT N1)
 };
 
 // Per-step bookkeeping record, info[t * kInfo + field]
@@ -1536,6 +1537,176 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       if (P.K > 0) reduce_actuation<D>(P, A, r, ai, dsig);
     }
     __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// NEXT N1: closed-loop controller embedded in P2G (Fig. 2 caption P:84):
+//   z_t = [target, CoM_k, V_k (k < K)] per rollout, CoM_k / V_k = mass-weighted means over the
+//   particles of actuator group k (DESIGN R20);  a_t = tanh(W z_t + b) -> act[r][t][k][:].
+// Reverse (chain rule, SPEC controller_adjoint): g_pre = dL/da_t * (1 - a_t^2), dL/dz = W^T g_pre
+// into dL/dx_p, dL/dv_p of state t (m_p / M_k); dL/dW = sum_t,r g_pre z^T, dL/db = sum g_pre.
+// ------------------------------------------------------------------------------------
+// segmented warp sum of NV values per distinct key (key < 0: no contribution), one global
+// atomic per distinct key and value; all 32 lanes call it
+template <int NV>
+__device__ __forceinline__ void warp_key_add(int key, const float (&v)[NV], float* dst, int stride) {
+  const int lane = threadIdx.x & 31;
+  unsigned todo = __ballot_sync(0xffffffffu, key >= 0);
+  while (todo) {
+    const int src = __ffs(todo) - 1;
+    const int k0 = __shfl_sync(0xffffffffu, key, src);
+    const bool mine = key == k0;
+    todo &= ~__ballot_sync(0xffffffffu, mine);
+#pragma unroll
+    for (int c = 0; c < NV; ++c) {
+      float s = mine ? v[c] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == src) atomicAdd(&dst[(size_t)k0 * stride + c], s);
+    }
+  }
+}
+
+// z value j of rollout r from the group sums acc[B][K][2D] (m x, m v) and 1/M_k
+template <int D>
+__device__ __forceinline__ float ctrl_z(const KParams& P, int r, int j, const float* target, const float* acc,
+                                        const float* Minv) {
+  if (j < D) return target[j];
+  j -= D;
+  const int half = P.K * D;
+  const int v = j >= half;
+  if (v) j -= half;
+  const int k = j / D, a = j % D;
+  return __ldcg(&acc[((size_t)r * P.K + k) * 2 * D + v * D + a]) * Minv[r * P.K + k];
+}
+
+template <int D>
+__global__ __launch_bounds__(256) void k_ctrl_observe(KParams P, const float* __restrict__ st,
+                                                      const int* __restrict__ orig, const float4* __restrict__ prm,
+                                                      const int* __restrict__ aid, float* acc, int* counter,
+                                                      const float* __restrict__ W, const float* __restrict__ b,
+                                                      const float* __restrict__ target, const float* __restrict__ Minv,
+                                                      float* __restrict__ act, float* __restrict__ z_t, int t) {
+  __shared__ int s_last;
+  const size_t NT = P.NT;
+  for (int j0 = blockIdx.x * blockDim.x; j0 < P.NT; j0 += gridDim.x * blockDim.x) {  // warp-uniform trips
+    const int j = j0 + threadIdx.x;
+    int key = -1;
+    float val[2 * D];
+#pragma unroll
+    for (int c = 0; c < 2 * D; ++c) val[c] = 0.f;
+    if (j < P.NT) {
+      const int u = orig[j];
+      const int k = aid[u];
+      if (k >= 0) {
+        key = (j / P.N) * P.K + k;
+        const float m = prm[u].x;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          val[a] = m * st[(size_t)comp_x<D>(a) * NT + j];
+          val[D + a] = m * st[(size_t)comp_v<D>(a) * NT + j];
+        }
+      }
+    }
+    warp_key_add<2 * D>(key, val, acc, 2 * D);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int KD = P.K * D;
+  for (int idx = threadIdx.x; idx < P.B * KD; idx += blockDim.x) {
+    const int r = idx / KD, i = idx % KD;
+    float pre = b[i];
+    for (int jz = 0; jz < P.nz; ++jz) pre = fmaf(W[(size_t)i * P.nz + jz], ctrl_z<D>(P, r, jz, target, acc, Minv), pre);
+    act[(((size_t)r * P.T + t) * P.K) * D + i] = tanhf(pre);
+  }
+  for (int idx = threadIdx.x; idx < P.B * P.nz; idx += blockDim.x)
+    z_t[idx] = ctrl_z<D>(P, idx / P.nz, idx % P.nz, target, acc, Minv);
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < P.B * P.K * 2 * D; idx += blockDim.x) acc[idx] = 0.f;
+  if (threadIdx.x == 0) *counter = 0;
+}
+
+// one CTA per rollout: g_pre (taped) and dL/dz = W^T g_pre
+template <int D>
+__global__ __launch_bounds__(256) void k_ctrl_adj_param(KParams P, const float* __restrict__ da,
+                                                        const float* __restrict__ act, const float* __restrict__ W,
+                                                        float* __restrict__ gpre_t, float* __restrict__ gz, int t) {
+  extern __shared__ float s_gpre[];  // [K D]
+  const int r = blockIdx.x, KD = P.K * D;
+  for (int i = threadIdx.x; i < KD; i += blockDim.x) {
+    const size_t o = (((size_t)r * P.T + t) * P.K) * D + i;
+    const float a = act[o];
+    const float g = da[o] * (1.f - a * a);
+    s_gpre[i] = g;
+    gpre_t[(size_t)r * KD + i] = g;
+  }
+  __syncthreads();
+  for (int jz = threadIdx.x; jz < P.nz; jz += blockDim.x) {
+    float acc = 0.f;
+    for (int i = 0; i < KD; ++i) acc = fmaf(W[(size_t)i * P.nz + jz], s_gpre[i], acc);
+    gz[(size_t)r * P.nz + jz] = acc;
+  }
+}
+
+// dL/dz -> dL/dx_p, dL/dv_p of state t (storage order t), closed-loop term
+template <int D>
+__global__ void k_ctrl_adj_state(KParams P, const float* __restrict__ gz, const int* __restrict__ orig,
+                                 const float4* __restrict__ prm, const int* __restrict__ aid,
+                                 const float* __restrict__ Minv, float* __restrict__ g) {
+  const size_t NT = P.NT;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.NT; j += gridDim.x * blockDim.x) {
+    const int u = orig[j];
+    const int k = aid[u];
+    if (k < 0) continue;
+    const int r = j / P.N;
+    const float w = prm[u].x * Minv[r * P.K + k];
+    const float* z = gz + (size_t)r * P.nz + D;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      g[(size_t)comp_x<D>(a) * NT + j] += w * z[k * D + a];
+      g[(size_t)comp_v<D>(a) * NT + j] += w * z[P.K * D + k * D + a];
+    }
+  }
+}
+
+// end of the backward: dL/dW[i][jz] = sum_{t,r} g_pre[t][r][i] z[t][r][jz], dL/db, dL/dtarget
+template <int D>
+__global__ void k_ctrl_adj_reduce(KParams P, int T, const float* __restrict__ gpre, const float* __restrict__ z,
+                                  const float* __restrict__ W, float* __restrict__ gW, float* __restrict__ gb,
+                                  float* __restrict__ gtarget) {
+  const int KD = P.K * D, n = KD * P.nz;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n + KD + D; idx += gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    if (idx < n) {
+      const int i = idx / P.nz, jz = idx % P.nz;
+      for (int q = 0; q < T * P.B; ++q) acc = fmaf(gpre[(size_t)q * KD + i], z[(size_t)q * P.nz + jz], acc);
+      gW[idx] = acc;
+    } else if (idx < n + KD) {
+      const int i = idx - n;
+      for (int q = 0; q < T * P.B; ++q) acc += gpre[(size_t)q * KD + i];
+      gb[i] = acc;
+    } else {
+      const int a = idx - n - KD;  // target enters z[0:D]: dL/dtarget = sum W[:, a]^T g_pre
+      for (int q = 0; q < T * P.B; ++q)
+        for (int i = 0; i < KD; ++i) acc = fmaf(W[(size_t)i * P.nz + a], gpre[(size_t)q * KD + i], acc);
+      gtarget[a] = acc;
+    }
+  }
+}
+
+// group masses M[r][k] (and counts) for 1/M_k
+__global__ void k_ctrl_mass(int NT, int N, int K, const float4* __restrict__ prm, const int* __restrict__ aid,
+                            float* __restrict__ M, int* __restrict__ cnt) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < NT; u += gridDim.x * blockDim.x) {
+    const int k = aid[u];
+    if (k < 0) continue;
+    atomicAdd(&M[(u / N) * K + k], prm[u].x);
+    atomicAdd(&cnt[(u / N) * K + k], 1);
   }
 }
 

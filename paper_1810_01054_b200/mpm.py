@@ -29,7 +29,8 @@ EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "m
            "mpm_last_error", "mpm_get_binning", "mpm_get_grid", "mpm_set_profiling",
            "mpm_get_profile", "mpm_launch_count", "mpm_get_step_info", "mpm_grad_mass",
            "mpm_add_seed", "mpm_clear_seeds", "mpm_enable_mass_grad", "mpm_set_slab",
-           "mpm_comm_unique_id", "mpm_comm_init", "mpm_group_forward", "mpm_group_backward")
+           "mpm_comm_unique_id", "mpm_comm_init", "mpm_group_forward", "mpm_group_backward",
+           "mpm_set_controller", "mpm_grad_controller")
 
 
 class MPMError(RuntimeError):
@@ -84,6 +85,8 @@ def load():
     L.mpm_clear_seeds.argtypes = [vp]
     L.mpm_launch_count.argtypes = [vp]
     L.mpm_launch_count.restype = i64
+    L.mpm_set_controller.argtypes = [vp, vp, vp, vp]
+    L.mpm_grad_controller.argtypes = [vp, vp, vp, vp]
     L.mpm_set_slab.argtypes = [vp, i32, i32, i32]
     L.mpm_comm_unique_id.argtypes = [C.c_char_p]
     L.mpm_comm_init.argtypes = [vp, i32, i32, C.c_char_p]
@@ -262,6 +265,29 @@ class MPM:
 
     def clear_seeds(self):
         self._check(self.L.mpm_clear_seeds(self.h))
+
+    # -- NEXT N1: closed-loop controller a_t = tanh(W z_t + b) ----------------------------
+    @property
+    def n_obs(self) -> int:
+        return self.cfg.dim * (1 + 2 * self.cfg.n_actuators)
+
+    def set_controller(self, W, b=None, target=None):
+        """W [K*d][nz], b [K*d], target [d] (nz = d (1 + 2K)); W=None switches it off."""
+        if W is None:
+            self._check(self.L.mpm_set_controller(self.h, None, None, None))
+            return
+        KD = self.cfg.n_actuators * self.cfg.dim
+        arrs = [_in(W, np.float32, (KD, self.n_obs)), _in(b, np.float32, (KD,)),
+                _in(target, np.float32, (self.cfg.dim,))]
+        self._check(self.L.mpm_set_controller(self.h, *[_ptr(a) for a in arrs]))
+
+    def grad_controller(self):
+        """(dL/dW, dL/db, dL/dtarget) from the last backward with the controller on."""
+        KD = self.cfg.n_actuators * self.cfg.dim
+        out = (np.empty((KD, self.n_obs), np.float32), np.empty(KD, np.float32),
+               np.empty(self.cfg.dim, np.float32))
+        self._check(self.L.mpm_grad_controller(self.h, *[_ptr(a) for a in out]))
+        return out
 
     # -- slab mode (SURVEY 8e) -----------------------------------------------------------
     def set_slab(self, x_lo: int, x_hi: int, halo_blocks: int = 1):
