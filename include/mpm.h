@@ -75,6 +75,11 @@ typedef struct {
   int32_t device;       /* CUDA device ordinal                                        */
   void* stream;         /* cudaStream_t or NULL                                       */
   int32_t grid_slots;   /* grid-block slots per step in the tape arena; 0 = automatic */
+  int32_t checkpoint_every; /* NEXT N2: 0 = the memo keeps every step (max_steps of tape);
+                           k > 0 = the tape keeps one k-step segment and full states every
+                           k steps (max_steps/k + 1 checkpoints); mpm_backward recomputes
+                           each earlier segment from its checkpoint (one extra forward),
+                           mpm_get_state / mpm_rewind of an evicted step recompute it      */
 } mpm_config;
 
 /* Create a context on config->device.  Validates the config (MPM_ERR_INVALID_ARG) and
@@ -103,7 +108,9 @@ int32_t mpm_tape_length(mpm_ctx ctx);
  * Clears the error latch and the gradients.                                               */
 mpm_status mpm_rewind(mpm_ctx ctx, int32_t t);
 
-/* State at tape step t (0 <= t <= tape length), user particle order.  NULL = skip. */
+/* State at tape step t (0 <= t <= tape length), user particle order.  NULL = skip.
+ * With checkpoint_every > 0 a step outside the resident segment is recomputed from the
+ * nearest checkpoint (and becomes resident).                                              */
 mpm_status mpm_get_state(mpm_ctx ctx, int32_t t, float* x, float* v, float* F, float* C);
 
 /* Reverse mode over the whole tape: seed dL/dstate at t = tape length, user order,
@@ -187,7 +194,9 @@ mpm_status mpm_group_backward(mpm_ctx* ctxs, int32_t n_ctx, const float* const* 
 
 /* ---- introspection, used by the parity tests (all synchronous) ---- */
 
-/* Binning of tape step t (north_star item 1): positions as stored for step t in the
+/* (Introspection calls need step t resident: with checkpoint_every > 0, inside the current
+ * segment; otherwise MPM_ERR_CALL_ORDER.)
+ * Binning of tape step t (north_star item 1): positions as stored for step t in the
  * internal storage order (x_store [B*N][dim]), the storage-to-user map orig [B*N], the
  * keys [B*N] computed from x_store, the stable sort perm [B*N] (sorted slot -> storage
  * index) and block_start [B*nb + 1], nb = (res/Bb)^dim, Bb = 4 (3D) / 8 (2D).  t < tape

@@ -77,6 +77,13 @@ struct mpm_ctx_s {
   int n_sm = 148;
   int occ_scatter = 2, occ_scatter_adj = 2, occ_g2p = 2, occ_p2gT = 2;
   int tape_len = 0;
+  // NEXT N2 checkpointing: the tape holds steps [seg0, seg0 + tape_cap] (segment-local slots);
+  // with checkpoint_every = k > 0, full states are checkpointed every k steps and the
+  // backward recomputes each earlier segment from its checkpoint
+  int tape_cap = 0, seg0 = 0, seg_end = 0, ck = 0, n_ck = 0, ck_valid = 0;
+  int res_end = 0;  // the states of steps [seg0, res_end] on the tape are valid
+  float* ck_state = nullptr;
+  int* ck_orig = nullptr;
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
   std::string last_error;
   int64_t launches = 0;
@@ -217,14 +224,19 @@ void drain_profile(mpm_ctx c) {
 }
 
 size_t NTs(mpm_ctx c) { return (size_t)c->P.NT; }
-float* state_at(mpm_ctx c, int t) { return c->tape_state + (size_t)t * c->S * NTs(c); }
-int* perm_at(mpm_ctx c, int t) { return c->tape_perm + (size_t)t * NTs(c); }
-int* orig_at(mpm_ctx c, int t) { return c->tape_orig + (size_t)t * NTs(c); }
-int* bs_at(mpm_ctx c, int t) { return c->tape_bs + (size_t)t * (c->P.NBT + 1); }
-int* slot_at(mpm_ctx c, int t) { return c->tape_slot + (size_t)t * c->P.NBT; }
-int* occ_at(mpm_ctx c, int t) { return c->tape_occ + (size_t)t * c->P.NBT; }
-int* touch_at(mpm_ctx c, int t) { return c->tape_touch + (size_t)t * c->P.NBT; }
-int* info_at(mpm_ctx c, int t) { return c->info + (size_t)t * kInfo; }
+// tape slot of global step t (segment-local; the caller guarantees seg0 <= t <= seg0 + tape_cap)
+size_t ti(mpm_ctx c, int t) { return (size_t)(t - c->seg0); }
+float* state_at(mpm_ctx c, int t) { return c->tape_state + ti(c, t) * c->S * NTs(c); }
+int* perm_at(mpm_ctx c, int t) { return c->tape_perm + ti(c, t) * NTs(c); }
+int* orig_at(mpm_ctx c, int t) { return c->tape_orig + ti(c, t) * NTs(c); }
+int* bs_at(mpm_ctx c, int t) { return c->tape_bs + ti(c, t) * (c->P.NBT + 1); }
+int* slot_at(mpm_ctx c, int t) { return c->tape_slot + ti(c, t) * c->P.NBT; }
+int* occ_at(mpm_ctx c, int t) { return c->tape_occ + ti(c, t) * c->P.NBT; }
+int* touch_at(mpm_ctx c, int t) { return c->tape_touch + ti(c, t) * c->P.NBT; }
+int* info_at(mpm_ctx c, int t) { return c->info + ti(c, t) * kInfo; }
+bool on_tape(mpm_ctx c, int t) { return t >= c->seg0 && t <= c->res_end && t <= c->tape_len; }
+float* ck_state_of(mpm_ctx c, int i) { return c->ck_state + (size_t)i * c->S * NTs(c); }
+int* ck_orig_of(mpm_ctx c, int i) { return c->ck_orig + (size_t)i * NTs(c); }
 
 int grid1d(size_t n, int bs = 256) { return (int)((n + bs - 1) / bs); }
 
@@ -315,7 +327,7 @@ template <int D>
 void launch_bin(mpm_ctx c, int t) {
   const KParams& P = c->P;
   launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->bflag, c->tile_sums); });
-  launch(c, KI_SCAN_B, [&] { k_scan_b<<<1, kThreads, 0, c->stream>>>(P, c->n_tiles, c->tile_sums, c->info, t, c->err); });
+  launch(c, KI_SCAN_B, [&] { k_scan_b<<<1, kThreads, 0, c->stream>>>(P, c->n_tiles, c->tile_sums, c->info, (int)ti(c, t), c->err); });
   launch(c, KI_SCAN_C, [&] {
     k_scan_c<<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->bflag, c->tile_sums, info_at(c, t), bs_at(c, t),
                                                       slot_at(c, t), occ_at(c, t), touch_at(c, t));
@@ -373,9 +385,24 @@ mpm_status exchange_local(mpm_ctx* cs, int n) {
 }
 
 // forward step t = phase A (binning, P2G [, window pack]) | exchange | phase B ([unpack,] G2P)
+// N2: the tape is full at step t (t - seg0 == tape_cap): state t becomes checkpoint t / k and
+// the first slot of a new segment (its keys / histogram are already in the work buffers)
+void roll_segment(mpm_ctx c, int t) {
+  const size_t bs = (size_t)c->S * NTs(c) * sizeof(float), bo = NTs(c) * sizeof(int);
+  const int i = t / c->ck;
+  cudaMemcpyAsync(ck_state_of(c, i), state_at(c, t), bs, cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemcpyAsync(ck_orig_of(c, i), orig_at(c, t), bo, cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemcpyAsync(c->tape_state, state_at(c, t), bs, cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemcpyAsync(c->tape_orig, orig_at(c, t), bo, cudaMemcpyDeviceToDevice, c->stream);
+  c->seg0 = t;
+  c->res_end = t;
+  c->ck_valid = std::max(c->ck_valid, i + 1);
+}
+
 template <int D>
 void forward_phase_a(mpm_ctx c, int t) {
   const KParams& P = c->P;
+  if (c->ck && t - c->seg0 == c->tape_cap) roll_segment(c, t);
   if (c->ctrl)  // N1: a_t = tanh(W z_t + b) from state t, before P2G reads act[t]
     launch(c, KI_CTRL, [&] {
       k_ctrl_observe<D><<<c->n_sm * 4, 256, 0, c->stream>>>(P, state_at(c, t), orig_at(c, t), c->prm, c->aid,
@@ -393,6 +420,7 @@ void forward_phase_a(mpm_ctx c, int t) {
 template <int D>
 void forward_phase_b(mpm_ctx c, int t) {
   const KParams& P = c->P;
+  c->res_end = t + 1;
   if (has_nbr(c)) launch_band_unpack(c, t, false, c->arena);
   StepArgs A = step_args(c, t);
   const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
@@ -411,7 +439,7 @@ void backward_phase_a(mpm_ctx c, int t) {
   A.grid = agrid_of(c, t);
   A.gin = c->bcur;
   A.gout = c->bnxt;
-  if (t == c->tape_len - 1)  // first backward step: prepare its buffer (later steps: by grid_T)
+  if (t == c->seg_end - 1)  // first backward step of a segment: prepare its buffer (later: by grid_T)
     launch(c, KI_ZERO, [&] { k_zero_slots<<<c->n_sm * 4, 256, 0, c->stream>>>(info_at(c, t), A.grid); });
   const int nbla = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter_adj));
   launch(c, KI_G2PT, [&] { k_block_scatter<D, true><<<nbla, kThreads, scatter_dyn_smem<D, true>(), c->stream>>>(P, A); });
@@ -428,7 +456,7 @@ void backward_phase_b(mpm_ctx c, int t) {
   if (has_nbr(c)) launch_band_unpack(c, t, true, A.grid);
   launch(c, KI_GRIDT, [&] {
     k_grid_adj<D><<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
-                                                       t > 0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
+                                                       t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
   if (c->mass_grad)
@@ -482,6 +510,9 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
                         const int32_t* aid) {
   const KParams& P = c->P;
   const size_t NT = P.NT;
+  c->seg0 = 0;  // a new rollout starts in tape slot 0
+  c->res_end = 0;
+  c->ck_valid = 0;
   // stage user arrays on the device (host or device pointers, UVA)
   float* sx = c->stage;
   float* sv = sx + NT * D;
@@ -508,6 +539,11 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   CK(cudaMemsetAsync(c->err, 0, sizeof(ErrLatch), c->stream));
   CK(cudaMemsetAsync(c->cnt, 0, (size_t)P.NBT * sizeof(int), c->stream));
   launch_keys<D>(c, 0);
+  if (c->ck) {  // N2: checkpoint 0 = the initial state
+    CK(cudaMemcpyAsync(ck_state_of(c, 0), state_at(c, 0), (size_t)c->S * NT * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(ck_orig_of(c, 0), orig_at(c, 0), NT * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+    c->ck_valid = 1;
+  }
   // automatic grid-slot capacity from the touched blocks of the initial state
   if (c->arena == nullptr) {
     launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->bflag, c->tile_sums); });
@@ -519,7 +555,7 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
     long per = c->cfg.grid_slots > 0 ? c->cfg.grid_slots
                                       : std::min<long>(P.NBT, 2 * touched + 64L * P.B + 64);
     c->P.slots_per_step = (int)per;
-    c->arena_slots = (size_t)per * (size_t)(c->cfg.max_steps + 1);
+    c->arena_slots = (size_t)per * (size_t)(c->tape_cap + 1);
     c->P.arena_slots = (int)std::min<size_t>(c->arena_slots, (size_t)0x7fffffff);
     mpm_status s = dalloc(c, &c->arena, c->arena_slots * kCPB);
     if (s) return s;
@@ -634,18 +670,55 @@ mpm_status backward_finish(mpm_ctx c) {
 
 size_t da_count(mpm_ctx c) { return (size_t)c->P.B * c->P.T * std::max(c->P.K, 1) * c->D; }
 
+// N2: make checkpoint i (step i k) the first slot of the tape and recompute the keys of its state
+template <int D>
+void restore_checkpoint(mpm_ctx c, int i) {
+  const size_t bs = (size_t)c->S * NTs(c) * sizeof(float), bo = NTs(c) * sizeof(int);
+  c->seg0 = i * c->ck;
+  c->res_end = c->seg0;
+  cudaMemcpyAsync(c->tape_state, ck_state_of(c, i), bs, cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemcpyAsync(c->tape_orig, ck_orig_of(c, i), bo, cudaMemcpyDeviceToDevice, c->stream);
+  cudaMemsetAsync(c->cnt, 0, (size_t)c->P.NBT * sizeof(int), c->stream);
+  launch_keys<D>(c, c->seg0);
+}
+
 template <int D>
 mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float* gF, const float* gC) {
   mpm_status s = backward_begin<D>(c, gx, gv, gF, gC);
   if (s) return s;
-  for (int t = c->tape_len - 1; t >= 0; --t) {
-    backward_phase_a<D>(c, t);
-    if (has_nbr(c)) {
-      s = exchange_nccl(c);
-      if (s) return s;
+  c->seg_end = c->tape_len;  // the current segment [seg0, tape_len) is on the tape
+  for (;;) {
+    for (int t = c->seg_end - 1; t >= c->seg0; --t) {
+      backward_phase_a<D>(c, t);
+      if (has_nbr(c)) {
+        s = exchange_nccl(c);
+        if (s) return s;
+      }
+      backward_phase_b<D>(c, t);
+      backward_step_end<D>(c, t);
     }
-    backward_phase_b<D>(c, t);
-    backward_step_end<D>(c, t);
+    if (c->seg0 == 0) break;
+    // N2: recompute the previous segment from its checkpoint, then continue the reverse pass
+    const int end = c->seg0;
+    restore_checkpoint<D>(c, (end - 1) / c->ck);
+    for (int t = c->seg0; t < end; ++t) {
+      forward_phase_a<D>(c, t);
+      if (has_nbr(c)) {
+        s = exchange_nccl(c);
+        if (s) return s;
+      }
+      forward_phase_b<D>(c, t);
+    }
+    c->seg_end = end;
+    // the carried adjoint is in the storage order of the evicted run's state `end`
+    // (= checkpoint end / k); map it to the recomputed order of that state
+    const int NT = (int)NTs(c);
+    launch(c, KI_MISC, [&] { k_invert_perm<<<grid1d(NT), 256, 0, c->stream>>>(NT, orig_at(c, end), c->scratch); });
+    launch(c, KI_MISC, [&] {
+      k_remap_adjoint<<<grid1d(NT), 256, 0, c->stream>>>(NT, c->S, ck_orig_of(c, end / c->ck), c->scratch, c->bcur,
+                                                         c->bnxt);
+    });
+    std::swap(c->bcur, c->bnxt);
   }
   s = backward_finish(c);
   if (s) return s;
@@ -702,10 +775,33 @@ mpm_status do_grad(mpm_ctx c, float* dx0, float* dv0, float* dF0, float* dC0, fl
   return sync_and_check(c, "grad");
 }
 
+// N2: make state t resident on the tape (restore the nearest checkpoint at or before t and
+// recompute forward to t); no-op when it already is.  Requires t <= tape_len.
+template <int D>
+mpm_status bring_to_tape(mpm_ctx c, int t) {
+  if (on_tape(c, t)) return MPM_OK;
+  if (!c->ck) return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape");
+  const int i = std::min(t / c->ck, c->ck_valid - 1);
+  restore_checkpoint<D>(c, i);
+  for (int q = c->seg0; q < t; ++q) {
+    forward_phase_a<D>(c, q);
+    if (has_nbr(c)) {
+      mpm_status s = exchange_nccl(c);
+      if (s) return s;
+    }
+    forward_phase_b<D>(c, q);
+  }
+  return sync_and_check(c, "checkpoint recompute");
+}
+
 template <int D>
 mpm_status do_rewind(mpm_ctx c, int t) {
-  CK(cudaMemsetAsync(c->cnt, 0, (size_t)c->P.NBT * sizeof(int), c->stream));
   CK(cudaMemsetAsync(c->err, 0, sizeof(ErrLatch), c->stream));
+  if (!on_tape(c, t)) {
+    mpm_status s = bring_to_tape<D>(c, t);
+    if (s) return s;
+  }
+  CK(cudaMemsetAsync(c->cnt, 0, (size_t)c->P.NBT * sizeof(int), c->stream));
   launch_keys<D>(c, t);
   mpm_status s = sync_and_check(c, "rewind");
   if (s) return s;
@@ -731,6 +827,7 @@ mpm_status group_check(mpm_ctx* cs, int32_t n) {
         c->tape_len != c0->tape_len)
       return fail(c, MPM_ERR_INVALID_ARG, "group contexts need one device, one stream, equal dim/res/tape length");
     if (n > 1 && !c->slab) return fail(c, MPM_ERR_INVALID_ARG, "group contexts need mpm_set_slab");
+    if (c->ck) return fail(c, MPM_ERR_INVALID_ARG, "group calls do not support checkpoint_every");
     if (c->slab) {
       const bool want_left = i > 0, want_right = i + 1 < n;
       if (c->left != want_left || c->right != want_right || (i + 1 < n && (c->x_hi != cs[i + 1]->x_lo ||
@@ -770,6 +867,7 @@ mpm_status group_backward(mpm_ctx* cs, int32_t n, const float* const* gx, const 
                                      gC ? gC[i] : nullptr);
     if (s) return s;
   }
+  for (int i = 0; i < n; ++i) cs[i]->seg_end = cs[i]->tape_len;
   for (int t = cs[0]->tape_len - 1; t >= 0; --t) {
     for (int i = 0; i < n; ++i) backward_phase_a<D>(cs[i], t);
     if (n > 1) {
@@ -830,6 +928,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   if (k.batch < 1 || k.n_particles < 1 || k.n_particles >= (1 << 25)) return bad("batch >= 1 and 1 <= n_particles < 2^25 required");
   if ((long long)k.batch * k.n_particles >= (1LL << 31)) return bad("batch * n_particles must be < 2^31");
   if (k.max_steps < 1) return bad("max_steps >= 1 required");
+  if (k.checkpoint_every < 0 || k.checkpoint_every > k.max_steps) return bad("0 <= checkpoint_every <= max_steps required");
   if (k.n_actuators < 0 || k.n_actuators > 64) return bad("n_actuators in [0, 64]");
   if (!(k.dt > 0.f)) return bad("dt > 0 required");
   if (k.bound < 0 || 2 * k.bound >= k.res) return bad("0 <= bound and 2*bound < res required");
@@ -896,17 +995,26 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   }
 
   const size_t NT = P.NT, T = k.max_steps, S = c->S, D = k.dim;
+  // N2: with checkpoint_every = k the tape holds one k-step segment, plus T/k + 1 checkpoints
+  c->ck = k.checkpoint_every;
+  c->tape_cap = c->ck ? c->ck : k.max_steps;
+  c->n_ck = c->ck ? k.max_steps / c->ck + 1 : 0;
+  const size_t TC = c->tape_cap;
   mpm_status s = MPM_OK;
 #define AL(ptr, n) \
   if (!s) s = dalloc(c, &c->ptr, (n))
-  AL(tape_state, (T + 1) * S * NT);
-  AL(tape_perm, T * NT);
-  AL(tape_orig, (T + 1) * NT);
-  AL(tape_bs, T * (size_t)(P.NBT + 1));
-  AL(tape_slot, T * (size_t)P.NBT);
-  AL(tape_occ, T * (size_t)P.NBT);
-  AL(tape_touch, T * (size_t)P.NBT);
-  AL(info, (T + 1) * kInfo);
+  AL(tape_state, (TC + 1) * S * NT);
+  AL(tape_perm, TC * NT);
+  AL(tape_orig, (TC + 1) * NT);
+  AL(tape_bs, TC * (size_t)(P.NBT + 1));
+  AL(tape_slot, TC * (size_t)P.NBT);
+  AL(tape_occ, TC * (size_t)P.NBT);
+  AL(tape_touch, TC * (size_t)P.NBT);
+  AL(info, (TC + 1) * kInfo);
+  if (c->ck) {
+    AL(ck_state, (size_t)c->n_ck * S * NT);
+    AL(ck_orig, (size_t)c->n_ck * NT);
+  }
   AL(key, NT);
   AL(cnt, (size_t)P.NBT);
   AL(tmp_pk, NT);
@@ -937,7 +1045,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   cudaMemset(c->err, 0, sizeof(ErrLatch));
   cudaMemset(c->cnt, 0, (size_t)P.NBT * sizeof(int));
   cudaMemset(c->act, 0, (size_t)P.B * T * std::max(P.K, 1) * D * sizeof(float));
-  cudaMemset(c->info, 0, (T + 1) * kInfo * sizeof(int));
+  cudaMemset(c->info, 0, (TC + 1) * kInfo * sizeof(int));
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     c->last_error = cudaGetErrorString(e);
@@ -993,6 +1101,10 @@ mpm_status mpm_forward(mpm_ctx c, int32_t n) {
     return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init, or use mpm_group_forward");
   cudaSetDevice(c->cfg.device);
   c->has_grad = false;
+  if (!on_tape(c, c->tape_len)) {  // N2: the tape end was evicted by a checkpointed backward
+    mpm_status s = c->D == 3 ? bring_to_tape<3>(c, c->tape_len) : bring_to_tape<2>(c, c->tape_len);
+    if (s) return s;
+  }
   return c->D == 3 ? do_forward<3>(c, n) : do_forward<2>(c, n);
 }
 
@@ -1010,6 +1122,10 @@ mpm_status mpm_get_state(mpm_ctx c, int32_t t, float* x, float* v, float* F, flo
   if (!c) return MPM_ERR_INVALID_ARG;
   if (!c->has_state || t < 0 || t > c->tape_len) return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape");
   cudaSetDevice(c->cfg.device);
+  if (!on_tape(c, t)) {  // N2: recompute from the nearest checkpoint
+    mpm_status s = c->D == 3 ? bring_to_tape<3>(c, t) : bring_to_tape<2>(c, t);
+    if (s) return s;
+  }
   return c->D == 3 ? do_get_state<3>(c, t, x, v, F, C) : do_get_state<2>(c, t, x, v, F, C);
 }
 
@@ -1020,6 +1136,10 @@ mpm_status mpm_backward(mpm_ctx c, const float* gx, const float* gv, const float
   if (has_nbr(c) && !c->comm)
     return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init, or use mpm_group_backward");
   cudaSetDevice(c->cfg.device);
+  if (!on_tape(c, c->tape_len)) {  // N2: bring the last segment back
+    mpm_status s = c->D == 3 ? bring_to_tape<3>(c, c->tape_len) : bring_to_tape<2>(c, c->tape_len);
+    if (s) return s;
+  }
   return c->D == 3 ? do_backward<3>(c, gx, gv, gF, gC) : do_backward<2>(c, gx, gv, gF, gC);
 }
 
@@ -1035,7 +1155,8 @@ const char* mpm_last_error(mpm_ctx c) { return c ? c->last_error.c_str() : "null
 mpm_status mpm_get_binning(mpm_ctx c, int32_t t, float* x_store, int32_t* orig, int32_t* keyo, int32_t* perm,
                            int32_t* block_start) {
   if (!c) return MPM_ERR_INVALID_ARG;
-  if (!c->has_state || t < 0 || t >= c->tape_len) return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape");
+  if (!c->has_state || t < 0 || t >= c->tape_len || t < c->seg0 || t + 1 > c->res_end)
+    return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape (checkpointed: not resident)");
   cudaSetDevice(c->cfg.device);
   const KParams& P = c->P;
   const size_t NT = P.NT;
@@ -1067,7 +1188,8 @@ mpm_status mpm_get_binning(mpm_ctx c, int32_t t, float* x_store, int32_t* orig, 
 
 mpm_status mpm_get_grid(mpm_ctx c, int32_t t, float* m, float* vbar) {
   if (!c) return MPM_ERR_INVALID_ARG;
-  if (!c->has_state || t < 0 || t >= c->tape_len) return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape");
+  if (!c->has_state || t < 0 || t >= c->tape_len || t < c->seg0 || t + 1 > c->res_end)
+    return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape (checkpointed: not resident)");
   cudaSetDevice(c->cfg.device);
   const KParams& P = c->P;
   size_t nn = 1;
@@ -1093,7 +1215,8 @@ mpm_status mpm_get_grid(mpm_ctx c, int32_t t, float* m, float* vbar) {
 
 mpm_status mpm_get_step_info(mpm_ctx c, int32_t t, int32_t out[3]) {
   if (!c || !out) return MPM_ERR_INVALID_ARG;
-  if (!c->has_state || t < 0 || t >= c->tape_len) return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape");
+  if (!c->has_state || t < 0 || t >= c->tape_len || t < c->seg0 || t + 1 > c->res_end)
+    return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape (checkpointed: not resident)");
   cudaSetDevice(c->cfg.device);
   int h[kInfo];
   CK(cudaMemcpy(h, info_at(c, t), sizeof(h), cudaMemcpyDeviceToHost));

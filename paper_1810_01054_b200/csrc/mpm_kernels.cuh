@@ -1710,6 +1710,20 @@ __global__ void k_ctrl_mass(int NT, int N, int K, const float4* __restrict__ prm
   }
 }
 
+// NEXT N2: at a segment boundary the recomputed forward may order state t differently from the
+// run whose adjoint is carried in (a last-bit change of x from the order of P2G's float atomics
+// can move a particle across a cell boundary): remap the adjoint through the user order.
+__global__ void k_invert_perm(int NT, const int* __restrict__ orig, int* __restrict__ inv) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < NT; j += gridDim.x * blockDim.x) inv[orig[j]] = j;
+}
+__global__ void k_remap_adjoint(int NT, int S, const int* __restrict__ old_orig, const int* __restrict__ inv_new,
+                                const float* __restrict__ src, float* __restrict__ dst) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < NT; j += gridDim.x * blockDim.x) {
+    const int jn = inv_new[old_orig[j]];
+    for (int c = 0; c < S; ++c) dst[(size_t)c * NT + jn] = src[(size_t)c * NT + j];
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // Slab mode.  A rank owns the particles of one x-slab; the only nodes two ranks
 // can both touch lie in a window of block-planes around each slab boundary, and the only
