@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -143,6 +144,7 @@ struct mpm_ctx_s {
   float* bnxt = nullptr;
   // profiling
   bool profiling = false;
+  bool pdl = true;  // programmatic dependent launches on the step path (MPM_PDL=0 disables)
   bool mass_grad = false;  // N3: compute dL/dm_p in P2G^T (opt-in)
   bool mass_grad_valid = false;
   std::vector<PendingEvent> pending;
@@ -221,6 +223,23 @@ void drain_profile(mpm_ctx c) {
     c->event_pool.push_back(p.b);
   }
   c->pending.clear();
+}
+
+// Launch of a step-path kernel: with c->pdl, as a programmatic dependent launch (the
+// kernel begins with MPM_PDL_ENTRY, so it still observes every write of its predecessor).
+template <class... KA, class... A>
+void kx(mpm_ctx c, void (*k)(KA...), dim3 g, dim3 b, size_t smem, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = g;
+  cfg.blockDim = b;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c->pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
 
 size_t NTs(mpm_ctx c) { return (size_t)c->P.NT; }
@@ -326,14 +345,14 @@ StepArgs step_args(mpm_ctx c, int t) {
 template <int D>
 void launch_bin(mpm_ctx c, int t) {
   const KParams& P = c->P;
-  launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->bflag, c->tile_sums); });
-  launch(c, KI_SCAN_B, [&] { k_scan_b<<<1, kThreads, 0, c->stream>>>(P, c->n_tiles, c->tile_sums, c->info, (int)ti(c, t), c->err); });
+  launch(c, KI_SCAN_A, [&] { kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums); });
+  launch(c, KI_SCAN_B, [&] { kx(c, k_scan_b, dim3(1), dim3(kThreads), 0, P, c->n_tiles, c->tile_sums, c->info, (int)ti(c, t), c->err); });
   launch(c, KI_SCAN_C, [&] {
-    k_scan_c<<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->bflag, c->tile_sums, info_at(c, t), bs_at(c, t),
+    kx(c, k_scan_c, dim3(c->n_tiles), dim3(kThreads), 0, P, c->bflag, c->tile_sums, info_at(c, t), bs_at(c, t),
                                                       slot_at(c, t), occ_at(c, t), touch_at(c, t));
   });
   launch(c, KI_SCATTER, [&] {
-    k_scatter<<<grid1d(P.NT), 256, 0, c->stream>>>(P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_pk, info_at(c, t), c->arena);
+    kx(c, k_scatter, dim3(grid1d(P.NT)), dim3(256), 0, P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_pk, info_at(c, t), c->arena);
   });
 }
 
@@ -343,14 +362,14 @@ bool has_nbr(mpm_ctx c) { return c->slab && (c->left || c->right); }
 // the step's adjoint buffer)
 void launch_band_pack(mpm_ctx c, int t, bool adj, const float4* g) {
   launch(c, KI_BANDP, [&] {
-    k_band_pack<<<c->n_sm * 4, 256, 0, c->stream>>>(c->band_blocks, c->gb_lo, c->gb_hi, slot_at(c, t), info_at(c, t),
+    kx(c, k_band_pack, dim3(c->n_sm * 4), dim3(256), 0, c->band_blocks, c->gb_lo, c->gb_hi, slot_at(c, t), info_at(c, t),
                                                     adj, g, c->left ? c->send_lo : nullptr,
                                                     c->right ? c->send_hi : nullptr);
   });
 }
 void launch_band_unpack(mpm_ctx c, int t, bool adj, float4* g) {
   launch(c, KI_BANDU, [&] {
-    k_band_unpack<<<c->n_sm * 4, 256, 0, c->stream>>>(c->band_blocks, c->gb_lo, c->gb_hi, slot_at(c, t), info_at(c, t),
+    kx(c, k_band_unpack, dim3(c->n_sm * 4), dim3(256), 0, c->band_blocks, c->gb_lo, c->gb_hi, slot_at(c, t), info_at(c, t),
                                                       adj, g, c->left ? c->recv_lo : nullptr,
                                                       c->right ? c->recv_hi : nullptr);
   });
@@ -405,7 +424,7 @@ void forward_phase_a(mpm_ctx c, int t) {
   if (c->ck && t - c->seg0 == c->tape_cap) roll_segment(c, t);
   if (c->ctrl)  // N1: a_t = tanh(W z_t + b) from state t, before P2G reads act[t]
     launch(c, KI_CTRL, [&] {
-      k_ctrl_observe<D><<<c->n_sm * 4, 256, 0, c->stream>>>(P, state_at(c, t), orig_at(c, t), c->prm, c->aid,
+      kx(c, k_ctrl_observe<D>, dim3(c->n_sm * 4), dim3(256), 0, P, state_at(c, t), orig_at(c, t), c->prm, c->aid,
                                                              c->ctrl_acc, c->ctrl_cnt, c->ctrl_W, c->ctrl_b,
                                                              c->ctrl_target, c->ctrl_Minv, c->act,
                                                              c->ztape + (size_t)t * P.B * P.nz, t);
@@ -413,7 +432,7 @@ void forward_phase_a(mpm_ctx c, int t) {
   launch_bin<D>(c, t);
   StepArgs A = step_args(c, t);
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
-  launch(c, KI_P2G, [&] { k_block_scatter<D, false><<<nblk, kThreads, scatter_dyn_smem<D, false>(), c->stream>>>(P, A); });
+  launch(c, KI_P2G, [&] { kx(c, k_block_scatter<D, false>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A); });
   if (has_nbr(c)) launch_band_pack(c, t, false, c->arena);
 }
 
@@ -424,7 +443,7 @@ void forward_phase_b(mpm_ctx c, int t) {
   if (has_nbr(c)) launch_band_unpack(c, t, false, c->arena);
   StepArgs A = step_args(c, t);
   const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
-  launch(c, KI_G2P, [&] { k_g2p<D><<<ng, kThreads, 0, c->stream>>>(P, A); });
+  launch(c, KI_G2P, [&] { kx(c, k_g2p<D>, dim3(ng), dim3(kThreads), 0, P, A); });
 }
 
 // adjoint grid buffer of backward step t (double-buffered by step parity)
@@ -440,9 +459,9 @@ void backward_phase_a(mpm_ctx c, int t) {
   A.gin = c->bcur;
   A.gout = c->bnxt;
   if (t == c->seg_end - 1)  // first backward step of a segment: prepare its buffer (later: by grid_T)
-    launch(c, KI_ZERO, [&] { k_zero_slots<<<c->n_sm * 4, 256, 0, c->stream>>>(info_at(c, t), A.grid); });
+    launch(c, KI_ZERO, [&] { kx(c, k_zero_slots, dim3(c->n_sm * 4), dim3(256), 0, info_at(c, t), A.grid); });
   const int nbla = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter_adj));
-  launch(c, KI_G2PT, [&] { k_block_scatter<D, true><<<nbla, kThreads, scatter_dyn_smem<D, true>(), c->stream>>>(P, A); });
+  launch(c, KI_G2PT, [&] { kx(c, k_block_scatter<D, true>, dim3(nbla), dim3(kThreads), scatter_dyn_smem<D, true>(), P, A); });
   if (has_nbr(c)) launch_band_pack(c, t, true, A.grid);
 }
 
@@ -455,23 +474,23 @@ void backward_phase_b(mpm_ctx c, int t) {
   A.gout = c->bnxt;
   if (has_nbr(c)) launch_band_unpack(c, t, true, A.grid);
   launch(c, KI_GRIDT, [&] {
-    k_grid_adj<D><<<c->n_sm * 8, 256, 0, c->stream>>>(P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
+    kx(c, k_grid_adj<D>, dim3(c->n_sm * 8), dim3(256), 0, P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
                                                        t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
   if (c->mass_grad)
-    launch(c, KI_P2GT, [&] { k_p2g_adj<D, true><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
+    launch(c, KI_P2GT, [&] { kx(c, k_p2g_adj<D, true>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A); });
   else
-    launch(c, KI_P2GT, [&] { k_p2g_adj<D, false><<<na, MPM_P2GT_THREADS, 0, c->stream>>>(P, A); });
+    launch(c, KI_P2GT, [&] { kx(c, k_p2g_adj<D, false>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A); });
   if (c->ctrl) {  // N1: controller adjoint of step t (needs this step's complete dL/da)
     const int KD = P.K * D;
     launch(c, KI_CTRLT, [&] {
-      k_ctrl_adj_param<D><<<P.B, 256, KD * sizeof(float), c->stream>>>(P, c->da, c->act, c->ctrl_W,
+      kx(c, k_ctrl_adj_param<D>, dim3(P.B), dim3(256), KD * sizeof(float), P, c->da, c->act, c->ctrl_W,
                                                                        c->gpre_tape + (size_t)t * P.B * KD,
                                                                        c->ctrl_gz, t);
     });
     launch(c, KI_CTRLT, [&] {
-      k_ctrl_adj_state<D><<<c->n_sm * 4, 256, 0, c->stream>>>(P, c->ctrl_gz, orig_at(c, t), c->prm, c->aid,
+      kx(c, k_ctrl_adj_state<D>, dim3(c->n_sm * 4), dim3(256), 0, P, c->ctrl_gz, orig_at(c, t), c->prm, c->aid,
                                                               c->ctrl_Minv, c->bnxt);
     });
   }
@@ -546,7 +565,7 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   }
   // automatic grid-slot capacity from the touched blocks of the initial state
   if (c->arena == nullptr) {
-    launch(c, KI_SCAN_A, [&] { k_scan_a<D><<<c->n_tiles, kThreads, 0, c->stream>>>(P, c->cnt, c->bflag, c->tile_sums); });
+    launch(c, KI_SCAN_A, [&] { kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums); });
     std::vector<int3> ts(c->n_tiles);
     CK(cudaMemcpyAsync(ts.data(), c->tile_sums, ts.size() * sizeof(int3), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -610,7 +629,7 @@ void add_step_seed(mpm_ctx c, int t, float* g) {
   const size_t NT = c->P.NT;
   const float* b = it->second;
   launch(c, KI_MISC, [&] {
-    k_seed<D><<<grid1d(NT), 256, 0, c->stream>>>(c->P, orig_at(c, t), b, b + NT * D, b + 2 * NT * D,
+    kx(c, k_seed<D>, dim3(grid1d(NT)), dim3(256), 0, c->P, orig_at(c, t), b, b + NT * D, b + 2 * NT * D,
                                                   b + 2 * NT * D + NT * D * D, g, 1);
   });
 }
@@ -632,7 +651,7 @@ mpm_status backward_begin(mpm_ctx c, const float* gx, const float* gv, const flo
   c->bcur = c->gA;
   c->bnxt = c->gB;
   launch(c, KI_MISC, [&] {
-    k_seed<D><<<grid1d(NT), 256, 0, c->stream>>>(P, orig_at(c, T), gx ? sx : nullptr, gv ? sv : nullptr,
+    kx(c, k_seed<D>, dim3(grid1d(NT)), dim3(256), 0, P, orig_at(c, T), gx ? sx : nullptr, gv ? sv : nullptr,
                                                   gF ? sF : nullptr, gC ? sC : nullptr, c->bcur, 0);
   });
   add_step_seed<D>(c, T, c->bcur);
@@ -943,6 +962,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   }
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, k.device);
   c->stream = (cudaStream_t)k.stream;
+  if (const char* e = getenv("MPM_PDL")) c->pdl = atoi(e) != 0;
   c->D = k.dim;
   c->S = 2 * k.dim + 2 * k.dim * k.dim;
   KParams& P = c->P;

@@ -41,6 +41,16 @@ constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks us
 constexpr int kScanTile = kThreads;  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
 
+// Programmatic dependent launch (sm_90+): a kernel of the step path waits for its
+// predecessor's completion (and memory) before touching any of its outputs, then lets its own
+// dependent start launching; with the PDL launch attribute the next kernel's launch and CTA
+// placement overlap this kernel's tail.  No-ops for ordinary launches.
+#define MPM_PDL_ENTRY()                                    \
+  do {                                                     \
+    asm volatile("griddepcontrol.wait;" ::: "memory");     \
+    asm volatile("griddepcontrol.launch_dependents;" ::);  \
+  } while (0)
+
 enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6, E_SLAB = 9 };
 
 template <int D> struct Dim;
@@ -513,6 +523,7 @@ template <int D>
 __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __restrict__ cnt,
                                                      unsigned* __restrict__ bflag,
                                                      int3* __restrict__ tile_sums) {
+  MPM_PDL_ENTRY();
   __shared__ int3 s_warp[kThreads / 32 + 1];
   const int gb = blockIdx.x * kScanTile + threadIdx.x;
   int c = 0, o = 0, t = 0;
@@ -528,6 +539,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __res
 // single CTA: exclusive scan of tile sums, per-step counts, arena base, overflow check
 __global__ void k_scan_b(KParams P, int n_tiles, int3* __restrict__ tile_sums, int* __restrict__ info,
                          int t, ErrLatch* err) {
+  MPM_PDL_ENTRY();
   __shared__ int3 s_warp[kThreads / 32 + 1];
   __shared__ int3 s_carry;
   if (threadIdx.x == 0) s_carry = make_int3(0, 0, 0);
@@ -570,6 +582,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const unsigned* 
                                                      int* __restrict__ slot_of,
                                                      int* __restrict__ occ_list,
                                                      int* __restrict__ touched_list) {
+  MPM_PDL_ENTRY();
   __shared__ int3 s_warp[kThreads / 32 + 1];
   const int ok = info_t[I_OK];
   const int base = info_t[I_BASE];
@@ -593,6 +606,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const unsigned* 
 __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __restrict__ block_start,
                           int* __restrict__ cnt, int2* __restrict__ tmp_pk,
                           const int* __restrict__ info_t, float4* __restrict__ arena) {
+  MPM_PDL_ENTRY();
   {
     const int nz = info_t[I_NTOUCH] * kCPB;
     float4* z = arena + (size_t)info_t[I_BASE] * kCPB;
@@ -628,6 +642,7 @@ __device__ __forceinline__ void adj_prepare(int* __restrict__ info_t, float4* __
 }
 
 __global__ void k_zero_slots(int* __restrict__ info_t, float4* __restrict__ g) {
+  MPM_PDL_ENTRY();
   adj_prepare(info_t, g, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
@@ -689,6 +704,7 @@ constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(fl
 
 template <int D, bool ADJ>
 __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
+  MPM_PDL_ENTRY();
   using DD = Dim<D>;
   using PY = Pay<D, ADJ>;
   constexpr int BB = DD::BB, TE = DD::TE, TN = DD::TN;
@@ -1136,6 +1152,7 @@ __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const 
 
 template <int D>
 __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepArgs A) {
+  MPM_PDL_ENTRY();
   __shared__ float4 s_v[Dim<D>::TN];
   __shared__ int s_blk;
   const size_t NT = P.NT;
@@ -1504,6 +1521,7 @@ __device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArg
 
 template <int D, bool MG>
 __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
+  MPM_PDL_ENTRY();
   __shared__ float4 s_v[Dim<D>::TN];
   __shared__ float4 s_a[Dim<D>::TN];
   __shared__ int s_blk;
@@ -1588,6 +1606,7 @@ __global__ __launch_bounds__(256) void k_ctrl_observe(KParams P, const float* __
                                                       const float* __restrict__ W, const float* __restrict__ b,
                                                       const float* __restrict__ target, const float* __restrict__ Minv,
                                                       float* __restrict__ act, float* __restrict__ z_t, int t) {
+  MPM_PDL_ENTRY();
   __shared__ int s_last;
   const size_t NT = P.NT;
   for (int j0 = blockIdx.x * blockDim.x; j0 < P.NT; j0 += gridDim.x * blockDim.x) {  // warp-uniform trips
@@ -1636,6 +1655,7 @@ template <int D>
 __global__ __launch_bounds__(256) void k_ctrl_adj_param(KParams P, const float* __restrict__ da,
                                                         const float* __restrict__ act, const float* __restrict__ W,
                                                         float* __restrict__ gpre_t, float* __restrict__ gz, int t) {
+  MPM_PDL_ENTRY();
   extern __shared__ float s_gpre[];  // [K D]
   const int r = blockIdx.x, KD = P.K * D;
   for (int i = threadIdx.x; i < KD; i += blockDim.x) {
@@ -1658,6 +1678,7 @@ template <int D>
 __global__ void k_ctrl_adj_state(KParams P, const float* __restrict__ gz, const int* __restrict__ orig,
                                  const float4* __restrict__ prm, const int* __restrict__ aid,
                                  const float* __restrict__ Minv, float* __restrict__ g) {
+  MPM_PDL_ENTRY();
   const size_t NT = P.NT;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.NT; j += gridDim.x * blockDim.x) {
     const int u = orig[j];
@@ -1738,6 +1759,7 @@ __global__ void k_remap_adjoint(int NT, int S, const int* __restrict__ old_orig,
 __global__ void k_band_pack(int nblk, int gb_lo, int gb_hi, const int* __restrict__ slot_of,
                             const int* __restrict__ info_t, int adj, const float4* __restrict__ g,
                             float4* __restrict__ out_lo, float4* __restrict__ out_hi) {
+  MPM_PDL_ENTRY();
   const int sub = adj ? info_t[I_BASE] : 0;
   const int n = nblk * kCPB;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += gridDim.x * blockDim.x) {
@@ -1753,6 +1775,7 @@ __global__ void k_band_pack(int nblk, int gb_lo, int gb_hi, const int* __restric
 __global__ void k_band_unpack(int nblk, int gb_lo, int gb_hi, const int* __restrict__ slot_of,
                               const int* __restrict__ info_t, int adj, float4* __restrict__ g,
                               const float4* __restrict__ in_lo, const float4* __restrict__ in_hi) {
+  MPM_PDL_ENTRY();
   const int sub = adj ? info_t[I_BASE] : 0;
   const int n = nblk * kCPB;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += gridDim.x * blockDim.x) {
@@ -1782,6 +1805,7 @@ template <int D>
 __global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int* __restrict__ touched_list,
                            const float4* __restrict__ arena, float4* __restrict__ ag,
                            int* __restrict__ info_prev, float4* __restrict__ ag_prev) {
+  MPM_PDL_ENTRY();
   if (info_prev) adj_prepare(info_prev, ag_prev, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   const int n = info_t[I_NTOUCH] * kCPB;
   const float4* g = arena + (size_t)info_t[I_BASE] * kCPB;
@@ -1830,6 +1854,7 @@ template <int D>
 __global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __restrict__ gx,
                        const float* __restrict__ gv, const float* __restrict__ gF,
                        const float* __restrict__ gC, float* __restrict__ g, int accumulate) {
+  MPM_PDL_ENTRY();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= P.NT) return;
   const size_t NT = P.NT;
