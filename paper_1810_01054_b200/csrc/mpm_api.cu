@@ -24,7 +24,7 @@ enum KernelId {
   KI_SCAN_A, KI_SCAN_B, KI_SCAN_C, KI_SCATTER, KI_P2G, KI_GRID, KI_G2P,
   KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC, KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_COUNT
 };
-const char* kKernelNames[KI_COUNT] = {"scan_a", "scan_b", "scan_c",  "scatter", "p2g",  "grid_update",
+const char* kKernelNames[KI_COUNT] = {"scan", "scan_b", "scan_c",  "scatter", "p2g",  "grid_update",
                                       "g2p",    "zero_adj", "g2p_T", "grid_T", "p2g_T", "misc",
                                       "band_pack", "band_unpack", "ctrl", "ctrl_T"};
 
@@ -106,6 +106,8 @@ struct mpm_ctx_s {
   int* scratch = nullptr;
   int* hist2 = nullptr;
   int3* tile_sums = nullptr;
+  ScanTileState scan{};   // single-pass binning scan: tile flags / aggregates / prefixes / ticket
+  unsigned scan_epoch = 0;
   int n_tiles = 0;
   ErrLatch* err = nullptr;
   int* dbad = nullptr;
@@ -345,11 +347,10 @@ StepArgs step_args(mpm_ctx c, int t) {
 template <int D>
 void launch_bin(mpm_ctx c, int t) {
   const KParams& P = c->P;
-  launch(c, KI_SCAN_A, [&] { kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums); });
-  launch(c, KI_SCAN_B, [&] { kx(c, k_scan_b, dim3(1), dim3(kThreads), 0, P, c->n_tiles, c->tile_sums, c->info, (int)ti(c, t), c->err); });
-  launch(c, KI_SCAN_C, [&] {
-    kx(c, k_scan_c, dim3(c->n_tiles), dim3(kThreads), 0, P, c->bflag, c->tile_sums, info_at(c, t), bs_at(c, t),
-                                                      slot_at(c, t), occ_at(c, t), touch_at(c, t));
+  const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
+  launch(c, KI_SCAN_A, [&] {
+    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles, c->info,
+       (int)ti(c, t), bs_at(c, t), slot_at(c, t), occ_at(c, t), touch_at(c, t), c->err, t);
   });
   launch(c, KI_SCATTER, [&] {
     kx(c, k_scatter, dim3(grid1d(P.NT)), dim3(256), 0, P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_pk, info_at(c, t), c->arena);
@@ -1041,6 +1042,10 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   AL(scratch, NT);
   AL(hist2, (size_t)P.NBT);
   AL(tile_sums, (size_t)c->n_tiles);
+  AL(scan.flag, (size_t)c->n_tiles);
+  AL(scan.agg, (size_t)c->n_tiles);
+  AL(scan.incl, (size_t)c->n_tiles);
+  AL(scan.ticket, 1);
   AL(bflag, (size_t)P.NBT);
   AL(err, 1);
   AL(dbad, 1);
@@ -1063,6 +1068,8 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
     return s;
   }
   cudaMemset(c->err, 0, sizeof(ErrLatch));
+  cudaMemset(c->scan.flag, 0, (size_t)c->n_tiles * sizeof(unsigned));
+  cudaMemset(c->scan.ticket, 0, sizeof(unsigned long long));
   cudaMemset(c->cnt, 0, (size_t)P.NBT * sizeof(int));
   cudaMemset(c->act, 0, (size_t)P.B * T * std::max(P.K, 1) * D * sizeof(float));
   cudaMemset(c->info, 0, (TC + 1) * kInfo * sizeof(int));

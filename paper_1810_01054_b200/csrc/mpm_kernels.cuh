@@ -601,6 +601,106 @@ __global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const unsigned* 
   if (gb == P.NBT - 1) block_start[P.NBT] = P.NT;
 }
 
+// Single-pass binning tables (replaces k_scan_a/b/c on the step path): one CTA per tile of
+// kScanTile blocks, taken in ticket order; block flags -> CTA scan -> decoupled look-back over
+// the preceding tiles (aggregate / inclusive prefix published with an epoch-tagged flag, so
+// the flags need no reset) -> block_start, occupied list, slot map, touched list.  The grid
+// slot of a touched block is checked against the per-step and arena capacities per block; the
+// last tile writes the step record (counts, arena base, zeroed work counters).
+struct ScanTileState {
+  unsigned* flag;          // [n_tiles]: epoch << 2 | status (1 = aggregate, 2 = inclusive prefix)
+  int3* agg;               // [n_tiles]
+  int3* incl;              // [n_tiles]
+  unsigned long long* ticket;
+};
+
+template <int D>
+__global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int* __restrict__ cnt, ScanTileState ts,
+                                                           unsigned epoch, int n_tiles, int* __restrict__ info,
+                                                           int tl, int* __restrict__ block_start,
+                                                           int* __restrict__ slot_of, int* __restrict__ occ_list,
+                                                           int* __restrict__ touched_list, ErrLatch* err, int t) {
+  MPM_PDL_ENTRY();
+  __shared__ int3 s_warp[kThreads / 32 + 1];
+  __shared__ int s_tile;
+  __shared__ int3 s_pre;
+  if (threadIdx.x == 0) s_tile = (int)(atomicAdd(ts.ticket, 1ull) % (unsigned long long)n_tiles);
+  __syncthreads();
+  const int tile = s_tile;
+  const int gb = tile * kScanTile + threadIdx.x;
+  int c = 0, o = 0, tc = 0;
+  if (gb < P.NBT) block_flags<D>(P, cnt, gb, c, o, tc);
+  int3 tot;
+  const int3 ex = cta_excl_scan3(make_int3(c, o, tc), s_warp, tot);
+  const unsigned ep = epoch << 2;
+  if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 tiles at a time
+    const int lane = threadIdx.x;
+    if (lane == 0) {
+      if (tile == 0) ts.incl[0] = tot; else ts.agg[tile] = tot;
+      __threadfence();
+      atomicExch(&ts.flag[tile], ep | (tile == 0 ? 2u : 1u));
+    }
+    int3 pre = make_int3(0, 0, 0);
+    for (int i = tile - 1; i >= 0; i -= 32) {
+      const int idx = i - lane;
+      unsigned f = ep | 2u;  // before tile 0: an empty inclusive prefix
+      int3 v = make_int3(0, 0, 0);
+      if (idx >= 0) {
+        do { f = *((volatile unsigned*)&ts.flag[idx]); } while ((f & ~3u) != ep || (f & 3u) == 0u);
+        __threadfence();
+        const volatile int* q = (const volatile int*)((f & 3u) == 2u ? &ts.incl[idx] : &ts.agg[idx]);
+        v = make_int3(q[0], q[1], q[2]);
+      }
+      const unsigned pm = __ballot_sync(0xffffffffu, (f & 3u) == 2u);
+      const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix (lowest lane)
+      if (lane > stop) v = make_int3(0, 0, 0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+        v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
+      }
+      pre.x += v.x; pre.y += v.y; pre.z += v.z;
+      if (pm) break;
+    }
+    if (lane == 0) {
+      if (tile > 0) {
+        ts.incl[tile] = make_int3(pre.x + tot.x, pre.y + tot.y, pre.z + tot.z);
+        __threadfence();
+        atomicExch(&ts.flag[tile], ep | 2u);
+      }
+      s_pre = pre;
+    }
+  }
+  __syncthreads();
+  const int3 pre = s_pre;
+  const int base = tl == 0 ? 0 : info[(tl - 1) * kInfo + I_BASE] + info[(tl - 1) * kInfo + I_NTOUCH];
+  const int cap = min(P.slots_per_step, P.arena_slots - base);
+  if (gb < P.NBT) {
+    block_start[gb] = ex.x + pre.x;
+    if (o) occ_list[ex.y + pre.y] = gb;
+    const int sl = ex.z + pre.z;
+    const bool fits = tc && sl < cap;
+    slot_of[gb] = fits ? base + sl : -1;
+    if (fits) touched_list[sl] = gb;
+  }
+  if (gb == P.NBT - 1) block_start[P.NBT] = P.NT;
+  if (tile == n_tiles - 1 && threadIdx.x == 0) {
+    const int ntouch = pre.z + tot.z;
+    const int ok = ntouch <= cap;
+    if (!ok) latch(err, E_TAPE_FULL, t, ntouch);
+    int* I = info + tl * kInfo;
+    I[I_NOCC] = ok ? pre.y + tot.y : 0;
+    I[I_NTOUCH] = ok ? ntouch : 0;
+    I[I_BASE] = base;
+    I[I_WORK] = 0;
+    I[I_WORK2] = 0;
+    I[I_WORK3] = 0;
+    I[I_WORK4] = 0;
+    I[I_OK] = ok;
+  }
+}
+
 // counting-sort scatter by block (positions inside a block are fixed up by k_block_scatter);
 // also zeroes the grid slots of step t (the P2G flush accumulates into them)
 __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __restrict__ block_start,

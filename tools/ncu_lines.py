@@ -6,9 +6,9 @@ import subprocess
 import sys
 
 
-def main(rep, kern, top=30):
+def main(rep, kern, top=30, skip=0):
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
-                          "--launch-skip", "0", "--launch-count", "1", "--print-source", "cuda,sass"],
+                          "--launch-skip", str(skip), "--launch-count", "1", "--print-source", "cuda,sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hi = [i for i, r in enumerate(rows) if "Warp Stall Sampling (All Samples)" in r][0]
@@ -30,4 +30,4 @@ def main(rep, kern, top=30):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30)
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30, int(sys.argv[4]) if len(sys.argv) > 4 else 0)
