@@ -145,11 +145,13 @@ ALG_BYTES = {
 }
 
 
-def _traffic(kernel):
-    """dram bytes per launch from the committed ncu summary, if any (profiles/*.json)."""
+def _traffic(kernel, workload):
+    """dram bytes per launch of `kernel` from the committed ncu capture (profiles/
+    ncu_traffic.json) when it was taken on this workload, else None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
-        return json.load(open(path))["per_launch_dram_bytes"][kernel]
+        d = json.load(open(path))
+        return d["per_launch_dram_bytes"][kernel] if d.get("workload") == workload else None
     except Exception:
         return None
 
@@ -243,7 +245,7 @@ def run_ours(args):
     d = per_kernel[dom]
     prof_total = sum(v["ms_total"] for v in per_kernel.values())
     roofline = {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak, "unit": "GB/s",
-                "frac": round(d["gbs"] / peak, 4), "traffic": _traffic(dom),
+                "frac": round(d["gbs"] / peak, 4), "traffic": _traffic(dom, args.workload),
                 "peak_source": peak_src, "share_of_step": round(d["ms_total"] / prof_total, 3),
                 "alg_bytes_per_launch": d["alg_bytes_per_launch"],
                 "per_kernel": per_kernel}

@@ -1,5 +1,5 @@
 """Key counters per captured kernel from an ncu report (--page raw --csv):
-  python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--traffic-json profiles/ncu_traffic.json]
+  python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--traffic-json profiles/ncu_traffic.json --workload C4]
 --traffic-json writes dram__bytes_read.sum + dram__bytes_write.sum per launch (mean over the
 captured launches of each kernel), keyed by bench.py's kernel names (roofline "traffic")."""
 import csv
@@ -70,10 +70,14 @@ def main(rep, traffic_json=None):
         print("   stalls: " + " ".join(f"{k}={v:.2f}" for k, v in st))
     if traffic_json:
         per = {k: round(sum(v) / len(v)) for k, v in traffic.items()}
-        json.dump({"source": rep, "per_launch_dram_bytes": per,
+        json.dump({"source": rep, "workload": WORKLOAD, "per_launch_dram_bytes": per,
                    "captured_launches": {k: len(v) for k, v in traffic.items()}}, open(traffic_json, "w"), indent=1)
 
 
+WORKLOAD = "C4"
+
 if __name__ == "__main__":
     tj = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
+    if "--workload" in sys.argv:
+        WORKLOAD = sys.argv[sys.argv.index("--workload") + 1]
     main(sys.argv[1], tj)
