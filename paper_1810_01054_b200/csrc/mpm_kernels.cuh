@@ -801,6 +801,10 @@ struct StepArgs {
 
 template <int D, bool ADJ>
 constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(float); }
+// payload slot of chunk position p: consumer threads of consecutive cells read positions
+// ~2^d apart, which would share 4 banks; the XOR with (p >> 5) spreads them over 32 (kCap is
+// a multiple of 32, so this permutes [0, kCap))
+__device__ __forceinline__ int pay_slot(int p) { return p ^ ((p >> 5) & 7); }
 
 template <int D, bool ADJ>
 __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
@@ -917,11 +921,12 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 #pragma unroll
         for (int a = 0; a < D; ++a) x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
         make_stencil<D>(x, P.fres, sc);
+        const int ps = pay_slot(pi);
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           f[a] = sc.fx[a];
 #pragma unroll
-          for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][pi] = sc.w[a][o];
+          for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][ps] = sc.w[a][o];
         }
         if (ADJ) {
           int cl[D];
@@ -968,7 +973,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
             for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], f[b], acc);
             Av[a] = acc;
           }
-          if (PY::M >= 0) s_pay[PY::M < 0 ? 0 : PY::M][pi] = pr.x;
+          if (PY::M >= 0) s_pay[PY::M < 0 ? 0 : PY::M][ps] = pr.x;
         } else {
           // steps A and B: g_v = gv + dt gx ; g_C = gC + dt gF F^T
           const float* gi = A.gin;
@@ -1003,9 +1008,9 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
         }
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-          s_pay[PY::A + a][pi] = Av[a];
+          s_pay[PY::A + a][ps] = Av[a];
 #pragma unroll
-          for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][pi] = Bm[a][b];
+          for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][ps] = Bm[a][b];
         }
       }
       __syncthreads();
@@ -1017,7 +1022,8 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
       if (tid < 3 * kCPB) {
         const int i0 = ADJ ? s_cstart[c] : max(s_cstart[c], lo) - lo;
         const int i1 = ADJ ? s_cursor[c] + 1 : min(s_cstart[c + 1], hi) - lo;
-        for (int i = i0; i < i1; ++i) {
+        for (int i0s = i0; i0s < i1; ++i0s) {
+          const int i = pay_slot(i0s);
           const float wx = s_pay[PY::W + ox][i];
           float Ax[3];
 #pragma unroll
