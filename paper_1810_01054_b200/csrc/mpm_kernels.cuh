@@ -801,10 +801,11 @@ struct StepArgs {
 
 template <int D, bool ADJ>
 constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(float); }
-// payload slot of chunk position p: consumer threads of consecutive cells read positions
-// ~2^d apart, which would share 4 banks; the XOR with (p >> 5) spreads them over 32 (kCap is
-// a multiple of 32, so this permutes [0, kCap))
-__device__ __forceinline__ int pay_slot(int p) { return p ^ ((p >> 5) & 7); }
+// payload slot of chunk position p: a warp of consumer threads reads cells whose particles
+// sit ~2^d (2D: consecutive cells) or 2^d * {1, 4, 16} (3D thread order below) positions
+// apart, which would share 4 banks; the XOR of the low 3 bits with (p >> 5) ^ (p >> 7)
+// spreads them over 32.  It permutes every aligned group of 8, so [0, kCap) maps onto itself.
+__device__ __forceinline__ int pay_slot(int p) { return p ^ (((p >> 5) ^ (p >> 7)) & 7); }
 
 template <int D, bool ADJ>
 __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
@@ -906,7 +907,10 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
     }
 
     // ---- chunks of kCap particles: produce payload, consume per (cell, ox), phase-write ----
-    const int ox = tid / kCPB, c = tid % kCPB;
+    // consumer thread -> (ox, cell).  3D: cell z fastest, then x, then y, so the 8 threads of a
+    // quarter-warp write tile nodes 36 float4 apart in x (conflict-free 128-bit phase writes)
+    const int ox = tid / kCPB;
+    const int c = D == 3 ? ((((tid >> 2) & 3) * 4 + ((tid >> 4) & 3)) * 4 + (tid & 3)) : tid % kCPB;
     for (int lo = 0; lo < n; lo += kCap) {
       const int hi = min(n, lo + kCap);
       if (ADJ && lo > 0) {  // later chunks of an oversize block: reset the cell sub-ranges
