@@ -353,7 +353,7 @@ void launch_bin(mpm_ctx c, int t) {
        (int)ti(c, t), bs_at(c, t), slot_at(c, t), occ_at(c, t), touch_at(c, t), c->err, t);
   });
   launch(c, KI_SCATTER, [&] {
-    kx(c, k_scatter, dim3(grid1d(P.NT)), dim3(256), 0, P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_pk, info_at(c, t), c->arena);
+    kx(c, k_scatter, dim3(std::max(1, std::min(grid1d(P.NT), c->n_sm * 8))), dim3(256), 0, P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_pk, info_at(c, t), c->arena);
   });
 }
 

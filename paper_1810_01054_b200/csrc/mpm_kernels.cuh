@@ -38,7 +38,8 @@ constexpr int kCPB = 64;         // cells (and nodes) per grid block
 constexpr int kThreads = 256;    // CTA size of the block-tile kernels
 constexpr int kCap = 512;        // particles per producer chunk
 constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks use scratch)
-constexpr int kScanTile = kThreads;  // grid blocks per scan tile (one per thread)
+constexpr int kScanTile = kThreads;
+constexpr int kScatQ = 4;        // particles per thread in k_scatter  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
 
 // Programmatic dependent launch (sm_90+): a kernel of the step path waits for its
@@ -713,21 +714,36 @@ __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __rest
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += gridDim.x * blockDim.x)
       z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  bool valid = j < NT;
-  const int kj = valid ? key[j] : 0;
-  int gb = kj / kCPB;
-  unsigned vm = __ballot_sync(0xffffffffu, valid);
-  if (!valid) return;
-  unsigned peers = __match_any_sync(vm, gb);
-  int lane = threadIdx.x & 31;
-  int leader = __ffs(peers) - 1;
-  int n = __popc(peers);
-  int old = 0;
-  if (lane == leader) old = atomicSub(&cnt[gb], n);
-  old = __shfl_sync(peers, old, leader);
-  int rank = __popc(peers & ((1u << lane) - 1));
-  tmp_pk[block_start[gb] + old - n + rank] = make_int2(j, kj);  // (storage index, key)
+  // kScatQ particles per thread, their key -> block_start loads issued together (the chain
+  // key -> block_start -> cursor -> store is latency bound; ILP across particles hides it)
+  const int stride = gridDim.x * blockDim.x;
+  for (int j0 = blockIdx.x * blockDim.x; j0 < NT; j0 += stride * kScatQ) {  // warp-uniform
+    int kj[kScatQ], bs[kScatQ];
+#pragma unroll
+    for (int q = 0; q < kScatQ; ++q) {
+      const int j = j0 + threadIdx.x + q * stride;
+      kj[q] = j < NT ? __ldg(&key[j]) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < kScatQ; ++q) bs[q] = kj[q] >= 0 ? __ldg(&block_start[kj[q] / kCPB]) : 0;
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < kScatQ; ++q) {
+      const bool valid = kj[q] >= 0;
+      const unsigned vm = __ballot_sync(0xffffffffu, valid);
+      if (valid) {
+        const int gb = kj[q] / kCPB;
+        const unsigned peers = __match_any_sync(vm, gb);
+        const int leader = __ffs(peers) - 1;
+        const int n = __popc(peers);
+        int old = 0;
+        if (lane == leader) old = atomicSub(&cnt[gb], n);
+        old = __shfl_sync(peers, old, leader);
+        const int rank = __popc(peers & ((1u << lane) - 1));
+        tmp_pk[bs[q] + old - n + rank] = make_int2(j0 + threadIdx.x + q * stride, kj[q]);  // (storage index, key)
+      }
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------
