@@ -44,6 +44,7 @@ class _Cfg(C.Structure):
         ("dim", C.c_int), ("res", C.c_int), ("n", C.c_int), ("n_act", C.c_int),
         ("dt", C.c_double), ("gravity", C.c_double * 3), ("bound", C.c_int),
         ("friction", C.c_double * 6), ("act_strength", C.c_double), ("eps", C.c_double),
+        ("material", C.c_int),
     ]
 
 
@@ -69,6 +70,11 @@ def lib():
         L.orc_psi.argtypes = [C.c_int, dp, C.c_double, C.c_double]
         L.orc_pk1.argtypes = [C.c_int, dp, C.c_double, C.c_double, dp]
         L.orc_dPdF.argtypes = [C.c_int, dp, C.c_double, C.c_double, dp]
+        L.orc_psi_fcr.restype = C.c_double
+        L.orc_psi_fcr.argtypes = [C.c_int, dp, C.c_double, C.c_double]
+        L.orc_pk1_fcr.argtypes = [C.c_int, dp, C.c_double, C.c_double, dp]
+        L.orc_dPdF_fcr.argtypes = [C.c_int, dp, C.c_double, C.c_double, dp]
+        L.orc_polar.argtypes = [C.c_int, dp, dp]
         L.orc_lame.argtypes = [C.c_double, C.c_double, dp, dp]
         L.orc_project.argtypes = [C.c_int, dp, dp, C.c_double, C.c_double, dp]
         L.orc_project_adj.argtypes = [C.c_int, dp, dp, C.c_double, C.c_double, dp, dp]
@@ -119,12 +125,13 @@ class Config:
     act_strength: float = 0.0
     n_act: int = 0
     eps: float = 1e-10  # R7
+    material: int = 0   # 0 = neo-Hookean (R1), 1 = fixed-corotated (R21)
 
     def c(self, n: int) -> _Cfg:
         g = list(self.gravity) + [0.0] * (3 - len(self.gravity))
         f = list(self.friction) + [0.0] * (6 - len(self.friction))
         return _Cfg(self.dim, self.res, n, self.n_act, self.dt, (C.c_double * 3)(*g[:3]),
-                    self.bound, (C.c_double * 6)(*f[:6]), self.act_strength, self.eps)
+                    self.bound, (C.c_double * 6)(*f[:6]), self.act_strength, self.eps, self.material)
 
 
 class OracleError(RuntimeError):
@@ -282,25 +289,39 @@ def weights(xg: float):
     return base.value, w, dw
 
 
-def psi(F, mu, lam) -> float:
+def psi(F, mu, lam, material: int = 0) -> float:
     F = _dv(F)
-    return lib().orc_psi(F.shape[0], _d(F.reshape(-1).copy()), mu, lam)
+    f = lib().orc_psi_fcr if material == 1 else lib().orc_psi
+    return f(F.shape[0], _d(F.reshape(-1).copy()), mu, lam)
 
 
-def pk1(F, mu, lam):
+def pk1(F, mu, lam, material: int = 0):
     F = _dv(F)
     d = F.shape[0]
     P = np.zeros((d, d))
-    lib().orc_pk1(d, _d(np.ascontiguousarray(F)), mu, lam, _d(P))
+    f = lib().orc_pk1_fcr if material == 1 else lib().orc_pk1
+    f(d, _d(np.ascontiguousarray(F)), mu, lam, _d(P))
     return P
 
 
-def dPdF(F, mu, lam):
+def dPdF(F, mu, lam, material: int = 0):
     F = _dv(F)
     d = F.shape[0]
     H = np.zeros((d, d, d, d))
-    lib().orc_dPdF(d, _d(np.ascontiguousarray(F)), mu, lam, _d(H))
+    f = lib().orc_dPdF_fcr if material == 1 else lib().orc_dPdF
+    f(d, _d(np.ascontiguousarray(F)), mu, lam, _d(H))
     return H
+
+
+def polar(F):
+    """R of the polar decomposition F = R S (fixed-corotated model, R21)."""
+    F = _dv(F)
+    d = F.shape[0]
+    R = np.zeros((d, d))
+    rc = lib().orc_polar(d, _d(np.ascontiguousarray(F)), _d(R))
+    if rc:
+        raise OracleError(rc)
+    return R
 
 
 def lame(E, nu):

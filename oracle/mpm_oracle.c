@@ -133,6 +133,158 @@ void orc_dPdF(int dim, const double* F, double mu, double lam, double* H) {
 }
 
 /* ------------------------------------------------------------------------------------ */
+/* Fixed-corotated model (NEXT N3, DESIGN R21): the paper names no psi  */
+/* (P:102-103); this is the second material the GPU offers.                               */
+/*   F = R S (polar), psi = mu |F - R|^2 + lam/2 (J - 1)^2, P = 2 mu (F - R) + lam (J-1) J F^-T */
+/* ------------------------------------------------------------------------------------ */
+
+/* symmetric 3x3 eigen-decomposition by cyclic Jacobi rotations: A = Q diag(ev) Q^T */
+static void jacobi3(const double* A_in, double* ev, double* Q) {
+  double A[9];
+  for (int i = 0; i < 9; ++i) { A[i] = A_in[i]; Q[i] = (i % 4 == 0) ? 1.0 : 0.0; }
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = A[1] * A[1] + A[2] * A[2] + A[5] * A[5];
+    double nrm = A[0] * A[0] + A[4] * A[4] + A[8] * A[8];
+    if (off <= 1e-34 * nrm) break;
+    for (int p = 0; p < 2; ++p)
+      for (int q = p + 1; q < 3; ++q) {
+        double apq = A[p * 3 + q];
+        if (apq == 0.0) continue;
+        double theta = (A[q * 3 + q] - A[p * 3 + p]) / (2.0 * apq);
+        double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        double c = 1.0 / sqrt(t * t + 1.0), sn = t * c;
+        /* A <- J^T A J with J the rotation in the (p, q) plane */
+        for (int k = 0; k < 3; ++k) {
+          double akp = A[k * 3 + p], akq = A[k * 3 + q];
+          A[k * 3 + p] = c * akp - sn * akq;
+          A[k * 3 + q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {
+          double apk = A[p * 3 + k], aqk = A[q * 3 + k];
+          A[p * 3 + k] = c * apk - sn * aqk;
+          A[q * 3 + k] = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < 3; ++k) {
+          double qkp = Q[k * 3 + p], qkq = Q[k * 3 + q];
+          Q[k * 3 + p] = c * qkp - sn * qkq;
+          Q[k * 3 + q] = sn * qkp + c * qkq;
+        }
+      }
+  }
+  for (int i = 0; i < 3; ++i) ev[i] = A[i * 4];
+}
+
+/* R of F = R S with S symmetric positive definite (det F > 0).  2D: SPEC's closed form,
+ * theta = atan2(F10 - F01, F00 + F11).  3D: S = (F^T F)^(1/2) by Jacobi, R = F S^-1. */
+int orc_polar(int dim, const double* F, double* R) {
+  if (!(orc_det(dim, F) > 0.0)) return ORC_ERR_INVERTED;
+  if (dim == 2) {
+    double th = atan2(F[2] - F[1], F[0] + F[3]);
+    R[0] = cos(th); R[1] = -sin(th); R[2] = sin(th); R[3] = cos(th);
+    return ORC_OK;
+  }
+  double FtF[9], ev[3], Q[9], Si[9];
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double acc = 0.0;
+      for (int c = 0; c < 3; ++c) acc += F[c * 3 + a] * F[c * 3 + b];
+      FtF[a * 3 + b] = acc;
+    }
+  jacobi3(FtF, ev, Q);
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double acc = 0.0;
+      for (int k = 0; k < 3; ++k) acc += Q[a * 3 + k] * Q[b * 3 + k] / sqrt(ev[k]);
+      Si[a * 3 + b] = acc;
+    }
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double acc = 0.0;
+      for (int c = 0; c < 3; ++c) acc += F[a * 3 + c] * Si[c * 3 + b];
+      R[a * 3 + b] = acc;
+    }
+  return ORC_OK;
+}
+
+double orc_psi_fcr(int dim, const double* F, double mu, double lam) {
+  double R[9];
+  orc_polar(dim, F, R);
+  double s = 0.0;
+  for (int i = 0; i < dim * dim; ++i) s += (F[i] - R[i]) * (F[i] - R[i]);
+  double J = orc_det(dim, F);
+  return mu * s + 0.5 * lam * (J - 1.0) * (J - 1.0);
+}
+
+void orc_pk1_fcr(int dim, const double* F, double mu, double lam, double* P) {
+  double R[9], Fi[9];
+  orc_polar(dim, F, R);
+  orc_inv(dim, F, Fi);
+  double J = orc_det(dim, F);
+  for (int a = 0; a < dim; ++a)
+    for (int b = 0; b < dim; ++b)
+      P[a * dim + b] = 2.0 * mu * (F[a * dim + b] - R[a * dim + b]) + lam * (J - 1.0) * J * Fi[b * dim + a];
+}
+
+/* dR for a perturbation dF (P:567's Hessian needs dR/dF):  with S = R^T F and
+ * M = R^T dF,  R^T dR = [w]x  where  (tr(S) I - S) w = axial(M - M^T)  (3D; [w]x S + S [w]x
+ * = [(tr(S) I - S) w]x for symmetric S), and w = (M_10 - M_01) / tr(S) in 2D. */
+static void polar_dR(int d, const double* F, const double* R, const double* dF, double* dR) {
+  double S[9], M[9], K[9];
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      double s = 0.0, m = 0.0;
+      for (int c = 0; c < d; ++c) {
+        s += R[c * d + a] * F[c * d + b];
+        m += R[c * d + a] * dF[c * d + b];
+      }
+      S[a * d + b] = s;
+      M[a * d + b] = m;
+    }
+  for (int i = 0; i < 9; ++i) K[i] = 0.0;
+  if (d == 2) {
+    double w = (M[2] - M[1]) / (S[0] + S[3]);
+    K[1] = -w; K[3] = w;  /* [[0, -w], [w, 0]] in the 3x3 layout of K */
+  } else {
+    double ax[3] = {M[7] - M[5], M[2] - M[6], M[3] - M[1]}; /* axial(M - M^T) */
+    double trS = S[0] + S[4] + S[8], A[9], Ai[9], w[3];
+    for (int i = 0; i < 9; ++i) A[i] = -S[i];
+    A[0] += trS; A[4] += trS; A[8] += trS;
+    orc_inv(3, A, Ai);
+    for (int a = 0; a < 3; ++a) w[a] = Ai[a * 3] * ax[0] + Ai[a * 3 + 1] * ax[1] + Ai[a * 3 + 2] * ax[2];
+    K[1] = -w[2]; K[2] = w[1]; K[3] = w[2]; K[5] = -w[0]; K[6] = -w[1]; K[7] = w[0];
+  }
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      double acc = 0.0;
+      for (int c = 0; c < d; ++c) acc += R[a * d + c] * K[c * 3 + b];
+      dR[a * d + b] = acc;
+    }
+}
+
+/* H[g][e][a][b] = dP_ge/dF_ab = 2 mu (d_ga d_eb - dR_ge/dF_ab)
+ *                + lam [ (J F^-T)_ge (J F^-T)_ab + (J - 1) J (Fi_ba Fi_eg - Fi_ea Fi_bg) ] */
+void orc_dPdF_fcr(int dim, const double* F, double mu, double lam, double* H) {
+  int d = dim;
+  double R[9], Fi[9];
+  orc_polar(d, F, R);
+  orc_inv(d, F, Fi);
+  double J = orc_det(d, F);
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      double dF[9] = {0}, dR[9];
+      dF[a * d + b] = 1.0;
+      polar_dR(d, F, R, dF, dR);
+      for (int g = 0; g < d; ++g)
+        for (int e = 0; e < d; ++e) {
+          double v = 2.0 * mu * (((g == a && e == b) ? 1.0 : 0.0) - dR[g * d + e]);
+          v += lam * (J * Fi[e * d + g]) * (J * Fi[b * d + a]);
+          v += lam * (J - 1.0) * J * (Fi[b * d + a] * Fi[e * d + g] - Fi[e * d + a] * Fi[b * d + g]);
+          H[((g * d + e) * d + a) * d + b] = v;
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------------------ */
 /* Friction projection, step L, forward definitions P:614-619 (R6, R7, R8).               */
 /* ------------------------------------------------------------------------------------ */
 void orc_project(int dim, const double* v, const double* n, double c, double eps, double* vs) {
@@ -323,7 +475,8 @@ static int particle_quantities(const orc_cfg* cfg, const double* rec, double mas
   if (!(q->J > 0.0)) return ORC_ERR_INVERTED; /* R14 */
   q->lnJ = log(q->J);
   orc_lame(E, nu, &q->mu, &q->lam);
-  orc_pk1(d, F, q->mu, q->lam, q->Pel);
+  if (cfg->material == 1) orc_pk1_fcr(d, F, q->mu, q->lam, q->Pel);
+  else orc_pk1(d, F, q->mu, q->lam, q->Pel);
   for (int i = 0; i < d * d; ++i) q->sigma[i] = 0.0;
   if (aid >= 0)
     for (int a = 0; a < d; ++a) q->sigma[a * d + a] = cfg->act_strength * act_t[aid * d + a]; /* R4 */
@@ -663,7 +816,8 @@ static int step_backward(const orc_cfg* cfg, const double* st, const double* st_
     }
     /* (H) P:561-568: first three terms */
     double H[81];
-    orc_dPdF(d, F, q->mu, q->lam, H);
+    if (cfg->material == 1) orc_dPdF_fcr(d, F, q->mu, q->lam, H);
+    else orc_dPdF(d, F, q->mu, q->lam, H);
     for (int a = 0; a < d; ++a)
       for (int b = 0; b < d; ++b) {
         double t1 = 0.0, t2 = 0.0, t3 = 0.0;
@@ -683,14 +837,20 @@ static int step_backward(const orc_cfg* cfg, const double* st, const double* st_
       }
     }
     /* material parameters (R19): dL/dmu = dP : dP/dmu, dL/dlam = dP : dP/dlam */
-    double Fi[9];
+    double Fi[9], Rp[9];
     orc_inv(d, F, Fi);
+    if (cfg->material == 1) orc_polar(d, F, Rp);
     double dmu = 0.0, dlam = 0.0;
     for (int a = 0; a < d; ++a)
       for (int b = 0; b < d; ++b) {
         double FinvT = Fi[b * d + a];
-        dmu += dP[a * d + b] * (F[a * d + b] - FinvT);
-        dlam += dP[a * d + b] * q->lnJ * FinvT;
+        if (cfg->material == 1) { /* dP/dmu = 2 (F - R), dP/dlam = (J - 1) J F^-T */
+          dmu += dP[a * d + b] * 2.0 * (F[a * d + b] - Rp[a * d + b]);
+          dlam += dP[a * d + b] * (q->J - 1.0) * q->J * FinvT;
+        } else {
+          dmu += dP[a * d + b] * (F[a * d + b] - FinvT);
+          dlam += dP[a * d + b] * q->lnJ * FinvT;
+        }
       }
     double Ev = E[pi], nv = nu[pi];
     double dmu_dE = 1.0 / (2.0 * (1.0 + nv));

@@ -35,6 +35,7 @@ typedef struct {
   double friction[6];  /* c per wall (-x,+x,-y,+y,-z,+z); c < 0 => sticky (R6)     */
   double act_strength; /* s in sigma_pa = s * Diag(a)  (R4)                         */
   double eps;          /* epsilon of step L (R7)                                    */
+  int material;        /* 0 = neo-Hookean (R1), 1 = fixed-corotated (NEXT N3, R21)   */
 } orc_cfg;
 
 enum { ORC_OK = 0, ORC_ERR_OUT_OF_DOMAIN = 1, ORC_ERR_INVERTED = 2, ORC_ERR_ARG = 3 };
@@ -48,6 +49,12 @@ void   orc_inv(int dim, const double* F, double* Finv);
 double orc_psi(int dim, const double* F, double mu, double lam);           /* R1 */
 void   orc_pk1(int dim, const double* F, double mu, double lam, double* P); /* R1 */
 void   orc_dPdF(int dim, const double* F, double mu, double lam, double* H);/* H[g][e][a][b] = dP_ge/dF_ab */
+/* fixed-corotated (NEXT N3, R21): psi = mu |F - R|^2 + lam/2 (J - 1)^2,
+ * P = 2 mu (F - R) + lam (J - 1) J F^-T, R the rotation of the polar decomposition F = R S */
+int    orc_polar(int dim, const double* F, double* R);
+double orc_psi_fcr(int dim, const double* F, double mu, double lam);
+void   orc_pk1_fcr(int dim, const double* F, double mu, double lam, double* P);
+void   orc_dPdF_fcr(int dim, const double* F, double mu, double lam, double* H);
 void   orc_lame(double E, double nu, double* mu, double* lam);
 void   orc_project(int dim, const double* v, const double* nrm, double c, double eps, double* vstar);
 void   orc_project_adj(int dim, const double* v, const double* nrm, double c, double eps,
