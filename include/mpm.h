@@ -80,6 +80,8 @@ typedef struct {
                            k steps (max_steps/k + 1 checkpoints); mpm_backward recomputes
                            each earlier segment from its checkpoint (one extra forward),
                            mpm_get_state / mpm_rewind of an evicted step recompute it      */
+  int32_t material;     /* NEXT N3 constitutive model: 0 = neo-Hookean (R1),
+                           1 = fixed-corotated, psi = mu |F - R|^2 + lam/2 (J - 1)^2 (R21)   */
 } mpm_config;
 
 /* Create a context on config->device.  Validates the config (MPM_ERR_INVALID_ARG) and

@@ -433,7 +433,10 @@ void forward_phase_a(mpm_ctx c, int t) {
   launch_bin<D>(c, t);
   StepArgs A = step_args(c, t);
   const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
-  launch(c, KI_P2G, [&] { kx(c, k_block_scatter<D, false>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A); });
+  if (P.material == 1)  // fixed-corotated (R21)
+    launch(c, KI_P2G, [&] { kx(c, k_block_scatter<D, false, 1>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A); });
+  else
+    launch(c, KI_P2G, [&] { kx(c, k_block_scatter<D, false>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A); });
   if (has_nbr(c)) launch_band_pack(c, t, false, c->arena);
 }
 
@@ -480,9 +483,15 @@ void backward_phase_b(mpm_ctx c, int t) {
   });
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
   if (c->mass_grad)
-    launch(c, KI_P2GT, [&] { kx(c, k_p2g_adj<D, true>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A); });
+    launch(c, KI_P2GT, [&] {
+      if (P.material == 1) kx(c, k_p2g_adj<D, true, 1>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
+      else kx(c, k_p2g_adj<D, true>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
+    });
   else
-    launch(c, KI_P2GT, [&] { kx(c, k_p2g_adj<D, false>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A); });
+    launch(c, KI_P2GT, [&] {
+      if (P.material == 1) kx(c, k_p2g_adj<D, false, 1>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
+      else kx(c, k_p2g_adj<D, false>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
+    });
   if (c->ctrl) {  // N1: controller adjoint of step t (needs this step's complete dL/da)
     const int KD = P.K * D;
     launch(c, KI_CTRLT, [&] {
@@ -948,6 +957,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   if (k.batch < 1 || k.n_particles < 1 || k.n_particles >= (1 << 25)) return bad("batch >= 1 and 1 <= n_particles < 2^25 required");
   if ((long long)k.batch * k.n_particles >= (1LL << 31)) return bad("batch * n_particles must be < 2^31");
   if (k.max_steps < 1) return bad("max_steps >= 1 required");
+  if (k.material != 0 && k.material != 1) return bad("material must be 0 (neo-Hookean) or 1 (fixed-corotated)");
   if (k.checkpoint_every < 0 || k.checkpoint_every > k.max_steps) return bad("0 <= checkpoint_every <= max_steps required");
   if (k.n_actuators < 0 || k.n_actuators > 64) return bad("n_actuators in [0, 64]");
   if (!(k.dt > 0.f)) return bad("dt > 0 required");
@@ -985,6 +995,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   P.act_s = k.act_strength;
   P.slab_lo = 0;
   P.slab_hi = k.res - 3;
+  P.material = k.material;
   c->n_tiles = (P.NBT + kScanTile - 1) / kScanTile;
   int occ = 0;
   // dynamic shared memory of the block-tile scatter (payload buffer) above the 48 KB default
@@ -992,6 +1003,8 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   cudaFuncSetAttribute(k_block_scatter<3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<3, true>());
   cudaFuncSetAttribute(k_block_scatter<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, false>());
   cudaFuncSetAttribute(k_block_scatter<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, true>());
+  cudaFuncSetAttribute(k_block_scatter<3, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<3, false>());
+  cudaFuncSetAttribute(k_block_scatter<2, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, false>());
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<3, false>, kThreads, scatter_dyn_smem<3, false>());
     c->occ_scatter = std::max(1, occ);

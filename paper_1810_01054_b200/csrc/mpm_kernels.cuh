@@ -73,6 +73,7 @@ struct KParams {
   int slots_per_step;                       // per-step cap of touched blocks
   int arena_slots;                          // capacity of the tape grid arena
   int slab_lo, slab_hi;                     // allowed base_x range (inclusive); slab mode
+  int material;                             // 0 = neo-Hookean (R1), 1 = fixed-corotated (R21)
   int nz;                                   // controller observation length d (1 + 2K) (NEXT N1)
 };
 
@@ -259,6 +260,97 @@ __device__ __forceinline__ void kirchhoff_h(const float (&H)[D][D], float mu, fl
       for (int c = 0; c < D; ++c) fsf = fmaf(F[a][c] * sig[c], F[b][c], fsf);
       float t = fmaf(mu, ffti<D>(H, a, b), fsf);
       if (a == b) t = fmaf(lam, lnJ, t);
+      tau[a][b] = t;
+      tau[b][a] = t;
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// Fixed-corotated material (NEXT N3, DESIGN R21), Kirchhoff form: with B = F F^T = V^2,
+//   tau = 2 mu (B - V) + lam J (J - 1) I + F Diag(sig) F^T.
+// E = B - I (exact from H) is diagonalised, E = Q diag(e) Q^T (cyclic Jacobi, fixed sweeps; robust
+// for the near-degenerate E of small strains); V has eigenvalues s = sqrt(1 + e), and
+// B - V = Q diag(e s / (s + 1)) Q^T carries no cancellation against I.
+// ------------------------------------------------------------------------------------
+template <int D> struct Stretch {
+  float s[D];     // eigenvalues of V
+  float g[D];     // eigenvalues of B - V
+  float Q[D][D];  // eigenvectors (columns)
+};
+
+template <int P, int Q_, int D>
+__device__ __forceinline__ void jacobi_rot(float (&A)[D][D], float (&Q)[D][D]) {
+  const float apq = A[P][Q_];
+  const float tau = A[Q_][Q_] - A[P][P];
+  const float t = 2.f * apq * copysignf(1.f, tau) / (fabsf(tau) + sqrtf(fmaf(tau, tau, 4.f * apq * apq)) + 1e-30f);
+  const float c = rsqrtf(fmaf(t, t, 1.f)), sn = t * c;
+  A[P][P] -= t * apq;
+  A[Q_][Q_] += t * apq;
+  A[P][Q_] = A[Q_][P] = 0.f;
+  if constexpr (D == 3) {
+    constexpr int R = 3 - P - Q_;
+    const float arp = A[R][P], arq = A[R][Q_];
+    A[R][P] = A[P][R] = c * arp - sn * arq;
+    A[R][Q_] = A[Q_][R] = sn * arp + c * arq;
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float qp = Q[k][P], qq = Q[k][Q_];
+    Q[k][P] = c * qp - sn * qq;
+    Q[k][Q_] = sn * qp + c * qq;
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void left_stretch(const float (&H)[D][D], Stretch<D>& st) {
+  float A[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      A[a][b] = ffti<D>(H, a, b);
+      st.Q[a][b] = a == b ? 1.f : 0.f;
+    }
+  if constexpr (D == 2) {
+    jacobi_rot<0, 1, 2>(A, st.Q);  // exact for 2x2
+  } else {
+#pragma unroll
+    for (int sweep = 0; sweep < 5; ++sweep) {
+      jacobi_rot<0, 1, 3>(A, st.Q);
+      jacobi_rot<0, 2, 3>(A, st.Q);
+      jacobi_rot<1, 2, 3>(A, st.Q);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float e = fmaxf(A[k][k], -0.999999f);
+    const float sk = sqrtf(1.f + e);
+    st.s[k] = sk;
+    st.g[k] = e * sk / (sk + 1.f);
+  }
+}
+
+// tau for the fixed-corotated model (R21, S1)
+template <int D>
+__device__ __forceinline__ void kirchhoff_fcr(const float (&H)[D][D], float mu, float lam, const float* sig,
+                                              float (&tau)[D][D], float jm1) {
+  Stretch<D> st;
+  left_stretch<D>(H, st);
+  float F[D][D];
+  F_of_H<D>(H, F);
+  const float lj = lam * (1.f + jm1) * jm1;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = a; b < D; ++b) {
+      float fsf = 0.f, bv = 0.f;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        fsf = fmaf(F[a][c] * sig[c], F[b][c], fsf);
+        bv = fmaf(st.Q[a][c] * st.g[c], st.Q[b][c], bv);
+      }
+      float t = fmaf(2.f * mu, bv, fsf);
+      if (a == b) t += lj;
       tau[a][b] = t;
       tau[b][a] = t;
     }
@@ -823,7 +915,7 @@ constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(fl
 // spreads them over 32.  It permutes every aligned group of 8, so [0, kCap) maps onto itself.
 __device__ __forceinline__ int pay_slot(int p) { return p ^ (((p >> 5) ^ (p >> 7)) & 7); }
 
-template <int D, bool ADJ>
+template <int D, bool ADJ, int MAT = 0>
 __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   using DD = Dim<D>;
@@ -978,7 +1070,8 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
           if (!(jm1 > -1.f)) latch(A.err, E_INVERTED, A.t, u);
           const float lnJ = log1pf(jm1);
           float tau[D][D];
-          kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, lnJ);
+          if constexpr (MAT == 1) kirchhoff_fcr<D>(H, pr.z, pr.w, sig, tau, jm1);  // R21
+          else kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, lnJ);
           // B = dx G = -4 res dt V tau + m dx C ;  A = m v - B fx
           const float kk = 4.f * P.fres * P.dt * pr.y;
           const float mdx = pr.x * P.dx;
@@ -1460,7 +1553,7 @@ __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, 
   pass_row<D, 2, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
 }
 
-template <int D, bool MG>
+template <int D, bool MG, int MAT>
 __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArgs& A, const float4* s_v,
                                                  const float4* s_a, const float4& aref, const int* bc,
                                                  int r, int k, int& aid_out, float* dsig_out) {
@@ -1531,7 +1624,8 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   {
     float H[D][D], tau[D][D], q0[D];
     load_H<D>(A.st, NT, j, H);
-    kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, log1pf(det1m<D>(H)));
+    if constexpr (MAT == 1) kirchhoff_fcr<D>(H, pr.z, pr.w, sig, tau, det1m<D>(H));
+    else kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, log1pf(det1m<D>(H)));
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       q0[a] = pr.x * __ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]);
@@ -1576,6 +1670,48 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   float trT = 0.f;
 #pragma unroll
   for (int a = 0; a < D; ++a) trT += T[a][a];
+  // fixed-corotated (R21): tau_el = 2 mu (B - V) + lam J (J - 1) I.  With Y solving
+  // V Y + Y V = sym(T) (diagonal in V's eigenbasis: Y' = (Q^T sym(T) Q) / (s_i + s_j)),
+  // dL/dF = 2 mu ((T + T^T) F - 2 Y F) + lam (2J - 1) J tr(T) F^-T;  dL/dmu = 2 T : (B - V)
+  float YF[D][D] = {}, dmu_fcr = 0.f;
+  if constexpr (MAT == 1) {
+    Stretch<D> sv;
+    left_stretch<D>(H, sv);
+    float M[D][D], Y[D][D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+      for (int q = 0; q < D; ++q) {
+        float acc = 0.f;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) acc = fmaf(sv.Q[a][i] * 0.5f * (T[a][b] + T[b][a]), sv.Q[b][q], acc);
+        M[i][q] = acc;
+      }
+#pragma unroll
+    for (int i = 0; i < D; ++i) dmu_fcr = fmaf(2.f * sv.g[i], M[i][i], dmu_fcr);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+          for (int q = 0; q < D; ++q) acc = fmaf(sv.Q[a][i] * M[i][q] / (sv.s[i] + sv.s[q]), sv.Q[b][q], acc);
+        Y[a][b] = acc;
+      }
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) {
+        float acc = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) acc = fmaf(Y[a][c], F[c][b], acc);
+        YF[a][b] = acc;
+      }
+  }
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -1587,8 +1723,14 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         acc = fmaf(P.dt * Cn[c][a], gi[(size_t)comp_F<D>(c, b) * NT + k], acc);
         tf = fmaf(T[a][c] + T[c][a], F[c][b], tf);
       }
-      acc = fmaf(pr.z + sig[b], tf, acc);  // mu (T+T^T) F + (T+T^T) F sigma
-      acc = fmaf(pr.w * trT, FiT[a][b], acc);
+      if constexpr (MAT == 1) {
+        acc = fmaf(2.f * pr.z + sig[b], tf, acc);  // 2 mu (T+T^T) F + (T+T^T) F sigma
+        acc = fmaf(-4.f * pr.z, YF[a][b], acc);
+        acc = fmaf(pr.w * (2.f * J - 1.f) * J * trT, FiT[a][b], acc);
+      } else {
+        acc = fmaf(pr.z + sig[b], tf, acc);  // mu (T+T^T) F + (T+T^T) F sigma
+        acc = fmaf(pr.w * trT, FiT[a][b], acc);
+      }
       go[(size_t)comp_F<D>(a, b) * NT + j] = acc;
     }
   float dmu = 0.f;
@@ -1601,10 +1743,11 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
 #pragma unroll
       for (int c = 0; c < D; ++c) tf = fmaf(T[b][c], F[c][a], tf);
       ds = fmaf(F[b][a], tf, ds);
-      dmu = fmaf(T[a][b], ffti<D>(H, a, b), dmu);  // T : (F F^T - I), formed from H
+      if constexpr (MAT == 0) dmu = fmaf(T[a][b], ffti<D>(H, a, b), dmu);  // T : (F F^T - I), formed from H
     }
     dsig_out[a] = P.act_s * ds;
   }
+  if constexpr (MAT == 1) dmu = dmu_fcr;
   A.dmu[u] = dmu0 + dmu;  // plain RMW (unique per particle): measured 36 us faster than a fp32 RED
   if (MG) {
     // NEXT N3: dL/dm_p = sum_i W dm_i + v . sum_i W dp_i + C : Q  (chain rule through Eqs. 3-5;
@@ -1618,7 +1761,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     }
     A.dmass[u] = dm0 + gmass;
   }
-  A.dlam[u] = dlam0 + trT * lnJ;
+  A.dlam[u] = dlam0 + trT * (MAT == 1 ? J * jm1 : lnJ);  // dtau/dlam = J (J - 1) I (R21) | ln J I (R1)
   aid_out = ai;
 }
 
@@ -1645,7 +1788,7 @@ __device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArg
   }
 }
 
-template <int D, bool MG>
+template <int D, bool MG, int MAT = 0>
 __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   __shared__ float4 s_v[Dim<D>::TN];
@@ -1676,7 +1819,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       const int i = i0 + threadIdx.x;
       int ai = -1;
       float dsig[D] = {};
-      if (i < n) p2g_adj_particle<D, MG>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
+      if (i < n) p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
       __syncwarp();
       if (P.K > 0) reduce_actuation<D>(P, A, r, ai, dsig);
     }

@@ -45,7 +45,8 @@ class _Config(C.Structure):
                 ("n_particles", C.c_int32), ("max_steps", C.c_int32), ("n_actuators", C.c_int32),
                 ("dt", C.c_float), ("gravity", C.c_float * 3), ("bound", C.c_int32),
                 ("friction", C.c_float * 6), ("act_strength", C.c_float), ("device", C.c_int32),
-                ("stream", C.c_void_p), ("grid_slots", C.c_int32), ("checkpoint_every", C.c_int32)]
+                ("stream", C.c_void_p), ("grid_slots", C.c_int32), ("checkpoint_every", C.c_int32),
+                ("material", C.c_int32)]
 
 
 _lib = None
@@ -137,6 +138,7 @@ class Config:
     stream: int = 0
     grid_slots: int = 0
     checkpoint_every: int = 0  # NEXT N2: 0 = full memo; k = k-step segments + checkpoints
+    material: int = 0          # NEXT N3: 0 = neo-Hookean (R1), 1 = fixed-corotated (R21)
 
     @classmethod
     def from_scene(cls, sc, max_steps=None, **kw):
@@ -151,7 +153,7 @@ class Config:
         return _Config(self.dim, self.res, self.batch, self.n_particles, self.max_steps,
                        self.n_actuators, self.dt, (C.c_float * 3)(*g[:3]), self.bound,
                        (C.c_float * 6)(*f[:6]), self.act_strength, self.device,
-                       self.stream or None, self.grid_slots, self.checkpoint_every)
+                       self.stream or None, self.grid_slots, self.checkpoint_every, self.material)
 
 
 class MPM:

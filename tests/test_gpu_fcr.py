@@ -1,0 +1,58 @@
+"""NEXT N3 on the GPU: the fixed-corotated material (config.material = 1, DESIGN R21) --
+state and every gradient family vs the oracle, whose fixed-corotated path follows the paper's
+dP/dF route (dR/dF of the polar decomposition) while the kernels use the Kirchhoff form with a
+Lyapunov solve on the left stretch: independent derivations."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1810_01054_b200 import mpm, scenes
+from tests.helpers import oracle_cfg, oracle_params, oracle_state, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name,T,tol_state", [("tiny2", 40, 1e-4), ("tiny3", 30, 1e-4), ("C2", 100, 1e-3),
+                                              ("C3", 60, 1e-3)])
+def test_fcr_state_and_gradients_vs_oracle(name, T, tol_state):
+    if name == "tiny2":
+        sc = scenes.tiny(2, seed=61, res=32, n_cells=(8, 8), steps=T, K=2, s=40.0)
+    elif name == "tiny3":
+        sc = scenes.tiny(3, seed=62, res=32, n_cells=(6, 6, 6), steps=T, K=2, s=40.0)
+    else:
+        sc = scenes.CONFIGS[name](steps=T)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, material=1))
+    sim.set_scene(sc)
+    sim.forward(T)
+    x, v, F, Cm = sim.get_state(T)
+    cfg = oracle_cfg(sc, material=1)
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    traj = oracle.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, act[:T], T)
+    ox, ov, oC, oF = oracle.unpack(traj[T], sc.dim)
+    for k, a, b in (("x", x, ox), ("v", v, ov), ("F", F, oF), ("C", Cm, oC)):
+        assert rel_err(a, b) < tol_state, (k, rel_err(a, b))
+    rng = np.random.default_rng(5)
+    w = rng.standard_normal(traj[T].shape)
+    wx, wv, wC, wF = oracle.unpack(w, sc.dim)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    g0, gE, gnu, ga = oracle.backward(cfg, traj, m, vol, E, nu, aid, act[:T], w)
+    gx, gv, gC, gF = oracle.unpack(g0, sc.dim)
+    errs = {k: rel_err(a, b) for k, a, b in (
+        ("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF), ("dC0", g["dC0"], gC),
+        ("dE", g["dE"], gE), ("dnu", g["dnu"], gnu), ("da", g["da"][0, :T], ga))}
+    assert all(e < 1e-3 for e in errs.values()), errs
+
+
+def test_fcr_one_step_tight():
+    """One step: state within the north_star's 1e-5."""
+    sc = scenes.tiny(3, seed=63, res=32, n_cells=(6, 6, 6), steps=1, K=2, s=40.0)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=1, material=1))
+    sim.set_scene(sc)
+    sim.forward(1)
+    cfg = oracle_cfg(sc, material=1)
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    traj = oracle.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, act[:1], 1)
+    for a, b in zip(sim.get_state(1), (lambda u: (u[0], u[1], u[3], u[2]))(oracle.unpack(traj[1], 3))):
+        assert rel_err(a, b) < 1e-5
