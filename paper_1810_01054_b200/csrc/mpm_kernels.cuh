@@ -22,6 +22,12 @@
 #ifndef MPM_P2GT_MINB
 #define MPM_P2GT_MINB 4
 #endif
+#ifndef MPM_P2GT_PF
+#define MPM_P2GT_PF 0  // block-prologue L2 prefetch of the records: measured 12 us slower (the loads overlap anyway)
+#endif
+#ifndef MPM_G2P_PF
+#define MPM_G2P_PF 1
+#endif
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
 #endif
@@ -1386,11 +1392,13 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
     float4 vref, aref_unused;
+#if MPM_G2P_PF
     for (int i = threadIdx.x; i < n; i += kThreads) {  // this block's x, F -> L2
       const int j = __ldg(&A.perm[s + i]);
       prefetch_record(A.st, NT, j, 0, D);
       prefetch_record(A.st, NT, j, comp_F<D>(0, 0), D * D);
     }
+#endif
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += kThreads) {
@@ -1807,12 +1815,14 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
     float4 vref, aref;  // block-centre shifts (see stage_tile)
+#if MPM_P2GT_PF
     for (int i = threadIdx.x; i < n; i += MPM_P2GT_THREADS) {  // this block's particle records -> L2
       const int k = s + i, j = __ldg(&A.perm[k]), u = __ldg(&A.orig_next[k]);
       prefetch_record(A.st, NT, j, 0, Dim<D>::S);
       prefetch_record(A.gin, NT, k, 0, Dim<D>::S);
       prefetch_l2(&A.prm[u]);
     }
+#endif
     stage_tile<D, true, MPM_P2GT_THREADS>(P, A, r, bc, s_v, s_a, abase, vref, aref);
     __syncthreads();
     for (int i0 = 0; i0 < n; i0 += MPM_P2GT_THREADS) {  // uniform trip count: whole warps reach the reduction
