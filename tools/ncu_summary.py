@@ -8,9 +8,10 @@ import json
 import subprocess
 import sys
 
-BENCH_NAME = {"k_block_scatter<3, 0>": "p2g", "k_block_scatter<3, 1>": "g2p_T", "k_g2p<3>": "g2p",
-              "k_p2g_adj<3, 0>": "p2g_T", "k_p2g_adj<3, 1>": "p2g_T_massgrad", "k_grid_adj<3>": "grid_T",
-              "k_scan_a<3>": "scan_a", "k_scan_b": "scan_b", "k_scan_c": "scan_c", "k_scatter": "scatter"}
+BENCH_NAME = {"k_block_scatter<3, 0, 0>": "p2g", "k_block_scatter<3, 1, 0>": "g2p_T", "k_g2p<3>": "g2p",
+              "k_p2g_adj<3, 0, 0>": "p2g_T", "k_p2g_adj<3, 1, 0>": "p2g_T_massgrad", "k_grid_adj<3>": "grid_T",
+              "k_scan_lookback<3>": "scan", "k_scatter": "scatter",
+              "k_block_scatter<3, 0, 1>": "p2g_fcr", "k_p2g_adj<3, 0, 1>": "p2g_T_fcr"}
 
 KEYS = [
     ("time_us", "gpu__time_duration.sum", "us"),
