@@ -173,3 +173,23 @@ def test_slab_config_errors():
     with pytest.raises(mpm.MPMError) as e:
         u.set_slab(0, 32, 1)
     assert e.value.status == "MPM_ERR_INVALID_ARG"
+
+
+def test_nccl_transport_single_rank():
+    """The NCCL path itself (dlopen of libnccl, ncclCommInitRank, the da all-reduce) on a
+    one-rank communicator: a whole-domain slab with a communicator equals the plain run."""
+    T = 10
+    sc = scenes.tiny(3, seed=16, res=32, n_cells=(6, 6, 6), steps=T, K=2, s=40.0)
+    a = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    a.set_scene(sc)
+    b = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    b.set_slab(0, sc.res, 1)
+    b.comm_init(0, 1, mpm.comm_unique_id())
+    b.set_scene(sc)
+    w = np.random.default_rng(17).standard_normal((sc.n, 3)).astype(np.float32)  # not the CoM loss (dE = 0)
+    for s_ in (a, b):
+        s_.forward(T)
+        s_.backward(w)
+    ga, gb = a.grad(), b.grad()
+    for k in ("dx0", "dv0", "dE", "da"):
+        assert rel_err(gb[k], ga[k]) < 1e-5, k
