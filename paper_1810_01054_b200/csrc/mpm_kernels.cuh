@@ -28,6 +28,9 @@
 #ifndef MPM_G2P_PF
 #define MPM_G2P_PF 1
 #endif
+#ifndef MPM_FFMA2
+#define MPM_FFMA2 1  // packed fp32x2 FMAs (sm_100 FFMA2) in the stencil sums
+#endif
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
 #endif
@@ -1356,6 +1359,43 @@ template <int D, int OX, int OY>
 __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const Stencil<D>& sc,
                                         const float4& vref, float* S, float (&M)[D][D]) {
   const float wxy = sc.w[0][OX] * sc.w[1][OY];
+#if MPM_FFMA2
+  if constexpr (D == 3) {
+    // row sums a0 = sum_oz wz v, a1 = sum_oz oz wz v with packed fp32x2 FMAs on (x, y)
+    // (sm_100 FFMA2: per component the same fused op as fmaf), z as scalar FMAs
+    float2 a0 = make_float2(0.f, 0.f), a1 = a0;
+    float a0z = 0.f, a1z = 0.f;
+#pragma unroll
+    for (int oz = 0; oz < 3; ++oz) {
+      const float4 g = s_v[tile_idx<D, OX, OY, 0>(lb) + oz];
+      const float wz = sc.w[2][oz];
+      const float2 vxy = make_float2(g.x, g.y);
+      a0 = __ffma2_rn(make_float2(wz, wz), vxy, a0);
+      a0z = fmaf(wz, g.z, a0z);
+      if (oz) {
+        const float ow = (float)oz * wz;
+        a1 = __ffma2_rn(make_float2(ow, ow), vxy, a1);
+        a1z = fmaf(ow, g.z, a1z);
+      }
+    }
+    const float2 w2 = make_float2(wxy, wxy);
+    float2 sxy = __ffma2_rn(w2, a0, make_float2(S[0], S[1]));
+    S[0] = sxy.x; S[1] = sxy.y; S[2] = fmaf(wxy, a0z, S[2]);
+    if (OX) {
+      const float2 m = __ffma2_rn(make_float2((float)OX * wxy, (float)OX * wxy), a0, make_float2(M[0][0], M[1][0]));
+      M[0][0] = m.x; M[1][0] = m.y; M[2][0] = fmaf((float)OX * wxy, a0z, M[2][0]);
+    }
+    if (OY) {
+      const float2 m = __ffma2_rn(make_float2((float)OY * wxy, (float)OY * wxy), a0, make_float2(M[0][1], M[1][1]));
+      M[0][1] = m.x; M[1][1] = m.y; M[2][1] = fmaf((float)OY * wxy, a0z, M[2][1]);
+    }
+    {
+      const float2 m = __ffma2_rn(w2, a1, make_float2(M[0][2], M[1][2]));
+      M[0][2] = m.x; M[1][2] = m.y; M[2][2] = fmaf(wxy, a1z, M[2][2]);
+    }
+    return;
+  }
+#endif
   float Sxy[D], Zxy[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) Sxy[a] = Zxy[a] = 0.f;
