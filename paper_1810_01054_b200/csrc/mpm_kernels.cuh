@@ -31,6 +31,12 @@
 #ifndef MPM_FFMA2
 #define MPM_FFMA2 1  // packed fp32x2 FMAs (sm_100 FFMA2) in the stencil sums
 #endif
+#ifndef MPM_FFMA2_SCAT
+#define MPM_FFMA2_SCAT 1
+#endif
+#ifndef MPM_FFMA2_P2GT
+#define MPM_FFMA2_P2GT 0  // ... in P2G^T too: measured 3 us slower (128-register cliff: pair alignment spills)
+#endif
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
 #endif
@@ -1158,6 +1164,23 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 #pragma unroll
             for (int oy = 0; oy < 3; ++oy) {
               const float wxy = wx * s_pay[PY::W + 3 + oy][i];
+#if MPM_FFMA2_SCAT
+              // node value A + oy B1 + oz B2 and the accumulation as packed fp32x2 FMAs:
+              // (x, y) and (z, m) pairs (sm_100 FFMA2; per component the same fused op)
+              const float2 rxy = __ffma2_rn(make_float2((float)oy, (float)oy), make_float2(B1[0], B1[1]),
+                                            make_float2(Ax[0], Ax[1]));
+              const float rz = fmaf((float)oy, B1[2], Ax[2]);
+#pragma unroll
+              for (int oz = 0; oz < 3; ++oz) {
+                const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
+                float4& q = acc[oy * 3 + oz];
+                const float2 vxy = oz ? __ffma2_rn(make_float2((float)oz, (float)oz), make_float2(B2[0], B2[1]), rxy) : rxy;
+                const float vz = oz ? fmaf((float)oz, B2[2], rz) : rz;
+                const float2 qxy = __ffma2_rn(make_float2(W, W), vxy, make_float2(q.x, q.y));
+                const float2 qzw = __ffma2_rn(make_float2(W, W), make_float2(vz, ADJ ? 0.f : mp), make_float2(q.z, q.w));
+                q = make_float4(qxy.x, qxy.y, qzw.x, ADJ ? q.w : qzw.y);
+              }
+#else
 #pragma unroll
               for (int oz = 0; oz < 3; ++oz) {
                 const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
@@ -1167,6 +1190,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
                 q.z = fmaf(W, Ax[2] + (float)oy * B1[2] + (float)oz * B2[2], q.z);
                 if (!ADJ) q.w = fmaf(W, mp, q.w);
               }
+#endif
             }
           } else {
             float B1[2];
@@ -1582,6 +1606,86 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
   }
 }
 
+// 3-D pass with packed fp32x2 FMAs (sm_100 FFMA2): the (x, y) components of S, M and the
+// (g0, g1) / (t1, t2) pairs advance in one instruction; per component the same fused op as fmaf
+struct PassAcc2 {
+  float2 S, M0, M1, M2, g01;  // (x, y) of S, M[.][0..2], (g0, g1)
+  float Sz, Mz0, Mz1, Mz2, g2, Se;
+};
+
+template <int OX, int OY, bool WS>
+__device__ __forceinline__ void pass_row2(const float4* tile, const int* lb, const float (&w)[3][3],
+                                          const float (&dw)[3][3], const float* c0, const float (&Cm)[3][3],
+                                          float em, PassAcc2& R) {
+  float cxy[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    cxy[a] = c0[a];
+    if (OX) cxy[a] = fmaf((float)OX, Cm[a][0], cxy[a]);
+    if (OY) cxy[a] = fmaf((float)OY, Cm[a][1], cxy[a]);
+  }
+  float2 A0 = make_float2(0.f, 0.f), A1 = A0, t12 = A0;
+  float A0z = 0.f, A1z = 0.f, Aw = 0.f;
+#pragma unroll
+  for (int oz = 0; oz < 3; ++oz) {
+    const float4 q = tile[tile_idx<3, OX, OY, 0>(lb) + oz];
+    float sv = em * q.w;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) sv = fmaf((&q.x)[a], oz == 0 ? cxy[a] : fmaf((float)oz, Cm[a][2], cxy[a]), sv);
+    const float wz = w[2][oz];
+    const float2 fxy = make_float2(q.x, q.y);
+    A0 = __ffma2_rn(make_float2(wz, wz), fxy, A0);
+    A0z = fmaf(wz, q.z, A0z);
+    if (oz) {
+      const float ow = (float)oz * wz;
+      A1 = __ffma2_rn(make_float2(ow, ow), fxy, A1);
+      A1z = fmaf(ow, q.z, A1z);
+    }
+    t12 = __ffma2_rn(make_float2(wz, dw[2][oz]), make_float2(sv, sv), t12);
+    if (WS) Aw = fmaf(wz, q.w, Aw);
+  }
+  const float wx = w[0][OX], wy = w[1][OY], wxy = wx * wy;
+  if (WS) R.Se = fmaf(wxy, Aw, R.Se);
+  const float2 gw = __fmul2_rn(make_float2(dw[0][OX], wx), make_float2(wy, dw[1][OY]));
+  R.g01 = __ffma2_rn(gw, make_float2(t12.x, t12.x), R.g01);
+  R.g2 = fmaf(wxy, t12.y, R.g2);
+  const float2 w2 = make_float2(wxy, wxy);
+  R.S = __ffma2_rn(w2, A0, R.S);
+  R.Sz = fmaf(wxy, A0z, R.Sz);
+  if (OX) {
+    const float v = (float)OX * wxy;
+    R.M0 = __ffma2_rn(make_float2(v, v), A0, R.M0);
+    R.Mz0 = fmaf(v, A0z, R.Mz0);
+  }
+  if (OY) {
+    const float v = (float)OY * wxy;
+    R.M1 = __ffma2_rn(make_float2(v, v), A0, R.M1);
+    R.Mz1 = fmaf(v, A0z, R.Mz1);
+  }
+  R.M2 = __ffma2_rn(w2, A1, R.M2);
+  R.Mz2 = fmaf(wxy, A1z, R.Mz2);
+}
+
+template <bool WS>
+__device__ __forceinline__ void stencil_pass2(const float4* tile, const int* lb, const float (&w)[3][3],
+                                              const float (&dw)[3][3], const float* c0, const float (&Cm)[3][3],
+                                              float em, PassAcc<3>& Ro) {
+  PassAcc2 R;
+  R.S = R.M0 = R.M1 = R.M2 = R.g01 = make_float2(0.f, 0.f);
+  R.Sz = R.Mz0 = R.Mz1 = R.Mz2 = R.g2 = R.Se = 0.f;
+  pass_row2<0, 0, WS>(tile, lb, w, dw, c0, Cm, em, R); pass_row2<0, 1, WS>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row2<0, 2, WS>(tile, lb, w, dw, c0, Cm, em, R); pass_row2<1, 0, WS>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row2<1, 1, WS>(tile, lb, w, dw, c0, Cm, em, R); pass_row2<1, 2, WS>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row2<2, 0, WS>(tile, lb, w, dw, c0, Cm, em, R); pass_row2<2, 1, WS>(tile, lb, w, dw, c0, Cm, em, R);
+  pass_row2<2, 2, WS>(tile, lb, w, dw, c0, Cm, em, R);
+  Ro.S[0] = R.S.x; Ro.S[1] = R.S.y; Ro.S[2] = R.Sz;
+  Ro.M[0][0] = R.M0.x; Ro.M[1][0] = R.M0.y; Ro.M[2][0] = R.Mz0;
+  Ro.M[0][1] = R.M1.x; Ro.M[1][1] = R.M1.y; Ro.M[2][1] = R.Mz1;
+  Ro.M[0][2] = R.M2.x; Ro.M[1][2] = R.M2.y; Ro.M[2][2] = R.Mz2;
+  Ro.g[0] = R.g01.x; Ro.g[1] = R.g01.y; Ro.g[2] = R.g2;
+  Ro.Se = R.Se;
+}
+
 template <int D, bool WS>
 __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, const float (&w)[D][3],
                                              const float (&dw)[D][3], const float* c0,
@@ -1594,6 +1698,12 @@ __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, 
     for (int b = 0; b < D; ++b) R.M[a][b] = 0.f;
   }
   R.Se = 0.f;
+#if MPM_FFMA2_P2GT
+  if constexpr (D == 3) {
+    stencil_pass2<WS>(tile, lb, w, dw, c0, Cm, em, R);  // ref is zero at every call site
+    return;
+  }
+#endif
   pass_row<D, 0, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 0, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
   pass_row<D, 0, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
   pass_row<D, 1, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
