@@ -35,7 +35,7 @@
 #define MPM_FFMA2_SCAT 1
 #endif
 #ifndef MPM_FFMA2_P2GT
-#define MPM_FFMA2_P2GT 0  // ... in P2G^T too: measured 3 us slower (128-register cliff: pair alignment spills)
+#define MPM_FFMA2_P2GT 0  // ... in P2G^T (bit 0: v-pass, bit 1: dp-pass): both measured 3 us slower (128-register cliff)
 #endif
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
@@ -1686,7 +1686,7 @@ __device__ __forceinline__ void stencil_pass2(const float4* tile, const int* lb,
   Ro.Se = R.Se;
 }
 
-template <int D, bool WS>
+template <int D, bool WS, bool F2 = false>
 __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, const float (&w)[D][3],
                                              const float (&dw)[D][3], const float* c0,
                                              const float (&Cm)[D][D], float em, const float4& ref,
@@ -1698,12 +1698,10 @@ __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, 
     for (int b = 0; b < D; ++b) R.M[a][b] = 0.f;
   }
   R.Se = 0.f;
-#if MPM_FFMA2_P2GT
-  if constexpr (D == 3) {
+  if constexpr (D == 3 && F2) {
     stencil_pass2<WS>(tile, lb, w, dw, c0, Cm, em, R);  // ref is zero at every call site
     return;
   }
-#endif
   pass_row<D, 0, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 0, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
   pass_row<D, 0, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
   pass_row<D, 1, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
@@ -1760,7 +1758,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         u0[a] = fmaf(-U[a][b], sc.fx[b], u0[a]);
       }
     }
-    stencil_pass<D, false>(s_v, lb, sc.w, dw, u0, U, 0.f, make_float4(0.f, 0.f, 0.f, 0.f), Rv);
+    stencil_pass<D, false, (MPM_FFMA2_P2GT & 1) != 0>(s_v, lb, sc.w, dw, u0, U, 0.f, make_float4(0.f, 0.f, 0.f, 0.f), Rv);
     // dx term -4 res^2 g_C^T v^{t+1} = -res U^T S_v
 #pragma unroll
     for (int a = 0; a < D; ++a) {
@@ -1793,7 +1791,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         q0[a] = fmaf(-Gm[a][b], sc.fx[b], q0[a]);
       }
     }
-    stencil_pass<D, MG>(s_a, lb, sc.w, dw, q0, Gm, pr.x, make_float4(0.f, 0.f, 0.f, 0.f), Rd);
+    stencil_pass<D, MG, (MPM_FFMA2_P2GT & 2) != 0>(s_a, lb, sc.w, dw, q0, Gm, pr.x, make_float4(0.f, 0.f, 0.f, 0.f), Rd);
   }
   const float m = pr.x;
   float* go = A.gout;
