@@ -1383,8 +1383,7 @@ template <int D, int OX, int OY>
 __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const Stencil<D>& sc,
                                         const float4& vref, float* S, float (&M)[D][D]) {
   const float wxy = sc.w[0][OX] * sc.w[1][OY];
-#if MPM_FFMA2
-  if constexpr (D == 3) {
+  if constexpr (D == 3 && MPM_FFMA2) {
     // row sums a0 = sum_oz wz v, a1 = sum_oz oz wz v with packed fp32x2 FMAs on (x, y)
     // (sm_100 FFMA2: per component the same fused op as fmaf), z as scalar FMAs
     float2 a0 = make_float2(0.f, 0.f), a1 = a0;
@@ -1417,25 +1416,24 @@ __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const 
       const float2 m = __ffma2_rn(w2, a1, make_float2(M[0][2], M[1][2]));
       M[0][2] = m.x; M[1][2] = m.y; M[2][2] = fmaf(wxy, a1z, M[2][2]);
     }
-    return;
-  }
-#endif
-  float Sxy[D], Zxy[D];
-#pragma unroll
-  for (int a = 0; a < D; ++a) Sxy[a] = Zxy[a] = 0.f;
-  if constexpr (D == 3) {
-    g2p_node<D, OX, OY, 0>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
-    g2p_node<D, OX, OY, 1>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
-    g2p_node<D, OX, OY, 2>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
   } else {
-    g2p_node<D, OX, OY, 0>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
-  }
+    float Sxy[D], Zxy[D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    S[a] += Sxy[a];
-    if (OX) M[a][0] = fmaf((float)OX, Sxy[a], M[a][0]);
-    if (OY) M[a][1] = fmaf((float)OY, Sxy[a], M[a][1]);
-    if constexpr (D == 3) M[a][2] += Zxy[a];
+    for (int a = 0; a < D; ++a) Sxy[a] = Zxy[a] = 0.f;
+    if constexpr (D == 3) {
+      g2p_node<D, OX, OY, 0>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
+      g2p_node<D, OX, OY, 1>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
+      g2p_node<D, OX, OY, 2>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
+    } else {
+      g2p_node<D, OX, OY, 0>(s_v, lb, sc, vref, wxy, Sxy, Zxy);
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      S[a] += Sxy[a];
+      if (OX) M[a][0] = fmaf((float)OX, Sxy[a], M[a][0]);
+      if (OY) M[a][1] = fmaf((float)OY, Sxy[a], M[a][1]);
+      if constexpr (D == 3) M[a][2] += Zxy[a];
+    }
   }
 }
 
@@ -1952,7 +1950,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
   __shared__ int s_blk;
   const int n_occ = A.info_t[I_NOCC];
   const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
-  const size_t NT = P.NT;
+  [[maybe_unused]] const size_t NT = P.NT;  // used by the optional record prefetch (MPM_P2GT_PF)
   for (;;) {
     if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
     __syncthreads();
