@@ -2,6 +2,8 @@
 seeded fp32 inputs.  Bars (BASELINE.json north_star): binning bit-exact; state within 1e-5
 relative after 1 step and 1e-3 after 100 steps; gradients within 1e-3 relative
 (norm-wise per field, reading R16)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -229,3 +231,17 @@ def test_mass_gradient_and_running_loss_parity(d, T):
     g2 = sim.grad()
     g0b, *_ = oracle.backward(cfg, traj, m, vol, E, nu, aid, act[:T], W[T])
     assert rel_err(g2["dx0"], oracle.unpack(g0b, d)[0]) < 1e-3
+
+
+def test_c_abi_demo_program(tmp_path):
+    """The boundary is a plain C ABI: examples/c_api_demo.c (no Python, no torch) builds
+    with gcc against include/mpm.h + libmpm.so and reproduces the CoM closed form."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "c_api_demo")
+    lib = os.path.join(root, "paper_1810_01054_b200")
+    subprocess.check_call(["gcc", "-std=c99", "-O2", "-I", os.path.join(root, "include"),
+                           os.path.join(root, "examples", "c_api_demo.c"), "-L", lib, "-lmpm",
+                           f"-Wl,-rpath,{lib}", "-lm", "-o", exe])
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
