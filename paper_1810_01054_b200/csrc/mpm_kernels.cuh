@@ -54,7 +54,8 @@ constexpr int kThreads = 256;    // CTA size of the block-tile kernels
 constexpr int kCap = 512;        // particles per producer chunk
 constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks use scratch)
 constexpr int kScanTile = kThreads;
-constexpr int kScatQ = 4;        // particles per thread in k_scatter  // grid blocks per scan tile (one per thread)
+constexpr int kScatQ = 4;        // particles per thread in k_scatter
+constexpr int kMaxAct = 64;      // n_actuators cap (mpm_create validates)  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
 
 // Programmatic dependent launch (sm_90+): a kernel of the step path waits for its
@@ -1920,11 +1921,13 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
 }
 
 // Segmented warp reduction of the actuation gradient (step K -> dL/da[r][t][k]): one
-// butterfly sum and one global atomic per distinct actuator id in the warp.  Called by all
-// 32 lanes (key < 0 = no contribution).
+// butterfly sum per distinct actuator id in the warp, added by one lane into the warp's own
+// shared-memory slot; the CTA sums its warps' slots and adds them to global memory once per
+// rollout it worked on (one global RED per actuator component per CTA instead of per warp:
+// every warp adding to the same K*D addresses serialised in L2).  Called by all 32 lanes
+// (key < 0 = no contribution).
 template <int D>
-__device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArgs& A, int r, int key,
-                                                 const float* v) {
+__device__ __forceinline__ void reduce_actuation(float* w_da, int key, const float* v) {
   const int lane = threadIdx.x & 31;
   unsigned todo = __ballot_sync(0xffffffffu, key >= 0);
   while (todo) {
@@ -1937,7 +1940,7 @@ __device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArg
       float s = mine ? v[a] : 0.f;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == src) atomicAdd(&A.da[(((size_t)r * P.T + A.t) * P.K + k0) * D + a], s);
+      if (lane == src) w_da[k0 * D + a] += s;  // this warp's slot: one lane per key, no atomics
     }
   }
 }
@@ -1945,12 +1948,29 @@ __device__ __forceinline__ void reduce_actuation(const KParams& P, const StepArg
 template <int D, bool MG, int MAT = 0>
 __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
+  constexpr int NW = MPM_P2GT_THREADS / 32;
   __shared__ float4 s_v[Dim<D>::TN];
   __shared__ float4 s_a[Dim<D>::TN];
   __shared__ int s_blk;
+  __shared__ float s_da[NW][kMaxAct * D];  // per-warp dL/da[r][t][:][:] partial sums
+  __shared__ int s_da_r;                   // the rollout they belong to (-1: none)
   const int n_occ = A.info_t[I_NOCC];
   const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
   [[maybe_unused]] const size_t NT = P.NT;  // used by the optional record prefetch (MPM_P2GT_PF)
+  const int KD = P.K * D;
+  for (int q = threadIdx.x; q < NW * kMaxAct * D; q += MPM_P2GT_THREADS) (&s_da[0][0])[q] = 0.f;
+  if (threadIdx.x == 0) s_da_r = -1;
+  auto flush_da = [&](int rr) {  // all threads, after a barrier: sum the warps' slots
+    for (int q = threadIdx.x; q < KD; q += MPM_P2GT_THREADS) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        v += s_da[w][q];
+        s_da[w][q] = 0.f;
+      }
+      if (v != 0.f) atomicAdd(&A.da[((size_t)rr * P.T + A.t) * KD + q], v);
+    }
+  };
   for (;;) {
     if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
     __syncthreads();
@@ -1960,6 +1980,11 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
     const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
+    if (KD > 0 && r != s_da_r) {  // uniform: a new rollout -> flush the previous one's sums
+      if (s_da_r >= 0) flush_da(s_da_r);
+      __syncthreads();
+      if (threadIdx.x == 0) s_da_r = r;  // read again only after the next claim barrier
+    }
     float4 vref, aref;  // block-centre shifts (see stage_tile)
 #if MPM_P2GT_PF
     for (int i = threadIdx.x; i < n; i += MPM_P2GT_THREADS) {  // this block's particle records -> L2
@@ -1977,10 +2002,11 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       float dsig[D] = {};
       if (i < n) p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
       __syncwarp();
-      if (P.K > 0) reduce_actuation<D>(P, A, r, ai, dsig);
+      if (P.K > 0) reduce_actuation<D>(s_da[threadIdx.x >> 5], ai, dsig);
     }
     __syncthreads();
   }
+  if (KD > 0 && s_da_r >= 0) flush_da(s_da_r);
 }
 
 // ------------------------------------------------------------------------------------
