@@ -1293,6 +1293,10 @@ __device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, i
   for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
 }
 
+template <int D, bool TWO>
+__device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs& A, const int* node, int slot,
+                                                size_t abase, float4& v, float4& ad);
+
 // fetch one node of step t: velocity after the wall projection (v.w = m) and, optionally,
 // the adjoint node (dL/dp_i, dL/dm_i); zero outside the domain / untouched blocks
 template <int D, bool TWO>
@@ -1310,7 +1314,19 @@ __device__ __forceinline__ void fetch_node(const KParams& P, const StepArgs& A, 
   v = make_float4(0.f, 0.f, 0.f, 0.f);
   ad = v;
   if (!inside) return;
-  const int slot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+  fetch_node_slot<D, TWO>(P, A, node, __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]), abase, v, ad);
+}
+
+// the same with the node's grid slot already known (-1: untouched block)
+template <int D, bool TWO>
+__device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs& A, const int* node, int slot,
+                                                size_t abase, float4& v, float4& ad) {
+  using DD = Dim<D>;
+  int loc[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) loc[a] = node[a] & (DD::BB - 1);
+  v = make_float4(0.f, 0.f, 0.f, 0.f);
+  ad = v;
   if (slot < 0) return;
   const size_t addr = (size_t)slot * kCPB + cell_lin<D>(loc);
   const float4 pm = A.tgrid[addr];  // (p, m) as accumulated by P2G -- the memo's grid
@@ -1333,24 +1349,63 @@ __device__ __forceinline__ void fetch_node(const KParams& P, const StepArgs& A, 
 // the quadratic B-spline); the shift removes the common-mode velocity / adjoint so the fp32
 // cancellations in C' (Eq. 8) and in step J shrink to |v_i - vref|.  Callers add the
 // references back where an unshifted sum is needed (v' = S + vref, sum W dp = S_d + aref).
-template <int D, bool TWO, int NTH = kThreads>
+template <int D, bool TWO, int NTH = kThreads, bool SLOTS = TWO>
 __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, int r, const int* bc,
                                            float4* s_v, float4* s_a, size_t abase, float4& vref,
                                            float4& aref) {
   using DD = Dim<D>;
+  // SLOTS: the tile's nodes lie in the 2^D blocks bc + {0, 1}^D (TE = BB + 2 <= 2 BB): look
+  // their grid slots up once, so each node costs one global load instead of a dependent pair
+  // (pays for the extra barrier when two tiles are staged: P2G^T -4 us; G2P +1.3 us)
+  __shared__ int s_slots[1 << D];
+  if (!SLOTS) {
+    {
+      int node[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) node[a] = bc[a] * DD::BB + DD::BB / 2;
+      fetch_node<D, TWO>(P, A, r, node, abase, vref, aref);
+    }
+    for (int tn = threadIdx.x; tn < DD::TN; tn += NTH) {
+      int node[D];
+      int t = tn;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) { node[a] = bc[a] * DD::BB + t % DD::TE; t /= DD::TE; }
+      float4 v, ad;
+      fetch_node<D, TWO>(P, A, r, node, abase, v, ad);
+      s_v[tn] = make_float4(v.x - vref.x, v.y - vref.y, v.z - vref.z, v.w);
+      if (TWO) s_a[tn] = make_float4(ad.x - aref.x, ad.y - aref.y, ad.z - aref.z, ad.w - aref.w);
+    }
+    return;
+  }
+  if (threadIdx.x < (1 << D)) {
+    int nb_[D];
+    bool inside = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      nb_[a] = bc[a] + ((threadIdx.x >> (D - 1 - a)) & 1);
+      inside &= nb_[a] < P.nbpa;
+    }
+    s_slots[threadIdx.x] = inside ? __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]) : -1;
+  }
+  __syncthreads();
   {
     int node[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) node[a] = bc[a] * DD::BB + DD::BB / 2;
-    fetch_node<D, TWO>(P, A, r, node, abase, vref, aref);
+    fetch_node_slot<D, TWO>(P, A, node, s_slots[0], abase, vref, aref);
   }
   for (int tn = threadIdx.x; tn < DD::TN; tn += NTH) {
-    int node[D];
+    int node[D], sb = 0;
     int t = tn;
 #pragma unroll
-    for (int a = D - 1; a >= 0; --a) { node[a] = bc[a] * DD::BB + t % DD::TE; t /= DD::TE; }
+    for (int a = D - 1; a >= 0; --a) {
+      const int l = t % DD::TE;
+      node[a] = bc[a] * DD::BB + l;
+      sb |= (l >= DD::BB) << (D - 1 - a);
+      t /= DD::TE;
+    }
     float4 v, ad;
-    fetch_node<D, TWO>(P, A, r, node, abase, v, ad);
+    fetch_node_slot<D, TWO>(P, A, node, s_slots[sb], abase, v, ad);
     s_v[tn] = make_float4(v.x - vref.x, v.y - vref.y, v.z - vref.z, v.w);
     if (TWO) s_a[tn] = make_float4(ad.x - aref.x, ad.y - aref.y, ad.z - aref.z, ad.w - aref.w);
   }
