@@ -1349,52 +1349,34 @@ __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs
 // the quadratic B-spline); the shift removes the common-mode velocity / adjoint so the fp32
 // cancellations in C' (Eq. 8) and in step J shrink to |v_i - vref|.  Callers add the
 // references back where an unshifted sum is needed (v' = S + vref, sum W dp = S_d + aref).
-template <int D, bool TWO, int NTH = kThreads, bool SLOTS = TWO>
+template <int D, bool TWO, int NTH = kThreads>
 __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, int r, const int* bc,
                                            float4* s_v, float4* s_a, size_t abase, float4& vref,
                                            float4& aref) {
   using DD = Dim<D>;
-  // SLOTS: the tile's nodes lie in the 2^D blocks bc + {0, 1}^D (TE = BB + 2 <= 2 BB): look
-  // their grid slots up once, so each node costs one global load instead of a dependent pair
-  // (pays for the extra barrier when two tiles are staged: P2G^T -4 us; G2P +1.3 us)
-  __shared__ int s_slots[1 << D];
-  if (!SLOTS) {
-    {
-      int node[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) node[a] = bc[a] * DD::BB + DD::BB / 2;
-      fetch_node<D, TWO>(P, A, r, node, abase, vref, aref);
-    }
-    for (int tn = threadIdx.x; tn < DD::TN; tn += NTH) {
-      int node[D];
-      int t = tn;
-#pragma unroll
-      for (int a = D - 1; a >= 0; --a) { node[a] = bc[a] * DD::BB + t % DD::TE; t /= DD::TE; }
-      float4 v, ad;
-      fetch_node<D, TWO>(P, A, r, node, abase, v, ad);
-      s_v[tn] = make_float4(v.x - vref.x, v.y - vref.y, v.z - vref.z, v.w);
-      if (TWO) s_a[tn] = make_float4(ad.x - aref.x, ad.y - aref.y, ad.z - aref.z, ad.w - aref.w);
-    }
-    return;
-  }
-  if (threadIdx.x < (1 << D)) {
+  // the tile's nodes lie in the 2^D blocks bc + {0, 1}^D (TE = BB + 2 <= 2 BB): lanes 0..2^D-1
+  // of every warp look their grid slots up once and each node takes its slot by shuffle, so a
+  // node costs one global load instead of a dependent pair (no barrier needed)
+  const int lane = threadIdx.x & 31;
+  int myslot = -1;
+  if (lane < (1 << D)) {
     int nb_[D];
     bool inside = true;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      nb_[a] = bc[a] + ((threadIdx.x >> (D - 1 - a)) & 1);
+      nb_[a] = bc[a] + ((lane >> (D - 1 - a)) & 1);
       inside &= nb_[a] < P.nbpa;
     }
-    s_slots[threadIdx.x] = inside ? __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]) : -1;
+    if (inside) myslot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
   }
-  __syncthreads();
   {
     int node[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) node[a] = bc[a] * DD::BB + DD::BB / 2;
-    fetch_node_slot<D, TWO>(P, A, node, s_slots[0], abase, vref, aref);
+    fetch_node_slot<D, TWO>(P, A, node, __shfl_sync(0xffffffffu, myslot, 0), abase, vref, aref);
   }
-  for (int tn = threadIdx.x; tn < DD::TN; tn += NTH) {
+  for (int t0 = 0; t0 < DD::TN; t0 += NTH) {  // uniform trip count: whole warps reach the shuffle
+    const int tn = t0 + (int)threadIdx.x;
     int node[D], sb = 0;
     int t = tn;
 #pragma unroll
@@ -1404,10 +1386,13 @@ __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, 
       sb |= (l >= DD::BB) << (D - 1 - a);
       t /= DD::TE;
     }
-    float4 v, ad;
-    fetch_node_slot<D, TWO>(P, A, node, s_slots[sb], abase, v, ad);
-    s_v[tn] = make_float4(v.x - vref.x, v.y - vref.y, v.z - vref.z, v.w);
-    if (TWO) s_a[tn] = make_float4(ad.x - aref.x, ad.y - aref.y, ad.z - aref.z, ad.w - aref.w);
+    const int slot = __shfl_sync(0xffffffffu, myslot, sb);
+    if (tn < DD::TN) {
+      float4 v, ad;
+      fetch_node_slot<D, TWO>(P, A, node, slot, abase, v, ad);
+      s_v[tn] = make_float4(v.x - vref.x, v.y - vref.y, v.z - vref.z, v.w);
+      if (TWO) s_a[tn] = make_float4(ad.x - aref.x, ad.y - aref.y, ad.z - aref.z, ad.w - aref.w);
+    }
   }
 }
 
