@@ -1231,29 +1231,44 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
       __syncthreads();  // payload consumed, tile copies written
     }
 
-    // ---- flush: one vector RED per non-zero tile node ----
-    for (int tn = tid; tn < TN; tn += kThreads) {
-      float4 v0 = s_tile[0][tn], v1 = s_tile[1][tn], v2 = s_tile[2][tn];
-      float4 v = make_float4(v0.x + v1.x + v2.x, v0.y + v1.y + v2.y, v0.z + v1.z + v2.z, v0.w + v1.w + v2.w);
-      if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
-      int tl[D];
+    // ---- flush: one vector RED per non-zero tile node.  The tile spans the 2^D blocks
+    //      bc + {0, 1}^D: lanes 0..2^D-1 of each warp look their slots up, nodes take theirs by
+    //      shuffle (one dependent global load less per node) ----
+    int myslot = -1;
+    {
+      const int lane = tid & 31;
+      if (lane < (1 << D)) {
+        int nb_[D];
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          nb_[a] = bc[a] + ((lane >> (D - 1 - a)) & 1);
+          inside &= nb_[a] < P.nbpa;
+        }
+        if (inside) myslot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+      }
+    }
+    for (int t0 = 0; t0 < TN; t0 += kThreads) {  // uniform trip count: whole warps reach the shuffle
+      const int tn = t0 + tid;
+      int tl[D], sb = 0;
       {
         int t = tn;
 #pragma unroll
-        for (int a = D - 1; a >= 0; --a) { tl[a] = t % TE; t /= TE; }
+        for (int a = D - 1; a >= 0; --a) {
+          tl[a] = t % TE;
+          sb |= (tl[a] >= BB) << (D - 1 - a);
+          t /= TE;
+        }
       }
-      int nb_[D], loc[D];
-      bool inside = true;
+      const int slot = __shfl_sync(0xffffffffu, myslot, sb);
+      if (tn >= TN) continue;
+      float4 v0 = s_tile[0][tn], v1 = s_tile[1][tn], v2 = s_tile[2][tn];
+      float4 v = make_float4(v0.x + v1.x + v2.x, v0.y + v1.y + v2.y, v0.z + v1.z + v2.z, v0.w + v1.w + v2.w);
+      if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+      int loc[D];
 #pragma unroll
-      for (int a = 0; a < D; ++a) {
-        int gnode = bc[a] * BB + tl[a];
-        inside &= gnode < P.res;
-        nb_[a] = gnode >> DD::LOG_BB;
-        loc[a] = gnode & (BB - 1);
-      }
-      if (!inside) continue;
-      int slot = A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)];
-      if (slot < 0) continue;  // cannot happen (touched by construction); defensive
+      for (int a = 0; a < D; ++a) loc[a] = (bc[a] * BB + tl[a]) & (BB - 1);
+      if (slot < 0) continue;  // outside the domain / untouched (cannot happen for non-zero nodes)
       float4* dst = A.grid + (size_t)(ADJ ? slot - base_slot : slot) * kCPB + cell_lin<D>(loc);
       atomicAdd(dst, v);  // red.global.add.v4.f32
     }
