@@ -147,6 +147,7 @@ struct mpm_ctx_s {
   // profiling
   bool profiling = false;
   bool pdl = true;  // programmatic dependent launches on the step path (MPM_PDL=0 disables)
+  bool split = false;  // small problem: the gathers split blocks into particle ranges
   bool mass_grad = false;  // N3: compute dL/dm_p in P2G^T (opt-in)
   bool mass_grad_valid = false;
   std::vector<PendingEvent> pending;
@@ -447,11 +448,31 @@ void forward_phase_b(mpm_ctx c, int t) {
   if (has_nbr(c)) launch_band_unpack(c, t, false, c->arena);
   StepArgs A = step_args(c, t);
   const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
-  launch(c, KI_G2P, [&] { kx(c, k_g2p<D>, dim3(ng), dim3(kThreads), 0, P, A); });
+  launch(c, KI_G2P, [&] {
+    if (c->split) kx(c, k_g2p<D, true>, dim3(ng), dim3(kThreads), 0, P, A);  // small problems: blocks split
+    else kx(c, k_g2p<D>, dim3(ng), dim3(kThreads), 0, P, A);
+  });
 }
 
 // adjoint grid buffer of backward step t (double-buffered by step parity)
 float4* agrid_of(mpm_ctx c, int t) { return (t & 1) ? c->agrid1 : c->agrid; }
+
+// P2G^T variant: mass gradient on/off, material, block splitting for small problems
+template <int D, bool MG, int MAT>
+void launch_p2gT_v(mpm_ctx c, const KParams& P, const StepArgs& A, int na) {
+  if (c->split) kx(c, k_p2g_adj<D, MG, MAT, true>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
+  else kx(c, k_p2g_adj<D, MG, MAT, false>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
+}
+template <int D>
+void launch_p2gT(mpm_ctx c, const KParams& P, const StepArgs& A, int na) {
+  if (c->mass_grad) {
+    if (P.material == 1) launch_p2gT_v<D, true, 1>(c, P, A, na);
+    else launch_p2gT_v<D, true, 0>(c, P, A, na);
+  } else {
+    if (P.material == 1) launch_p2gT_v<D, false, 1>(c, P, A, na);
+    else launch_p2gT_v<D, false, 0>(c, P, A, na);
+  }
+}
 
 // backward step t = phase A ([zero,] G2P^T [, window pack]) | exchange | phase B ([unpack,]
 // grid^T, P2G^T); the particle adjoint flows c->bcur -> c->bnxt
@@ -482,16 +503,7 @@ void backward_phase_b(mpm_ctx c, int t) {
                                                        t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
-  if (c->mass_grad)
-    launch(c, KI_P2GT, [&] {
-      if (P.material == 1) kx(c, k_p2g_adj<D, true, 1>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
-      else kx(c, k_p2g_adj<D, true>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
-    });
-  else
-    launch(c, KI_P2GT, [&] {
-      if (P.material == 1) kx(c, k_p2g_adj<D, false, 1>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
-      else kx(c, k_p2g_adj<D, false>, dim3(na), dim3(MPM_P2GT_THREADS), 0, P, A);
-    });
+  launch(c, KI_P2GT, [&] { launch_p2gT<D>(c, P, A, na); });
   if (c->ctrl) {  // N1: controller adjoint of step t (needs this step's complete dL/da)
     const int KD = P.K * D;
     launch(c, KI_CTRLT, [&] {
@@ -997,6 +1009,8 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   P.slab_hi = k.res - 3;
   P.material = k.material;
   c->n_tiles = (P.NBT + kScanTile - 1) / kScanTile;
+  // fewer than ~400 particles per gather CTA slot: too few occupied blocks to fill the GPU
+  c->split = (long long)P.NT < 400LL * c->n_sm * 4;
   int occ = 0;
   // dynamic shared memory of the block-tile scatter (payload buffer) above the 48 KB default
   cudaFuncSetAttribute(k_block_scatter<3, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<3, false>());

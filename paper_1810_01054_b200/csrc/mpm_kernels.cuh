@@ -1300,6 +1300,32 @@ __device__ __forceinline__ void prefetch_record(const float* base, size_t NT, in
 // Weights are separable, W = wx(ox) wy(oy) wz(oz); oz-sums are formed first and folded
 // per (ox, oy), so the moments sum_i W v_i o_b cost O(1) per node.
 // ------------------------------------------------------------------------------------
+// Work items of the gathers: (occupied block, part of its particles).  Small problems (fewer
+// occupied blocks than CTAs) split each block into up to 8 particle ranges so that more CTAs
+// work (each stages its block's tile); large ones keep one item per block.
+template <bool SPLIT>
+__device__ __forceinline__ int work_parts(int n_occ) {
+  return SPLIT ? max(1, min(8, (int)gridDim.x / max(n_occ, 1))) : 1;
+}
+template <bool SPLIT>
+__device__ __forceinline__ bool work_item(const StepArgs& A, int wi, int n_occ, int parts, int& gb, int& s, int& n) {
+  if (!SPLIT) {
+    if (wi >= n_occ) return false;
+    gb = A.occ_list[wi];
+    s = A.block_start[gb];
+    n = A.block_start[gb + 1] - s;
+    return true;
+  }
+  if (wi >= n_occ * parts) return false;
+  const int bi = wi / parts, part = wi - bi * parts;
+  gb = A.occ_list[bi];
+  const int s0 = A.block_start[gb], n0 = A.block_start[gb + 1] - s0;
+  const int lo = n0 * part / parts, hi = n0 * (part + 1) / parts;
+  s = s0 + lo;
+  n = hi - lo;
+  return true;
+}
+
 template <int D>
 __device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, int* bc) {
   r = gb / P.nb;
@@ -1493,20 +1519,23 @@ __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const 
   }
 }
 
-template <int D>
+template <int D, bool SPLIT = false>
 __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   __shared__ float4 s_v[Dim<D>::TN];
   __shared__ int s_blk;
   const size_t NT = P.NT;
   const int n_occ = A.info_t[I_NOCC];
+  const int parts = work_parts<SPLIT>(n_occ);
   for (;;) {
     if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK3], 1);
     __syncthreads();
-    const int bi = s_blk;
-    if (bi >= n_occ) break;
-    const int gb = A.occ_list[bi];
-    const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
+    int gb, s, n;
+    if (!work_item<SPLIT>(A, s_blk, n_occ, parts, gb, s, n)) break;
+    if (SPLIT && n == 0) {  // uniform; every thread has read s_blk before thread 0 claims again
+      __syncthreads();
+      continue;
+    }
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
     float4 vref, aref_unused;
@@ -2000,7 +2029,7 @@ __device__ __forceinline__ void reduce_actuation(float* w_da, int key, const flo
   }
 }
 
-template <int D, bool MG, int MAT = 0>
+template <int D, bool MG, int MAT = 0, bool SPLIT = false>
 __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   constexpr int NW = MPM_P2GT_THREADS / 32;
@@ -2026,13 +2055,16 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       if (v != 0.f) atomicAdd(&A.da[((size_t)rr * P.T + A.t) * KD + q], v);
     }
   };
+  const int parts = work_parts<SPLIT>(n_occ);
   for (;;) {
     if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
     __syncthreads();
-    const int bi = s_blk;
-    if (bi >= n_occ) break;
-    const int gb = A.occ_list[bi];
-    const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
+    int gb, s, n;
+    if (!work_item<SPLIT>(A, s_blk, n_occ, parts, gb, s, n)) break;
+    if (SPLIT && n == 0) {  // uniform; every thread has read s_blk before thread 0 claims again
+      __syncthreads();
+      continue;
+    }
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
     if (KD > 0 && r != s_da_r) {  // uniform: a new rollout -> flush the previous one's sums
