@@ -486,7 +486,10 @@ void backward_phase_a(mpm_ctx c, int t) {
   if (t == c->seg_end - 1)  // first backward step of a segment: prepare its buffer (later: by grid_T)
     launch(c, KI_ZERO, [&] { kx(c, k_zero_slots, dim3(c->n_sm * 4), dim3(256), 0, info_at(c, t), A.grid); });
   const int nbla = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter_adj));
-  launch(c, KI_G2PT, [&] { kx(c, k_block_scatter<D, true>, dim3(nbla), dim3(kThreads), scatter_dyn_smem<D, true>(), P, A); });
+  launch(c, KI_G2PT, [&] {
+    if (c->split) kx(c, k_block_scatter<D, true, 0, true>, dim3(nbla), dim3(kThreads), scatter_dyn_smem<D, true>(), P, A);
+    else kx(c, k_block_scatter<D, true>, dim3(nbla), dim3(kThreads), scatter_dyn_smem<D, true>(), P, A);
+  });
   if (has_nbr(c)) launch_band_pack(c, t, true, A.grid);
 }
 
@@ -1019,6 +1022,8 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   cudaFuncSetAttribute(k_block_scatter<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, true>());
   cudaFuncSetAttribute(k_block_scatter<3, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<3, false>());
   cudaFuncSetAttribute(k_block_scatter<2, false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, false>());
+  cudaFuncSetAttribute(k_block_scatter<3, true, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<3, true>());
+  cudaFuncSetAttribute(k_block_scatter<2, true, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, scatter_dyn_smem<2, true>());
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<3, false>, kThreads, scatter_dyn_smem<3, false>());
     c->occ_scatter = std::max(1, occ);

@@ -931,7 +931,33 @@ constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(fl
 // spreads them over 32.  It permutes every aligned group of 8, so [0, kCap) maps onto itself.
 __device__ __forceinline__ int pay_slot(int p) { return p ^ (((p >> 5) ^ (p >> 7)) & 7); }
 
-template <int D, bool ADJ, int MAT = 0>
+// Work items of the gathers: (occupied block, part of its particles).  Small problems (fewer
+// occupied blocks than CTAs) split each block into up to 8 particle ranges so that more CTAs
+// work (each stages its block's tile); large ones keep one item per block.
+template <bool SPLIT>
+__device__ __forceinline__ int work_parts(int n_occ) {
+  return SPLIT ? max(1, min(8, (int)gridDim.x / max(n_occ, 1))) : 1;
+}
+template <bool SPLIT>
+__device__ __forceinline__ bool work_item(const StepArgs& A, int wi, int n_occ, int parts, int& gb, int& s, int& n) {
+  if (!SPLIT) {
+    if (wi >= n_occ) return false;
+    gb = A.occ_list[wi];
+    s = A.block_start[gb];
+    n = A.block_start[gb + 1] - s;
+    return true;
+  }
+  if (wi >= n_occ * parts) return false;
+  const int bi = wi / parts, part = wi - bi * parts;
+  gb = A.occ_list[bi];
+  const int s0 = A.block_start[gb], n0 = A.block_start[gb + 1] - s0;
+  const int lo = n0 * part / parts, hi = n0 * (part + 1) / parts;
+  s = s0 + lo;
+  n = hi - lo;
+  return true;
+}
+
+template <int D, bool ADJ, int MAT = 0, bool SPLIT = false>
 __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   using DD = Dim<D>;
@@ -952,13 +978,19 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
   const int n_occ = A.info_t[I_NOCC];
   const int base_slot = A.info_t[I_BASE];
 
+  // SPLIT (adjoint only; the forward sorts whole blocks): small problems give a block's
+  // particle ranges to several CTAs, each flushing its own partial tile with REDs
+  static_assert(!SPLIT || ADJ, "only the adjoint scatter splits blocks");
+  const int parts = work_parts<SPLIT>(n_occ);
   for (;;) {
     if (tid == 0) s_blk = atomicAdd(&A.info_t[work_field], 1);
     __syncthreads();
-    const int bi = s_blk;
-    if (bi >= n_occ) break;
-    const int gb = A.occ_list[bi];
-    const int s = A.block_start[gb], n = A.block_start[gb + 1] - s;
+    int gb, s, n;
+    if (!work_item<SPLIT>(A, s_blk, n_occ, parts, gb, s, n)) break;
+    if (SPLIT && n == 0) {  // uniform; every thread has read s_blk before thread 0 claims again
+      __syncthreads();
+      continue;
+    }
     const int r = gb / P.nb;
     int bc[D];
     {
@@ -1300,32 +1332,6 @@ __device__ __forceinline__ void prefetch_record(const float* base, size_t NT, in
 // Weights are separable, W = wx(ox) wy(oy) wz(oz); oz-sums are formed first and folded
 // per (ox, oy), so the moments sum_i W v_i o_b cost O(1) per node.
 // ------------------------------------------------------------------------------------
-// Work items of the gathers: (occupied block, part of its particles).  Small problems (fewer
-// occupied blocks than CTAs) split each block into up to 8 particle ranges so that more CTAs
-// work (each stages its block's tile); large ones keep one item per block.
-template <bool SPLIT>
-__device__ __forceinline__ int work_parts(int n_occ) {
-  return SPLIT ? max(1, min(8, (int)gridDim.x / max(n_occ, 1))) : 1;
-}
-template <bool SPLIT>
-__device__ __forceinline__ bool work_item(const StepArgs& A, int wi, int n_occ, int parts, int& gb, int& s, int& n) {
-  if (!SPLIT) {
-    if (wi >= n_occ) return false;
-    gb = A.occ_list[wi];
-    s = A.block_start[gb];
-    n = A.block_start[gb + 1] - s;
-    return true;
-  }
-  if (wi >= n_occ * parts) return false;
-  const int bi = wi / parts, part = wi - bi * parts;
-  gb = A.occ_list[bi];
-  const int s0 = A.block_start[gb], n0 = A.block_start[gb + 1] - s0;
-  const int lo = n0 * part / parts, hi = n0 * (part + 1) / parts;
-  s = s0 + lo;
-  n = hi - lo;
-  return true;
-}
-
 template <int D>
 __device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, int* bc) {
   r = gb / P.nb;
