@@ -140,7 +140,6 @@ ALG_BYTES = {
     "g2p": (48 + 96, 16),          # read x,F + write x,v,C,F ; read (vbar,m) per node
     "p2g_T": (96 + 20 + 96 + 96 + 16, 32),  # tape state, params, adj in, adj out, dmu/dlam RMW ; tape + adj node
     "g2p_T": (48 + 96, 16),        # x,F + adj in ; write dv per node
-    "grid_update": (0, 32),
     "grid_T": (0, 48),
 }
 

@@ -21,12 +21,11 @@ using namespace mpm;
 namespace {
 
 enum KernelId {
-  KI_SCAN_A, KI_SCAN_B, KI_SCAN_C, KI_SCATTER, KI_P2G, KI_GRID, KI_G2P,
-  KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC, KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_COUNT
+  KI_SCAN, KI_SCATTER, KI_P2G, KI_G2P, KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC,
+  KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_COUNT
 };
-const char* kKernelNames[KI_COUNT] = {"scan", "scan_b", "scan_c",  "scatter", "p2g",  "grid_update",
-                                      "g2p",    "zero_adj", "g2p_T", "grid_T", "p2g_T", "misc",
-                                      "band_pack", "band_unpack", "ctrl", "ctrl_T"};
+const char* kKernelNames[KI_COUNT] = {"scan",  "scatter", "p2g",       "g2p",         "zero_adj", "g2p_T", "grid_T",
+                                      "p2g_T", "misc",    "band_pack", "band_unpack", "ctrl",     "ctrl_T"};
 
 struct PendingEvent {
   cudaEvent_t a, b;
@@ -349,7 +348,7 @@ template <int D>
 void launch_bin(mpm_ctx c, int t) {
   const KParams& P = c->P;
   const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
-  launch(c, KI_SCAN_A, [&] {
+  launch(c, KI_SCAN, [&] {
     kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles, c->info,
        (int)ti(c, t), bs_at(c, t), slot_at(c, t), occ_at(c, t), touch_at(c, t), c->err, t);
   });
@@ -590,7 +589,7 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   }
   // automatic grid-slot capacity from the touched blocks of the initial state
   if (c->arena == nullptr) {
-    launch(c, KI_SCAN_A, [&] { kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums); });
+    launch(c, KI_MISC, [&] { kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums); });
     std::vector<int3> ts(c->n_tiles);
     CK(cudaMemcpyAsync(ts.data(), c->tile_sums, ts.size() * sizeof(int3), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));

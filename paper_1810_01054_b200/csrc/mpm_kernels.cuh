@@ -627,7 +627,8 @@ __device__ __forceinline__ int3 cta_excl_scan3(int3 v, int3* s_warp, int3& total
   return make_int3(wo.x + inc.x - v.x, wo.y + inc.y - v.y, wo.z + inc.z - v.z);
 }
 
-// flag word of a block: count | occupied << 30 | touched << 31
+// per-tile totals of (count, occupied, touched) -- used once by set_state to size the grid-slot
+// arena; flag word of a block: count | occupied << 30 | touched << 31
 template <int D>
 __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __restrict__ cnt,
                                                      unsigned* __restrict__ bflag,
@@ -645,72 +646,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __res
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
 }
 
-// single CTA: exclusive scan of tile sums, per-step counts, arena base, overflow check
-__global__ void k_scan_b(KParams P, int n_tiles, int3* __restrict__ tile_sums, int* __restrict__ info,
-                         int t, ErrLatch* err) {
-  MPM_PDL_ENTRY();
-  __shared__ int3 s_warp[kThreads / 32 + 1];
-  __shared__ int3 s_carry;
-  if (threadIdx.x == 0) s_carry = make_int3(0, 0, 0);
-  __syncthreads();
-  for (int base = 0; base < n_tiles; base += kThreads) {
-    int i = base + threadIdx.x;
-    int3 v = i < n_tiles ? tile_sums[i] : make_int3(0, 0, 0);
-    int3 tot;
-    int3 ex = cta_excl_scan3(v, s_warp, tot);
-    int3 cr = s_carry;
-    if (i < n_tiles) tile_sums[i] = make_int3(ex.x + cr.x, ex.y + cr.y, ex.z + cr.z);
-    __syncthreads();
-    if (threadIdx.x == 0) s_carry = make_int3(cr.x + tot.x, cr.y + tot.y, cr.z + tot.z);
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    int* I = info + t * kInfo;
-    int base = t == 0 ? 0 : info[(t - 1) * kInfo + I_BASE] + info[(t - 1) * kInfo + I_NTOUCH];
-    int ntouch = s_carry.z;
-    int ok = 1;
-    if (ntouch > P.slots_per_step || base + ntouch > P.arena_slots) {
-      latch(err, E_TAPE_FULL, t, ntouch);
-      ok = 0;
-    }
-    I[I_NOCC] = ok ? s_carry.y : 0;
-    I[I_NTOUCH] = ok ? ntouch : 0;
-    I[I_BASE] = base;
-    I[I_WORK] = 0;
-    I[I_WORK2] = 0;
-    I[I_WORK3] = 0;
-    I[I_WORK4] = 0;
-    I[I_OK] = ok;
-  }
-}
-
-__global__ __launch_bounds__(kThreads) void k_scan_c(KParams P, const unsigned* __restrict__ bflag,
-                                                     const int3* __restrict__ tile_pre,
-                                                     const int* __restrict__ info_t,
-                                                     int* __restrict__ block_start,
-                                                     int* __restrict__ slot_of,
-                                                     int* __restrict__ occ_list,
-                                                     int* __restrict__ touched_list) {
-  MPM_PDL_ENTRY();
-  __shared__ int3 s_warp[kThreads / 32 + 1];
-  const int ok = info_t[I_OK];
-  const int base = info_t[I_BASE];
-  const int gb = blockIdx.x * kScanTile + threadIdx.x;
-  const unsigned f = gb < P.NBT ? bflag[gb] : 0u;
-  const int c = (int)(f & 0x3fffffffu), o = (f >> 30) & 1, tc = f >> 31;
-  int3 tot;
-  int3 ex = cta_excl_scan3(make_int3(c, o, tc), s_warp, tot);
-  const int3 tp = tile_pre[blockIdx.x];
-  if (gb < P.NBT) {
-    block_start[gb] = ex.x + tp.x;
-    if (ok && o) occ_list[ex.y + tp.y] = gb;
-    slot_of[gb] = (ok && tc) ? base + ex.z + tp.z : -1;
-    if (ok && tc) touched_list[ex.z + tp.z] = gb;
-  }
-  if (gb == P.NBT - 1) block_start[P.NBT] = P.NT;
-}
-
-// Single-pass binning tables (replaces k_scan_a/b/c on the step path): one CTA per tile of
+// Single-pass binning tables of the step path: one CTA per tile of
 // kScanTile blocks, taken in ticket order; block flags -> CTA scan -> decoupled look-back over
 // the preceding tiles (aggregate / inclusive prefix published with an epoch-tagged flag, so
 // the flags need no reset) -> block_start, occupied list, slot map, touched list.  The grid
