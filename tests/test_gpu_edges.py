@@ -1,0 +1,158 @@
+"""Edge cases of the GPU path vs the oracle: a single particle, particles at the lowest and
+highest valid base index (wall bands on both sides), positions exactly on binning
+boundaries (x res - 1/2 integral: the fp32 floor decision, R17), and the maximum rollout size
+(n_particles = 2^25 - 1) with the exact centre-of-mass gradient."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1810_01054_b200 import mpm, scenes
+from tests.helpers import oracle_cfg, oracle_params, oracle_state, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _fb_vs_oracle(sc, T, tol=1e-4, gtol=1e-3):
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    sim.set_scene(sc)
+    sim.forward(T)
+    x, v, F, Cm = sim.get_state(T)
+    cfg = oracle_cfg(sc)
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    traj = oracle.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, act[:T], T)
+    ox, ov, oC, oF = oracle.unpack(traj[T], sc.dim)
+    # field-scale errors (R16 for degenerate references: C of a translating body is 0 in real
+    # arithmetic; its fp32 round-off is measured against C's natural scale 4 res |v|)
+    vmax = max(np.abs(ov).max(), 1e-6)
+    for k, a, b, scale in (("x", x, ox, 1.0), ("v", v, ov, vmax), ("F", F, oF, np.abs(oF).max()),
+                           ("C", Cm, oC, 4 * sc.res * vmax)):
+        err = np.abs(a - b).max() / scale
+        assert err < tol, (k, err)
+    w = np.random.default_rng(2).standard_normal(traj[T].shape)
+    wx, wv, wC, wF = oracle.unpack(w, sc.dim)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    g0, gE, gnu, ga = oracle.backward(cfg, traj, m, vol, E, nu, aid, act[:T], w)
+    gx, gv, gC, gF = oracle.unpack(g0, sc.dim)
+    ref = np.linalg.norm(gx)
+    for k, a, b in (("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF),
+                    ("dC0", g["dC0"], gC), ("dE", g["dE"], gE), ("dnu", g["dnu"], gnu)):
+        unit = float(np.max(E)) if k == "dnu" else 1.0  # dL/dnu carries a factor E relative to dL/dE
+        if np.linalg.norm(b) < 1e-9 * ref * unit:  # zero in real arithmetic (an undeformed particle)
+            assert np.linalg.norm(a) < 1e-6 * ref * unit, (k, np.linalg.norm(a))
+        else:
+            assert rel_err(a, b) < gtol, (k, rel_err(a, b))
+
+
+def _scene_from(sc, x, v=None):
+    """Replace the particles of a tiny scene by the given positions (same recipe otherwise)."""
+    n, d = x.shape
+    sc.x = x[None].astype(np.float32)
+    sc.v = (np.zeros((1, n, d)) if v is None else v[None]).astype(np.float32)
+    sc.F = np.tile(np.eye(d, dtype=np.float32), (1, n, 1, 1))
+    sc.C = np.zeros((1, n, d, d), np.float32)
+    vol = np.float32((1.0 / sc.res) ** d / 2 ** d)
+    sc.mass = np.full((1, n), vol, np.float32)
+    sc.vol = np.full((1, n), vol, np.float32)
+    sc.E = np.full((1, n), 1e3, np.float32)
+    sc.nu = np.full((1, n), 0.3, np.float32)
+    sc.actuator_id = (np.arange(n) % (sc.n_act + 1) - 1).astype(np.int32)[None]
+    return sc
+
+
+@pytest.mark.parametrize("d,T", [(2, 5), (3, 5)])
+def test_single_particle(d, T):
+    """One particle.  Its grid is a uniform field: every node's p/m equals v exactly in real
+    arithmetic and the C-adjoint's contribution to dL/dx0 is an exact cancellation, so the
+    fp32 rounding of p/m (~2 ulp per node) is amplified by step J's 4 res^2 terms (DESIGN R22):
+    with a random seed on every field the dx0 error grows ~1e-4 per step (2.4e-3 after 20
+    steps at res 32), hence 5 steps here and the 20-step check below without C/F seeds."""
+    sc = scenes.tiny(d, seed=71, res=32, steps=T, K=1, s=20.0)
+    x = np.full((1, d), 0.5, np.float32)
+    sc = _scene_from(sc, x, v=np.full((1, d), 0.3))
+    _fb_vs_oracle(sc, T)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_single_particle_long_xv_seed(d):
+    T = 20
+    sc = scenes.tiny(d, seed=71, res=32, steps=T, K=1, s=20.0)
+    sc = _scene_from(sc, np.full((1, d), 0.5, np.float32), v=np.full((1, d), 0.3))
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    sim.set_scene(sc)
+    sim.forward(T)
+    cfg = oracle_cfg(sc)
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    traj = oracle.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, act[:T], T)
+    w = np.random.default_rng(2).standard_normal(traj[T].shape)
+    w[:, 2 * d:] = 0.0
+    wx, wv, _, _ = oracle.unpack(w, d)
+    sim.backward(np.ascontiguousarray(wx, np.float32), np.ascontiguousarray(wv, np.float32))
+    g = sim.grad()
+    g0 = oracle.backward(cfg, traj, m, vol, E, nu, aid, act[:T], w)[0]
+    gx, gv, _, _ = oracle.unpack(g0, d)
+    assert rel_err(g["dx0"], gx) < 1e-3 and rel_err(g["dv0"], gv) < 1e-3
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_extreme_base_indices_in_both_wall_bands(d):
+    """Particles whose base index is 0 and res - 3 (the extreme valid values, R14): their
+    stencils cover the low and the high wall bands (friction on the floor, sticky walls off)."""
+    res = 32
+    sc = scenes.tiny(d, seed=72, res=res, steps=6, K=2, s=20.0)
+    rng = np.random.default_rng(73)
+    lo = (0.5 + rng.uniform(0.0, 0.99, (40, d))) / res          # base 0
+    hi = (res - 2.5 + rng.uniform(0.0, 0.99, (40, d))) / res    # base res - 3
+    x = np.concatenate([lo, hi]).astype(np.float32)
+    v = rng.standard_normal(x.shape) * 0.05
+    v[:40] = np.abs(v[:40])  # move inwards so the 6 steps stay in the domain
+    v[40:] = -np.abs(v[40:])
+    sc = _scene_from(sc, x, v)
+    _fb_vs_oracle(sc, 6)
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_binning_on_exact_cell_boundaries(d):
+    """x res - 1/2 integral (x on a cell boundary of the base decision): the binning is
+    bit-exact with the oracle's fp32 decision and the step matches."""
+    res = 64
+    sc = scenes.tiny(d, seed=74, res=res, steps=2, K=0)
+    g = np.arange(20, 30) + 0.5          # x res = k + 1/2  ->  base exactly k
+    mesh = np.stack(np.meshgrid(*([g] * d), indexing="ij"), -1).reshape(-1, d)
+    x = (mesh / res).astype(np.float32)
+    sc = _scene_from(sc, x)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=2))
+    sim.set_scene(sc)
+    sim.forward(2)
+    for t in (0, 1):
+        xs, orig, key, perm, bs = sim.get_binning(t)
+        okey, operm, obs = oracle.bin_particles(d, res, xs.reshape(1, -1, d))
+        np.testing.assert_array_equal(key, okey)
+        np.testing.assert_array_equal(perm, operm)
+        np.testing.assert_array_equal(bs, obs)
+    _fb_vs_oracle(sc, 2)
+
+
+def test_maximum_rollout_size():
+    """n_particles = 2^25 - 1 (the ABI maximum) in one 256^3 rollout: one step forward and
+    backward, exact CoM gradient (no wall contact, any internal stress)."""
+    n = (1 << 25) - 1
+    res = 256
+    rng = np.random.default_rng(75)
+    x = (rng.uniform(64.0, 192.0, (n, 3)) / res).astype(np.float32)
+    T = 1
+    sc = scenes.tiny(3, seed=76, res=res, steps=T, K=0)
+    sc = _scene_from(sc, x)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    sim.set_scene(sc)
+    sim.forward(T)
+    m = sc.mass[0].astype(np.float64)
+    seed = np.zeros((n, 3), np.float32)
+    seed[:, 0] = (m / m.sum()).astype(np.float32)
+    sim.backward(seed)
+    g = sim.grad()
+    M = m.sum()
+    assert rel_err(g["dx0"][:, 0], m / M) < 1e-4
+    assert rel_err(g["dv0"][:, 0], T * sc.dt * m / M) < 1e-4
+    assert np.abs(g["dx0"][:, 1:]).max() < 1e-4 / n
