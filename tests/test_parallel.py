@@ -142,3 +142,45 @@ def test_gloo_world2_slab_partition_agrees():
     assert lo0 == 0 and hi0 == lo1 and hi1 == 64
     assert c0 == c1 == n0 == n1
     assert same0 and same1 and mn0 == mx0 == 1 and e0 == 0.0 and e1 == 0.0
+
+
+def _comm_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import torch.distributed as dist
+    from paper_1810_01054_b200 import mpm
+    d = parallel.init_from_env("gloo")
+    if rank == 0:
+        mpm.comm_unique_id = lambda: bytes(np.random.default_rng(1234).integers(0, 256, 128, dtype=np.uint8))
+    else:  # only rank 0 may create the id; the others must receive it
+        def _no(*_):
+            raise AssertionError("comm_unique_id called on a non-zero rank")
+        mpm.comm_unique_id = _no
+
+    class Recorder:  # stands in for an MPM context: records what comm_init receives
+        def comm_init(self, r, w, uid):
+            self.got = (r, w, uid)
+
+    rec = Recorder()
+    parallel.init_slab_comm(rec, d)
+    q.put((rank, rec.got[0], rec.got[1], rec.got[2].hex()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_slab_comm_handshake():
+    """init_slab_comm: rank 0 creates the NCCL id, torch.distributed broadcasts it, every rank
+    joins with (its rank, world, the same id)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_comm_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=240) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, a0, w0, u0), (r1, a1, w1, u1) = res
+    assert (a0, a1, w0, w1) == (0, 1, 2, 2) and u0 == u1 and len(u0) == 256
