@@ -31,6 +31,9 @@
 #ifndef MPM_FFMA2
 #define MPM_FFMA2 1  // packed fp32x2 FMAs (sm_100 FFMA2) in the stencil sums
 #endif
+#ifndef MPM_SCAT_PF
+#define MPM_SCAT_PF 1
+#endif
 #ifndef MPM_FFMA2_SCAT
 #define MPM_FFMA2_SCAT 1
 #endif
@@ -859,6 +862,15 @@ struct StepArgs {
   int t;
 };
 
+// L2 prefetch of one particle's SoA record (ncomp components at index j) -- issued for a
+// block's particles before its tile is staged, so the particle loop's loads hit L2
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_record(const float* base, size_t NT, int j, int c0, int ncomp) {
+  for (int c = c0; c < c0 + ncomp; ++c) prefetch_l2(base + (size_t)c * NT + j);
+}
+
 template <int D, bool ADJ>
 constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(float); }
 // payload slot of chunk position p: a warp of consumer threads reads cells whose particles
@@ -954,6 +966,11 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
           pj[q] = e.x;
           pc[q] = e.y & (kCPB - 1);
           atomicAdd(&s_hist[pc[q]], 1);
+#if MPM_SCAT_PF
+          // the producer reads this particle's record after the sort: start fetching it now
+          prefetch_record(A.st, NT, e.x, 0, Dim<D>::S);
+          prefetch_l2(&A.orig[e.x]);
+#endif
         }
       }
       for (int i = tid + 2 * kThreads; i < n; i += kThreads) atomicAdd(&s_hist[A.tmp_pk[s + i].y & (kCPB - 1)], 1);
@@ -1250,14 +1267,6 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 // vbar = p / m + dt g and the projection per node while staging its tile (fetch_node).
 // ------------------------------------------------------------------------------------
 
-// L2 prefetch of one particle's SoA record (ncomp components at index j) -- issued for a
-// block's particles before its tile is staged, so the particle loop's loads hit L2
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-__device__ __forceinline__ void prefetch_record(const float* base, size_t NT, int j, int c0, int ncomp) {
-  for (int c = c0; c < c0 + ncomp; ++c) prefetch_l2(base + (size_t)c * NT + j);
-}
 
 // ------------------------------------------------------------------------------------
 // Block-tile gathers (G2P, P2G^T).  One CTA per occupied grid block (dynamic work
