@@ -112,7 +112,9 @@ mpm_status mpm_rewind(mpm_ctx ctx, int32_t t);
 
 /* State at tape step t (0 <= t <= tape length), user particle order.  NULL = skip.
  * With checkpoint_every > 0 a step outside the resident segment is recomputed from the
- * nearest checkpoint (and becomes resident).                                              */
+ * nearest checkpoint (and becomes resident).  In slab mode with a communicator that
+ * recompute exchanges windows, so the call is then collective over the ranks (as are
+ * mpm_forward, mpm_rewind and mpm_backward).                                              */
 mpm_status mpm_get_state(mpm_ctx ctx, int32_t t, float* x, float* v, float* F, float* C);
 
 /* Reverse mode over the whole tape: seed dL/dstate at t = tape length, user order,
