@@ -144,15 +144,19 @@ ALG_BYTES = {
 }
 
 
-def _traffic(kernel, workload):
-    """dram bytes per launch of `kernel` from the committed ncu capture (profiles/
+def _ncu(field, kernel, workload):
+    """`field` per launch of `kernel` from the committed ncu capture (profiles/
     ncu_traffic.json) when it was taken on this workload, else None."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(path))
-        return d["per_launch_dram_bytes"][kernel] if d.get("workload") == workload else None
+        return d[field][kernel] if d.get("workload") == workload else None
     except Exception:
         return None
+
+
+def _traffic(kernel, workload):
+    return _ncu("per_launch_dram_bytes", kernel, workload)
 
 
 # ---------------------------------------------------------------------------------------
@@ -248,6 +252,14 @@ def run_ours(args):
                 "peak_source": peak_src, "share_of_step": round(d["ms_total"] / prof_total, 3),
                 "alg_bytes_per_launch": d["alg_bytes_per_launch"],
                 "per_kernel": per_kernel}
+    # issue view (these kernels are latency / issue bound): warp instructions per launch from
+    # the committed ncu capture over 4 schedulers x SMs x the max SM clock, vs the measured time
+    inst = _ncu("per_launch_warp_instructions", dom, args.workload)
+    if inst:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        floor_us = inst / (4 * sms * 1965e6) * 1e6
+        roofline["issue_view"] = {"warp_instructions_per_launch": inst, "issue_floor_us": round(floor_us, 1),
+                                  "measured_us": d["us_per_launch"], "frac": round(floor_us / d["us_per_launch"], 3)}
 
     # e2e through the public API with pinned host buffers: set_state (H2D), forward,
     # backward (seed H2D), grad (D2H), every pass

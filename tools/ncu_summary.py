@@ -50,6 +50,7 @@ def main(rep, traffic_json=None):
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     traffic = {}
+    instr = {}
     stall = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
              and h.endswith("_per_issue_active.ratio")]
     for r in rows[2:]:
@@ -63,6 +64,8 @@ def main(rep, traffic_json=None):
             b = sum(float(r[hdr.index(k)].replace(",", "")) * TO_MB.get(units[hdr.index(k)], 1.0) * 1e6
                     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
             traffic.setdefault(BENCH_NAME.get(name, name), []).append(b)
+            inst = float(r[hdr.index("smsp__inst_executed.sum")].replace(",", ""))
+            instr.setdefault(BENCH_NAME.get(name, name), []).append(inst)
         except (ValueError, IndexError):
             pass
         st = sorted(((hdr[i][34:-27], float(r[i] or 0)) for i in stall), key=lambda x: -x[1])[:5]
@@ -72,6 +75,7 @@ def main(rep, traffic_json=None):
     if traffic_json:
         per = {k: round(sum(v) / len(v)) for k, v in traffic.items()}
         json.dump({"source": rep, "workload": WORKLOAD, "per_launch_dram_bytes": per,
+                   "per_launch_warp_instructions": {k: round(sum(v) / len(v)) for k, v in instr.items()},
                    "captured_launches": {k: len(v) for k, v in traffic.items()}}, open(traffic_json, "w"), indent=1)
 
 
