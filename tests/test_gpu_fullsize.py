@@ -205,3 +205,35 @@ def test_batched_quadrupeds_per_rollout():
         for k, a, b in (("dx0", g["dx0"][sl], gx), ("dv0", g["dv0"][sl], gv), ("dF0", g["dF0"][sl], gF),
                         ("dE", g["dE"][sl], gE), ("da", g["da"][r, :T], ga)):
             assert rel_err(a, b) < 1e-3, (r, k, rel_err(a, b))
+
+
+def test_c5b_full_batch_sampled_rollouts():
+    """C5b at full size in bench.py's N = 1 launch configuration: 64 quadruped rollouts
+    (1,916,928 particles, per-rollout actuation phase and E scale) in one context, 20 steps
+    forward + backward; rollouts 0, 31 and 63 in full vs the oracle (state and gradients)."""
+    T = 20
+    sc = scenes.quadruped_3d(batch=64, steps=T, e_scale=True)
+    sim = _sim(sc, T)
+    sim.forward(T)
+    x, v, F, Cm = sim.get_state(T)
+    rng = np.random.default_rng(8)
+    S = oracle.S_of(3)
+    w = rng.standard_normal((sc.batch * sc.n, S))
+    wx, wv, wC, wF = oracle.unpack(w, 3)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    cfg = oracle_cfg(sc)
+    for r in (0, 31, 63):
+        sl = slice(r * sc.n, (r + 1) * sc.n)
+        st, prm, aid, act = _orc_inputs(sc, r)
+        traj = oracle.forward(cfg, st, *prm, aid, act[:T], T)
+        ox, ov, oC, oF = oracle.unpack(traj[T], 3)
+        for k, a, b in (("x", x[sl], ox), ("v", v[sl], ov), ("F", F[sl], oF), ("C", Cm[sl], oC)):
+            assert rel_err(a, b) < 1e-4, (r, k, rel_err(a, b))
+        g0, gE, gnu, ga = oracle.backward(cfg, traj, *prm, aid, act[:T], w[sl])
+        gx, gv, gC, gF = oracle.unpack(g0, 3)
+        for k, a, b in (("dx0", g["dx0"][sl], gx), ("dv0", g["dv0"][sl], gv), ("dF0", g["dF0"][sl], gF),
+                        ("dC0", g["dC0"][sl], gC), ("dE", g["dE"][sl], gE), ("dnu", g["dnu"][sl], gnu),
+                        ("da", g["da"][r, :T], ga)):
+            assert rel_err(a, b) < 1e-3, (r, k, rel_err(a, b))
