@@ -8,10 +8,19 @@ import json
 import subprocess
 import sys
 
-BENCH_NAME = {"k_block_scatter<3, 0, 0>": "p2g", "k_block_scatter<3, 1, 0>": "g2p_T", "k_g2p<3>": "g2p",
-              "k_p2g_adj<3, 0, 0>": "p2g_T", "k_p2g_adj<3, 1, 0>": "p2g_T_massgrad", "k_grid_adj<3>": "grid_T",
-              "k_scan_lookback<3>": "scan", "k_scatter": "scatter",
-              "k_block_scatter<3, 0, 1>": "p2g_fcr", "k_p2g_adj<3, 0, 1>": "p2g_T_fcr"}
+def bench_name(kernel):
+    """bench.py's name of a captured kernel, from its template arguments (robust to added
+    defaulted parameters such as the small-problem SPLIT flag)."""
+    import re
+    m = re.match(r"(\w+)(?:<([^>]*)>)?", kernel)
+    base, args = m.group(1), [a.strip() for a in (m.group(2) or "").split(",") if a.strip()]
+    flag = lambda i: len(args) > i and args[i] in ("1", "true")
+    if base == "k_block_scatter":
+        return ("g2p_T" if flag(1) else "p2g") + ("_fcr" if flag(2) else "")
+    if base == "k_p2g_adj":
+        return "p2g_T" + ("_massgrad" if flag(1) else "") + ("_fcr" if flag(2) else "")
+    return {"k_g2p": "g2p", "k_grid_adj": "grid_T", "k_scan_lookback": "scan", "k_scatter": "scatter"}.get(base, kernel)
+
 
 KEYS = [
     ("time_us", "gpu__time_duration.sum", "us"),
@@ -63,9 +72,9 @@ def main(rep, traffic_json=None):
         try:
             b = sum(float(r[hdr.index(k)].replace(",", "")) * TO_MB.get(units[hdr.index(k)], 1.0) * 1e6
                     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-            traffic.setdefault(BENCH_NAME.get(name, name), []).append(b)
+            traffic.setdefault(bench_name(name), []).append(b)
             inst = float(r[hdr.index("smsp__inst_executed.sum")].replace(",", ""))
-            instr.setdefault(BENCH_NAME.get(name, name), []).append(inst)
+            instr.setdefault(bench_name(name), []).append(inst)
         except (ValueError, IndexError):
             pass
         st = sorted(((hdr[i][34:-27], float(r[i] or 0)) for i in stall), key=lambda x: -x[1])[:5]
