@@ -48,23 +48,24 @@ struct NcclApi {
 };
 
 const NcclApi* nccl_api() {
-  static NcclApi api{};
-  static int state = 0;  // 0 = not tried, 1 = ok, -1 = unavailable
-  if (state) return state > 0 ? &api : nullptr;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
-  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
-  bool ok = h != nullptr;
-#define NCCL_SYM(f)                                                    \
-  if (ok) {                                                            \
-    *reinterpret_cast<void**>(&api.f) = dlsym(h, "nccl" #f);            \
-    ok = api.f != nullptr;                                             \
+  // function-local static: initialised once, thread-safe (C++11)
+  static const NcclApi* const api = []() -> const NcclApi* {
+    static NcclApi a{};
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    bool ok = h != nullptr;
+#define NCCL_SYM(f)                                                  \
+  if (ok) {                                                          \
+    *reinterpret_cast<void**>(&a.f) = dlsym(h, "nccl" #f);            \
+    ok = a.f != nullptr;                                             \
   }
-  NCCL_SYM(GetUniqueId) NCCL_SYM(CommInitRank) NCCL_SYM(CommDestroy) NCCL_SYM(Send) NCCL_SYM(Recv)
-  NCCL_SYM(AllReduce) NCCL_SYM(GroupStart) NCCL_SYM(GroupEnd) NCCL_SYM(GetErrorString)
+    NCCL_SYM(GetUniqueId) NCCL_SYM(CommInitRank) NCCL_SYM(CommDestroy) NCCL_SYM(Send) NCCL_SYM(Recv)
+    NCCL_SYM(AllReduce) NCCL_SYM(GroupStart) NCCL_SYM(GroupEnd) NCCL_SYM(GetErrorString)
 #undef NCCL_SYM
-  state = ok ? 1 : -1;
-  return ok ? &api : nullptr;
+    return ok ? &a : nullptr;
+  }();
+  return api;
 }
 
 }  // namespace
@@ -1254,6 +1255,12 @@ mpm_status mpm_get_grid(mpm_ctx c, int32_t t, float* m, float* vbar) {
   for (int a = 0; a < c->D; ++a) nn *= P.res;
   nn *= P.B;
   float *dm = nullptr, *dv = nullptr;
+  struct Free {  // temporaries released on every return path
+    float** p[2];
+    ~Free() {
+      for (float** q : p) cudaFree(*q);
+    }
+  } guard{{&dm, &dv}};
   mpm_status s = MPM_OK;
   CK(cudaMalloc(&dm, nn * sizeof(float)));
   CK(cudaMalloc(&dv, nn * c->D * sizeof(float)));
@@ -1266,8 +1273,6 @@ mpm_status mpm_get_grid(mpm_ctx c, int32_t t, float* m, float* vbar) {
   if (m) CK(cudaMemcpyAsync(m, dm, nn * sizeof(float), cudaMemcpyDefault, c->stream));
   if (vbar) CK(cudaMemcpyAsync(vbar, dv, nn * c->D * sizeof(float), cudaMemcpyDefault, c->stream));
   s = sync_and_check(c, "get_grid");
-  cudaFree(dm);
-  cudaFree(dv);
   return s;
 }
 
