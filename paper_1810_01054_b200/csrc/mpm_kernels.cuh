@@ -946,6 +946,21 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 #pragma unroll
       for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
     }
+    // the tile's 2^D block slots (flush): looked up now, used at the end
+    int myslot = -1;
+    {
+      const int lane = tid & 31;
+      if (lane < (1 << D)) {
+        int nb_[D];
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          nb_[a] = bc[a] + ((lane >> (D - 1 - a)) & 1);
+          inside &= nb_[a] < P.nbpa;
+        }
+        if (inside) myslot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+      }
+    }
     if (tid < kCPB) {
       s_hist[tid] = 0;
       if (ADJ) { s_cstart[tid] = 0x7fffffff; s_cursor[tid] = -1; }  // per-chunk [first, last] of a cell
@@ -1219,20 +1234,6 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
     // ---- flush: one vector RED per non-zero tile node.  The tile spans the 2^D blocks
     //      bc + {0, 1}^D: lanes 0..2^D-1 of each warp look their slots up, nodes take theirs by
     //      shuffle (one dependent global load less per node) ----
-    int myslot = -1;
-    {
-      const int lane = tid & 31;
-      if (lane < (1 << D)) {
-        int nb_[D];
-        bool inside = true;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          nb_[a] = bc[a] + ((lane >> (D - 1 - a)) & 1);
-          inside &= nb_[a] < P.nbpa;
-        }
-        if (inside) myslot = __ldg(&A.slot_of[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
-      }
-    }
     for (int t0 = 0; t0 < TN; t0 += kThreads) {  // uniform trip count: whole warps reach the shuffle
       const int tn = t0 + tid;
       int tl[D], sb = 0;
