@@ -57,7 +57,9 @@ typedef enum {
   MPM_ERR_TAPE_FULL = 6,     /* forward beyond max_steps, or grid-slot arena full    */
   MPM_ERR_CALL_ORDER = 7,    /* e.g. backward before forward, grad before backward   */
   MPM_ERR_COMM = 8,          /* NCCL failure (slab mode)                             */
-  MPM_ERR_OUT_OF_SLAB = 9    /* particle left its slab's halo (slab mode, see below) */
+  MPM_ERR_OUT_OF_SLAB = 9,   /* particle left its slab's halo (slab mode, see below) */
+  MPM_ERR_CFL = 10           /* fuse_g2p2g: a particle moved too far in one step for the
+                                dilated grid of the next step (needs |v| dt < dx)          */
 } mpm_status;
 
 typedef struct {
@@ -82,6 +84,13 @@ typedef struct {
                            mpm_get_state / mpm_rewind of an evicted step recompute it      */
   int32_t material;     /* NEXT N3 constitutive model: 0 = neo-Hookean (R1),
                            1 = fixed-corotated, psi = mu |F - R|^2 + lam/2 (J - 1)^2 (R21)   */
+  int32_t fuse_g2p2g;   /* NEXT N2: 1 = fused forward, one particle pass per
+                           step: the G2P of step t also scatters step t+1's P2G into a
+                           grid allocated as the one-block dilation of step t's occupied
+                           blocks (results equal the unfused path up to fp32 summation
+                           order).  Requires |v| dt < dx (else MPM_ERR_CFL); ignored in
+                           slab mode and with a controller (N1 needs state t+1 before
+                           step t+1's P2G).  0 = P2G and G2P as separate passes.          */
 } mpm_config;
 
 /* Create a context on config->device.  Validates the config (MPM_ERR_INVALID_ARG) and

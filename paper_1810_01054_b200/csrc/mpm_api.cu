@@ -22,10 +22,11 @@ namespace {
 
 enum KernelId {
   KI_SCAN, KI_SCATTER, KI_P2G, KI_G2P, KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC,
-  KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_COUNT
+  KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_FUSE, KI_COUNT
 };
 const char* kKernelNames[KI_COUNT] = {"scan",  "scatter", "p2g",       "g2p",         "zero_adj", "g2p_T", "grid_T",
-                                      "p2g_T", "misc",    "band_pack", "band_unpack", "ctrl",     "ctrl_T"};
+                                      "p2g_T", "misc",    "band_pack", "band_unpack", "ctrl",     "ctrl_T",
+                                      "g2p2g"};
 
 struct PendingEvent {
   cudaEvent_t a, b;
@@ -83,6 +84,8 @@ struct mpm_ctx_s {
   // backward recomputes each earlier segment from its checkpoint
   int tape_cap = 0, seg0 = 0, seg_end = 0, ck = 0, n_ck = 0, ck_valid = 0;
   int res_end = 0;  // the states of steps [seg0, res_end] on the tape are valid
+  int fused_grid = -1;  // fused forward: the step whose grid the previous G2P2G already built
+  int occ_fuse = 2;
   float* ck_state = nullptr;
   int* ck_orig = nullptr;
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
@@ -285,6 +288,12 @@ mpm_status check_latch(mpm_ctx c) {
     c->poisoned = true;
     return fail(c, MPM_ERR_TAPE_FULL, buf);
   }
+  if (h.code == E_FUSE) {
+    snprintf(buf, sizeof buf, "particle %d moved more than the fused step's grid dilation allows at step %d "
+             "(fuse_g2p2g needs |v| dt < dx)", h.particle, h.step);
+    c->poisoned = true;
+    return fail(c, MPM_ERR_CFL, buf);
+  }
   if (h.code == E_SLAB) {
     snprintf(buf, sizeof buf, "particle %d left its slab's halo (base x outside [%d, %d]) at step %d", h.particle,
              c->P.slab_lo, c->P.slab_hi, h.step);
@@ -344,17 +353,40 @@ StepArgs step_args(mpm_ctx c, int t) {
   return A;
 }
 
+void launch_scatter(mpm_ctx c, int t, const int* za, const int* zb);
+
 // binning tables of step t from the keys/histogram of state t
 template <int D>
 void launch_bin(mpm_ctx c, int t) {
   const KParams& P = c->P;
   const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
   launch(c, KI_SCAN, [&] {
-    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles, c->info,
-       (int)ti(c, t), bs_at(c, t), slot_at(c, t), occ_at(c, t), touch_at(c, t), c->err, t);
+    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
+       info_at(c, t), bs_at(c, t), occ_at(c, t), info_at(c, t), ti(c, t) ? info_at(c, t - 1) : nullptr,
+       slot_at(c, t), touch_at(c, t), c->err, t);
   });
+  launch_scatter(c, t, info_at(c, t), nullptr);
+}
+
+// block-grouping of step t's particles; zeroes the grid slots of the step records za, zb
+void launch_scatter(mpm_ctx c, int t, const int* za, const int* zb) {
+  const KParams& P = c->P;
   launch(c, KI_SCATTER, [&] {
-    kx(c, k_scatter, dim3(std::max(1, std::min(grid1d(P.NT), c->n_sm * 8))), dim3(256), 0, P.NT, c->key, bs_at(c, t), c->cnt, c->tmp_pk, info_at(c, t), c->arena);
+    kx(c, k_scatter, dim3(std::max(1, std::min(grid1d(P.NT), c->n_sm * 8))), dim3(256), 0, P.NT, c->key, bs_at(c, t),
+       c->cnt, c->tmp_pk, za, zb, c->arena);
+  });
+}
+
+// NEXT N2 fused forward: binning of step t (info_bin non-null) and/or the dilated grid-slot
+// table of step t+1 (grid = true)
+template <int D>
+void launch_bin_fused(mpm_ctx c, int t, bool bin, bool grid) {
+  const KParams& P = c->P;
+  const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
+  launch(c, KI_SCAN, [&] {
+    kx(c, k_scan_lookback<D, true>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
+       bin ? info_at(c, t) : nullptr, bs_at(c, t), occ_at(c, t), grid ? info_at(c, t + 1) : nullptr, info_at(c, t),
+       grid ? slot_at(c, t + 1) : nullptr, grid ? touch_at(c, t + 1) : nullptr, c->err, t);
   });
 }
 
@@ -452,6 +484,89 @@ void forward_phase_b(mpm_ctx c, int t) {
     if (c->split) kx(c, k_g2p<D, true>, dim3(ng), dim3(kThreads), 0, P, A);  // small problems: blocks split
     else kx(c, k_g2p<D>, dim3(ng), dim3(kThreads), 0, P, A);
   });
+}
+
+// NEXT N2 fused forward (config.fuse_g2p2g): step t's G2P also scatters step t+1's P2G
+// (k_g2p2g) when step t+1 is in the same forward range and segment; grid t+1's slot map is
+// then the dilation of step t's occupied blocks.  Per fused step: scan (binning t + grid t+1
+// table) -> k_scatter (block grouping, zero grid t+1) -> k_g2p2g (cell sort of t, G2P, P2G
+// of t+1): 3 launches, one particle pass.  A step whose grid is not yet built (the first
+// of a range or of a segment) runs the unfused P2G first.
+bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !c->slab && !c->ctrl; }
+
+template <int D, bool SORT, bool SCAT>
+void launch_fused(mpm_ctx c, const StepArgs& A) {
+  const KParams& P = c->P;
+  const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_fuse));
+  const size_t dyn = SCAT ? fuse_dyn_smem<D>() : 0;
+  if (P.material == 1) kx(c, k_g2p2g<D, 1, SORT, SCAT>, dim3(ng), dim3(kThreads), dyn, P, A);
+  else kx(c, k_g2p2g<D, 0, SORT, SCAT>, dim3(ng), dim3(kThreads), dyn, P, A);
+}
+
+template <int D>
+void forward_fused_step(mpm_ctx c, int t, int t_end) {
+  const KParams& P = c->P;
+  if (c->ck && t - c->seg0 == c->tape_cap) {
+    roll_segment(c, t);
+    c->fused_grid = -1;
+  }
+  const bool have = c->fused_grid == t;
+  const bool next = t + 1 < t_end && (int)ti(c, t + 1) < c->tape_cap;
+  StepArgs A = step_args(c, t);
+  A.slot_next = next ? slot_at(c, t + 1) : nullptr;
+  if (!have) {
+    // the unfused P2G of step t builds grid t (with its own, undilated slot map)
+    const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
+    launch(c, KI_SCAN, [&] {
+      kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
+         info_at(c, t), bs_at(c, t), occ_at(c, t), info_at(c, t), ti(c, t) ? info_at(c, t - 1) : nullptr,
+         slot_at(c, t), touch_at(c, t), c->err, t);
+    });
+    if (next) launch_bin_fused<D>(c, t, false, true);
+    launch_scatter(c, t, info_at(c, t), next ? info_at(c, t + 1) : nullptr);
+    const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
+    launch(c, KI_P2G, [&] {
+      if (P.material == 1) kx(c, k_block_scatter<D, false, 1>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A);
+      else kx(c, k_block_scatter<D, false>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A);
+    });
+    if (next) {
+      launch(c, KI_FUSE, [&] { launch_fused<D, false, true>(c, A); });
+    } else {
+      const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_g2p));
+      launch(c, KI_G2P, [&] {
+        if (c->split) kx(c, k_g2p<D, true>, dim3(ng), dim3(kThreads), 0, P, A);
+        else kx(c, k_g2p<D>, dim3(ng), dim3(kThreads), 0, P, A);
+      });
+    }
+  } else {
+    launch_bin_fused<D>(c, t, true, next);
+    launch_scatter(c, t, next ? info_at(c, t + 1) : nullptr, nullptr);
+    launch(c, KI_FUSE, [&] {
+      if (next) launch_fused<D, true, true>(c, A);
+      else launch_fused<D, true, false>(c, A);
+    });
+  }
+  c->res_end = t + 1;
+  c->fused_grid = next ? t + 1 : -1;
+}
+
+// forward steps [t0, t1) (slab mode: with the window exchange between the phases)
+template <int D>
+mpm_status forward_range(mpm_ctx c, int t0, int t1) {
+  c->fused_grid = -1;
+  if (fuse_on(c)) {
+    for (int t = t0; t < t1; ++t) forward_fused_step<D>(c, t, t1);
+    return MPM_OK;
+  }
+  for (int t = t0; t < t1; ++t) {
+    forward_phase_a<D>(c, t);
+    if (has_nbr(c)) {
+      mpm_status s = exchange_nccl(c);
+      if (s) return s;
+    }
+    forward_phase_b<D>(c, t);
+  }
+  return MPM_OK;
 }
 
 // adjoint grid buffer of backward step t (double-buffered by step parity)
@@ -590,7 +705,10 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   }
   // automatic grid-slot capacity from the touched blocks of the initial state
   if (c->arena == nullptr) {
-    launch(c, KI_MISC, [&] { kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums); });
+    launch(c, KI_MISC, [&] {
+      if (c->cfg.fuse_g2p2g) kx(c, k_scan_a<D, true>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums);
+      else kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums);
+    });
     std::vector<int3> ts(c->n_tiles);
     CK(cudaMemcpyAsync(ts.data(), c->tile_sums, ts.size() * sizeof(int3), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -631,16 +749,9 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
 
 template <int D>
 mpm_status do_forward(mpm_ctx c, int n) {
-  for (int i = 0; i < n; ++i) {
-    const int t = c->tape_len + i;
-    forward_phase_a<D>(c, t);
-    if (has_nbr(c)) {
-      mpm_status s = exchange_nccl(c);
-      if (s) return s;
-    }
-    forward_phase_b<D>(c, t);
-  }
-  mpm_status s = sync_and_check(c, "forward");
+  mpm_status s = forward_range<D>(c, c->tape_len, c->tape_len + n);
+  if (s) return s;
+  s = sync_and_check(c, "forward");
   if (s) return s;
   c->tape_len += n;
   return MPM_OK;
@@ -745,14 +856,8 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
     // N2: recompute the previous segment from its checkpoint, then continue the reverse pass
     const int end = c->seg0;
     restore_checkpoint<D>(c, (end - 1) / c->ck);
-    for (int t = c->seg0; t < end; ++t) {
-      forward_phase_a<D>(c, t);
-      if (has_nbr(c)) {
-        s = exchange_nccl(c);
-        if (s) return s;
-      }
-      forward_phase_b<D>(c, t);
-    }
+    s = forward_range<D>(c, c->seg0, end);
+    if (s) return s;
     c->seg_end = end;
     // the carried adjoint is in the storage order of the evicted run's state `end`
     // (= checkpoint end / k); map it to the recomputed order of that state
@@ -827,14 +932,8 @@ mpm_status bring_to_tape(mpm_ctx c, int t) {
   if (!c->ck) return fail(c, MPM_ERR_CALL_ORDER, "step not on the tape");
   const int i = std::min(t / c->ck, c->ck_valid - 1);
   restore_checkpoint<D>(c, i);
-  for (int q = c->seg0; q < t; ++q) {
-    forward_phase_a<D>(c, q);
-    if (has_nbr(c)) {
-      mpm_status s = exchange_nccl(c);
-      if (s) return s;
-    }
-    forward_phase_b<D>(c, q);
-  }
+  mpm_status s = forward_range<D>(c, c->seg0, t);
+  if (s) return s;
   return sync_and_check(c, "checkpoint recompute");
 }
 
@@ -974,6 +1073,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   if (k.max_steps < 1) return bad("max_steps >= 1 required");
   if (k.material != 0 && k.material != 1) return bad("material must be 0 (neo-Hookean) or 1 (fixed-corotated)");
   if (k.checkpoint_every < 0 || k.checkpoint_every > k.max_steps) return bad("0 <= checkpoint_every <= max_steps required");
+  if (k.fuse_g2p2g != 0 && k.fuse_g2p2g != 1) return bad("fuse_g2p2g must be 0 or 1");
   if (k.n_actuators < 0 || k.n_actuators > 64) return bad("n_actuators in [0, 64]");
   if (!(k.dt > 0.f)) return bad("dt > 0 required");
   if (k.bound < 0 || 2 * k.bound >= k.res) return bad("0 <= bound and 2*bound < res required");
@@ -1034,6 +1134,16 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
     c->occ_scatter = std::max(1, occ);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_block_scatter<2, true>, kThreads, scatter_dyn_smem<2, true>());
     c->occ_scatter_adj = std::max(1, occ);
+  }
+  {  // NEXT N2 fused forward: payload buffer in dynamic shared memory
+#define FA(D, MAT, SORT) \
+  cudaFuncSetAttribute(k_g2p2g<D, MAT, SORT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fuse_dyn_smem<D>())
+    FA(3, 0, false); FA(3, 0, true); FA(3, 1, false); FA(3, 1, true);
+    FA(2, 0, false); FA(2, 0, true); FA(2, 1, false); FA(2, 1, true);
+#undef FA
+    if (k.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<3, 0, true, true>, kThreads, fuse_dyn_smem<3>());
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<2, 0, true, true>, kThreads, fuse_dyn_smem<2>());
+    c->occ_fuse = std::max(1, occ);
   }
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<3>, kThreads, 0);

@@ -31,6 +31,9 @@
 #ifndef MPM_FFMA2
 #define MPM_FFMA2 1  // packed fp32x2 FMAs (sm_100 FFMA2) in the stencil sums
 #endif
+#ifndef MPM_FUSE_MINB
+#define MPM_FUSE_MINB 3
+#endif
 #ifndef MPM_SCAT_PF
 #define MPM_SCAT_PF 1
 #endif
@@ -71,7 +74,7 @@ constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
     asm volatile("griddepcontrol.launch_dependents;" ::);  \
   } while (0)
 
-enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6, E_SLAB = 9 };
+enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6, E_SLAB = 9, E_FUSE = 10 };
 
 template <int D> struct Dim;
 template <> struct Dim<3> {
@@ -575,7 +578,11 @@ __global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __rest
 // Three kernels: (a) per-block flags + tile sums (one block per thread), (b) one CTA scans
 // the tile sums and sets the step record, (c) tile-local scans write the tables.
 // ------------------------------------------------------------------------------------
-template <int D>
+// DIL (fused G2P2G, NEXT N2): the grid of step t+1 built while step t's particles are in
+// hand -- a particle of block b moves less than a cell per step, so its step-(t+1) stencil
+// lies in blocks b + {-1, 0, 1}^D: touched(b) = some block b + delta, delta in {-1,0,1}^D,
+// holds particles at step t.
+template <int D, bool DIL = false>
 __device__ __forceinline__ void block_flags(const KParams& P, const int* cnt, int gb, int& c,
                                             int& o, int& tch) {
   c = cnt[gb];
@@ -586,16 +593,31 @@ __device__ __forceinline__ void block_flags(const KParams& P, const int* cnt, in
 #pragma unroll
   for (int a = D - 1; a >= 0; --a) { b[a] = t % P.nbpa; t /= P.nbpa; }
   int any = 0;
+  if constexpr (DIL) {
 #pragma unroll
-  for (int dl = 0; dl < (1 << D); ++dl) {
-    int nb_[D];
-    bool ok = true;
+    for (int dl = 0; dl < Dim<D>::NS; ++dl) {
+      int nb_[D], q = dl;
+      bool ok = true;
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      nb_[a] = b[a] - ((dl >> (D - 1 - a)) & 1);
-      ok &= nb_[a] >= 0;
+      for (int a = D - 1; a >= 0; --a) {
+        nb_[a] = b[a] + q % 3 - 1;
+        q /= 3;
+        ok &= (nb_[a] >= 0) & (nb_[a] < P.nbpa);
+      }
+      if (ok) any |= __ldg(&cnt[r * P.nb + block_lin<D>(nb_, P.nbpa)]) > 0;
     }
-    if (ok) any |= __ldg(&cnt[r * P.nb + block_lin<D>(nb_, P.nbpa)]) > 0;
+  } else {
+#pragma unroll
+    for (int dl = 0; dl < (1 << D); ++dl) {
+      int nb_[D];
+      bool ok = true;
+#pragma unroll
+      for (int a = 0; a < D; ++a) {
+        nb_[a] = b[a] - ((dl >> (D - 1 - a)) & 1);
+        ok &= nb_[a] >= 0;
+      }
+      if (ok) any |= __ldg(&cnt[r * P.nb + block_lin<D>(nb_, P.nbpa)]) > 0;
+    }
   }
   tch = any;
 }
@@ -632,7 +654,7 @@ __device__ __forceinline__ int3 cta_excl_scan3(int3 v, int3* s_warp, int3& total
 
 // per-tile totals of (count, occupied, touched) -- used once by set_state to size the grid-slot
 // arena; flag word of a block: count | occupied << 30 | touched << 31
-template <int D>
+template <int D, bool DIL = false>
 __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __restrict__ cnt,
                                                      unsigned* __restrict__ bflag,
                                                      int3* __restrict__ tile_sums) {
@@ -641,7 +663,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __res
   const int gb = blockIdx.x * kScanTile + threadIdx.x;
   int c = 0, o = 0, t = 0;
   if (gb < P.NBT) {
-    block_flags<D>(P, cnt, gb, c, o, t);
+    block_flags<D, DIL>(P, cnt, gb, c, o, t);
     bflag[gb] = (unsigned)c | ((unsigned)o << 30) | ((unsigned)t << 31);
   }
   int3 tot;
@@ -662,12 +684,18 @@ struct ScanTileState {
   unsigned long long* ticket;
 };
 
-template <int D>
+// Outputs in two groups: the binning of step t (block_start, occupied list, info_bin's counts
+// and work counters; skipped when info_bin is null) and the grid-slot table of one grid
+// (slot map, touched list, info_grid's touched count / arena base; skipped when info_grid is
+// null) -- step t's own grid, or with DIL step t+1's (fused G2P2G).  The arena base follows
+// the previous grid's slots (info_gprev; null = the segment's first grid, base 0).
+template <int D, bool DIL = false>
 __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int* __restrict__ cnt, ScanTileState ts,
-                                                           unsigned epoch, int n_tiles, int* __restrict__ info,
-                                                           int tl, int* __restrict__ block_start,
-                                                           int* __restrict__ slot_of, int* __restrict__ occ_list,
-                                                           int* __restrict__ touched_list, ErrLatch* err, int t) {
+                                                           unsigned epoch, int n_tiles, int* __restrict__ info_bin,
+                                                           int* __restrict__ block_start, int* __restrict__ occ_list,
+                                                           int* __restrict__ info_grid, const int* __restrict__ info_gprev,
+                                                           int* __restrict__ slot_of, int* __restrict__ touched_list,
+                                                           ErrLatch* err, int t) {
   MPM_PDL_ENTRY();
   __shared__ int3 s_warp[kThreads / 32 + 1];
   __shared__ int s_tile;
@@ -677,7 +705,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
   const int tile = s_tile;
   const int gb = tile * kScanTile + threadIdx.x;
   int c = 0, o = 0, tc = 0;
-  if (gb < P.NBT) block_flags<D>(P, cnt, gb, c, o, tc);
+  if (gb < P.NBT) block_flags<D, DIL>(P, cnt, gb, c, o, tc);
   int3 tot;
   const int3 ex = cta_excl_scan3(make_int3(c, o, tc), s_warp, tot);
   const unsigned ep = epoch << 2;
@@ -722,42 +750,51 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
   }
   __syncthreads();
   const int3 pre = s_pre;
-  const int base = tl == 0 ? 0 : info[(tl - 1) * kInfo + I_BASE] + info[(tl - 1) * kInfo + I_NTOUCH];
+  const int base = info_gprev ? info_gprev[I_BASE] + info_gprev[I_NTOUCH] : 0;
   const int cap = min(P.slots_per_step, P.arena_slots - base);
   if (gb < P.NBT) {
-    block_start[gb] = ex.x + pre.x;
-    if (o) occ_list[ex.y + pre.y] = gb;
-    const int sl = ex.z + pre.z;
-    const bool fits = tc && sl < cap;
-    slot_of[gb] = fits ? base + sl : -1;
-    if (fits) touched_list[sl] = gb;
+    if (info_bin) {
+      block_start[gb] = ex.x + pre.x;
+      if (o) occ_list[ex.y + pre.y] = gb;
+    }
+    if (info_grid) {
+      const int sl = ex.z + pre.z;
+      const bool fits = tc && sl < cap;
+      slot_of[gb] = fits ? base + sl : -1;
+      if (fits) touched_list[sl] = gb;
+    }
   }
-  if (gb == P.NBT - 1) block_start[P.NBT] = P.NT;
+  if (info_bin && gb == P.NBT - 1) block_start[P.NBT] = P.NT;
   if (tile == n_tiles - 1 && threadIdx.x == 0) {
     const int ntouch = pre.z + tot.z;
     const int ok = ntouch <= cap;
-    if (!ok) latch(err, E_TAPE_FULL, t, ntouch);
-    int* I = info + tl * kInfo;
-    I[I_NOCC] = ok ? pre.y + tot.y : 0;
-    I[I_NTOUCH] = ok ? ntouch : 0;
-    I[I_BASE] = base;
-    I[I_WORK] = 0;
-    I[I_WORK2] = 0;
-    I[I_WORK3] = 0;
-    I[I_WORK4] = 0;
-    I[I_OK] = ok;
+    if (info_grid) {
+      if (!ok) latch(err, E_TAPE_FULL, DIL ? t + 1 : t, ntouch);
+      info_grid[I_NTOUCH] = ok ? ntouch : 0;
+      info_grid[I_BASE] = base;
+      info_grid[I_OK] = ok;
+    }
+    if (info_bin) {
+      info_bin[I_NOCC] = (ok || info_grid != info_bin) ? pre.y + tot.y : 0;
+      info_bin[I_WORK] = 0;
+      info_bin[I_WORK2] = 0;
+      info_bin[I_WORK3] = 0;
+      info_bin[I_WORK4] = 0;
+    }
   }
 }
 
 // counting-sort scatter by block (positions inside a block are fixed up by k_block_scatter);
 // also zeroes the grid slots of step t (the P2G flush accumulates into them)
 __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __restrict__ block_start,
-                          int* __restrict__ cnt, int2* __restrict__ tmp_pk,
-                          const int* __restrict__ info_t, float4* __restrict__ arena) {
+                          int* __restrict__ cnt, int2* __restrict__ tmp_pk, const int* __restrict__ zero_a,
+                          const int* __restrict__ zero_b, float4* __restrict__ arena) {
   MPM_PDL_ENTRY();
-  {
-    const int nz = info_t[I_NTOUCH] * kCPB;
-    float4* z = arena + (size_t)info_t[I_BASE] * kCPB;
+  // the grid slots the next scatter accumulates into (zero_a, zero_b: step records or null)
+  for (const int* zi : {zero_a, zero_b}) {
+    if (!zi) continue;
+    const int nz = zi[I_NTOUCH] * kCPB;
+    float4* z = arena + (size_t)zi[I_BASE] * kCPB;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nz; i += gridDim.x * blockDim.x)
       z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -842,6 +879,7 @@ struct StepArgs {
   const int* block_start;
   const int* occ_list;
   const int* slot_of;
+  const int* slot_next;   // fused G2P2G: slot map of grid t+1
   const int* touched_list;
   int* info_t;            // info of step t
   float4* grid;           // tape arena (forward) ; adjoint grid (ADJ)
@@ -905,13 +943,248 @@ __device__ __forceinline__ bool work_item(const StepArgs& A, int wi, int n_occ, 
   return true;
 }
 
+// P2G payload of one particle (Eq. 4 with P_total F^T = tau, R1/R21 + actuation S1):
+//   B = dx G = -4 res dt V tau + m dx C,  A = m v - B fx   (node value w_o (A + B o))
+// t = the step whose actuation applies; latches an inverted element (det F <= 0).
+template <int D, int MAT>
+__device__ __forceinline__ void p2g_payload(const KParams& P, const StepArgs& A, int r, int t, int u, const float4& pr,
+                                            const float (&v)[D], const float (&H)[D][D], const float (&Cm)[D][D],
+                                            const float (&f)[D], float (&Av)[D], float (&Bm)[D][D]) {
+  float sig[D];
+  const int ai = A.aid[u];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    sig[a] = ai >= 0 ? P.act_s * A.act[(((size_t)r * P.T + t) * P.K + ai) * D + a] : 0.f;
+  const float jm1 = det1m<D>(H);  // J - 1
+  if (!(jm1 > -1.f)) latch(A.err, E_INVERTED, t, u);
+  const float lnJ = log1pf(jm1);
+  float tau[D][D];
+  if constexpr (MAT == 1) kirchhoff_fcr<D>(H, pr.z, pr.w, sig, tau, jm1);  // R21
+  else kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, lnJ);
+  const float kk = 4.f * P.fres * P.dt * pr.y;
+  const float mdx = pr.x * P.dx;
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) Bm[a][b] = fmaf(-kk, tau[a][b], mdx * Cm[a][b]);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    float acc = pr.x * v[a];
+#pragma unroll
+    for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], f[b], acc);
+    Av[a] = acc;
+  }
+}
+
+// exclusive scan of the kCPB = 64 cell counts by warp 0: s_cstart[0..64], s_cursor = starts
+__device__ __forceinline__ void cell_scan(const int* s_hist, int* s_cstart, int* s_cursor, int tid) {
+  static_assert(kCPB == 64, "two cells per lane");
+  if (tid < 32) {
+    int v0 = s_hist[tid], v1 = s_hist[tid + 32];
+    int i0 = v0, i1 = v1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, i0, o);
+      int b = __shfl_up_sync(0xffffffffu, i1, o);
+      if (tid >= o) { i0 += a; i1 += b; }
+    }
+    int tot0 = __shfl_sync(0xffffffffu, i0, 31);
+    s_cstart[tid] = i0 - v0;
+    s_cstart[tid + 32] = tot0 + i1 - v1;
+    s_cursor[tid] = i0 - v0;
+    s_cursor[tid + 32] = tot0 + i1 - v1;
+    if (tid == 31) s_cstart[kCPB] = tot0 + i1;
+  }
+}
+
+// Forward in-block sort (P2G prologue): the block's particles, grouped by k_scatter in
+// (storage index, key) pairs, are sorted by (cell, storage index) (stable, R18) into
+// perm[s .. s+n); s_cstart gets the cells' ranges.  CTA-wide (contains barriers).
+template <int D, bool PF_XF = false>
+__device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs& A, int s, int n, int tid,
+                                                int* s_hist, int* s_cstart, int* s_cursor, int* s_sort) {
+  const size_t NT = P.NT;
+  // (storage index, cell) of this thread's first two particles stay in registers
+  int pj[2] = {0, 0}, pc[2] = {0, 0};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int i = tid + q * kThreads;
+    if (i < n) {
+      const int2 e = A.tmp_pk[s + i];
+      pj[q] = e.x;
+      pc[q] = e.y & (kCPB - 1);
+      atomicAdd(&s_hist[pc[q]], 1);
+#if MPM_SCAT_PF
+      // the producer reads this particle's record after the sort: start fetching it now
+      // (PF_XF: the fused G2P2G reads x and F only)
+      if (PF_XF) {
+        prefetch_record(A.st, NT, e.x, 0, D);
+        prefetch_record(A.st, NT, e.x, comp_F<D>(0, 0), D * D);
+      } else {
+        prefetch_record(A.st, NT, e.x, 0, Dim<D>::S);
+      }
+      prefetch_l2(&A.orig[e.x]);
+#endif
+    }
+  }
+  for (int i = tid + 2 * kThreads; i < n; i += kThreads) atomicAdd(&s_hist[A.tmp_pk[s + i].y & (kCPB - 1)], 1);
+  __syncthreads();
+  cell_scan(s_hist, s_cstart, s_cursor, tid);
+  __syncthreads();
+  int* buf = (n <= kSortCap) ? s_sort : (A.scratch + s);
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (tid + q * kThreads < n) buf[atomicAdd(&s_cursor[pc[q]], 1)] = pj[q];
+  for (int i = tid + 2 * kThreads; i < n; i += kThreads) {
+    const int2 e = A.tmp_pk[s + i];
+    buf[atomicAdd(&s_cursor[e.y & (kCPB - 1)], 1)] = e.x;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += kThreads) {
+    const int j = buf[i];
+    int c = 0;  // cell of position i: the last c with cstart[c] <= i (binary search)
+#pragma unroll
+    for (int step = kCPB / 2; step > 0; step >>= 1)
+      if (s_cstart[c + step] <= i) c += step;
+    const int lo = s_cstart[c], hi = s_cstart[c + 1];
+    int rank = 0;
+    for (int q = lo; q < hi; ++q) rank += buf[q] < j;
+    A.perm[s + lo + rank] = j;  // stable: ties by storage index (R18)
+  }
+  __syncthreads();
+}
+
+// Scatter consumer: thread (ox, c), c = cell, accumulates the NSUB nodes c + (ox, *) of the
+// payload positions [i0, i1) (ORD: through the order s_ord) in registers, then writes them
+// into tile copy ox in NSUB conflict-free phases (64-thread named barriers).
+template <int D, bool ADJ, bool ORD>
+__device__ __forceinline__ void scatter_consume(const float (*s_pay)[kCap], float4 (*s_tile)[Dim<D>::TN], int i0,
+                                                int i1, const short* s_ord, int ox, int c, int tid) {
+  using PY = Pay<D, ADJ>;
+  constexpr int BB = Dim<D>::BB, TE = Dim<D>::TE;
+  constexpr int NSUB = (D == 3) ? 9 : 3;
+  // consumer: thread (ox, c), c = cell, accumulates NSUB nodes
+  float4 acc[NSUB];
+#pragma unroll
+  for (int q = 0; q < NSUB; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tid < 3 * kCPB) {
+    for (int i0s = i0; i0s < i1; ++i0s) {
+      const int i = pay_slot(ORD ? (int)s_ord[i0s] : i0s);
+      const float wx = s_pay[PY::W + ox][i];
+      float Ax[3];
+#pragma unroll
+      for (int a = 0; a < D; ++a) Ax[a] = s_pay[PY::A + a][i] + (float)ox * s_pay[PY::B + a * D + 0][i];
+      const float mp = ADJ ? 0.f : s_pay[PY::M < 0 ? 0 : PY::M][i];
+      if (D == 3) {
+        float B1[3], B2[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) { B1[a] = s_pay[PY::B + a * D + 1][i]; B2[a] = s_pay[PY::B + a * D + 2 % D][i]; }
+#pragma unroll
+        for (int oy = 0; oy < 3; ++oy) {
+          const float wxy = wx * s_pay[PY::W + 3 + oy][i];
+#if MPM_FFMA2_SCAT
+          // node value A + oy B1 + oz B2 and the accumulation as packed fp32x2 FMAs:
+          // (x, y) and (z, m) pairs (sm_100 FFMA2; per component the same fused op)
+          const float2 rxy = __ffma2_rn(make_float2((float)oy, (float)oy), make_float2(B1[0], B1[1]),
+                                        make_float2(Ax[0], Ax[1]));
+          const float rz = fmaf((float)oy, B1[2], Ax[2]);
+#pragma unroll
+          for (int oz = 0; oz < 3; ++oz) {
+            const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
+            float4& q = acc[oy * 3 + oz];
+            const float2 vxy = oz ? __ffma2_rn(make_float2((float)oz, (float)oz), make_float2(B2[0], B2[1]), rxy) : rxy;
+            const float vz = oz ? fmaf((float)oz, B2[2], rz) : rz;
+            const float2 qxy = __ffma2_rn(make_float2(W, W), vxy, make_float2(q.x, q.y));
+            const float2 qzw = __ffma2_rn(make_float2(W, W), make_float2(vz, ADJ ? 0.f : mp), make_float2(q.z, q.w));
+            q = make_float4(qxy.x, qxy.y, qzw.x, ADJ ? q.w : qzw.y);
+          }
+#else
+#pragma unroll
+          for (int oz = 0; oz < 3; ++oz) {
+            const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
+            float4& q = acc[oy * 3 + oz];
+            q.x = fmaf(W, Ax[0] + (float)oy * B1[0] + (float)oz * B2[0], q.x);
+            q.y = fmaf(W, Ax[1] + (float)oy * B1[1] + (float)oz * B2[1], q.y);
+            q.z = fmaf(W, Ax[2] + (float)oy * B1[2] + (float)oz * B2[2], q.z);
+            if (!ADJ) q.w = fmaf(W, mp, q.w);
+          }
+#endif
+        }
+      } else {
+        float B1[2];
+#pragma unroll
+        for (int a = 0; a < 2; ++a) B1[a] = s_pay[PY::B + a * D + 1][i];
+#pragma unroll
+        for (int oy = 0; oy < 3; ++oy) {
+          const float W = wx * s_pay[PY::W + 3 + oy][i];
+          float4& q = acc[oy];
+          q.x = fmaf(W, Ax[0] + (float)oy * B1[0], q.x);
+          q.y = fmaf(W, Ax[1] + (float)oy * B1[1], q.y);
+          if (!ADJ) q.w = fmaf(W, mp, q.w);
+        }
+      }
+    }
+  }
+  // phase-write: in phase q the 64 threads of copy ox write the distinct nodes c + (ox, q);
+  // only threads of the same copy can collide across phases -> 64-thread named barriers
+  if (tid < 3 * kCPB) {
+    int cc[D];
+    {
+      int t = c;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) { cc[a] = t % BB; t /= BB; }
+    }
+#pragma unroll
+    for (int q = 0; q < NSUB; ++q) {
+      int tl;
+      if (D == 3) tl = ((cc[0] + ox) * TE + cc[1] + q / 3) * TE + cc[D - 1] + q % 3;
+      else tl = (cc[0] + ox) * TE + cc[D - 1] + q;
+      float4 v = s_tile[ox][tl];
+      v.x += acc[q].x; v.y += acc[q].y; v.z += acc[q].z; v.w += acc[q].w;
+      s_tile[ox][tl] = v;
+      if (q + 1 < NSUB) asm volatile("bar.sync %0, %1;" ::"r"(1 + ox), "r"(kCPB) : "memory");
+    }
+  }
+}
+
+// Scatter flush: the 3 tile copies summed, one vector RED (red.global.add.v4.f32) per
+// non-zero node into its grid slot; myslot (lanes 0..2^D-1) = the slots of blocks bc + {0,1}^D.
+template <int D, bool ADJ>
+__device__ __forceinline__ void scatter_flush(const KParams& P, float4* grid, const float4 (*s_tile)[Dim<D>::TN],
+                                              const int* bc, int myslot, int base_slot, int tid) {
+  constexpr int BB = Dim<D>::BB, TE = Dim<D>::TE, TN = Dim<D>::TN;
+  for (int t0 = 0; t0 < TN; t0 += kThreads) {  // uniform trip count: whole warps reach the shuffle
+    const int tn = t0 + tid;
+    int tl[D], sb = 0;
+    {
+      int t = tn;
+#pragma unroll
+      for (int a = D - 1; a >= 0; --a) {
+        tl[a] = t % TE;
+        sb |= (tl[a] >= BB) << (D - 1 - a);
+        t /= TE;
+      }
+    }
+    const int slot = __shfl_sync(0xffffffffu, myslot, sb);
+    if (tn >= TN) continue;
+    float4 v0 = s_tile[0][tn], v1 = s_tile[1][tn], v2 = s_tile[2][tn];
+    float4 v = make_float4(v0.x + v1.x + v2.x, v0.y + v1.y + v2.y, v0.z + v1.z + v2.z, v0.w + v1.w + v2.w);
+    if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
+    int loc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) loc[a] = (bc[a] * BB + tl[a]) & (BB - 1);
+    if (slot < 0) continue;  // outside the domain / untouched (cannot happen for non-zero nodes)
+    float4* dst = grid + (size_t)(ADJ ? slot - base_slot : slot) * kCPB + cell_lin<D>(loc);
+    atomicAdd(dst, v);  // red.global.add.v4.f32
+  }
+}
+
 template <int D, bool ADJ, int MAT = 0, bool SPLIT = false>
 __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   using DD = Dim<D>;
   using PY = Pay<D, ADJ>;
-  constexpr int BB = DD::BB, TE = DD::TE, TN = DD::TN;
-  constexpr int NSUB = (D == 3) ? 9 : 3;  // nodes per (cell, ox) thread
+  constexpr int BB = DD::BB, TN = DD::TN;
   __shared__ int s_hist[kCPB];
   __shared__ int s_cstart[kCPB + 1];
   __shared__ int s_cursor[kCPB];
@@ -968,67 +1241,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
     for (int i = tid; i < 3 * TN; i += kThreads) (&s_tile[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
 
-    // ---- forward: cell ranges + the stable in-block sort by (cell, index).  The adjoint
-    //      (perm already sorted) finds each cell's sub-range per chunk in the producer. ----
-    if (!ADJ) {
-      // (storage index, cell) of this thread's first two particles stay in registers
-      int pj[2] = {0, 0}, pc[2] = {0, 0};
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int i = tid + q * kThreads;
-        if (i < n) {
-          const int2 e = A.tmp_pk[s + i];
-          pj[q] = e.x;
-          pc[q] = e.y & (kCPB - 1);
-          atomicAdd(&s_hist[pc[q]], 1);
-#if MPM_SCAT_PF
-          // the producer reads this particle's record after the sort: start fetching it now
-          prefetch_record(A.st, NT, e.x, 0, Dim<D>::S);
-          prefetch_l2(&A.orig[e.x]);
-#endif
-        }
-      }
-      for (int i = tid + 2 * kThreads; i < n; i += kThreads) atomicAdd(&s_hist[A.tmp_pk[s + i].y & (kCPB - 1)], 1);
-      __syncthreads();
-      if (tid < 32) {
-        int v0 = s_hist[tid], v1 = s_hist[tid + 32];
-        int i0 = v0, i1 = v1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          int a = __shfl_up_sync(0xffffffffu, i0, o);
-          int b = __shfl_up_sync(0xffffffffu, i1, o);
-          if (tid >= o) { i0 += a; i1 += b; }
-        }
-        int tot0 = __shfl_sync(0xffffffffu, i0, 31);
-        s_cstart[tid] = i0 - v0;
-        s_cstart[tid + 32] = tot0 + i1 - v1;
-        s_cursor[tid] = i0 - v0;
-        s_cursor[tid + 32] = tot0 + i1 - v1;
-        if (tid == 31) s_cstart[kCPB] = tot0 + i1;
-      }
-      __syncthreads();
-      int* buf = (n <= kSortCap) ? s_sort : (A.scratch + s);
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        if (tid + q * kThreads < n) buf[atomicAdd(&s_cursor[pc[q]], 1)] = pj[q];
-      for (int i = tid + 2 * kThreads; i < n; i += kThreads) {
-        const int2 e = A.tmp_pk[s + i];
-        buf[atomicAdd(&s_cursor[e.y & (kCPB - 1)], 1)] = e.x;
-      }
-      __syncthreads();
-      for (int i = tid; i < n; i += kThreads) {
-        const int j = buf[i];
-        int c = 0;  // cell of position i: the last c with cstart[c] <= i (binary search)
-#pragma unroll
-        for (int step = kCPB / 2; step > 0; step >>= 1)
-          if (s_cstart[c + step] <= i) c += step;
-        const int lo = s_cstart[c], hi = s_cstart[c + 1];
-        int rank = 0;
-        for (int q = lo; q < hi; ++q) rank += buf[q] < j;
-        A.perm[s + lo + rank] = j;  // stable: ties by storage index (R18)
-      }
-      __syncthreads();
-    }
+    if (!ADJ) block_cell_sort<D>(P, A, s, n, tid, s_hist, s_cstart, s_cursor, s_sort);
 
     // ---- chunks of kCap particles: produce payload, consume per (cell, ox), phase-write ----
     // consumer thread -> (ox, cell).  3D: cell z fastest, then x, then y, so the 8 threads of a
@@ -1077,31 +1290,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
               Cm[a][b] = A.st[(size_t)comp_C<D>(a, b) * NT + j];
             }
           }
-          float sig[D];
-          const int ai = A.aid[u];
-#pragma unroll
-          for (int a = 0; a < D; ++a)
-            sig[a] = ai >= 0 ? P.act_s * A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a] : 0.f;
-          const float jm1 = det1m<D>(H);  // J - 1
-          if (!(jm1 > -1.f)) latch(A.err, E_INVERTED, A.t, u);
-          const float lnJ = log1pf(jm1);
-          float tau[D][D];
-          if constexpr (MAT == 1) kirchhoff_fcr<D>(H, pr.z, pr.w, sig, tau, jm1);  // R21
-          else kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, lnJ);
-          // B = dx G = -4 res dt V tau + m dx C ;  A = m v - B fx
-          const float kk = 4.f * P.fres * P.dt * pr.y;
-          const float mdx = pr.x * P.dx;
-#pragma unroll
-          for (int a = 0; a < D; ++a)
-#pragma unroll
-            for (int b = 0; b < D; ++b) Bm[a][b] = fmaf(-kk, tau[a][b], mdx * Cm[a][b]);
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            float acc = pr.x * v[a];
-#pragma unroll
-            for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], f[b], acc);
-            Av[a] = acc;
-          }
+          p2g_payload<D, MAT>(P, A, r, A.t, u, pr, v, H, Cm, f, Av, Bm);
           if (PY::M >= 0) s_pay[PY::M < 0 ? 0 : PY::M][ps] = pr.x;
         } else {
           // steps A and B: g_v = gv + dt gx ; g_C = gC + dt gF F^T
@@ -1144,89 +1333,10 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
       }
       __syncthreads();
 
-      // consumer: thread (ox, c), c = cell, accumulates NSUB nodes
-      float4 acc[NSUB];
-#pragma unroll
-      for (int q = 0; q < NSUB; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (tid < 3 * kCPB) {
-        const int i0 = ADJ ? s_cstart[c] : max(s_cstart[c], lo) - lo;
-        const int i1 = ADJ ? s_cursor[c] + 1 : min(s_cstart[c + 1], hi) - lo;
-        for (int i0s = i0; i0s < i1; ++i0s) {
-          const int i = pay_slot(i0s);
-          const float wx = s_pay[PY::W + ox][i];
-          float Ax[3];
-#pragma unroll
-          for (int a = 0; a < D; ++a) Ax[a] = s_pay[PY::A + a][i] + (float)ox * s_pay[PY::B + a * D + 0][i];
-          const float mp = ADJ ? 0.f : s_pay[PY::M < 0 ? 0 : PY::M][i];
-          if (D == 3) {
-            float B1[3], B2[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) { B1[a] = s_pay[PY::B + a * D + 1][i]; B2[a] = s_pay[PY::B + a * D + 2 % D][i]; }
-#pragma unroll
-            for (int oy = 0; oy < 3; ++oy) {
-              const float wxy = wx * s_pay[PY::W + 3 + oy][i];
-#if MPM_FFMA2_SCAT
-              // node value A + oy B1 + oz B2 and the accumulation as packed fp32x2 FMAs:
-              // (x, y) and (z, m) pairs (sm_100 FFMA2; per component the same fused op)
-              const float2 rxy = __ffma2_rn(make_float2((float)oy, (float)oy), make_float2(B1[0], B1[1]),
-                                            make_float2(Ax[0], Ax[1]));
-              const float rz = fmaf((float)oy, B1[2], Ax[2]);
-#pragma unroll
-              for (int oz = 0; oz < 3; ++oz) {
-                const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
-                float4& q = acc[oy * 3 + oz];
-                const float2 vxy = oz ? __ffma2_rn(make_float2((float)oz, (float)oz), make_float2(B2[0], B2[1]), rxy) : rxy;
-                const float vz = oz ? fmaf((float)oz, B2[2], rz) : rz;
-                const float2 qxy = __ffma2_rn(make_float2(W, W), vxy, make_float2(q.x, q.y));
-                const float2 qzw = __ffma2_rn(make_float2(W, W), make_float2(vz, ADJ ? 0.f : mp), make_float2(q.z, q.w));
-                q = make_float4(qxy.x, qxy.y, qzw.x, ADJ ? q.w : qzw.y);
-              }
-#else
-#pragma unroll
-              for (int oz = 0; oz < 3; ++oz) {
-                const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
-                float4& q = acc[oy * 3 + oz];
-                q.x = fmaf(W, Ax[0] + (float)oy * B1[0] + (float)oz * B2[0], q.x);
-                q.y = fmaf(W, Ax[1] + (float)oy * B1[1] + (float)oz * B2[1], q.y);
-                q.z = fmaf(W, Ax[2] + (float)oy * B1[2] + (float)oz * B2[2], q.z);
-                if (!ADJ) q.w = fmaf(W, mp, q.w);
-              }
-#endif
-            }
-          } else {
-            float B1[2];
-#pragma unroll
-            for (int a = 0; a < 2; ++a) B1[a] = s_pay[PY::B + a * D + 1][i];
-#pragma unroll
-            for (int oy = 0; oy < 3; ++oy) {
-              const float W = wx * s_pay[PY::W + 3 + oy][i];
-              float4& q = acc[oy];
-              q.x = fmaf(W, Ax[0] + (float)oy * B1[0], q.x);
-              q.y = fmaf(W, Ax[1] + (float)oy * B1[1], q.y);
-              if (!ADJ) q.w = fmaf(W, mp, q.w);
-            }
-          }
-        }
-      }
-      // phase-write: in phase q the 64 threads of copy ox write the distinct nodes c + (ox, q);
-      // only threads of the same copy can collide across phases -> 64-thread named barriers
-      if (tid < 3 * kCPB) {
-        int cc[D];
-        {
-          int t = c;
-#pragma unroll
-          for (int a = D - 1; a >= 0; --a) { cc[a] = t % BB; t /= BB; }
-        }
-#pragma unroll
-        for (int q = 0; q < NSUB; ++q) {
-          int tl;
-          if (D == 3) tl = ((cc[0] + ox) * TE + cc[1] + q / 3) * TE + cc[D - 1] + q % 3;
-          else tl = (cc[0] + ox) * TE + cc[D - 1] + q;
-          float4 v = s_tile[ox][tl];
-          v.x += acc[q].x; v.y += acc[q].y; v.z += acc[q].z; v.w += acc[q].w;
-          s_tile[ox][tl] = v;
-          if (q + 1 < NSUB) asm volatile("bar.sync %0, %1;" ::"r"(1 + ox), "r"(kCPB) : "memory");
-        }
+      {
+        const int i0 = (tid < 3 * kCPB) ? (ADJ ? s_cstart[c] : max(s_cstart[c], lo) - lo) : 0;
+        const int i1 = (tid < 3 * kCPB) ? (ADJ ? s_cursor[c] + 1 : min(s_cstart[c + 1], hi) - lo) : 0;
+        scatter_consume<D, ADJ, false>(s_pay, s_tile, i0, i1, nullptr, ox, c, tid);
       }
       __syncthreads();  // payload consumed, tile copies written
     }
@@ -1234,30 +1344,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
     // ---- flush: one vector RED per non-zero tile node.  The tile spans the 2^D blocks
     //      bc + {0, 1}^D: lanes 0..2^D-1 of each warp look their slots up, nodes take theirs by
     //      shuffle (one dependent global load less per node) ----
-    for (int t0 = 0; t0 < TN; t0 += kThreads) {  // uniform trip count: whole warps reach the shuffle
-      const int tn = t0 + tid;
-      int tl[D], sb = 0;
-      {
-        int t = tn;
-#pragma unroll
-        for (int a = D - 1; a >= 0; --a) {
-          tl[a] = t % TE;
-          sb |= (tl[a] >= BB) << (D - 1 - a);
-          t /= TE;
-        }
-      }
-      const int slot = __shfl_sync(0xffffffffu, myslot, sb);
-      if (tn >= TN) continue;
-      float4 v0 = s_tile[0][tn], v1 = s_tile[1][tn], v2 = s_tile[2][tn];
-      float4 v = make_float4(v0.x + v1.x + v2.x, v0.y + v1.y + v2.y, v0.z + v1.z + v2.z, v0.w + v1.w + v2.w);
-      if (v.x == 0.f && v.y == 0.f && v.z == 0.f && v.w == 0.f) continue;
-      int loc[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) loc[a] = (bc[a] * BB + tl[a]) & (BB - 1);
-      if (slot < 0) continue;  // outside the domain / untouched (cannot happen for non-zero nodes)
-      float4* dst = A.grid + (size_t)(ADJ ? slot - base_slot : slot) * kCPB + cell_lin<D>(loc);
-      atomicAdd(dst, v);  // red.global.add.v4.f32
-    }
+    scatter_flush<D, ADJ>(P, A.grid, s_tile, bc, myslot, base_slot, tid);
     __syncthreads();
   }
 }
@@ -1471,6 +1558,72 @@ __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const 
   }
 }
 
+// G2P of the particle at sorted position k (Eqs. 7-10): writes state t+1 at k, its user
+// index, key and the block histogram of step t+1; returns the new x, v, C and H = F - I in
+// registers (the fused G2P2G scatters them) and whether the new base index is valid.
+// COH: perm was written by this kernel (the fused sort) -- a coherent load, not the
+// read-only path.
+template <int D, bool COH = false>
+__device__ __forceinline__ bool g2p_particle(const KParams& P, const StepArgs& A, const float4* s_v,
+                                             const float4& vref, const int* bc, int r, int k, float (&x)[D],
+                                             float (&vn)[D], float (&Cn)[D][D], float (&Hn)[D][D], int& u) {
+  const size_t NT = P.NT;
+  const int j = COH ? __ldcg(&A.perm[k]) : __ldg(&A.perm[k]);
+  float H[D][D];  // H = F - I
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
+#pragma unroll
+    for (int b = 0; b < D; ++b) H[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
+  }
+  u = __ldg(&A.orig[j]);
+  Stencil<D> sc;
+  make_stencil<D>(x, P.fres, sc);
+  int lb[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) lb[a] = sc.base[a] - bc[a] * Dim<D>::BB;
+  float S[D], M[D][D];
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    S[a] = 0.f;
+#pragma unroll
+    for (int b = 0; b < D; ++b) M[a][b] = 0.f;
+  }
+  g2p_row<D, 0, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 0, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 0, 2>(s_v, lb, sc, vref, S, M);
+  g2p_row<D, 1, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 1, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 1, 2>(s_v, lb, sc, vref, S, M);
+  g2p_row<D, 2, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 2, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 2, 2>(s_v, lb, sc, vref, S, M);
+  float* out = A.st_next;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+#pragma unroll
+    for (int b = 0; b < D; ++b) Cn[a][b] = 4.f * P.fres * fmaf(-S[a], sc.fx[b], M[a][b]);
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      // F' = (I + dt C') F  <=>  H' = H + dt C' (I + H)  (Eq. 9 on H = F - I)
+      float acc = fmaf(P.dt, Cn[a][b], H[a][b]);
+#pragma unroll
+      for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[a][c], H[c][b], acc);
+      Hn[a][b] = acc;
+      out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
+      out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[a][b];
+    }
+    vn[a] = S[a] + (&vref.x)[a];
+    out[(size_t)comp_v<D>(a) * NT + k] = vn[a];
+    x[a] = fmaf(P.dt, vn[a], x[a]);
+    out[(size_t)comp_x<D>(a) * NT + k] = x[a];
+  }
+  A.orig_next[k] = u;
+  int gbn, key;
+  const int e = key_of<D>(x, r, P, gbn, key);
+  if (e) latch(A.err, e, A.t + 1, u);
+  A.key_next[k] = key;
+  // block histogram of step t+1 (threads of a warp mostly share one block)
+  const unsigned am = __activemask();
+  const unsigned peers = __match_any_sync(am, gbn);
+  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&A.cnt[gbn], __popc(peers));
+  return e == E_OK;
+}
+
 template <int D, bool SPLIT = false>
 __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
@@ -1501,60 +1654,179 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += kThreads) {
-      const int k = s + i;
-      const int j = __ldg(&A.perm[k]);
-      float x[D], H[D][D];  // H = F - I
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
-#pragma unroll
-        for (int b = 0; b < D; ++b) H[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
-      }
-      const int u = __ldg(&A.orig[j]);
-      Stencil<D> sc;
-      make_stencil<D>(x, P.fres, sc);
-      int lb[D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) lb[a] = sc.base[a] - bc[a] * Dim<D>::BB;
-      float S[D], M[D][D];
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        S[a] = 0.f;
-#pragma unroll
-        for (int b = 0; b < D; ++b) M[a][b] = 0.f;
-      }
-      g2p_row<D, 0, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 0, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 0, 2>(s_v, lb, sc, vref, S, M);
-      g2p_row<D, 1, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 1, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 1, 2>(s_v, lb, sc, vref, S, M);
-      g2p_row<D, 2, 0>(s_v, lb, sc, vref, S, M); g2p_row<D, 2, 1>(s_v, lb, sc, vref, S, M); g2p_row<D, 2, 2>(s_v, lb, sc, vref, S, M);
-      float* out = A.st_next;
-#pragma unroll
-      for (int a = 0; a < D; ++a) {
-        float Cn[D];
-#pragma unroll
-        for (int b = 0; b < D; ++b) Cn[b] = 4.f * P.fres * fmaf(-S[a], sc.fx[b], M[a][b]);
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-          // F' = (I + dt C') F  <=>  H' = H + dt C' (I + H)  (Eq. 9 on H = F - I)
-          float acc = fmaf(P.dt, Cn[b], H[a][b]);
-#pragma unroll
-          for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[c], H[c][b], acc);
-          out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
-          out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[b];
-        }
-        const float vn = S[a] + (&vref.x)[a];
-        out[(size_t)comp_v<D>(a) * NT + k] = vn;
-        x[a] = fmaf(P.dt, vn, x[a]);
-        out[(size_t)comp_x<D>(a) * NT + k] = x[a];
-      }
-      A.orig_next[k] = u;
-      int gbn, key;
-      if (const int e = key_of<D>(x, r, P, gbn, key)) latch(A.err, e, A.t + 1, u);
-      A.key_next[k] = key;
-      // block histogram of step t+1 (threads of a warp mostly share one block)
-      const unsigned am = __activemask();
-      const unsigned peers = __match_any_sync(am, gbn);
-      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&A.cnt[gbn], __popc(peers));
+      float x[D], vn[D], Cn[D][D], Hn[D][D];
+      int u;
+      g2p_particle<D>(P, A, s_v, vref, bc, r, s + i, x, vn, Cn, Hn, u);
     }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// Fused G2P2G (NEXT N2): one pass over the particles per step.  CTA per occupied
+// block of step t: [SORT: the in-block cell sort of step t (perm)] -> stage grid t (fused grid
+// update) -> G2P of each particle (state t+1 written to the tape) -> [SCAT: with the new
+// state still in registers, the step-(t+1) stress and P2G payload -> in-CTA counting sort by
+// the new cell -> the tile consumer -> RED flush into grid t+1].  Grid t+1's slot map is the
+// dilated one (k_scan_lookback<D, true>): a particle whose new base cell left its block (a
+// few per block) adds its 3^D nodes with direct vector REDs instead of through the tile.
+// The (p, m) accumulated are those of the unfused P2G of step t+1 up to fp32 summation order.
+// Saves the P2G re-read of the state (x, v, C, F, 96 B) and one launch per step.
+// ------------------------------------------------------------------------------------
+template <int D>
+constexpr int fuse_dyn_smem() { return Pay<D, false>::N * kCap * (int)sizeof(float); }
+
+// direct scatter of one particle's 3^D nodes into grid t+1 (escapees of the tile)
+template <int D>
+__device__ __forceinline__ void scatter_direct(const KParams& P, const StepArgs& A, int r, int u,
+                                               const Stencil<D>& sc, float m, const float (&Av)[D],
+                                               const float (&Bm)[D][D]) {
+  using DD = Dim<D>;
+#pragma unroll
+  for (int q = 0; q < DD::NS; ++q) {
+    int o[D], nb_[D], loc[D], t = q;
+    float W = 1.f;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      o[a] = t % 3;
+      t /= 3;
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      W *= sc.w[a][o[a]];
+      const int node = sc.base[a] + o[a];
+      nb_[a] = node >> DD::LOG_BB;
+      loc[a] = node & (DD::BB - 1);
+    }
+    const int slot = __ldg(&A.slot_next[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+    if (slot < 0) {  // moved more than the dilation allows (|v| dt >= dx)
+      latch(A.err, E_FUSE, A.t + 1, u);
+      return;
+    }
+    float val[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float acc = Av[a];
+#pragma unroll
+      for (int b = 0; b < D; ++b) acc = fmaf((float)o[b], Bm[a][b], acc);
+      val[a] = W * acc;
+    }
+    atomicAdd(A.grid + (size_t)slot * kCPB + cell_lin<D>(loc), make_float4(val[0], val[1], val[2], W * m));
+  }
+}
+
+template <int D, int MAT, bool SORT, bool SCAT>
+__global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, StepArgs A) {
+  MPM_PDL_ENTRY();
+  using DD = Dim<D>;
+  using PY = Pay<D, false>;
+  constexpr int BB = DD::BB, TN = DD::TN;
+  __shared__ int s_hist[kCPB];
+  __shared__ int s_cstart[kCPB + 1];
+  __shared__ int s_cursor[kCPB];
+  __shared__ int s_sort[SORT ? kSortCap : 1];
+  __shared__ float4 s_v[TN];
+  __shared__ float4 s_tile[3][SCAT ? TN : 1];
+  __shared__ short s_cell[SCAT ? kCap : 1];
+  __shared__ short s_ord[SCAT ? kCap : 1];
+  extern __shared__ __align__(16) unsigned char s_dyn[];
+  float (*s_pay)[kCap] = reinterpret_cast<float (*)[kCap]>(s_dyn);  // [PY::N][kCap], dynamic (SCAT)
+  __shared__ int s_blk;
+  const int tid = threadIdx.x;
+  const int n_occ = A.info_t[I_NOCC];
+  const int ox = tid / kCPB;
+  const int c = D == 3 ? ((((tid >> 2) & 3) * 4 + ((tid >> 4) & 3)) * 4 + (tid & 3)) : tid % kCPB;
+  for (;;) {
+    if (tid == 0) s_blk = atomicAdd(&A.info_t[I_WORK3], 1);
+    __syncthreads();
+    int gb, s, n;
+    if (!work_item<false>(A, s_blk, n_occ, 1, gb, s, n)) break;
+    int r, bc[D];
+    block_coords<D>(P, gb, r, bc);
+    int myslot = -1;  // grid t+1 slots of the tile's blocks bc + {0, 1}^D (flush)
+    if (SCAT) {
+      const int lane = tid & 31;
+      if (lane < (1 << D)) {
+        int nb_[D];
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          nb_[a] = bc[a] + ((lane >> (D - 1 - a)) & 1);
+          inside &= nb_[a] < P.nbpa;
+        }
+        if (inside) myslot = __ldg(&A.slot_next[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+      }
+      for (int i = tid; i < 3 * TN; i += kThreads) (&s_tile[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (SORT) {
+      if (tid < kCPB) s_hist[tid] = 0;
+      __syncthreads();
+      block_cell_sort<D, true>(P, A, s, n, tid, s_hist, s_cstart, s_cursor, s_sort);
+    }
+    float4 vref, aref_unused;
+    stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
+    __syncthreads();
+    for (int lo = 0; lo < n; lo += kCap) {
+      const int hi = min(n, lo + kCap);
+      if (SCAT) {
+        if (tid < kCPB) s_hist[tid] = 0;
+        __syncthreads();
+      }
+      for (int pi = tid; pi < hi - lo; pi += kThreads) {
+        float x[D], vn[D], Cn[D][D], Hn[D][D];
+        int u;
+        const bool ok = g2p_particle<D, SORT>(P, A, s_v, vref, bc, r, s + lo + pi, x, vn, Cn, Hn, u);
+        if constexpr (SCAT) {
+          Stencil<D> sc;
+          make_stencil<D>(x, P.fres, sc);
+          int lb[D];
+          bool inb = true;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            lb[a] = sc.base[a] - bc[a] * BB;
+            inb &= (lb[a] >= 0) & (lb[a] < BB);
+          }
+          const float4 pr = __ldg(&A.prm[u]);  // m, V, mu, lam
+          float Av[D], Bm[D][D];
+          p2g_payload<D, MAT>(P, A, r, A.t + 1, u, pr, vn, Hn, Cn, sc.fx, Av, Bm);
+          int cell = -1;
+          if (ok && inb) {
+            cell = cell_lin<D>(lb);
+            const int ps = pay_slot(pi);
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+              for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][ps] = sc.w[a][o];
+            s_pay[PY::M][ps] = pr.x;
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+              s_pay[PY::A + a][ps] = Av[a];
+#pragma unroll
+              for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][ps] = Bm[a][b];
+            }
+            atomicAdd(&s_hist[cell], 1);
+          } else if (ok) {
+            scatter_direct<D>(P, A, r, u, sc, pr.x, Av, Bm);
+          }
+          s_cell[pi] = (short)cell;
+        }
+      }
+      if constexpr (SCAT) {
+        __syncthreads();
+        cell_scan(s_hist, s_cstart, s_cursor, tid);
+        __syncthreads();
+        for (int pi = tid; pi < hi - lo; pi += kThreads) {
+          const int cl = s_cell[pi];
+          if (cl >= 0) s_ord[atomicAdd(&s_cursor[cl], 1)] = (short)pi;
+        }
+        __syncthreads();
+        const int i0 = tid < 3 * kCPB ? s_cstart[c] : 0;
+        const int i1 = tid < 3 * kCPB ? s_cstart[c + 1] : 0;
+        scatter_consume<D, false, true>(s_pay, s_tile, i0, i1, s_ord, ox, c, tid);
+        __syncthreads();
+      }
+    }
+    if constexpr (SCAT) scatter_flush<D, false>(P, A.grid, s_tile, bc, myslot, 0, tid);
     __syncthreads();
   }
 }

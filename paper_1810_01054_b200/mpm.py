@@ -21,7 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libmpm.so")
 
 STATUS = {0: "MPM_OK", 1: "MPM_ERR_INVALID_ARG", 2: "MPM_ERR_OOM", 3: "MPM_ERR_CUDA",
           4: "MPM_ERR_OUT_OF_DOMAIN", 5: "MPM_ERR_INVERTED", 6: "MPM_ERR_TAPE_FULL",
-          7: "MPM_ERR_CALL_ORDER", 8: "MPM_ERR_COMM", 9: "MPM_ERR_OUT_OF_SLAB"}
+          7: "MPM_ERR_CALL_ORDER", 8: "MPM_ERR_COMM", 9: "MPM_ERR_OUT_OF_SLAB",
+          10: "MPM_ERR_CFL"}
 
 # every symbol include/mpm.h declares
 EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "mpm_forward",
@@ -46,7 +47,7 @@ class _Config(C.Structure):
                 ("dt", C.c_float), ("gravity", C.c_float * 3), ("bound", C.c_int32),
                 ("friction", C.c_float * 6), ("act_strength", C.c_float), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("grid_slots", C.c_int32), ("checkpoint_every", C.c_int32),
-                ("material", C.c_int32)]
+                ("material", C.c_int32), ("fuse_g2p2g", C.c_int32)]
 
 
 _lib = None
@@ -139,6 +140,7 @@ class Config:
     grid_slots: int = 0
     checkpoint_every: int = 0  # NEXT N2: 0 = full memo; k = k-step segments + checkpoints
     material: int = 0          # NEXT N3: 0 = neo-Hookean (R1), 1 = fixed-corotated (R21)
+    fuse_g2p2g: int = 0        # NEXT N2: 1 = fused forward (one particle pass per step)
 
     @classmethod
     def from_scene(cls, sc, max_steps=None, **kw):
@@ -153,7 +155,8 @@ class Config:
         return _Config(self.dim, self.res, self.batch, self.n_particles, self.max_steps,
                        self.n_actuators, self.dt, (C.c_float * 3)(*g[:3]), self.bound,
                        (C.c_float * 6)(*f[:6]), self.act_strength, self.device,
-                       self.stream or None, self.grid_slots, self.checkpoint_every, self.material)
+                       self.stream or None, self.grid_slots, self.checkpoint_every, self.material,
+                       self.fuse_g2p2g)
 
 
 class MPM:

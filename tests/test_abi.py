@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 @pytest.mark.parametrize("bad", [
     dict(dim=4), dict(res=100), dict(res=8), dict(batch=0), dict(n_particles=0),
     dict(max_steps=0), dict(n_actuators=-1), dict(dt=0.0), dict(bound=40),
-    dict(material=2), dict(checkpoint_every=-1), dict(checkpoint_every=5),
+    dict(material=2), dict(checkpoint_every=-1), dict(checkpoint_every=5), dict(fuse_g2p2g=2),
 ])
 def test_config_validation_is_host_side(bad):
     kw = dict(dim=3, res=64, batch=1, n_particles=10, max_steps=4, dt=1e-4)

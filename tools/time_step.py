@@ -1,5 +1,6 @@
 """Per-kernel device time of the C4 forward + backward step (CUDA events around every
-launch inside libmpm).  Usage: python tools/time_step.py [steps] [lib_path]"""
+launch inside libmpm).  Usage: python tools/time_step.py [steps] [lib_path]
+(MPM_FUSE=1 in the environment: the fused G2P2G forward, NEXT N2)"""
 import json
 import os
 import sys
@@ -17,7 +18,8 @@ def main():
     if len(sys.argv) > 2:
         mpm.LIB_PATH = sys.argv[2]
     sc = scenes.slab_3d(steps=K)
-    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=K))
+    fuse = int(os.environ.get("MPM_FUSE", "0"))
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=K, fuse_g2p2g=fuse))
     sim.set_scene(sc)
     m = sc.mass.reshape(-1).astype(np.float64)
     seed = np.zeros((sc.n, 3), np.float32)
@@ -33,7 +35,7 @@ def main():
     prof = sim.profile()
     tot = sum(v[0] for v in prof.values())
     out = {k: round(1e3 * v[0] / max(v[1], 1), 2) for k, v in prof.items() if v[1]}
-    print(json.dumps({"lib": os.path.basename(mpm.LIB_PATH), "us_per_launch": out,
+    print(json.dumps({"lib": os.path.basename(mpm.LIB_PATH), "fuse": fuse, "us_per_launch": out,
                       "us_per_FB_step": round(1e3 * tot / K, 1)}))
 
 
