@@ -48,7 +48,7 @@ WORKLOADS = {
 SEG = 200  # max steps per tape segment (tape memory ~ 100 MB per step at C4)
 
 
-def _cfg_dict(K, W, n_gpus, sc, workload="C4", slabs=None):
+def _cfg_dict(K, W, n_gpus, sc, workload="C4", slabs=None, fuse=0):
     par = "single GPU"
     if n_gpus > 1:
         par = (f"x-slab sharded x{n_gpus}, slabs {slabs}, NCCL halo-window sums" if workload == "C5a"
@@ -56,6 +56,8 @@ def _cfg_dict(K, W, n_gpus, sc, workload="C4", slabs=None):
     return {"workload": WORKLOADS[workload], "particles_per_rank": int(sc.batch * sc.n),
             "rollouts_per_rank": int(sc.batch), "grid": f"{sc.res}^3", "dim": 3, "dt": sc.dt,
             "steps_per_pass": K, "warmup": W, "parallelism": par,
+            "forward": ("fused G2P2G, one particle pass per step (NEXT N2)" if fuse and workload != "C5a"
+                        else "P2G + G2P passes"),
             "l2": (f"inputs larger than L2: per-step state {sc.batch * sc.n * 96 / 2**20:.0f} MiB read + written, "
                    f"tape of K states")}
 
@@ -141,6 +143,7 @@ ALG_BYTES = {
     "p2g_T": (96 + 20 + 96 + 96 + 16, 32),  # tape state, params, adj in, adj out, dmu/dlam RMW ; tape + adj node
     "g2p_T": (48 + 96, 16),        # x,F + adj in ; write dv per node
     "grid_T": (0, 48),
+    "g2p2g": (48 + 96 + 20, 32),   # fused (NEXT N2): read x,F + write x,v,C,F + params ; read grid t, write grid t+1
 }
 
 
@@ -176,7 +179,8 @@ def run_ours(args):
     tape = max(seg, min(W, SEG), 1)
     sc, total_particles, slabs, mtot = make_scene(args.workload, rank, world, tape)
     stream = torch.cuda.current_stream(dev)
-    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=tape, device=dev.index, stream=stream.cuda_stream))
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=tape, device=dev.index, stream=stream.cuda_stream,
+                                        fuse_g2p2g=args.fuse))
     if slabs is not None:
         sim.set_slab(*slabs[rank], 1)
         if world > 1:
@@ -301,7 +305,7 @@ def run_ours(args):
             "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "weak" if args.workload == "C4" else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded jittered-lattice slab)",
-            "config": _cfg_dict(K, W, world, sc, args.workload, slabs),
+            "config": _cfg_dict(K, W, world, sc, args.workload, slabs, args.fuse),
             "fwd": {"value": (total_particles * K / (fwd_ms / 1e3)) if fwd_ms else None,
                     "ms_per_step": (fwd_ms / K) if fwd_ms else None},
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
@@ -389,6 +393,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
+    ap.add_argument("--fuse", type=int, default=1, choices=[0, 1],
+                    help="fused G2P2G forward (NEXT N2); slab mode (C5a) always runs P2G + G2P")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

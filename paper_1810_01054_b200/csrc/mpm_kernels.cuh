@@ -948,10 +948,10 @@ __device__ __forceinline__ bool work_item(const StepArgs& A, int wi, int n_occ, 
 // t = the step whose actuation applies; latches an inverted element (det F <= 0).
 template <int D, int MAT>
 __device__ __forceinline__ void p2g_payload(const KParams& P, const StepArgs& A, int r, int t, int u, const float4& pr,
-                                            const float (&v)[D], const float (&H)[D][D], const float (&Cm)[D][D],
-                                            const float (&f)[D], float (&Av)[D], float (&Bm)[D][D]) {
+                                            int ai, const float (&v)[D], const float (&H)[D][D],
+                                            const float (&Cm)[D][D], const float (&f)[D], float (&Av)[D],
+                                            float (&Bm)[D][D]) {
   float sig[D];
-  const int ai = A.aid[u];
 #pragma unroll
   for (int a = 0; a < D; ++a)
     sig[a] = ai >= 0 ? P.act_s * A.act[(((size_t)r * P.T + t) * P.K + ai) * D + a] : 0.f;
@@ -1290,7 +1290,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
               Cm[a][b] = A.st[(size_t)comp_C<D>(a, b) * NT + j];
             }
           }
-          p2g_payload<D, MAT>(P, A, r, A.t, u, pr, v, H, Cm, f, Av, Bm);
+          p2g_payload<D, MAT>(P, A, r, A.t, u, pr, A.aid[u], v, H, Cm, f, Av, Bm);
           if (PY::M >= 0) s_pay[PY::M < 0 ? 0 : PY::M][ps] = pr.x;
         } else {
           // steps A and B: g_v = gv + dt gx ; g_C = gC + dt gF F^T
@@ -1563,10 +1563,11 @@ __device__ __forceinline__ void g2p_row(const float4* s_v, const int* lb, const 
 // registers (the fused G2P2G scatters them) and whether the new base index is valid.
 // COH: perm was written by this kernel (the fused sort) -- a coherent load, not the
 // read-only path.
-template <int D, bool COH = false>
+template <int D, bool COH = false, bool PRM = false>
 __device__ __forceinline__ bool g2p_particle(const KParams& P, const StepArgs& A, const float4* s_v,
                                              const float4& vref, const int* bc, int r, int k, float (&x)[D],
-                                             float (&vn)[D], float (&Cn)[D][D], float (&Hn)[D][D], int& u) {
+                                             float (&vn)[D], float (&Cn)[D][D], float (&Hn)[D][D], int& u,
+                                             float4* pr = nullptr, int* ai = nullptr) {
   const size_t NT = P.NT;
   const int j = COH ? __ldcg(&A.perm[k]) : __ldg(&A.perm[k]);
   float H[D][D];  // H = F - I
@@ -1577,6 +1578,10 @@ __device__ __forceinline__ bool g2p_particle(const KParams& P, const StepArgs& A
     for (int b = 0; b < D; ++b) H[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
   }
   u = __ldg(&A.orig[j]);
+  if (PRM) {  // the fused P2G's parameters: issued now, consumed after the gather
+    *pr = __ldg(&A.prm[u]);
+    *ai = __ldg(&A.aid[u]);
+  }
   Stencil<D> sc;
   make_stencil<D>(x, P.fres, sc);
   int lb[D];
@@ -1676,42 +1681,50 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
 template <int D>
 constexpr int fuse_dyn_smem() { return Pay<D, false>::N * kCap * (int)sizeof(float); }
 
-// direct scatter of one particle's 3^D nodes into grid t+1 (escapees of the tile)
+// the escapees' nodes (NS per escapee, one (escapee, node) pair per thread of the idle group
+// [0, nthr)) as direct vector REDs into grid t+1; node value w_o (A + B o), mass w_o m from the
+// escapee's payload slot
 template <int D>
-__device__ __forceinline__ void scatter_direct(const KParams& P, const StepArgs& A, int r, int u,
-                                               const Stencil<D>& sc, float m, const float (&Av)[D],
-                                               const float (&Bm)[D][D]) {
+__device__ __forceinline__ void scatter_escapees(const KParams& P, const StepArgs& A, int r, const int* bc,
+                                                 const float (*s_pay)[kCap], const short* s_cell,
+                                                 const short* s_ord, int nesc, int it, int nthr) {
   using DD = Dim<D>;
-#pragma unroll
-  for (int q = 0; q < DD::NS; ++q) {
-    int o[D], nb_[D], loc[D], t = q;
+  using PY = Pay<D, false>;
+  for (int idx = it; idx < nesc * DD::NS; idx += nthr) {
+    const int e = idx / DD::NS;
+    int q = idx - e * DD::NS;
+    const int pi = s_ord[kCap - 1 - e];
+    const int pk = -2 - (int)s_cell[pi];
+    const int ps = pay_slot(pi);
+    int o[D], nb_[D], loc[D];
     float W = 1.f;
 #pragma unroll
     for (int a = D - 1; a >= 0; --a) {
-      o[a] = t % 3;
-      t /= 3;
+      o[a] = q % 3;
+      q /= 3;
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      W *= sc.w[a][o[a]];
-      const int node = sc.base[a] + o[a];
+      const int lb = ((pk >> (4 * (D - 1 - a))) & 15) - 8;
+      const int node = bc[a] * DD::BB + lb + o[a];
+      W *= s_pay[PY::W + a * 3 + o[a]][ps];
       nb_[a] = node >> DD::LOG_BB;
       loc[a] = node & (DD::BB - 1);
     }
     const int slot = __ldg(&A.slot_next[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
     if (slot < 0) {  // moved more than the dilation allows (|v| dt >= dx)
-      latch(A.err, E_FUSE, A.t + 1, u);
-      return;
+      latch(A.err, E_FUSE, A.t + 1, -1);
+      continue;
     }
     float val[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      float acc = Av[a];
+      float acc = s_pay[PY::A + a][ps];
 #pragma unroll
-      for (int b = 0; b < D; ++b) acc = fmaf((float)o[b], Bm[a][b], acc);
+      for (int b = 0; b < D; ++b) acc = fmaf((float)o[b], s_pay[PY::B + a * D + b][ps], acc);
       val[a] = W * acc;
     }
-    atomicAdd(A.grid + (size_t)slot * kCPB + cell_lin<D>(loc), make_float4(val[0], val[1], val[2], W * m));
+    atomicAdd(A.grid + (size_t)slot * kCPB + cell_lin<D>(loc), make_float4(val[0], val[1], val[2], W * s_pay[PY::M][ps]));
   }
 }
 
@@ -1731,7 +1744,7 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
   __shared__ short s_ord[SCAT ? kCap : 1];
   extern __shared__ __align__(16) unsigned char s_dyn[];
   float (*s_pay)[kCap] = reinterpret_cast<float (*)[kCap]>(s_dyn);  // [PY::N][kCap], dynamic (SCAT)
-  __shared__ int s_blk;
+  __shared__ int s_blk, s_nesc;
   const int tid = threadIdx.x;
   const int n_occ = A.info_t[I_NOCC];
   const int ox = tid / kCPB;
@@ -1770,12 +1783,14 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
       const int hi = min(n, lo + kCap);
       if (SCAT) {
         if (tid < kCPB) s_hist[tid] = 0;
+        if (tid == 0) s_nesc = 0;
         __syncthreads();
       }
       for (int pi = tid; pi < hi - lo; pi += kThreads) {
         float x[D], vn[D], Cn[D][D], Hn[D][D];
-        int u;
-        const bool ok = g2p_particle<D, SORT>(P, A, s_v, vref, bc, r, s + lo + pi, x, vn, Cn, Hn, u);
+        int u, ai = -1;
+        float4 pr;  // m, V, mu, lam
+        const bool ok = g2p_particle<D, SORT, SCAT>(P, A, s_v, vref, bc, r, s + lo + pi, x, vn, Cn, Hn, u, &pr, &ai);
         if constexpr (SCAT) {
           Stencil<D> sc;
           make_stencil<D>(x, P.fres, sc);
@@ -1786,12 +1801,10 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
             lb[a] = sc.base[a] - bc[a] * BB;
             inb &= (lb[a] >= 0) & (lb[a] < BB);
           }
-          const float4 pr = __ldg(&A.prm[u]);  // m, V, mu, lam
           float Av[D], Bm[D][D];
-          p2g_payload<D, MAT>(P, A, r, A.t + 1, u, pr, vn, Hn, Cn, sc.fx, Av, Bm);
+          p2g_payload<D, MAT>(P, A, r, A.t + 1, u, pr, ai, vn, Hn, Cn, sc.fx, Av, Bm);
           int cell = -1;
-          if (ok && inb) {
-            cell = cell_lin<D>(lb);
+          if (ok) {
             const int ps = pay_slot(pi);
 #pragma unroll
             for (int a = 0; a < D; ++a)
@@ -1804,9 +1817,28 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
 #pragma unroll
               for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][ps] = Bm[a][b];
             }
-            atomicAdd(&s_hist[cell], 1);
-          } else if (ok) {
-            scatter_direct<D>(P, A, r, u, sc, pr.x, Av, Bm);
+            if (inb) {
+              cell = cell_lin<D>(lb);
+              atomicAdd(&s_hist[cell], 1);
+            } else {
+              // escapee (new base cell outside the block; CFL keeps it within a few cells):
+              // its nodes go out as direct REDs after the sort, by the threads the consumer
+              // leaves idle.  Code -2 - packed (lb + 8, 4 bits per axis); its index is kept
+              // at the top of s_ord (the block's own particles fill it from the bottom).
+              int pk = 0;
+              bool near = true;
+#pragma unroll
+              for (int a = 0; a < D; ++a) {
+                near &= (lb[a] >= -8) & (lb[a] < 8);
+                pk = (pk << 4) | ((lb[a] + 8) & 15);
+              }
+              if (near) {
+                cell = -2 - pk;
+                s_ord[kCap - 1 - atomicAdd(&s_nesc, 1)] = (short)pi;
+              } else {
+                latch(A.err, E_FUSE, A.t + 1, u);
+              }
+            }
           }
           s_cell[pi] = (short)cell;
         }
@@ -1823,6 +1855,8 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
         const int i0 = tid < 3 * kCPB ? s_cstart[c] : 0;
         const int i1 = tid < 3 * kCPB ? s_cstart[c + 1] : 0;
         scatter_consume<D, false, true>(s_pay, s_tile, i0, i1, s_ord, ox, c, tid);
+        if (tid >= 3 * kCPB) scatter_escapees<D>(P, A, r, bc, s_pay, s_cell, s_ord, s_nesc, tid - 3 * kCPB,
+                                                 kThreads - 3 * kCPB);
         __syncthreads();
       }
     }
