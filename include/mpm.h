@@ -88,9 +88,10 @@ typedef struct {
                            step: the G2P of step t also scatters step t+1's P2G into a
                            grid allocated as the one-block dilation of step t's occupied
                            blocks (results equal the unfused path up to fp32 summation
-                           order).  Requires |v| dt < dx (else MPM_ERR_CFL); ignored in
-                           slab mode and with a controller (N1 needs state t+1 before
-                           step t+1's P2G).  0 = P2G and G2P as separate passes.          */
+                           order).  Requires |v| dt < dx (else MPM_ERR_CFL); ignored for
+                           a slab with neighbours (its window exchange sits between P2G and
+                           G2P) and with a controller (N1 needs state t+1 before step
+                           t+1's P2G).  0 = P2G and G2P as separate passes.              */
 } mpm_config;
 
 /* Create a context on config->device.  Validates the config (MPM_ERR_INVALID_ARG) and

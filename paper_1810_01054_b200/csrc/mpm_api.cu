@@ -492,7 +492,9 @@ void forward_phase_b(mpm_ctx c, int t) {
 // table) -> k_scatter (block grouping, zero grid t+1) -> k_g2p2g (cell sort of t, G2P, P2G
 // of t+1): 3 launches, one particle pass.  A step whose grid is not yet built (the first
 // of a range or of a segment) runs the unfused P2G first.
-bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !c->slab && !c->ctrl; }
+// (a slab with neighbours exchanges its windows between P2G and G2P: not fusable; a slab
+// without neighbours -- the whole domain, bench.py's C5a at N = 1 -- is)
+bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !has_nbr(c) && !c->ctrl; }
 
 template <int D, bool SORT, bool SCAT>
 void launch_fused(mpm_ctx c, const StepArgs& A) {

@@ -127,3 +127,23 @@ def test_c5a_two_slabs_full_size(c5a):
     _com_check(sc, g)
     for s in sims:
         s.close()
+
+
+def test_c5a_fused_forward_full_size(c5a):
+    """NEXT N2 at full size: the fused G2P2G forward (bench.py's N = 1 configuration: one
+    whole-domain slab, no neighbours) gives the unfused state and the exact CoM gradient."""
+    sc, ref = c5a
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, fuse_g2p2g=1))
+    sim.set_slab(0, sc.res, 1)
+    sim.set_scene(sc)
+    sim.set_profiling(True)
+    sim.forward(T)
+    assert sim.profile()["g2p2g"][1] == T
+    for a, b in zip(sim.get_state(T), ref.get_state(T)):
+        assert rel_err(a, b) < 1e-5
+    m = sc.mass[0].astype(np.float64)
+    seed = np.zeros((sc.n, 3), np.float32)
+    seed[:, 0] = m / m.sum()
+    sim.backward(seed)
+    _com_check(sc, sim.grad())
+    sim.close()

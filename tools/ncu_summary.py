@@ -19,6 +19,8 @@ def bench_name(kernel):
         return ("g2p_T" if flag(1) else "p2g") + ("_fcr" if flag(2) else "")
     if base == "k_p2g_adj":
         return "p2g_T" + ("_massgrad" if flag(1) else "") + ("_fcr" if flag(2) else "")
+    if base == "k_g2p2g":
+        return "g2p2g" + ("_fcr" if len(args) > 1 and args[1] == "1" else "") + ("" if flag(3) else "_last")
     return {"k_g2p": "g2p", "k_grid_adj": "grid_T", "k_scan_lookback": "scan", "k_scatter": "scatter"}.get(base, kernel)
 
 
