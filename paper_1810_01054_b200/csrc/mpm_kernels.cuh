@@ -1680,6 +1680,11 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
 // ------------------------------------------------------------------------------------
 template <int D>
 constexpr int fuse_dyn_smem() { return Pay<D, false>::N * kCap * (int)sizeof(float); }
+// escapee code: the new base cell relative to the block, lb in [-EO, EO) per axis, EB bits
+// each (EO > Bb, so a neighbour block's cells fit; D * EB <= 14 keeps -2 - code in a short)
+template <int D> struct Esc { static constexpr int EB = D == 3 ? 4 : 5, EO = 1 << (EB - 1); };
+static_assert(Esc<3>::EO > Dim<3>::BB && Esc<2>::EO > Dim<2>::BB, "escapee code range");
+static_assert(3 * Esc<3>::EB <= 14 && 2 * Esc<2>::EB <= 14, "escapee code fits a short");
 
 // the escapees' nodes (NS per escapee, one (escapee, node) pair per thread of the idle group
 // [0, nthr)) as direct vector REDs into grid t+1; node value w_o (A + B o), mass w_o m from the
@@ -1690,6 +1695,7 @@ __device__ __forceinline__ void scatter_escapees(const KParams& P, const StepArg
                                                  const short* s_ord, int nesc, int it, int nthr) {
   using DD = Dim<D>;
   using PY = Pay<D, false>;
+  constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
   for (int idx = it; idx < nesc * DD::NS; idx += nthr) {
     const int e = idx / DD::NS;
     int q = idx - e * DD::NS;
@@ -1705,7 +1711,7 @@ __device__ __forceinline__ void scatter_escapees(const KParams& P, const StepArg
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      const int lb = ((pk >> (4 * (D - 1 - a))) & 15) - 8;
+      const int lb = ((pk >> (EB * (D - 1 - a))) & (2 * EO - 1)) - EO;
       const int node = bc[a] * DD::BB + lb + o[a];
       W *= s_pay[PY::W + a * 3 + o[a]][ps];
       nb_[a] = node >> DD::LOG_BB;
@@ -1734,6 +1740,7 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
   using DD = Dim<D>;
   using PY = Pay<D, false>;
   constexpr int BB = DD::BB, TN = DD::TN;
+  constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
   __shared__ int s_hist[kCPB];
   __shared__ int s_cstart[kCPB + 1];
   __shared__ int s_cursor[kCPB];
@@ -1823,14 +1830,14 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
             } else {
               // escapee (new base cell outside the block; CFL keeps it within a few cells):
               // its nodes go out as direct REDs after the sort, by the threads the consumer
-              // leaves idle.  Code -2 - packed (lb + 8, 4 bits per axis); its index is kept
+              // leaves idle.  Code -2 - packed (lb + EO, EB bits per axis); its index is kept
               // at the top of s_ord (the block's own particles fill it from the bottom).
               int pk = 0;
               bool near = true;
 #pragma unroll
               for (int a = 0; a < D; ++a) {
-                near &= (lb[a] >= -8) & (lb[a] < 8);
-                pk = (pk << 4) | ((lb[a] + 8) & 15);
+                near &= (lb[a] >= -EO) & (lb[a] < EO);
+                pk = (pk << EB) | ((lb[a] + EO) & (2 * EO - 1));
               }
               if (near) {
                 cell = -2 - pk;

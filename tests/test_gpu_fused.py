@@ -59,6 +59,28 @@ def test_fused_gradient_parity(d, T):
         assert rel_err(a, b) < 1e-3, (k, rel_err(a, b))
 
 
+@pytest.mark.parametrize("name,make,T", [
+    ("C1 2D block, 50 steps", lambda: scenes.block_2d(steps=50, perturb=True, batch=2), 50),
+    ("C2 2D walker, 100 steps", lambda: scenes.walker_2d(steps=100), 100),
+    ("C3 3D quadruped, 60 steps", lambda: scenes.quadruped_3d(steps=60), 60),
+])
+def test_fused_baseline_configs_vs_oracle(name, make, T):
+    """The small BASELINE configs through the fused forward (particles cross block faces in
+    every direction, 2D blocks are 8 cells wide): state vs the oracle (1e-3), every rollout."""
+    sc = make()
+    sim = _sim(sc, T, fuse_g2p2g=1)
+    sim.forward(T)
+    x, v, F, Cm = sim.get_state(T)
+    for r in range(sc.batch):
+        cfg = oracle_cfg(sc)
+        m, vol, E, nu, aid, act = oracle_params(sc, r)
+        traj = oracle.forward(cfg, oracle_state(sc, r), m, vol, E, nu, aid, act[:T], T)
+        ox, ov, oC, oF = oracle.unpack(traj[T], sc.dim)
+        sl = slice(r * sc.n, (r + 1) * sc.n)
+        for k, a, b in (("x", x[sl], ox), ("v", v[sl], ov), ("F", F[sl], oF), ("C", Cm[sl], oC)):
+            assert rel_err(a, b) < 1e-3, (name, r, k, rel_err(a, b))
+
+
 def test_fused_binning_bit_exact_and_grid_equal():
     """The fused run's binning (its own in-kernel cell sort) is bit-exact with the oracle's,
     and its memo grid (dilated slot map) holds the unfused (p, m) up to summation order."""

@@ -19,6 +19,9 @@ from paper_1810_01054_b200 import mpm, scenes  # noqa: E402
 PAPER_MS = {20: (0.392, 0.406), 40: (1.594, 1.774), 80: (10.501, 11.594)}  # Table I (F, B) per frame
 
 
+FUSE = int(os.environ.get("MPM_FUSE", "1"))  # fused G2P2G forward (NEXT N2), bench.py's default
+
+
 def main():
     K = int(sys.argv[1]) if len(sys.argv) > 1 else 100
     stream = torch.cuda.current_stream()
@@ -27,7 +30,7 @@ def main():
         res = 64 if n < 80 else 128
         sc = scenes.slab_3d(steps=K, cells=(c, c, c), res=res, y0=res // 4)
         sc.v[..., 1] = 0.0  # falls from rest under gravity
-        sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=K, stream=stream.cuda_stream))
+        sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=K, stream=stream.cuda_stream, fuse_g2p2g=FUSE))
         sim.set_scene(sc)
         seed = np.zeros((sc.n, 3), np.float32)
         seed[:, 0] = 1.0 / sc.n
@@ -47,7 +50,7 @@ def main():
         f = e[0].elapsed_time(e[1]) / K
         b = e[1].elapsed_time(e[2]) / K
         pf, pb = PAPER_MS[n]
-        print(json.dumps({"cube": f"{n}^3 particles", "particles": sc.n, "res": res, "steps": K,
+        print(json.dumps({"cube": f"{n}^3 particles", "fuse_g2p2g": FUSE, "particles": sc.n, "res": res, "steps": K,
                           "fwd_ms_per_step": round(f, 4), "bwd_ms_per_step": round(b, 4),
                           "fwd_particle_steps_per_s": sc.n / (f * 1e-3), "bwd_particle_steps_per_s": sc.n / (b * 1e-3),
                           "paper_1080ti_ms_per_frame": {"fwd": pf, "bwd": pb},

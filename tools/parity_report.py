@@ -100,5 +100,10 @@ if __name__ == "__main__":
     case("C3 fixed-corotated (N3, R21)", scenes.quadruped_3d(steps=100), 100, material=1)
     case("C2 fixed-corotated (N3, R21)", scenes.walker_2d(steps=200), 200, material=1)
     case("C3 checkpoint_every=16 (N2)", scenes.quadruped_3d(steps=100), 100, checkpoint_every=16)
+    case("C1 fused G2P2G (N2)", scenes.block_2d(steps=50, perturb=True), 50, fuse_g2p2g=1)
+    case("C2 fused G2P2G (N2), 500 steps", scenes.walker_2d(steps=500), 500, fuse_g2p2g=1)
+    case("C3 fused G2P2G (N2), 200 steps", scenes.quadruped_3d(steps=200), 200, fuse_g2p2g=1)
+    case("C3 fused G2P2G + checkpoint_every=16 + fixed-corotated", scenes.quadruped_3d(steps=100), 100,
+         fuse_g2p2g=1, checkpoint_every=16, material=1)
     controller_case("C2 closed-loop controller (N1), 200 steps", scenes.walker_2d(steps=200), 200)
     controller_case("C3 closed-loop controller (N1), 60 steps", scenes.quadruped_3d(steps=60), 60, 0.1)

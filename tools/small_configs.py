@@ -18,11 +18,14 @@ CASES = [("C1 configs[0] 2D block", scenes.block_2d, 50), ("C2 configs[1] 2D wal
          ("C3 configs[2] 3D quadruped", scenes.quadruped_3d, 200)]
 
 
+FUSE = int(os.environ.get("MPM_FUSE", "1"))  # fused G2P2G forward (NEXT N2), bench.py's default
+
+
 def main():
     stream = torch.cuda.current_stream()
     for name, make, T in CASES:
         sc = make(steps=T)
-        sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, stream=stream.cuda_stream))
+        sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, stream=stream.cuda_stream, fuse_g2p2g=FUSE))
         sim.set_scene(sc)
         m = sc.mass.reshape(-1).astype(np.float64)
         seed = np.zeros((sc.n, sc.dim), np.float32)
@@ -41,7 +44,7 @@ def main():
         e[2].record(stream)
         torch.cuda.synchronize()
         f, fb = e[0].elapsed_time(e[1]), e[0].elapsed_time(e[2])
-        print(json.dumps({"config": name, "particles": sc.n, "steps": T,
+        print(json.dumps({"config": name, "fuse_g2p2g": FUSE, "particles": sc.n, "steps": T,
                           "fwd_us_per_step": round(1e3 * f / T, 2), "fb_us_per_step": round(1e3 * fb / T, 2),
                           "fwd_particle_steps_per_s": sc.n * T / (f * 1e-3),
                           "fb_particle_steps_per_s": sc.n * T / (fb * 1e-3)}), flush=True)
