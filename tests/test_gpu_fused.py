@@ -197,3 +197,51 @@ def test_fused_cfl_violation_is_an_error():
     with pytest.raises(mpm.MPMError) as e:
         sim.forward(3)
     assert e.value.status == "MPM_ERR_CFL"
+
+
+def test_fused_mass_gradient_and_running_seeds_match_unfused():
+    """The backward features that read the memo grid (N3 dL/dm_p, N4 seeds at intermediate
+    states) give the unfused results over the fused forward's dilated grids."""
+    T = 16
+    sc = _tiny(3, T, 61)
+    rng = np.random.default_rng(8)
+    seeds = {t: [rng.standard_normal((sc.n, 3)).astype(np.float32) for _ in range(2)] for t in (5, 11)}
+    fin = [rng.standard_normal((sc.n, 3)).astype(np.float32) for _ in range(2)]
+    out = []
+    for fuse in (0, 1):
+        sim = _sim(sc, T, fuse_g2p2g=fuse)
+        sim.enable_mass_grad(True)
+        for t, (sx, sv) in seeds.items():
+            sim.add_seed(t, sx, sv)
+        sim.forward(T)
+        sim.backward(*fin)
+        out.append((sim.grad(), sim.grad_mass()))
+        sim.close()
+    (g0, m0), (g1, m1) = out
+    for key in ("dx0", "dv0", "dF0", "dC0", "dE", "dnu", "da"):
+        assert rel_err(g1[key], g0[key]) < 1e-4, key
+    assert rel_err(m1, m0) < 1e-4
+
+
+def test_fused_flag_ignored_with_controller():
+    """N1 needs state t+1 before step t+1's P2G: with a controller the fused flag runs the
+    unfused forward (same results, no g2p2g launches)."""
+    from oracle import controller as ctl
+    T = 8
+    sc = _tiny(3, T, 71)
+    K, d = sc.n_act, 3
+    rng = np.random.default_rng(9)
+    W = (0.1 * rng.standard_normal((K * d, ctl.n_obs(d, K)))).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, K * d).astype(np.float32)
+    target = rng.uniform(0.2, 0.8, d).astype(np.float32)
+    res = []
+    for fuse in (0, 1):
+        sim = _sim(sc, T, fuse_g2p2g=fuse)
+        sim.set_controller(W, b, target)
+        sim.set_profiling(True)
+        sim.forward(T)
+        assert sim.profile()["g2p2g"][1] == 0
+        res.append(sim.get_state(T))
+        sim.close()
+    for a, b in zip(*res):
+        assert rel_err(a, b) < 1e-6
