@@ -31,6 +31,9 @@
 #ifndef MPM_FFMA2
 #define MPM_FFMA2 1  // packed fp32x2 FMAs (sm_100 FFMA2) in the stencil sums
 #endif
+#ifndef MPM_FUSE_STAGE_FIRST
+#define MPM_FUSE_STAGE_FIRST 1
+#endif
 #ifndef MPM_FUSE_MINB
 #define MPM_FUSE_MINB 3
 #endif
@@ -1778,13 +1781,19 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
       }
       for (int i = tid; i < 3 * TN; i += kThreads) (&s_tile[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    float4 vref, aref_unused;
+#if MPM_FUSE_STAGE_FIRST
+    // grid t's tile first: its loads are independent of the sort and overlap its phases
+    stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
+#endif
     if (SORT) {
       if (tid < kCPB) s_hist[tid] = 0;
       __syncthreads();
       block_cell_sort<D, true>(P, A, s, n, tid, s_hist, s_cstart, s_cursor, s_sort);
     }
-    float4 vref, aref_unused;
+#if !MPM_FUSE_STAGE_FIRST
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
+#endif
     __syncthreads();
     for (int lo = 0; lo < n; lo += kCap) {
       const int hi = min(n, lo + kCap);
