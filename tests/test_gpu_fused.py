@@ -245,3 +245,46 @@ def test_fused_flag_ignored_with_controller():
         sim.close()
     for a, b in zip(*res):
         assert rel_err(a, b) < 1e-6
+
+
+@pytest.mark.parametrize("d", [2, 3])
+def test_fused_fast_diagonal_motion_escapees(d):
+    """A body moving 0.9 cells per step along the diagonal: every step a large share of the
+    particles leaves its block (escapees of the fused scatter) in every axis direction.  Both
+    forwards against the oracle at field scale (R16: C against 4 res |v|, whose fp32
+    cancellation under a large common-mode velocity depends on the summation order), and both
+    gradients against the oracle's."""
+    T = 10
+    res = 32
+    sc = scenes.tiny(d, seed=81 + d, res=res, n_cells=(6,) * d, steps=T, K=0,
+                     center=(10,) * d)
+    sc.gravity = (0.0,) * d
+    sign = np.array([1.0, -1.0, 1.0][:d])
+    sc.v[...] = (0.9 / (res * sc.dt) * sign / np.sqrt(d)).astype(np.float32)
+    cfg = oracle_cfg(sc)
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    traj = oracle.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, act[:T], T)
+    ox, ov, oC, oF = oracle.unpack(traj[T], d)
+    w = np.random.default_rng(4).standard_normal(traj[T].shape)
+    wx, wv, wC, wF = oracle.unpack(w, d)
+    g0, gE, gnu, _ = oracle.backward(cfg, traj, m, vol, E, nu, aid, act[:T], w)
+    gx, gv, gC, gF = oracle.unpack(g0, d)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    bb = 4 if d == 3 else 8
+    for fuse in (0, 1):
+        sim = _sim(sc, T, fuse_g2p2g=fuse)
+        sim.forward(T)
+        x, v, F, Cm = sim.get_state(T)
+        if fuse:
+            moved = np.any(np.floor(x * res - 0.5) // bb != np.floor(sc.x[0] * res - 0.5) // bb, axis=1)
+            assert moved.mean() > 0.5  # the escapee path is exercised
+        vmax = np.abs(ov).max()
+        for k, a, b, scale in (("x", x, ox, 1.0), ("v", v, ov, vmax), ("F", F, oF, np.abs(oF).max()),
+                               ("C", Cm, oC, 4 * res * vmax)):
+            assert np.abs(a - b).max() / scale < 1e-5, (fuse, k, np.abs(a - b).max() / scale)
+        sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+        g = sim.grad()
+        for k, a, b in (("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF),
+                        ("dC0", g["dC0"], gC), ("dE", g["dE"], gE), ("dnu", g["dnu"], gnu)):
+            assert rel_err(a, b) < 1e-3, (fuse, k, rel_err(a, b))
+        sim.close()
