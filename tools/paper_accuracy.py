@@ -19,6 +19,7 @@ sys.path.insert(0, ROOT)
 from paper_1810_01054_b200 import mpm, scenes  # noqa: E402
 
 PAPER_A1 = {1: 9.80e-8, 10: 4.74e-8, 100: 1.15e-7, 1000: 1.43e-5}
+FUSE = int(os.environ.get("MPM_FUSE", "0"))  # 1: the fused G2P2G forward (NEXT N2)
 PAPER_A2 = {1000: 2.69e-5}
 
 
@@ -31,7 +32,7 @@ def a1(T):
     sc.gravity = (0.0, -9.8, 0.0)
     sc.v[..., 0] = 0.2
     sc.v[..., 1] = 0.0
-    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, checkpoint_every=min(T, 100)))
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, checkpoint_every=min(T, 100), fuse_g2p2g=FUSE))
     sim.set_scene(sc)
     sim.forward(T)
     m = sc.mass[0].astype(np.float64)
@@ -42,7 +43,7 @@ def a1(T):
     g = sim.grad()
     ex = np.zeros(3)
     ex[0] = 1.0
-    out = {"case": "A1", "steps": T, "particles": sc.n,
+    out = {"case": "A1", "fuse_g2p2g": FUSE, "steps": T, "particles": sc.n,
            "rel_err_dx0": rel(g["dx0"], (m / M)[:, None] * ex),
            "rel_err_dv0": rel(g["dv0"], (T * sc.dt * m / M)[:, None] * ex),
            "paper_table2_f32": PAPER_A1[T]}
@@ -58,7 +59,7 @@ def a2(T):
     sc.x[..., 0] += np.float32(18.0 / res)  # start 18 cells closer to the +x wall
     sc.v[..., 0] = 1.0   # reaches the wall band within the horizon (6.4 cells)
     sc.v[..., 1] = 0.1
-    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, checkpoint_every=min(T, 100)))
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, checkpoint_every=min(T, 100), fuse_g2p2g=FUSE))
     sim.set_scene(sc)
     sim.forward(T)
     v = sim.get_state(T)[1]
@@ -70,7 +71,7 @@ def a2(T):
     sim.backward(seed)
     g = sim.grad()
     ey = np.array([0.0, 1.0, 0.0])
-    out = {"case": "A2", "steps": T, "particles": sc.n,
+    out = {"case": "A2", "fuse_g2p2g": FUSE, "steps": T, "particles": sc.n,
            "rel_err_dv0": rel(g["dv0"], (T * sc.dt * m / M)[:, None] * ey),
            "rel_err_dx0": rel(g["dx0"], (m / M)[:, None] * ey),
            "paper_table2_f32": PAPER_A2[T]}
