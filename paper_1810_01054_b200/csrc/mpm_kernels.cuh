@@ -34,8 +34,14 @@
 #ifndef MPM_FUSE_STAGE_FIRST
 #define MPM_FUSE_STAGE_FIRST 1
 #endif
+#ifndef MPM_FUSE_CAP
+#define MPM_FUSE_CAP 512
+#endif
+#ifndef MPM_FUSE_FX
+#define MPM_FUSE_FX 1
+#endif
 #ifndef MPM_FUSE_MINB
-#define MPM_FUSE_MINB 3
+#define MPM_FUSE_MINB (MPM_FUSE_FX ? 4 : 3)
 #endif
 #ifndef MPM_SCAT_PF
 #define MPM_SCAT_PF 1
@@ -867,6 +873,16 @@ __global__ void k_zero_slots(int* __restrict__ info_t, float4* __restrict__ g) {
 template <int D, bool ADJ> struct Pay;
 template <int D> struct Pay<D, false> { static constexpr int W = 0, M = 3 * D, A = M + 1, B = A + D, N = B + D * D; };
 template <int D> struct Pay<D, true> { static constexpr int W = 0, M = -1, A = 3 * D, B = A + D, N = B + D * D; };
+// compact forward payload of the fused G2P2G: the fractional position fx (D rows) in place of
+// the 3D stencil weights, which the consumer recomputes (bspl) -- 16 rows instead of 22 in 3D
+template <int D> struct PayF { static constexpr int W = 0, M = D, A = D + 1, B = A + D, N = B + D * D; };
+template <int D, bool ADJ, bool FX> struct PayOf { using T = Pay<D, ADJ>; };
+template <int D> struct PayOf<D, false, true> { using T = PayF<D>; };
+// quadratic B-spline weight of node offset o at fractional position f (make_stencil's arithmetic)
+__device__ __forceinline__ float bspl(float f, int o) {
+  const float u = o == 0 ? 1.5f - f : (o == 1 ? f - 1.0f : f - 0.5f);
+  return o == 1 ? 0.75f - u * u : 0.5f * u * u;
+}
 
 struct StepArgs {
   // forward and adjoint
@@ -1060,10 +1076,10 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
 // Scatter consumer: thread (ox, c), c = cell, accumulates the NSUB nodes c + (ox, *) of the
 // payload positions [i0, i1) (ORD: through the order s_ord) in registers, then writes them
 // into tile copy ox in NSUB conflict-free phases (64-thread named barriers).
-template <int D, bool ADJ, bool ORD>
-__device__ __forceinline__ void scatter_consume(const float (*s_pay)[kCap], float4 (*s_tile)[Dim<D>::TN], int i0,
+template <int D, bool ADJ, bool ORD, int CAP = kCap, bool FX = false>
+__device__ __forceinline__ void scatter_consume(const float (*s_pay)[CAP], float4 (*s_tile)[Dim<D>::TN], int i0,
                                                 int i1, const short* s_ord, int ox, int c, int tid) {
-  using PY = Pay<D, ADJ>;
+  using PY = typename PayOf<D, ADJ, FX>::T;
   constexpr int BB = Dim<D>::BB, TE = Dim<D>::TE;
   constexpr int NSUB = (D == 3) ? 9 : 3;
   // consumer: thread (ox, c), c = cell, accumulates NSUB nodes
@@ -1073,7 +1089,14 @@ __device__ __forceinline__ void scatter_consume(const float (*s_pay)[kCap], floa
   if (tid < 3 * kCPB) {
     for (int i0s = i0; i0s < i1; ++i0s) {
       const int i = pay_slot(ORD ? (int)s_ord[i0s] : i0s);
-      const float wx = s_pay[PY::W + ox][i];
+      // stencil weights: stored (W rows, 3 per axis) or recomputed from fx (FX: 1 row per axis)
+      float wyv[3], wzv[3];
+#pragma unroll
+      for (int o = 0; o < 3; ++o) {
+        wyv[o] = FX ? bspl(s_pay[PY::W + 1][i], o) : s_pay[PY::W + 3 + o][i];
+        wzv[o] = D == 3 ? (FX ? bspl(s_pay[PY::W + 2 % D][i], o) : s_pay[PY::W + 6 % (3 * D) + o][i]) : 0.f;
+      }
+      const float wx = FX ? bspl(s_pay[PY::W][i], ox) : s_pay[PY::W + ox][i];
       float Ax[3];
 #pragma unroll
       for (int a = 0; a < D; ++a) Ax[a] = s_pay[PY::A + a][i] + (float)ox * s_pay[PY::B + a * D + 0][i];
@@ -1084,7 +1107,7 @@ __device__ __forceinline__ void scatter_consume(const float (*s_pay)[kCap], floa
         for (int a = 0; a < 3; ++a) { B1[a] = s_pay[PY::B + a * D + 1][i]; B2[a] = s_pay[PY::B + a * D + 2 % D][i]; }
 #pragma unroll
         for (int oy = 0; oy < 3; ++oy) {
-          const float wxy = wx * s_pay[PY::W + 3 + oy][i];
+          const float wxy = wx * wyv[oy];
 #if MPM_FFMA2_SCAT
           // node value A + oy B1 + oz B2 and the accumulation as packed fp32x2 FMAs:
           // (x, y) and (z, m) pairs (sm_100 FFMA2; per component the same fused op)
@@ -1093,7 +1116,7 @@ __device__ __forceinline__ void scatter_consume(const float (*s_pay)[kCap], floa
           const float rz = fmaf((float)oy, B1[2], Ax[2]);
 #pragma unroll
           for (int oz = 0; oz < 3; ++oz) {
-            const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
+            const float W = wxy * wzv[oz];
             float4& q = acc[oy * 3 + oz];
             const float2 vxy = oz ? __ffma2_rn(make_float2((float)oz, (float)oz), make_float2(B2[0], B2[1]), rxy) : rxy;
             const float vz = oz ? fmaf((float)oz, B2[2], rz) : rz;
@@ -1104,7 +1127,7 @@ __device__ __forceinline__ void scatter_consume(const float (*s_pay)[kCap], floa
 #else
 #pragma unroll
           for (int oz = 0; oz < 3; ++oz) {
-            const float W = wxy * s_pay[PY::W + 6 % (3 * D) + oz][i];
+            const float W = wxy * wzv[oz];
             float4& q = acc[oy * 3 + oz];
             q.x = fmaf(W, Ax[0] + (float)oy * B1[0] + (float)oz * B2[0], q.x);
             q.y = fmaf(W, Ax[1] + (float)oy * B1[1] + (float)oz * B2[1], q.y);
@@ -1119,7 +1142,7 @@ __device__ __forceinline__ void scatter_consume(const float (*s_pay)[kCap], floa
         for (int a = 0; a < 2; ++a) B1[a] = s_pay[PY::B + a * D + 1][i];
 #pragma unroll
         for (int oy = 0; oy < 3; ++oy) {
-          const float W = wx * s_pay[PY::W + 3 + oy][i];
+          const float W = wx * wyv[oy];
           float4& q = acc[oy];
           q.x = fmaf(W, Ax[0] + (float)oy * B1[0], q.x);
           q.y = fmaf(W, Ax[1] + (float)oy * B1[1], q.y);
@@ -1681,8 +1704,13 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
 // The (p, m) accumulated are those of the unfused P2G of step t+1 up to fp32 summation order.
 // Saves the P2G re-read of the state (x, v, C, F, 96 B) and one launch per step.
 // ------------------------------------------------------------------------------------
+constexpr int kCapF = MPM_FUSE_CAP;  // particles per chunk of the fused kernel (payload buffer)
+static_assert(kCapF % 256 == 0 && kCapF <= kCap, "pay_slot permutes aligned groups of 8 within the chunk");
 template <int D>
-constexpr int fuse_dyn_smem() { return Pay<D, false>::N * kCap * (int)sizeof(float); }
+constexpr int fuse_dyn_smem() {  // payload buffer; also holds the in-block sort (kSortCap ints)
+  return (PayOf<D, false, MPM_FUSE_FX>::T::N * kCapF > kSortCap ? PayOf<D, false, MPM_FUSE_FX>::T::N * kCapF : kSortCap) *
+         (int)sizeof(float);
+}
 // escapee code: the new base cell relative to the block, lb in [-EO, EO) per axis, EB bits
 // each (EO > Bb, so a neighbour block's cells fit; D * EB <= 14 keeps -2 - code in a short)
 template <int D> struct Esc { static constexpr int EB = D == 3 ? 4 : 5, EO = 1 << (EB - 1); };
@@ -1692,17 +1720,17 @@ static_assert(3 * Esc<3>::EB <= 14 && 2 * Esc<2>::EB <= 14, "escapee code fits a
 // the escapees' nodes (NS per escapee, one (escapee, node) pair per thread of the idle group
 // [0, nthr)) as direct vector REDs into grid t+1; node value w_o (A + B o), mass w_o m from the
 // escapee's payload slot
-template <int D>
+template <int D, int CAP = kCap, bool FX = false>
 __device__ __forceinline__ void scatter_escapees(const KParams& P, const StepArgs& A, int r, const int* bc,
-                                                 const float (*s_pay)[kCap], const short* s_cell,
+                                                 const float (*s_pay)[CAP], const short* s_cell,
                                                  const short* s_ord, int nesc, int it, int nthr) {
   using DD = Dim<D>;
-  using PY = Pay<D, false>;
+  using PY = typename PayOf<D, false, FX>::T;
   constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
   for (int idx = it; idx < nesc * DD::NS; idx += nthr) {
     const int e = idx / DD::NS;
     int q = idx - e * DD::NS;
-    const int pi = s_ord[kCap - 1 - e];
+    const int pi = s_ord[CAP - 1 - e];
     const int pk = -2 - (int)s_cell[pi];
     const int ps = pay_slot(pi);
     int o[D], nb_[D], loc[D];
@@ -1716,7 +1744,7 @@ __device__ __forceinline__ void scatter_escapees(const KParams& P, const StepArg
     for (int a = 0; a < D; ++a) {
       const int lb = ((pk >> (EB * (D - 1 - a))) & (2 * EO - 1)) - EO;
       const int node = bc[a] * DD::BB + lb + o[a];
-      W *= s_pay[PY::W + a * 3 + o[a]][ps];
+      W *= FX ? bspl(s_pay[PY::W + a][ps], o[a]) : s_pay[PY::W + a * 3 + o[a]][ps];
       nb_[a] = node >> DD::LOG_BB;
       loc[a] = node & (DD::BB - 1);
     }
@@ -1741,19 +1769,20 @@ template <int D, int MAT, bool SORT, bool SCAT>
 __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   using DD = Dim<D>;
-  using PY = Pay<D, false>;
+  using PY = typename PayOf<D, false, MPM_FUSE_FX>::T;
   constexpr int BB = DD::BB, TN = DD::TN;
   constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
   __shared__ int s_hist[kCPB];
   __shared__ int s_cstart[kCPB + 1];
   __shared__ int s_cursor[kCPB];
-  __shared__ int s_sort[SORT ? kSortCap : 1];
+  __shared__ int s_sort_st[(SORT && !SCAT) ? kSortCap : 1];  // SCAT: the sort uses the payload area
   __shared__ float4 s_v[TN];
   __shared__ float4 s_tile[3][SCAT ? TN : 1];
-  __shared__ short s_cell[SCAT ? kCap : 1];
-  __shared__ short s_ord[SCAT ? kCap : 1];
+  __shared__ short s_cell[SCAT ? kCapF : 1];
+  __shared__ short s_ord[SCAT ? kCapF : 1];
   extern __shared__ __align__(16) unsigned char s_dyn[];
-  float (*s_pay)[kCap] = reinterpret_cast<float (*)[kCap]>(s_dyn);  // [PY::N][kCap], dynamic (SCAT)
+  float (*s_pay)[kCapF] = reinterpret_cast<float (*)[kCapF]>(s_dyn);  // [PY::N][kCapF], dynamic (SCAT)
+  int* s_sort = SCAT ? reinterpret_cast<int*>(s_dyn) : s_sort_st;  // the sort is done before the payload is written
   __shared__ int s_blk, s_nesc;
   const int tid = threadIdx.x;
   const int n_occ = A.info_t[I_NOCC];
@@ -1795,8 +1824,8 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
 #endif
     __syncthreads();
-    for (int lo = 0; lo < n; lo += kCap) {
-      const int hi = min(n, lo + kCap);
+    for (int lo = 0; lo < n; lo += kCapF) {
+      const int hi = min(n, lo + kCapF);
       if (SCAT) {
         if (tid < kCPB) s_hist[tid] = 0;
         if (tid == 0) s_nesc = 0;
@@ -1823,9 +1852,14 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
           if (ok) {
             const int ps = pay_slot(pi);
 #pragma unroll
-            for (int a = 0; a < D; ++a)
+            for (int a = 0; a < D; ++a) {
+              if (MPM_FUSE_FX) {
+                s_pay[PY::W + a][ps] = sc.fx[a];
+              } else {
 #pragma unroll
-              for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][ps] = sc.w[a][o];
+                for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][ps] = sc.w[a][o];
+              }
+            }
             s_pay[PY::M][ps] = pr.x;
 #pragma unroll
             for (int a = 0; a < D; ++a) {
@@ -1850,7 +1884,7 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
               }
               if (near) {
                 cell = -2 - pk;
-                s_ord[kCap - 1 - atomicAdd(&s_nesc, 1)] = (short)pi;
+                s_ord[kCapF - 1 - atomicAdd(&s_nesc, 1)] = (short)pi;
               } else {
                 latch(A.err, E_FUSE, A.t + 1, u);
               }
@@ -1870,9 +1904,10 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
         __syncthreads();
         const int i0 = tid < 3 * kCPB ? s_cstart[c] : 0;
         const int i1 = tid < 3 * kCPB ? s_cstart[c + 1] : 0;
-        scatter_consume<D, false, true>(s_pay, s_tile, i0, i1, s_ord, ox, c, tid);
-        if (tid >= 3 * kCPB) scatter_escapees<D>(P, A, r, bc, s_pay, s_cell, s_ord, s_nesc, tid - 3 * kCPB,
-                                                 kThreads - 3 * kCPB);
+        scatter_consume<D, false, true, kCapF, MPM_FUSE_FX>(s_pay, s_tile, i0, i1, s_ord, ox, c, tid);
+        if (tid >= 3 * kCPB)
+          scatter_escapees<D, kCapF, MPM_FUSE_FX>(P, A, r, bc, s_pay, s_cell, s_ord, s_nesc, tid - 3 * kCPB,
+                                                  kThreads - 3 * kCPB);
         __syncthreads();
       }
     }
