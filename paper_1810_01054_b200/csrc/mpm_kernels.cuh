@@ -58,8 +58,11 @@
 #ifndef MPM_SCAT_MINB
 #define MPM_SCAT_MINB 3
 #endif
+#ifndef MPM_SCATA_FX
+#define MPM_SCATA_FX 1
+#endif
 #ifndef MPM_SCATA_MINB
-#define MPM_SCATA_MINB 3
+#define MPM_SCATA_MINB (MPM_SCATA_FX ? 4 : 3)
 #endif
 
 namespace mpm {
@@ -876,8 +879,10 @@ template <int D> struct Pay<D, true> { static constexpr int W = 0, M = -1, A = 3
 // compact forward payload of the fused G2P2G: the fractional position fx (D rows) in place of
 // the 3D stencil weights, which the consumer recomputes (bspl) -- 16 rows instead of 22 in 3D
 template <int D> struct PayF { static constexpr int W = 0, M = D, A = D + 1, B = A + D, N = B + D * D; };
+template <int D> struct PayFA { static constexpr int W = 0, M = -1, A = D, B = A + D, N = B + D * D; };  // adjoint
 template <int D, bool ADJ, bool FX> struct PayOf { using T = Pay<D, ADJ>; };
 template <int D> struct PayOf<D, false, true> { using T = PayF<D>; };
+template <int D> struct PayOf<D, true, true> { using T = PayFA<D>; };
 // quadratic B-spline weight of node offset o at fractional position f (make_stencil's arithmetic)
 __device__ __forceinline__ float bspl(float f, int o) {
   const float u = o == 0 ? 1.5f - f : (o == 1 ? f - 1.0f : f - 0.5f);
@@ -928,8 +933,10 @@ __device__ __forceinline__ void prefetch_record(const float* base, size_t NT, in
   for (int c = c0; c < c0 + ncomp; ++c) prefetch_l2(base + (size_t)c * NT + j);
 }
 
+// G2P^T's payload carries fx instead of the stencil weights (MPM_SCATA_FX; 15 rows in 3D)
+__host__ __device__ constexpr bool scat_fx(bool adj) { return adj && MPM_SCATA_FX; }
 template <int D, bool ADJ>
-constexpr int scatter_dyn_smem() { return Pay<D, ADJ>::N * kCap * (int)sizeof(float); }
+constexpr int scatter_dyn_smem() { return PayOf<D, ADJ, scat_fx(ADJ)>::T::N * kCap * (int)sizeof(float); }
 // payload slot of chunk position p: a warp of consumer threads reads cells whose particles
 // sit ~2^d (2D: consecutive cells) or 2^d * {1, 4, 16} (3D thread order below) positions
 // apart, which would share 4 banks; the XOR of the low 3 bits with (p >> 5) ^ (p >> 7)
@@ -1209,7 +1216,8 @@ template <int D, bool ADJ, int MAT = 0, bool SPLIT = false>
 __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) void k_block_scatter(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   using DD = Dim<D>;
-  using PY = Pay<D, ADJ>;
+  constexpr bool FX = scat_fx(ADJ);
+  using PY = typename PayOf<D, ADJ, FX>::T;
   constexpr int BB = DD::BB, TN = DD::TN;
   __shared__ int s_hist[kCPB];
   __shared__ int s_cstart[kCPB + 1];
@@ -1292,8 +1300,12 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           f[a] = sc.fx[a];
+          if (FX) {
+            s_pay[PY::W + a][ps] = sc.fx[a];
+          } else {
 #pragma unroll
-          for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][ps] = sc.w[a][o];
+            for (int o = 0; o < 3; ++o) s_pay[PY::W + a * 3 + o][ps] = sc.w[a][o];
+          }
         }
         if (ADJ) {
           int cl[D];
@@ -1362,7 +1374,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
       {
         const int i0 = (tid < 3 * kCPB) ? (ADJ ? s_cstart[c] : max(s_cstart[c], lo) - lo) : 0;
         const int i1 = (tid < 3 * kCPB) ? (ADJ ? s_cursor[c] + 1 : min(s_cstart[c + 1], hi) - lo) : 0;
-        scatter_consume<D, ADJ, false>(s_pay, s_tile, i0, i1, nullptr, ox, c, tid);
+        scatter_consume<D, ADJ, false, kCap, FX>(s_pay, s_tile, i0, i1, nullptr, ox, c, tid);
       }
       __syncthreads();  // payload consumed, tile copies written
     }
