@@ -55,8 +55,11 @@
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
 #endif
+#ifndef MPM_SCAT_FX
+#define MPM_SCAT_FX 1
+#endif
 #ifndef MPM_SCAT_MINB
-#define MPM_SCAT_MINB 3
+#define MPM_SCAT_MINB (MPM_SCAT_FX ? 4 : 3)
 #endif
 #ifndef MPM_SCATA_FX
 #define MPM_SCATA_FX 1
@@ -934,9 +937,12 @@ __device__ __forceinline__ void prefetch_record(const float* base, size_t NT, in
 }
 
 // G2P^T's payload carries fx instead of the stencil weights (MPM_SCATA_FX; 15 rows in 3D)
-__host__ __device__ constexpr bool scat_fx(bool adj) { return adj && MPM_SCATA_FX; }
+__host__ __device__ constexpr bool scat_fx(bool adj) { return adj ? MPM_SCATA_FX : MPM_SCAT_FX; }
 template <int D, bool ADJ>
-constexpr int scatter_dyn_smem() { return PayOf<D, ADJ, scat_fx(ADJ)>::T::N * kCap * (int)sizeof(float); }
+constexpr int scatter_dyn_smem() {  // payload buffer (forward FX: also the in-block sort, kSortCap ints)
+  return (PayOf<D, ADJ, scat_fx(ADJ)>::T::N * kCap > kSortCap || ADJ ? PayOf<D, ADJ, scat_fx(ADJ)>::T::N * kCap : kSortCap) *
+         (int)sizeof(float);
+}
 // payload slot of chunk position p: a warp of consumer threads reads cells whose particles
 // sit ~2^d (2D: consecutive cells) or 2^d * {1, 4, 16} (3D thread order below) positions
 // apart, which would share 4 banks; the XOR of the low 3 bits with (p >> 5) ^ (p >> 7)
@@ -1222,9 +1228,10 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
   __shared__ int s_hist[kCPB];
   __shared__ int s_cstart[kCPB + 1];
   __shared__ int s_cursor[kCPB];
-  __shared__ int s_sort[ADJ ? 1 : kSortCap];
+  __shared__ int s_sort_st[(ADJ || scat_fx(ADJ)) ? 1 : kSortCap];  // forward FX: the sort uses the payload area
   extern __shared__ __align__(16) unsigned char s_dyn[];
   float (*s_pay)[kCap] = reinterpret_cast<float (*)[kCap]>(s_dyn);  // [PY::N][kCap], dynamic
+  int* s_sort = scat_fx(ADJ) ? reinterpret_cast<int*>(s_dyn) : s_sort_st;  // done before the payload is written
   __shared__ float4 s_tile[3][TN];
   __shared__ int s_blk;
   const int tid = threadIdx.x;
