@@ -156,3 +156,29 @@ def test_maximum_rollout_size():
     assert rel_err(g["dx0"][:, 0], m / M) < 1e-4
     assert rel_err(g["dv0"][:, 0], T * sc.dt * m / M) < 1e-4
     assert np.abs(g["dx0"][:, 1:]).max() < 1e-4 / n
+
+
+@pytest.mark.parametrize("d", [2, 3])
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_zero_step_trajectory(d, fuse):
+    """The degenerate horizon T = 0 (the memo holds state 0 only): forward(0) leaves the
+    state unchanged, and the backward of a 0-step memo returns the seed itself as dL/dstate_0
+    with zero material and actuation gradients (nothing was simulated)."""
+    sc = scenes.tiny(d, seed=77, res=32, steps=3, K=2, s=20.0)
+    cfg = mpm.Config.from_scene(sc, max_steps=3)
+    cfg.fuse_g2p2g = fuse
+    sim = mpm.MPM(cfg)
+    sim.set_scene(sc)
+    sim.forward(0)
+    NT = sim.NT
+    x, v, F, Cm = sim.get_state(0)
+    np.testing.assert_array_equal(x, sc.x.reshape(NT, d))
+    np.testing.assert_array_equal(v, sc.v.reshape(NT, d))
+    rng = np.random.default_rng(78)
+    seeds = [rng.standard_normal(s).astype(np.float32) for s in ((NT, d), (NT, d), (NT, d, d), (NT, d, d))]
+    sim.backward(*seeds)
+    g = sim.grad()
+    for k, s in zip(("dx0", "dv0", "dF0", "dC0"), seeds):
+        np.testing.assert_array_equal(g[k], s)
+    assert not np.any(g["dE"]) and not np.any(g["dnu"]) and not np.any(g["da"])
+
