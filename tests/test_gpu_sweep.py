@@ -88,3 +88,77 @@ def test_random_scene_forward_backward(i):
         pairs.append(("dm", sim.grad_mass(), ogm))
     for k, a, b in pairs:
         assert rel_err(a, b) < 1e-3, (k, rel_err(a, b), o)
+
+
+N_BATCH_CASES = 32
+
+
+def _batch_case(i):
+    """B rollouts of the same size in one context (the batch dimension of the launch grid, C5b):
+    each its own block placement, velocities, F0, C0, E, actuation, so the rollouts' blocks
+    interleave in the block table differently at every step."""
+    import dataclasses
+    rng = np.random.default_rng(9500 + i)
+    d = 2 + i % 2
+    B = int(rng.integers(2, 5))
+    res = int(rng.choice([16, 32]))
+    n_cells = tuple(int(c) for c in rng.integers(1, 7, d))
+    K = int(rng.integers(0, 3))
+    T = int(rng.integers(2, 9))
+    fric = tuple(float(rng.choice([0.0, 0.5])) for _ in range(2 * d)) + (0.0,) * (6 - 2 * d)
+    g = tuple(float(v) for v in rng.uniform(-10.0, 10.0, d))
+    s = float(rng.uniform(0.0, 50.0))
+    parts = []
+    for r in range(B):
+        lo = tuple(int(rng.integers(1, res - n_cells[a] - 1)) for a in range(d))
+        parts.append(scenes.tiny(d, seed=9600 + 16 * i + r, res=res, n_cells=n_cells, center=lo, steps=T, K=K,
+                                 s=s, gravity=g, friction=fric))
+    cat = lambda k: np.concatenate([getattr(p, k) for p in parts], axis=0)
+    sc = dataclasses.replace(parts[0], **{k: cat(k) for k in ("x", "v", "F", "C", "mass", "vol", "E", "nu",
+                                                                "actuator_id", "act")})
+    return sc, T, dict(fuse=int(rng.integers(0, 2)), material=int(i % 4 == 3))
+
+
+@pytest.mark.parametrize("i", range(N_BATCH_CASES))
+def test_random_batch_forward_backward(i):
+    sc, T, o = _batch_case(i)
+    d, B, n = sc.dim, sc.batch, sc.n
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, material=o["material"], fuse_g2p2g=o["fuse"]))
+    sim.set_scene(sc)
+    sim.forward(T)
+    for t in range(T):  # a1: keys (rollout, block, cell), stable ties, over the whole batch
+        xs, orig, key, perm, bs = sim.get_binning(t)
+        okey, operm, obs = oracle.bin_particles(d, sc.res, xs.reshape(B, n, d))
+        np.testing.assert_array_equal(key, okey)
+        np.testing.assert_array_equal(perm, operm)
+        np.testing.assert_array_equal(bs, obs)
+    x, v, F, Cm = sim.get_state(T)
+    rng = np.random.default_rng(9700 + i)
+    seeds, trajs, cfg = [], [], oracle_cfg(sc, material=o["material"])
+    for r in range(B):
+        m, vol, E, nu, aid, act = oracle_params(sc, r)
+        traj = oracle.forward(cfg, oracle_state(sc, r), m, vol, E, nu, aid, act[:T], T)
+        trajs.append(traj)
+        ox, ov, oC, oF = oracle.unpack(traj[T], d)
+        sl = slice(r * n, (r + 1) * n)
+        vmax = max(np.abs(ov).max(), 1e-6)
+        for k, a, b, scale in (("x", x[sl], ox, 1.0), ("v", v[sl], ov, vmax),
+                               ("F", F[sl], oF, np.abs(oF).max()), ("C", Cm[sl], oC, 4 * sc.res * vmax)):
+            err = np.abs(a - b).max() / scale
+            assert err < 1e-4, (r, k, err)
+        seeds.append(rng.standard_normal(traj[T].shape))
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    un = [oracle.unpack(w, d) for w in seeds]
+    sim.backward(*(f32(np.concatenate([u[q] for u in un])) for q in (0, 1, 3, 2)))  # x, v, F, C
+    g = sim.grad()
+    for r in range(B):
+        m, vol, E, nu, aid, act = oracle_params(sc, r)
+        g0, gE, gnu, ga = oracle.backward(cfg, trajs[r], m, vol, E, nu, aid, act[:T], seeds[r])
+        gx, gv, gC, gF = oracle.unpack(g0, d)
+        sl = slice(r * n, (r + 1) * n)
+        pairs = [("dx0", g["dx0"][sl], gx), ("dv0", g["dv0"][sl], gv), ("dF0", g["dF0"][sl], gF),
+                 ("dC0", g["dC0"][sl], gC), ("dE", g["dE"][sl], gE), ("dnu", g["dnu"][sl], gnu)]
+        if sc.n_act > 0:
+            pairs.append(("da", g["da"][r, :T], ga))
+        for k, a, b in pairs:
+            assert rel_err(a, b) < 1e-3, (r, k, rel_err(a, b), o)
