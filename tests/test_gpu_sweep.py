@@ -162,3 +162,42 @@ def test_random_batch_forward_backward(i):
             pairs.append(("da", g["da"][r, :T], ga))
         for k, a, b in pairs:
             assert rel_err(a, b) < 1e-3, (r, k, rel_err(a, b), o)
+
+
+N_SLAB_CASES = 24
+
+
+def _slab_case(i):
+    """One body spread along x, split into G x-slabs at particle-balanced block
+    boundaries: random slab count, halo width, grid, body extent, drift speed across the
+    slab boundaries, gravity, friction and actuators."""
+    from paper_1810_01054_b200 import parallel
+    rng = np.random.default_rng(9800 + i)
+    d = 2 + i % 2
+    res = int(rng.choice([32, 64])) if d == 3 else int(rng.choice([64, 128]))
+    nbp = res // parallel.block_size(d)
+    halo = int(rng.choice([1, 1, 2]))
+    G = int(rng.integers(2, min(4, nbp // (2 * halo)) + 1))
+    nx = int(rng.integers(res // 2, res - 4))
+    n_cells = (nx,) + tuple(int(c) for c in rng.integers(1, 5, d - 1))
+    lo = (int(rng.integers(1, res - nx - 1)),) + tuple(int(rng.integers(4, res - 9)) for _ in range(d - 1))
+    T = int(rng.integers(2, 11))
+    fric = tuple(float(rng.choice([0.0, 0.5])) for _ in range(2 * d)) + (0.0,) * (6 - 2 * d)
+    g = tuple(float(v) for v in rng.uniform(-10.0, 10.0, d))
+    v0 = (float(rng.choice([-1.0, 1.0]) * rng.uniform(0.0, 8.0)),) + (0.0,) * (d - 1)
+    sc = scenes.tiny(d, seed=9900 + i, res=res, n_cells=n_cells, center=lo, steps=T,
+                     K=int(rng.integers(0, 3)), s=float(rng.uniform(0.0, 50.0)), gravity=g,
+                     friction=fric, v0=v0)
+    while G > 2:  # every slab owns particles (the ABI requires n_particles >= 1 per context)
+        bounds = parallel.slab_partition(sc.x[0], sc.res, d, G, halo)
+        if all(len(parallel.slab_members(sc.x[0], sc.res, a, b)) for a, b in bounds):
+            break
+        G -= 1
+    return sc, T, G, halo
+
+
+@pytest.mark.parametrize("i", range(N_SLAB_CASES))
+def test_random_slab_split(i):
+    from tests.test_gpu_slab import _check_slab_run
+    sc, T, G, halo = _slab_case(i)
+    _check_slab_run(sc, T, G, halo, seed=9950 + i)
