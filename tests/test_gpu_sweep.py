@@ -201,3 +201,55 @@ def test_random_slab_split(i):
     from tests.test_gpu_slab import _check_slab_run
     sc, T, G, halo = _slab_case(i)
     _check_slab_run(sc, T, G, halo, seed=9950 + i)
+
+
+N_CTRL_CASES = 16
+
+
+@pytest.mark.parametrize("i", range(N_CTRL_CASES))
+def test_random_controller(i):
+    """NEXT N1 on random scenes: a_t = tanh(W z_t + b) from the state each step, random
+    actuator count, weight scale, bias and target; state, every state/parameter gradient and
+    dL/dW, dL/db, dL/dtarget against the controller oracle (oracle/controller.py)."""
+    from oracle import controller as ctl
+    rng = np.random.default_rng(10100 + i)
+    d = 2 + i % 2
+    res = int(rng.choice([16, 32]))
+    n_cells = tuple(int(c) for c in rng.integers(2, 9, d))
+    lo = tuple(int(rng.integers(1, res - n_cells[a] - 1)) for a in range(d))
+    K = int(rng.integers(1, 5))
+    T = int(rng.integers(2, 16))
+    sc = scenes.tiny(d, seed=10200 + i, res=res, n_cells=n_cells, center=lo, steps=T, K=K,
+                     s=float(rng.uniform(10.0, 50.0)),
+                     friction=tuple(float(rng.choice([0.0, 0.5])) for _ in range(2 * d)) + (0.0,) * (6 - 2 * d))
+    nz = ctl.n_obs(d, K)
+    W = (rng.standard_normal((K * d, nz)) * rng.uniform(0.05, 1.0)).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, K * d).astype(np.float32)
+    target = rng.uniform(0.2, 0.8, d).astype(np.float32)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    sim.set_scene(sc)
+    sim.set_controller(W, b, target)
+    sim.forward(T)
+    x, v, F, Cm = sim.get_state(T)
+    w = rng.standard_normal((sc.n, oracle.S_of(d)))
+    wx, wv, wC, wF = oracle.unpack(w, d)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    gW, gb, gt = sim.grad_controller()
+    cfg = oracle_cfg(sc)
+    m, vol, E, nu, aid, _ = oracle_params(sc)
+    W64, b64, t64 = W.astype(np.float64), b.astype(np.float64), target.astype(np.float64)
+    traj, acts, zs = ctl.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, W64, b64, t64, T)
+    ox, ov, oC, oF = oracle.unpack(traj[T], d)
+    for k, a_, b_ in (("x", x, ox), ("v", v, ov), ("F", F, oF), ("C", Cm, oC)):
+        assert rel_err(a_, b_) < 1e-3, (k, rel_err(a_, b_))
+    og, ogE, ognu, ogW, ogb, ogt, oga = ctl.backward(cfg, traj, m, vol, E, nu, aid, W64, b64, acts, zs, w)
+    gx, gv, gC, gF = oracle.unpack(og, d)
+    errs = {k: rel_err(a_, b_) for k, a_, b_ in (
+        ("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF), ("dC0", g["dC0"], gC),
+        ("dE", g["dE"], ogE), ("dnu", g["dnu"], ognu), ("da", g["da"][0, :T], oga),
+        ("dW", gW, ogW), ("db", gb, ogb), ("dtarget", gt, ogt))}
+    bad = {k: e for k, e in errs.items() if not e < 1e-3}
+    assert not bad, errs
+    sim.close()
