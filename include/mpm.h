@@ -231,8 +231,22 @@ mpm_status mpm_get_step_info(mpm_ctx ctx, int32_t t, int32_t out[3]);
 mpm_status mpm_set_profiling(mpm_ctx ctx, int32_t on);
 mpm_status mpm_get_profile(mpm_ctx ctx, int32_t* n_kernels, float* ms, int64_t* launches,
                            char* names, int32_t names_len);
-/* Total kernel launches issued by this context since creation. */
+/* Total kernel launches issued by this context since creation (a replayed graph counts the
+ * kernels it launches). */
 int64_t mpm_launch_count(mpm_ctx ctx);
+
+/* CUDA graphs for the step loops (off by default).  With on != 0, the launches of an
+ * mpm_forward(n) call -- and of the backward's loop over the memo's steps -- are captured
+ * into a CUDA graph the first time a (direction, start step, step count) occurs and replayed
+ * on later calls with the same triple (the launch-bound small configurations: P:167 and
+ * P:218 put the paper's TF overheads on per-op launches).  The graph computes exactly what
+ * the launches do: same kernels, same arguments, same stream order.  Loops that cannot be
+ * captured run as plain launches: n < 2 steps, checkpoint_every > 0 (recompute segments
+ * synchronise), slab neighbours (NCCL), profiling on.  Graphs are dropped when a call changes
+ * what the loops launch (mpm_set_controller, a new mpm_add_seed step, mpm_clear_seeds,
+ * mpm_enable_mass_grad) and on mpm_set_graphs(ctx, 0) / mpm_destroy.
+ * Errors: MPM_ERR_INVALID_ARG if config.stream is NULL (the legacy stream cannot be captured). */
+mpm_status mpm_set_graphs(mpm_ctx ctx, int32_t on);
 
 #ifdef __cplusplus
 }

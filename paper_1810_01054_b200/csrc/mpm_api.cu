@@ -149,6 +149,16 @@ struct mpm_ctx_s {
   float* bnxt = nullptr;
   // profiling
   bool profiling = false;
+  // mpm_set_graphs: step loops captured once per (direction, start, length) and replayed as
+  // CUDA graphs; the host-side effects of a capture (launch count, scan epochs) are replayed too
+  bool graphs = false;
+  struct GraphRec {
+    int dir, t0, n;
+    cudaGraphExec_t exec;
+    int64_t launches;
+    unsigned epochs;
+  };
+  std::vector<GraphRec> gcache;
   bool pdl = true;  // programmatic dependent launches on the step path (MPM_PDL=0 disables)
   bool split = false;  // small problem: the gathers split blocks into particle ranges
   bool mass_grad = false;  // N3: compute dL/dm_p in P2G^T (opt-in)
@@ -249,6 +259,14 @@ void kx(mpm_ctx c, void (*k)(KA...), dim3 g, dim3 b, size_t smem, A&&... args) {
 }
 
 size_t NTs(mpm_ctx c) { return (size_t)c->P.NT; }
+
+void drop_graphs(mpm_ctx c) {
+  if (c->gcache.empty()) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& g : c->gcache) cudaGraphExecDestroy(g.exec);
+  c->gcache.clear();
+}
+
 // tape slot of global step t (segment-local; the caller guarantees seg0 <= t <= seg0 + tape_cap)
 size_t ti(mpm_ctx c, int t) { return (size_t)(t - c->seg0); }
 float* state_at(mpm_ctx c, int t) { return c->tape_state + ti(c, t) * c->S * NTs(c); }
@@ -749,9 +767,59 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   return MPM_OK;
 }
 
+// A step loop can be a replayed graph when its launches depend on (direction, start, length)
+// only: no host synchronisation or NCCL inside (no slab neighbours, no checkpoint segments),
+// no per-launch profiling events, a non-legacy stream.  At least two steps: the binning scan's
+// tile flags carry the epoch of the last scan, and a graph whose first and last scan are the
+// same launch could read its own stale flags on the next replay.
+bool graphs_ok(mpm_ctx c, int n) {
+  return c->graphs && c->stream && !c->profiling && !has_nbr(c) && !c->comm && c->ck == 0 && n >= 2;
+}
+
+// Run body() -- which launches a step loop and advances the host state -- directly, or
+// capture it into a graph on first use and replay it after.  The replay applies the host
+// effects a capture records: the launch count and the scan epochs (later scans take fresh
+// epochs, never one baked into a graph).  `after` restores the rest of the host state.
+template <class F, class G>
+mpm_status run_graphed(mpm_ctx c, int dir, int t0, int n, F&& body, G&& after) {
+  if (!graphs_ok(c, n)) return body();
+  for (auto& g : c->gcache)
+    if (g.dir == dir && g.t0 == t0 && g.n == n) {
+      c->launches += g.launches;
+      c->scan_epoch += g.epochs;
+      after();
+      CK(cudaGraphLaunch(g.exec, c->stream));
+      return MPM_OK;
+    }
+  const int64_t l0 = c->launches;
+  const unsigned e0 = c->scan_epoch;
+  CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  mpm_status s = body();
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+  if (s) {
+    if (graph) cudaGraphDestroy(graph);
+    return s;
+  }
+  if (e != cudaSuccess) return cuda_fail(c, e, "graph capture");
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_fail(c, e, "graph instantiate");
+  c->gcache.push_back({dir, t0, n, exec, c->launches - l0, c->scan_epoch - e0});
+  CK(cudaGraphLaunch(exec, c->stream));
+  return MPM_OK;
+}
+
 template <int D>
 mpm_status do_forward(mpm_ctx c, int n) {
-  mpm_status s = forward_range<D>(c, c->tape_len, c->tape_len + n);
+  const int t0 = c->tape_len;
+  mpm_status s = run_graphed(
+      c, 0, t0, n, [&] { return forward_range<D>(c, t0, t0 + n); },
+      [&] {  // forward_range's host effects (checkpoint-free: seg0 is unchanged)
+        c->res_end = t0 + n;
+        c->fused_grid = -1;
+      });
   if (s) return s;
   s = sync_and_check(c, "forward");
   if (s) return s;
@@ -845,15 +913,28 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
   if (s) return s;
   c->seg_end = c->tape_len;  // the current segment [seg0, tape_len) is on the tape
   for (;;) {
-    for (int t = c->seg_end - 1; t >= c->seg0; --t) {
-      backward_phase_a<D>(c, t);
-      if (has_nbr(c)) {
-        s = exchange_nccl(c);
-        if (s) return s;
-      }
-      backward_phase_b<D>(c, t);
-      backward_step_end<D>(c, t);
-    }
+    float* const b0 = c->bcur;
+    float* const b1 = c->bnxt;
+    const int steps = c->seg_end - c->seg0;
+    s = run_graphed(
+        c, 1, c->seg0, steps,
+        [&]() -> mpm_status {
+          for (int t = c->seg_end - 1; t >= c->seg0; --t) {
+            backward_phase_a<D>(c, t);
+            if (has_nbr(c)) {
+              mpm_status q = exchange_nccl(c);
+              if (q) return q;
+            }
+            backward_phase_b<D>(c, t);
+            backward_step_end<D>(c, t);
+          }
+          return MPM_OK;
+        },
+        [&] {  // the adjoint buffers swap once per step
+          c->bcur = (steps & 1) ? b1 : b0;
+          c->bnxt = (steps & 1) ? b0 : b1;
+        });
+    if (s) return s;
     if (c->seg0 == 0) break;
     // N2: recompute the previous segment from its checkpoint, then continue the reverse pass
     const int end = c->seg0;
@@ -1239,6 +1320,7 @@ void mpm_destroy(mpm_ctx c) {
     cudaEventDestroy(p.b);
   }
   for (auto e : c->event_pool) cudaEventDestroy(e);
+  drop_graphs(c);
   delete c;
 }
 
@@ -1442,6 +1524,15 @@ mpm_status mpm_get_profile(mpm_ctx c, int32_t* n_kernels, float* ms, int64_t* la
 
 int64_t mpm_launch_count(mpm_ctx c) { return c ? c->launches : -1; }
 
+mpm_status mpm_set_graphs(mpm_ctx c, int32_t on) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  if (on && !c->stream) return fail(c, MPM_ERR_INVALID_ARG, "CUDA graphs need config.stream (not the legacy default stream)");
+  cudaSetDevice(c->cfg.device);
+  if (!on) drop_graphs(c);
+  c->graphs = on != 0;
+  return MPM_OK;
+}
+
 mpm_status mpm_add_seed(mpm_ctx c, int32_t t, const float* dLdx, const float* dLdv, const float* dLdF,
                         const float* dLdC) {
   if (!c || t < 0 || t > c->cfg.max_steps) return MPM_ERR_INVALID_ARG;
@@ -1450,6 +1541,7 @@ mpm_status mpm_add_seed(mpm_ctx c, int32_t t, const float* dLdx, const float* dL
   const size_t n = NT * (2 * D + 2 * D * D);
   float*& b = c->seeds[t];
   if (!b) {
+    drop_graphs(c);  // a new seed step: the backward graphs do not launch its k_seed
     mpm_status s = dalloc(c, &b, n);
     if (s) {
       c->seeds.erase(t);
@@ -1471,6 +1563,7 @@ mpm_status mpm_clear_seeds(mpm_ctx c) {
   if (!c) return MPM_ERR_INVALID_ARG;
   cudaSetDevice(c->cfg.device);
   cudaStreamSynchronize(c->stream);
+  drop_graphs(c);
   for (auto& kv : c->seeds) cudaFree(kv.second);
   c->seeds.clear();
   return MPM_OK;
@@ -1478,6 +1571,7 @@ mpm_status mpm_clear_seeds(mpm_ctx c) {
 
 mpm_status mpm_enable_mass_grad(mpm_ctx c, int32_t on) {
   if (!c) return MPM_ERR_INVALID_ARG;
+  if ((on != 0) != c->mass_grad) drop_graphs(c);  // P2G^T variant baked into backward graphs
   c->mass_grad = on != 0;
   c->mass_grad_valid = false;
   return MPM_OK;
@@ -1593,6 +1687,7 @@ mpm_status mpm_group_backward(mpm_ctx* cs, int32_t n, const float* const* dLdx, 
 mpm_status mpm_set_controller(mpm_ctx c, const float* W, const float* b, const float* target) {
   if (!c) return MPM_ERR_INVALID_ARG;
   cudaSetDevice(c->cfg.device);
+  drop_graphs(c);  // the controller kernels (and P.nz) are baked into captured step loops
   if (!W) {
     c->ctrl = false;
     return MPM_OK;

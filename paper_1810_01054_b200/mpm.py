@@ -31,7 +31,7 @@ EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "m
            "mpm_get_profile", "mpm_launch_count", "mpm_get_step_info", "mpm_grad_mass",
            "mpm_add_seed", "mpm_clear_seeds", "mpm_enable_mass_grad", "mpm_set_slab",
            "mpm_comm_unique_id", "mpm_comm_init", "mpm_group_forward", "mpm_group_backward",
-           "mpm_set_controller", "mpm_grad_controller")
+           "mpm_set_controller", "mpm_grad_controller", "mpm_set_graphs")
 
 
 class MPMError(RuntimeError):
@@ -79,6 +79,7 @@ def load():
     L.mpm_get_binning.argtypes = [vp, i32, vp, vp, vp, vp, vp]
     L.mpm_get_grid.argtypes = [vp, i32, vp, vp]
     L.mpm_set_profiling.argtypes = [vp, i32]
+    L.mpm_set_graphs.argtypes = [vp, i32]
     L.mpm_get_profile.argtypes = [vp, C.POINTER(i32), vp, vp, C.c_char_p, i32]
     L.mpm_get_step_info.argtypes = [vp, i32, vp]
     L.mpm_grad_mass.argtypes = [vp, vp]
@@ -336,6 +337,15 @@ class MPM:
 
     def set_profiling(self, on: bool):
         self._check(self.L.mpm_set_profiling(self.h, 1 if on else 0))
+
+    def launch_count(self) -> int:
+        """Kernels launched by this context so far (include/mpm.h mpm_launch_count)."""
+        return int(self.L.mpm_launch_count(self.h))
+
+    def set_graphs(self, on: bool = True):
+        """Replay the step loops as CUDA graphs (include/mpm.h mpm_set_graphs; needs
+        Config.stream)."""
+        self._check(self.L.mpm_set_graphs(self.h, 1 if on else 0))
 
     def profile(self):
         n = C.c_int32(32)
