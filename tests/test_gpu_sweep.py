@@ -253,3 +253,48 @@ def test_random_controller(i):
     bad = {k: e for k, e in errs.items() if not e < 1e-3}
     assert not bad, errs
     sim.close()
+
+
+@pytest.mark.parametrize("i", range(0, 64, 4))
+def test_random_scene_graph_replay(i):
+    """The sweep's scenes with the step loops replayed as CUDA graphs (mpm_set_graphs): the
+    first pass captures (or, for checkpointed runs, falls back to plain launches), the second
+    replays; both against the oracle."""
+    import torch
+    sc, T, o = _case(i)
+    d = sc.dim
+    stream = torch.cuda.Stream()
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, material=o["material"], fuse_g2p2g=o["fuse"],
+                                        checkpoint_every=o["ck"], stream=stream.cuda_stream))
+    sim.set_scene(sc)
+    sim.set_graphs(True)
+    sim.enable_mass_grad(o["mass_grad"])
+    cfg = oracle_cfg(sc, material=o["material"])
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    traj = oracle.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, act[:T], T)
+    W = np.zeros(traj.shape)
+    W[T] = np.random.default_rng(9400 + i).standard_normal(traj[T].shape)
+    g0, gE, gnu, ga, ogm = oracle.backward_ex(cfg, traj, m, vol, E, nu, aid, act[:T], W)
+    gx, gv, gC, gF = oracle.unpack(g0, d)
+    ox, ov, oC, oF = oracle.unpack(traj[T], d)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    wx, wv, wC, wF = oracle.unpack(W[T], d)
+    for _ in range(2):
+        sim.rewind(0)
+        sim.forward(T)
+        x, v, F, Cm = sim.get_state(T)
+        vmax = max(np.abs(ov).max(), 1e-6)
+        for k, a, b, scale in (("x", x, ox, 1.0), ("v", v, ov, vmax), ("F", F, oF, np.abs(oF).max()),
+                               ("C", Cm, oC, 4 * sc.res * vmax)):
+            assert np.abs(a - b).max() / scale < 1e-4, k
+        sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+        g = sim.grad()
+        pairs = [("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF),
+                 ("dC0", g["dC0"], gC), ("dE", g["dE"], gE), ("dnu", g["dnu"], gnu)]
+        if sc.n_act > 0:
+            pairs.append(("da", g["da"][0, :T], ga))
+        if o["mass_grad"]:
+            pairs.append(("dm", sim.grad_mass(), ogm))
+        for k, a, b in pairs:
+            assert rel_err(a, b) < 1e-3, (k, rel_err(a, b), o)
+    sim.close()
