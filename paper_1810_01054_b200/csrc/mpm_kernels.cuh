@@ -89,6 +89,27 @@ constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
     asm volatile("griddepcontrol.launch_dependents;" ::);  \
   } while (0)
 
+// Debug builds (-DMPM_DEBUG_BOUNDS=1; tools/build_variant.sh): index checks on the shared-
+// memory tiles, payload and sort buffers and the grid-slot arena; a violated check prints
+// the site and traps.  Compiled out otherwise.
+#ifndef MPM_DEBUG_BOUNDS
+#define MPM_DEBUG_BOUNDS 0
+#endif
+#if MPM_DEBUG_BOUNDS
+#define MPM_CHECK(cond)                                                                  \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("MPM_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__, \
+             blockIdx.x, threadIdx.x);                                                   \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define MPM_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6, E_SLAB = 9, E_FUSE = 10 };
 
 template <int D> struct Dim;
@@ -1066,7 +1087,11 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
   int* buf = (n <= kSortCap) ? s_sort : (A.scratch + s);
 #pragma unroll
   for (int q = 0; q < 2; ++q)
-    if (tid + q * kThreads < n) buf[atomicAdd(&s_cursor[pc[q]], 1)] = pj[q];
+    if (tid + q * kThreads < n) {
+      const int at = atomicAdd(&s_cursor[pc[q]], 1);
+      MPM_CHECK(at >= 0 && at < n);
+      buf[at] = pj[q];
+    }
   for (int i = tid + 2 * kThreads; i < n; i += kThreads) {
     const int2 e = A.tmp_pk[s + i];
     buf[atomicAdd(&s_cursor[e.y & (kCPB - 1)], 1)] = e.x;
@@ -1178,6 +1203,7 @@ __device__ __forceinline__ void scatter_consume(const float (*s_pay)[CAP], float
       int tl;
       if (D == 3) tl = ((cc[0] + ox) * TE + cc[1] + q / 3) * TE + cc[D - 1] + q % 3;
       else tl = (cc[0] + ox) * TE + cc[D - 1] + q;
+      MPM_CHECK(tl >= 0 && tl < Dim<D>::TN);
       float4 v = s_tile[ox][tl];
       v.x += acc[q].x; v.y += acc[q].y; v.z += acc[q].z; v.w += acc[q].w;
       s_tile[ox][tl] = v;
@@ -1304,6 +1330,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
         for (int a = 0; a < D; ++a) x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
         make_stencil<D>(x, P.fres, sc);
         const int ps = pay_slot(pi);
+        MPM_CHECK(ps >= 0 && ps < kCap);
 #pragma unroll
         for (int a = 0; a < D; ++a) {
           f[a] = sc.fx[a];
@@ -1454,6 +1481,7 @@ __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs
   ad = v;
   if (slot < 0) return;
   const size_t addr = (size_t)slot * kCPB + cell_lin<D>(loc);
+  MPM_CHECK(slot < P.arena_slots);
   const float4 pm = A.tgrid[addr];  // (p, m) as accumulated by P2G -- the memo's grid
   if (!(pm.w > 0.f)) return;        // empty node: v = 0 (R13), no adjoint
   // grid operation (Eq. 6 + gravity, R5): vbar = p / m + dt g, then the wall projection (R6)
@@ -1524,6 +1552,8 @@ __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, 
 template <int D, int OX, int OY, int OZ>
 __device__ __forceinline__ int tile_idx(const int* lb) {
   constexpr int TE = Dim<D>::TE;
+#pragma unroll
+  for (int a = 0; a < D; ++a) MPM_CHECK(lb[a] >= 0 && lb[a] <= TE - 3);  // stencil inside the tile
   if constexpr (D == 3) return ((lb[0] + OX) * TE + lb[1] + OY) * TE + lb[2] + OZ;
   else return (lb[0] + OX) * TE + lb[1] + OY;
 }
@@ -1752,6 +1782,7 @@ __device__ __forceinline__ void scatter_escapees(const KParams& P, const StepArg
     const int pi = s_ord[CAP - 1 - e];
     const int pk = -2 - (int)s_cell[pi];
     const int ps = pay_slot(pi);
+    MPM_CHECK(ps >= 0 && ps < CAP);
     int o[D], nb_[D], loc[D];
     float W = 1.f;
 #pragma unroll
@@ -1870,6 +1901,7 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
           int cell = -1;
           if (ok) {
             const int ps = pay_slot(pi);
+            MPM_CHECK(ps >= 0 && ps < kCapF);
 #pragma unroll
             for (int a = 0; a < D; ++a) {
               if (MPM_FUSE_FX) {
@@ -1918,7 +1950,11 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
         __syncthreads();
         for (int pi = tid; pi < hi - lo; pi += kThreads) {
           const int cl = s_cell[pi];
-          if (cl >= 0) s_ord[atomicAdd(&s_cursor[cl], 1)] = (short)pi;
+          if (cl >= 0) {
+            const int at = atomicAdd(&s_cursor[cl], 1);
+            MPM_CHECK(at >= 0 && at < kCapF - s_nesc);
+            s_ord[at] = (short)pi;
+          }
         }
         __syncthreads();
         const int i0 = tid < 3 * kCPB ? s_cstart[c] : 0;
