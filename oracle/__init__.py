@@ -22,12 +22,16 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "mpm_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# tools/mutation_check.py points this at a mutated build of mpm_oracle.c (never the product)
+_LIB_OVERRIDE = os.environ.get("MPM_ORACLE_LIB")
 
 ORC_OK, ORC_ERR_OUT_OF_DOMAIN, ORC_ERR_INVERTED, ORC_ERR_ARG = 0, 1, 2, 3
 
 
 def build(force: bool = False) -> str:
     """Compile mpm_oracle.c into liboracle.so (gcc, -O2, no fast-math, no FP contraction)."""
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
         os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "mpm_oracle.h"))
     ):
@@ -54,8 +58,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(_LIB)
+        L = C.CDLL(build())
         dp = C.POINTER(C.c_double)
         ip = C.POINTER(C.c_int)
         fp = C.POINTER(C.c_float)

@@ -7,7 +7,7 @@ import pytest
 import oracle
 from oracle import controller as ctl
 from paper_1810_01054_b200 import mpm, scenes
-from tests.helpers import oracle_cfg, oracle_params, oracle_state, rel_err
+from tests.helpers import assert_grads, oracle_cfg, oracle_params, oracle_state, rel_err
 
 pytestmark = pytest.mark.gpu
 
@@ -58,12 +58,9 @@ def test_controller_state_and_gradients_vs_oracle(name, T, scale):
     og, ogE, ognu, ogW, ogb, ogt, oga = ctl.backward(cfg, traj, m, vol, E, nu, aid, W.astype(np.float64),
                                                      b.astype(np.float64), acts, zs, w)
     gx, gv, gC, gF = oracle.unpack(og, sc.dim)
-    errs = {k: rel_err(a_, b_) for k, a_, b_ in (
-        ("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF), ("dC0", g["dC0"], gC),
-        ("dE", g["dE"], ogE), ("dnu", g["dnu"], ognu), ("da", g["da"][0, :T], oga),
-        ("dW", gW, ogW), ("db", gb, ogb), ("dtarget", gt, ogt))}
-    bad = {k: e for k, e in errs.items() if not e < 1e-3}
-    assert not bad, errs
+    assert_grads([("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF), ("dC0", g["dC0"], gC),
+                  ("dE", g["dE"], ogE), ("dnu", g["dnu"], ognu), ("da", g["da"][0, :T], oga),
+                  ("dW", gW, ogW), ("db", gb, ogb), ("dtarget", gt, ogt)])
     sim.close()
 
 
@@ -85,8 +82,8 @@ def test_controller_batch_rollouts_share_parameters():
         tot[1] += res[4]
         sl = slice(r * sc.n, (r + 1) * sc.n)
         gx = oracle.unpack(res[0], sc.dim)[0]
-        assert rel_err(g["dx0"][sl], gx) < 1e-3
-    assert rel_err(gW, tot[0]) < 1e-3 and rel_err(gb, tot[1]) < 1e-3
+        assert_grads([("dx0", g["dx0"][sl], gx)], ctx=r)
+    assert_grads([("dW", gW, tot[0]), ("db", gb, tot[1])])
 
 
 def test_controller_errors_and_off_switch():

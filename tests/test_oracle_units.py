@@ -248,3 +248,30 @@ def test_grid_node_adjoint_fd():
         assert abs(dm - Jm @ g) < 2e-6 * max(1, abs(Jm @ g))
         checked += 1
     assert checked > 1000
+
+
+def test_wall_bands_golden():
+    """Hand-derived step L per wall band (golden/walls.txt): pins which wall gets which c and
+    normal sign in the oracle's band geometry (R6), the sticky flag per wall, the R < 0 full
+    stop, the axis order at corners, and the adjoint (steps L, D, E) on the same nodes."""
+    n_rows = 0
+    for row in _rows("walls.txt"):
+        lhs, rhs = row.split("->")
+        t = lhs.split()
+        kind, d = t[0], int(t[1])
+        fr = tuple(float(s) for s in t[2:8])
+        node = [int(s) for s in t[8:8 + d]]
+        m = float(t[8 + d])
+        p = [float(s) for s in t[9 + d:9 + 2 * d]]
+        exp = [float(s) for s in rhs.split()]
+        cfg = oracle.Config(dim=d, res=16, dt=1e-3, gravity=(0.0, 0.0, 0.0), bound=3, friction=fr)
+        if kind == "fwd":
+            _, v = oracle.grid_node(cfg, node, m, p)
+            np.testing.assert_allclose(v, exp, atol=1e-8, err_msg=row)
+        else:
+            g = [float(s) for s in t[9 + 2 * d:9 + 3 * d]]
+            dp, dm = oracle.grid_node_adj(cfg, node, m, p, g)
+            np.testing.assert_allclose(dp, exp[:d], atol=1e-8, err_msg=row)
+            assert abs(dm - exp[d]) < 1e-8, (row, dm)
+        n_rows += 1
+    assert n_rows >= 20

@@ -1,7 +1,13 @@
 """Key counters per captured kernel from an ncu report (--page raw --csv):
   python tools/ncu_summary.py gpurun_out/prof.ncu-rep [--traffic-json profiles/ncu_traffic.json --workload C4]
+      [--allow-missing]
 --traffic-json writes dram__bytes_read.sum + dram__bytes_write.sum per launch (mean over the
-captured launches of each kernel), keyed by bench.py's kernel names (roofline "traffic")."""
+captured launches of each kernel), keyed by bench.py's kernel names (roofline "traffic").
+
+Every counter in KEYS must be in the report: `--set full` does not collect the L2 reduction /
+atomic counters, so the capture command adds them explicitly (EXTRA_METRICS, printed by
+`python tools/ncu_summary.py --metrics`).  A missing counter is an error (exit 2) unless
+--allow-missing is given -- a summary must not silently drop the evidence it is meant to carry."""
 import csv
 import io
 import json
@@ -40,8 +46,16 @@ KEYS = [
     ("l2_hit", "lts__t_sector_hit_rate.pct", 1),
     ("red_sect_K", "lts__t_sectors_op_red.sum", 1e-3),
     ("atom_sect_K", "lts__t_sectors_op_atom.sum", 1e-3),
+    ("red_req_K", "lts__t_requests_op_red.sum", 1e-3),
+    ("l1_red_req_K", "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum", 1e-3),
+    ("l1_atom_req_K", "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", 1e-3),
     ("shared_wf_M", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", 1e-6),
 ]
+# counters outside `--set full` that the capture must request with --metrics (sm_100 names,
+# checked with `ncu --query-metrics --chip gb100`)
+EXTRA_METRICS = ["lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "lts__t_requests_op_red.sum",
+                 "l1tex__t_requests_pipe_lsu_mem_global_op_red.sum",
+                 "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum"]
 
 
 TO_US = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "s": 1e6, "second": 1e6}
@@ -56,10 +70,15 @@ def _scale(sc, unit):
     return sc
 
 
-def main(rep, traffic_json=None):
+def main(rep, traffic_json=None, allow_missing=False):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
+    missing = [key for _, key, _ in KEYS if key not in hdr]
+    if missing and not allow_missing:
+        sys.stderr.write("ncu_summary: counters missing from the report (capture with --set full --metrics "
+                         + ",".join(EXTRA_METRICS) + "): " + ", ".join(missing) + "\n")
+        sys.exit(2)
     traffic = {}
     instr = {}
     stall = [i for i, h in enumerate(hdr) if h.startswith("smsp__average_warps_issue_stalled_")
@@ -71,6 +90,9 @@ def main(rep, traffic_json=None):
             if key in hdr and r[hdr.index(key)] not in ("", "n/a"):
                 i = hdr.index(key)
                 out.append(f"{short}={float(r[i].replace(',', '')) * _scale(sc, units[i]):.4g}")
+            elif not allow_missing:
+                sys.stderr.write(f"ncu_summary: {key} has no value for {name}\n")
+                sys.exit(2)
         try:
             b = sum(float(r[hdr.index(k)].replace(",", "")) * TO_MB.get(units[hdr.index(k)], 1.0) * 1e6
                     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
@@ -93,7 +115,10 @@ def main(rep, traffic_json=None):
 WORKLOAD = "C4"
 
 if __name__ == "__main__":
+    if "--metrics" in sys.argv:
+        print(",".join(EXTRA_METRICS))
+        sys.exit(0)
     tj = sys.argv[sys.argv.index("--traffic-json") + 1] if "--traffic-json" in sys.argv else None
     if "--workload" in sys.argv:
         WORKLOAD = sys.argv[sys.argv.index("--workload") + 1]
-    main(sys.argv[1], tj)
+    main(sys.argv[1], tj, "--allow-missing" in sys.argv)

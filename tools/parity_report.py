@@ -1,5 +1,5 @@
-"""Parity margins: norm-wise relative error (reading R16) of the CUDA path vs the fp64 oracle,
-per field, for the BASELINE configs C1-C3 and a C5b-style batch; prints one JSON line per case.
+"""Parity margins: norm-wise relative error (reading R16) and element-wise error at the field
+scale (tests/helpers.elem_err) of the CUDA path vs the fp64 oracle, per field, for the BASELINE configs C1-C3 and a C5b-style batch; prints one JSON line per case.
 Run on a GPU box:  python tools/parity_report.py > profiles/parity_margins.jsonl"""
 import json
 import os
@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 
 import oracle  # noqa: E402  (test infrastructure; this is a report tool, not the product)
 from paper_1810_01054_b200 import mpm, scenes  # noqa: E402
-from tests.helpers import oracle_cfg, rel_err  # noqa: E402
+from tests.helpers import elem_err, oracle_cfg, rel_err, wall_scenes  # noqa: E402
 
 
 def case(name, sc, T, r=0, **cfgkw):
@@ -44,10 +44,12 @@ def case(name, sc, T, r=0, **cfgkw):
     seeds[T] = w[r]
     g0, gE, gnu, ga, ogm = oracle.backward_ex(cfg, traj, *prm, aid, act, seeds)
     gx, gv, gC, gF = oracle.unpack(g0, sc.dim)
-    out["grad"] = {k: rel_err(a, b) for k, a, b in (
+    gp = (
         ("dx0", g["dx0"][sl], gx), ("dv0", g["dv0"][sl], gv), ("dF0", g["dF0"][sl], gF),
         ("dC0", g["dC0"][sl], gC), ("dE", g["dE"][sl], gE), ("dnu", g["dnu"][sl], gnu),
-        ("da", g["da"][r, :T], ga), ("dm", gm[sl], ogm))}
+        ("da", g["da"][r, :T], ga), ("dm", gm[sl], ogm))
+    out["grad"] = {k: rel_err(a, b) for k, a, b in gp}
+    out["grad_elem"] = {k: elem_err(a, b) for k, a, b in gp}
     out["oracle_s"] = round(time.time() - t0, 1)
     sim.close()
     print(json.dumps(out), flush=True)
@@ -81,10 +83,11 @@ def controller_case(name, sc, T, scale=0.2):
     og, _, _, ogW, ogb, ogt, _ = ctl.backward(cfg, traj, m, vol, E, nu, sc.actuator_id[0], W.astype(np.float64),
                                              b.astype(np.float64), acts, zs, w)
     gx, gv, gC, gF = oracle.unpack(og, d)
+    gp = (("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dW", gW, ogW), ("db", gb, ogb), ("dtarget", gt, ogt))
     out = {"case": name, "steps": T, "particles": sc.n,
            "state": {k: rel_err(a_, b_) for k, a_, b_ in (("x", x, ox), ("v", v, ov), ("F", F, oF), ("C", Cm, oC))},
-           "grad": {k: rel_err(a_, b_) for k, a_, b_ in (("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv),
-                                                         ("dW", gW, ogW), ("db", gb, ogb), ("dtarget", gt, ogt))},
+           "grad": {k: rel_err(a_, b_) for k, a_, b_ in gp},
+           "grad_elem": {k: elem_err(a_, b_) for k, a_, b_ in gp},
            "oracle_s": round(time.time() - t0, 1)}
     sim.close()
     print(json.dumps(out), flush=True)
@@ -107,3 +110,7 @@ if __name__ == "__main__":
          fuse_g2p2g=1, checkpoint_every=16, material=1)
     controller_case("C2 closed-loop controller (N1), 200 steps", scenes.walker_2d(steps=200), 200)
     controller_case("C3 closed-loop controller (N1), 60 steps", scenes.quadruped_3d(steps=60), 60, 0.1)
+    # step L with every wall kind: sticky (c < 0) and full-stop (c >= 1, R < 0 -> H(R) = 0) walls
+    for d in (2, 3):
+        for name, sc in wall_scenes(d, 60):
+            case(name, sc, 60)
