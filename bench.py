@@ -162,6 +162,17 @@ def _traffic(kernel, workload):
     return _ncu("per_launch_dram_bytes", kernel, workload)
 
 
+# The paper's own speed numbers (Table I): context, not a target --
+# another GPU (GTX 1080 Ti), a falling cube whose grid, dt, E, nu are not printed, "time
+# per frame" read as one step per frame.  vs_baseline stays null (BASELINE.json publishes none).
+PAPER_TABLE_I = {
+    "hardware": "NVIDIA GTX 1080 Ti (PAPER.md:183)", "source": "PAPER.md:190-197, Table I (3D falling cube)",
+    "assumption": "1 MLS-MPM step per frame (the paper does not say)",
+    "cubes": {str(n): {"fwd_ms": f, "bwd_ms": b, "fwd_bwd_particle_steps_per_s": round(n / ((f + b) * 1e-3))}
+              for n, f, b in ((8000, 0.392, 0.406), (64000, 1.594, 1.774), (512000, 10.501, 11.594))},
+}
+
+
 # ---------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------
@@ -309,7 +320,7 @@ def run_ours(args):
             "fwd": {"value": (total_particles * K / (fwd_ms / 1e3)) if fwd_ms else None,
                     "ms_per_step": (fwd_ms / K) if fwd_ms else None},
             "roofline": roofline, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary()}
+            "clocks": clk.summary(), "paper": PAPER_TABLE_I}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         if args.workload == "C4":
             line["cpu_baseline"] = cpu_baseline_full(sc)
@@ -329,58 +340,101 @@ def run_ours(args):
 # ---------------------------------------------------------------------------------------
 # oracle legs (CPU): cpu_baseline of our line, and the --impl reference arm
 # ---------------------------------------------------------------------------------------
-def _oracle_fb(sc, n_steps):
+def cpu_info():
+    """CPU model (/proc/cpuinfo, as lscpu reports it), logical CPUs and the CPUs this process may use."""
+    model = None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "usable_cpus": usable}
+
+
+def _oracle_fb(sc, n_steps, variant="serial64"):
+    """Forward n_steps + backward (seed: CoM_x) of rollout 0 with one oracle build: serial64 (the
+    oracle as it stands), serial32, omp64, omp32 (oracle.forward_backward_timing)."""
     import oracle
     cfg = oracle.Config(dim=sc.dim, res=sc.res, dt=sc.dt, gravity=sc.gravity, bound=sc.bound,
                         friction=sc.friction, act_strength=sc.act_strength, n_act=sc.n_act)
     st = oracle.pack(sc.x[0], sc.v[0], sc.C[0], sc.F[0])
     prm = [a[0].astype(np.float64) for a in (sc.mass, sc.vol, sc.E, sc.nu)]
-    t0 = time.perf_counter()
-    traj = oracle.forward(cfg, st, *prm, sc.actuator_id[0], sc.act[0][:n_steps].astype(np.float64), n_steps)
-    t1 = time.perf_counter()
-    seed = np.zeros_like(traj[-1])
+    act = sc.act[0][:max(n_steps, 1)].astype(np.float64)
+    seed = np.zeros_like(st)
     seed[:, 0] = prm[0] / prm[0].sum()
-    oracle.backward(cfg, traj, *prm, sc.actuator_id[0], sc.act[0][:n_steps].astype(np.float64), seed)
-    t2 = time.perf_counter()
-    return t1 - t0, t2 - t0
+    f, fb, _ = oracle.forward_backward_timing(cfg, st, *prm, sc.actuator_id[0], act, seed, n_steps, variant)
+    return f, fb
 
 
 def cpu_baseline_full(sc, what="full C4 state"):
-    """The oracle as it stands (fp64, single thread): 1 forward + 1 backward step of the
-    given state (~10-30 s of CPU work)."""
-    f, fb = _oracle_fb(sc, 1)
+    """The CPU oracle timed on this host: 1 forward + 1 backward step of the given
+    state with the serial fp64 oracle as it stands, its fp32 build, and the OpenMP builds (fp64
+    and fp32) at all usable cores with fixed-order merges of per-chunk grids.  value = the OpenMP
+    fp64 rate (the fair multithreaded CPU number); ~15-40 s of CPU work in total."""
+    import oracle
     n = sc.batch * sc.n
-    return {"value": n / fb, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{what} ({n} particles), 1 forward + 1 backward step, fp64, 1 thread; "
-                      f"forward alone {n / f:.4g} particle-steps/s"}
+    rates = {}
+    for v in ("omp64", "omp32", "serial64", "serial32"):
+        f, fb = _oracle_fb(sc, 1, v)
+        rates[v] = {"fwd_bwd": n / fb, "fwd": n / f}
+    threads = oracle.omp_threads()
+    info = cpu_info()
+    return {"value": rates["omp64"]["fwd_bwd"], "unit": UNIT, "cores": threads, "threads": threads,
+            "kind": "oracle", **info,
+            "fp64": {"threads": rates["omp64"], "1_thread": rates["serial64"]},
+            "fp32": {"threads": rates["omp32"], "1_thread": rates["serial32"]},
+            "sample": f"{what} ({n} particles), 1 forward + 1 backward step per variant; value = fp64 OpenMP "
+                      f"build at {threads} threads (per-chunk scatter grids merged in fixed order); the serial fp64 "
+                      f"oracle as it stands: {rates['serial64']['fwd_bwd']:.4g} particle-steps/s"}
+
+
+REF_BUDGET_S = 150.0  # wall-clock budget of the reference arm's timed steps
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle as it stands, on the same metric/config/unit; each
-    step is a bounded sample of the C4 workload (a sub-slab at the same density)."""
+    """--impl reference: the CPU oracle (fp64, OpenMP build at all usable cores) on the same
+    metric / config / unit.  Each step is one forward + one backward step of the FULL C4 state
+    (1,048,576 particles, the bench workload) when K steps fit REF_BUDGET_S; otherwise of a
+    sub-slab of the same slab at the same density, sized to fit."""
+    import oracle
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     K, W = args.steps, args.warmup
-    cells = (32, 16, 32) if K + W <= 40 else (16, 16, 16)
-    sc = scenes.slab_3d(seed=0, steps=2, cells=cells)
+    full = scenes.slab_3d(seed=0, steps=2)
+    f, fb = _oracle_fb(full, 1, "omp64")  # first warm-up step, on the full state
+    sc, cells = full, (64, 32, 64)
+    if fb * K > REF_BUDGET_S:
+        for cells in ((32, 32, 64), (32, 16, 32), (16, 16, 16), (8, 8, 8)):
+            if fb * K * (cells[0] * cells[1] * cells[2]) / (64 * 32 * 64) <= REF_BUDGET_S:
+                break
+        sc = scenes.slab_3d(seed=0, steps=2, cells=cells)
     n = sc.batch * sc.n
-    for _ in range(W):
-        _oracle_fb(sc, 1)
+    for _ in range(W - 1):
+        _oracle_fb(sc, 1, "omp64")
     t0 = time.perf_counter()
     for _ in range(K):
-        _oracle_fb(sc, 1)
+        _oracle_fb(sc, 1, "omp64")
     dt = time.perf_counter() - t0
     value = n * K / dt
-    full = scenes.slab_3d(seed=0, steps=1)
-    sample = (f"sub-slab {cells[0]}x{cells[1]}x{cells[2]} cells of the C4 slab at the same density "
-              f"({n} particles, 128^3 grid), 1 forward + 1 backward step per step, fp64, 1 thread")
+    threads = oracle.omp_threads()
+    what = ("the full C4 state" if sc is full else
+            f"a sub-slab {cells[0]}x{cells[1]}x{cells[2]} cells of the C4 slab at the same density")
+    sample = (f"{what} ({n} particles, 128^3 grid), 1 forward + 1 backward step per step, fp64, OpenMP build "
+              f"at {threads} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded jittered-lattice slab)",
-            "config": _cfg_dict(K, W, args.gpus, full, "C4"),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "config": {**_cfg_dict(K, W, args.gpus, full, "C4"), "same_config": sc is full},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "threads": threads, "kind": "oracle",
+                             "sample": sample, **cpu_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

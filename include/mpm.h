@@ -156,6 +156,8 @@ mpm_status mpm_add_seed(mpm_ctx ctx, int32_t t, const float* dLdx, const float* 
                         const float* dLdF, const float* dLdC);
 mpm_status mpm_clear_seeds(mpm_ctx ctx);
 
+/* Message of the last failed call on ctx; with ctx = NULL, why the calling thread's last
+ * mpm_create failed (invalid config field, cudaSetDevice, OOM size), or "null context".   */
 const char* mpm_last_error(mpm_ctx ctx);
 
 /* ---- NEXT N1: closed-loop controller embedded in P2G (Fig. 2 caption P:84) ----
@@ -244,8 +246,11 @@ int64_t mpm_launch_count(mpm_ctx ctx);
  * captured run as plain launches: n < 2 steps, checkpoint_every > 0 (recompute segments
  * synchronise), slab neighbours (NCCL), profiling on.  Graphs are dropped when a call changes
  * what the loops launch (mpm_set_controller, a new mpm_add_seed step, mpm_clear_seeds,
- * mpm_enable_mass_grad) and on mpm_set_graphs(ctx, 0) / mpm_destroy.
- * Errors: MPM_ERR_INVALID_ARG if config.stream is NULL (the legacy stream cannot be captured). */
+ * mpm_enable_mass_grad) and on mpm_set_graphs(ctx, 0) / mpm_destroy; at most 16 executables
+ * are kept (least recently used dropped first).
+ * Errors: MPM_ERR_INVALID_ARG if config.stream is NULL (the legacy stream cannot be captured).
+ * A capture or instantiation failure returns MPM_ERR_CUDA and poisons the context (its host
+ * bookkeeping advanced for launches that never ran): call mpm_set_state before the next step. */
 mpm_status mpm_set_graphs(mpm_ctx ctx, int32_t on);
 
 #ifdef __cplusplus

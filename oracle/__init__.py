@@ -370,3 +370,88 @@ def grid_node_adj(cfg: Config, node, m, p, dv):
     cc = cfg.c(0)
     lib().orc_grid_node_adj(C.byref(cc), _i(node), float(m), _d(p), _d(dv), _d(dp), C.byref(dm))
     return dp, dm.value
+
+
+# ---- timing builds (bench.py cpu_baseline) -------------------------------------
+# mpm_oracle_omp.c = this oracle's per-particle / per-node functions in OpenMP loops with
+# per-chunk scatter grids merged in fixed chunk order; mpm_oracle_f32.c = the same compiled with
+# float arithmetic.  Neither adds arithmetic of the method (tests/test_oracle_omp.py checks them
+# against the serial fp64 oracle).
+_OMP_LIBS = {}
+
+
+def build_omp(fp32: bool = False, force: bool = False) -> str:
+    src = os.path.join(_HERE, "mpm_oracle_f32.c" if fp32 else "mpm_oracle_omp.c")
+    out = os.path.join(_HERE, "liboracle_omp32.so" if fp32 else "liboracle_omp.so")
+    deps = [src, _SRC, os.path.join(_HERE, "mpm_oracle_omp.c"), os.path.join(_HERE, "mpm_oracle.h")]
+    if force or not os.path.exists(out) or os.path.getmtime(out) < max(os.path.getmtime(p) for p in deps):
+        tmp = out + f".tmp{os.getpid()}"
+        flags = ["-fsingle-precision-constant"] if fp32 else []
+        subprocess.check_call(["gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+                               "-shared", *flags, "-I", _HERE, "-o", tmp, src, "-lm"])
+        os.replace(tmp, out)
+    return out
+
+
+class _Cfg32(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int), ("res", C.c_int), ("n", C.c_int), ("n_act", C.c_int),
+        ("dt", C.c_float), ("gravity", C.c_float * 3), ("bound", C.c_int),
+        ("friction", C.c_float * 6), ("act_strength", C.c_float), ("eps", C.c_float),
+        ("material", C.c_int),
+    ]
+
+
+def _omp_lib(fp32: bool):
+    if fp32 not in _OMP_LIBS:
+        L = C.CDLL(build_omp(fp32))
+        L.orc_omp_threads.restype = C.c_int
+        _OMP_LIBS[fp32] = L
+    return _OMP_LIBS[fp32]
+
+
+def omp_threads() -> int:
+    """Threads the OpenMP build uses (OMP_NUM_THREADS or all cores)."""
+    return _omp_lib(False).orc_omp_threads()
+
+
+def forward_backward_timing(cfg: Config, state0, mass, vol, E, nu, act_id, act, seed, n_steps: int,
+                            variant: str = "omp64"):
+    """Forward n_steps + backward from `seed` with one of the timing builds: "serial64" (the
+    oracle as it stands), "serial32", "omp64", "omp32".  Returns (forward s, forward+backward s,
+    dL/dstate_0).  The serial ones run the OpenMP libraries' serial entry points (orc_forward /
+    orc_backward compiled there), the omp ones orc_forward_omp / orc_backward_omp."""
+    import time
+    fp32 = variant.endswith("32")
+    L = _omp_lib(fp32)
+    omp = variant.startswith("omp")
+    ft = np.float32 if fp32 else np.float64
+    cp = (lambda a: a.ctypes.data_as(C.POINTER(C.c_float))) if fp32 else _d
+    n, S = np.asarray(state0).shape
+    traj = np.zeros((n_steps + 1, n, S), ft)
+    traj[0] = state0
+    mass, vol, E, nu, act, seed = (np.ascontiguousarray(np.asarray(a), ft) for a in (mass, vol, E, nu, act, seed))
+    aid = np.ascontiguousarray(np.asarray(act_id, np.int32))
+    if fp32:
+        cc = _Cfg32(cfg.dim, cfg.res, n, cfg.n_act, cfg.dt, (C.c_float * 3)(*cfg.gravity), cfg.bound,
+                    (C.c_float * 6)(*cfg.friction), cfg.act_strength, cfg.eps, cfg.material)
+    else:
+        cc = cfg.c(n)
+    err = np.zeros(2, np.int32)
+    g0 = np.zeros((n, S), ft)
+    gE = np.zeros(n, ft)
+    gnu = np.zeros(n, ft)
+    ga = np.zeros((max(n_steps, 1), max(cfg.n_act, 1), cfg.dim), ft)
+    fwd = L.orc_forward_omp if omp else L.orc_forward
+    bwd = L.orc_backward_omp if omp else L.orc_backward
+    t0 = time.perf_counter()
+    rc = fwd(C.byref(cc), n_steps, cp(traj), cp(mass), cp(vol), cp(E), cp(nu), _i(aid), cp(act), _i(err))
+    t1 = time.perf_counter()
+    if rc:
+        raise OracleError(rc, tuple(err))
+    rc = bwd(C.byref(cc), n_steps, cp(traj), cp(mass), cp(vol), cp(E), cp(nu), _i(aid), cp(act), cp(seed),
+             cp(g0), cp(gE), cp(gnu), cp(ga))
+    t2 = time.perf_counter()
+    if rc:
+        raise OracleError(rc)
+    return t1 - t0, t2 - t0, g0

@@ -522,11 +522,45 @@ typedef struct {
   double* v;    /* [nn][d]  after projection                            */
 } grid_t;
 
+/* P2G of one particle (Eqs. 3, 5) into the grid arrays m, p; node ni is stored at
+ * m[ni - lo] (lo = 0: the whole grid; the OpenMP timing build scatters a thread's particles
+ * into a private sub-range, oracle/mpm_oracle_omp.c). */
+static void p2g_particle(const orc_cfg* cfg, const double* rec, double mass, const pq_t* q,
+                         double* m, double* p, int lo) {
+  int d = cfg->dim, ns = n_stencil(d);
+  double dx = 1.0 / (double)cfg->res;
+  const double* x = rec;
+  const double* v = rec + d;
+  for (int s = 0; s < ns; ++s) {
+    int o[MAXD], i[MAXD];
+    stencil_offset(d, s, o);
+    double W = 1.0, dpos[MAXD];
+    for (int a = 0; a < d; ++a) {
+      i[a] = q->base[a] + o[a];
+      W *= orc_N(x[a] / dx - (double)i[a]); /* N(x_i - x_p), R2 */
+      dpos[a] = (double)i[a] * dx - x[a];   /* x_i - x_p        */
+    }
+    int ni = node_index(cfg, i) - lo;
+    m[ni] += W * mass; /* Eq. 3 */
+    for (int a = 0; a < d; ++a) {
+      double Gd = 0.0;
+      for (int b = 0; b < d; ++b) Gd += q->G[a * d + b] * dpos[b];
+      p[ni * d + a] += W * (mass * v[a] + Gd); /* Eq. 5 */
+    }
+  }
+}
+
+/* the grid operation of node ni (Eq. 6 + R5/R6) */
+static void grid_node_at(const orc_cfg* cfg, grid_t* g, int ni) {
+  int d = cfg->dim, node[MAXD], r = ni;
+  for (int a = d - 1; a >= 0; --a) { node[a] = r % cfg->res; r /= cfg->res; }
+  orc_grid_node(cfg, node, g->m[ni], g->p + ni * d, g->vbar + ni * d, g->v + ni * d);
+}
+
 static int p2g_and_grid(const orc_cfg* cfg, const double* st, const double* mass,
                         const double* vol, const double* E, const double* nu, const int* act_id,
                         const double* act_t, grid_t* g, pq_t* pq, int* bad) {
-  int d = cfg->dim, S = S_of(d), nn = nodes_of(cfg), ns = n_stencil(d);
-  double dx = 1.0 / (double)cfg->res;
+  int d = cfg->dim, S = S_of(d), nn = nodes_of(cfg);
   memset(g->m, 0, sizeof(double) * nn);
   memset(g->p, 0, sizeof(double) * nn * d);
   for (int pi = 0; pi < cfg->n; ++pi) {
@@ -534,40 +568,18 @@ static int p2g_and_grid(const orc_cfg* cfg, const double* st, const double* mass
     int err = particle_quantities(cfg, rec, mass[pi], vol[pi], E[pi], nu[pi], act_id[pi],
                                   act_t, &pq[pi]);
     if (err) { *bad = pi; return err; }
-    const double* x = rec;
-    const double* v = rec + d;
-    for (int s = 0; s < ns; ++s) {
-      int o[MAXD], i[MAXD];
-      stencil_offset(d, s, o);
-      double W = 1.0, dpos[MAXD];
-      for (int a = 0; a < d; ++a) {
-        i[a] = pq[pi].base[a] + o[a];
-        W *= orc_N(x[a] / dx - (double)i[a]); /* N(x_i - x_p), R2 */
-        dpos[a] = (double)i[a] * dx - x[a];   /* x_i - x_p        */
-      }
-      int ni = node_index(cfg, i);
-      g->m[ni] += W * mass[pi]; /* Eq. 3 */
-      for (int a = 0; a < d; ++a) {
-        double Gd = 0.0;
-        for (int b = 0; b < d; ++b) Gd += pq[pi].G[a * d + b] * dpos[b];
-        g->p[ni * d + a] += W * (mass[pi] * v[a] + Gd); /* Eq. 5 */
-      }
-    }
+    p2g_particle(cfg, rec, mass[pi], &pq[pi], g->m, g->p, 0);
   }
-  int node[MAXD];
-  for (int ni = 0; ni < nn; ++ni) {
-    int r = ni;
-    for (int a = d - 1; a >= 0; --a) { node[a] = r % cfg->res; r /= cfg->res; }
-    orc_grid_node(cfg, node, g->m[ni], g->p + ni * d, g->vbar + ni * d, g->v + ni * d);
-  }
+  for (int ni = 0; ni < nn; ++ni) grid_node_at(cfg, g, ni);
   return ORC_OK;
 }
 
-static void g2p(const orc_cfg* cfg, const double* st, const grid_t* g, const pq_t* pq,
-                double* out) {
+/* G2P of particle pi (Eqs. 7-10) */
+static void g2p_particle(const orc_cfg* cfg, const double* st, const grid_t* g, const pq_t* pq,
+                         double* out, int pi) {
   int d = cfg->dim, S = S_of(d), ns = n_stencil(d);
   double dx = 1.0 / (double)cfg->res;
-  for (int pi = 0; pi < cfg->n; ++pi) {
+  {
     const double* rec = st + (size_t)pi * S;
     const double* x = rec;
     const double* F = rec + 2 * d + d * d;
@@ -605,6 +617,11 @@ static void g2p(const orc_cfg* cfg, const double* st, const grid_t* g, const pq_
       xo[a] = x[a] + cfg->dt * vn[a]; /* Eq. 10 */
     }
   }
+}
+
+static void g2p(const orc_cfg* cfg, const double* st, const grid_t* g, const pq_t* pq,
+                double* out) {
+  for (int pi = 0; pi < cfg->n; ++pi) g2p_particle(cfg, st, g, pq, out, pi);
 }
 
 static int alloc_grid(const orc_cfg* cfg, grid_t* g) {
@@ -675,14 +692,71 @@ int orc_forward(const orc_cfg* cfg, int n_steps, double* traj, const double* mas
 /* ------------------------------------------------------------------------------------ */
 /* backward of one step n: adjoint record of state n+1 -> adjoint record of state n       */
 /* ------------------------------------------------------------------------------------ */
+/* (C) P:515-521 for particle pi: scatter into dvi (node ni stored at dvi[(ni - lo) d]) */
+static void g2pT_particle(const orc_cfg* cfg, const double* st, const pq_t* pq, const double* gvh,
+                          const double* gCh, double* dvi, int lo, int pi) {
+  int d = cfg->dim, S = S_of(d), ns = n_stencil(d);
+  double dx = 1.0 / (double)cfg->res;
+  const double* x = st + (size_t)pi * S;
+  for (int s = 0; s < ns; ++s) {
+    int o[MAXD], i[MAXD];
+    stencil_offset(d, s, o);
+    double W = 1.0, dpos[MAXD];
+    for (int a = 0; a < d; ++a) {
+      i[a] = pq[pi].base[a] + o[a];
+      W *= orc_N(x[a] / dx - (double)i[a]);
+      dpos[a] = (double)i[a] * dx - x[a];
+    }
+    int ni = node_index(cfg, i) - lo;
+    for (int a = 0; a < d; ++a) {
+      double cd = 0.0;
+      for (int b = 0; b < d; ++b) cd += gCh[(pi * d + a) * d + b] * dpos[b];
+      dvi[ni * d + a] += gvh[pi * d + a] * W + 4.0 / (dx * dx) * W * cd;
+    }
+  }
+}
+
+/* (L) P:609-635, (D) P:525-530, (E) P:534-540 of node ni */
+static void grid_node_adj_at(const orc_cfg* cfg, const grid_t* g, const double* dvi, double* dpi,
+                             double* dmi, int ni) {
+  int d = cfg->dim, node[MAXD], r = ni;
+  for (int a = d - 1; a >= 0; --a) { node[a] = r % cfg->res; r /= cfg->res; }
+  orc_grid_node_adj(cfg, node, g->m[ni], g->p + ni * d, dvi + ni * d, dpi + ni * d, &dmi[ni]);
+}
+
+/* (A) P:496-501, (B) P:504-509 of particle pi, with the carry-over note P:511 (gin already
+ * holds dL/dv^{n+1}, dL/dC^{n+1} from the later step) */
+static void stepAB_particle(const orc_cfg* cfg, const double* st, const double* gin, double* gvh,
+                            double* gCh, int pi) {
+  int d = cfg->dim, S = S_of(d);
+  const double* gr = gin + (size_t)pi * S;
+  const double* gx = gr;
+  const double* gv = gr + d;
+  const double* gC = gr + 2 * d;
+  const double* gF = gr + 2 * d + d * d;
+  const double* F = st + (size_t)pi * S + 2 * d + d * d;
+  for (int a = 0; a < d; ++a) gvh[pi * d + a] = gv[a] + cfg->dt * gx[a];
+  for (int a = 0; a < d; ++a)
+    for (int b = 0; b < d; ++b) {
+      double s = 0.0;
+      for (int c = 0; c < d; ++c) s += gF[a * d + c] * F[b * d + c];
+      gCh[(pi * d + a) * d + b] = gC[a * d + b] + cfg->dt * s;
+    }
+}
+
+static void p2gT_particle(const orc_cfg* cfg, const double* st, const double* st_next,
+                          const double* mass, const double* vol, const double* E, const double* nu,
+                          const int* act_id, const double* gin, double* gout, double* gE, double* gnu,
+                          double* ga_t, double* gm, const grid_t* g, const pq_t* pq, const double* gvh,
+                          const double* gCh, const double* dpi, const double* dmi, int pi);
+
 static int step_backward(const orc_cfg* cfg, const double* st, const double* st_next,
                          const double* mass, const double* vol, const double* E,
                          const double* nu, const int* act_id, const double* act_t,
                          const double* gin, double* gout, double* gE, double* gnu,
                          double* ga_t, double* gm, grid_t* g, pq_t* pq, double* dvi, double* dpi,
                          double* dmi) {
-  int d = cfg->dim, S = S_of(d), nn = nodes_of(cfg), ns = n_stencil(d);
-  double dx = 1.0 / (double)cfg->res, res = (double)cfg->res;
+  int d = cfg->dim, nn = nodes_of(cfg);
   int bad = -1;
   /* recompute step n's grid from the memo */
   int err = p2g_and_grid(cfg, st, mass, vol, E, nu, act_id, act_t, g, pq, &bad);
@@ -691,53 +765,31 @@ static int step_backward(const orc_cfg* cfg, const double* st, const double* st_
   double* gvh = (double*)malloc(sizeof(double) * (size_t)(cfg->n > 0 ? cfg->n : 1) * d);
   double* gCh = (double*)malloc(sizeof(double) * (size_t)(cfg->n > 0 ? cfg->n : 1) * d * d);
 
-  /* (A) P:496-501 and (B) P:504-509, plus the carry-over note P:511 (gin already holds
-   * dL/dv^{n+1}, dL/dC^{n+1} from the later step).                                      */
-  for (int pi = 0; pi < cfg->n; ++pi) {
-    const double* gr = gin + (size_t)pi * S;
-    const double* gx = gr;
-    const double* gv = gr + d;
-    const double* gC = gr + 2 * d;
-    const double* gF = gr + 2 * d + d * d;
-    const double* F = st + (size_t)pi * S + 2 * d + d * d;
-    for (int a = 0; a < d; ++a) gvh[pi * d + a] = gv[a] + cfg->dt * gx[a];
-    for (int a = 0; a < d; ++a)
-      for (int b = 0; b < d; ++b) {
-        double s = 0.0;
-        for (int c = 0; c < d; ++c) s += gF[a * d + c] * F[b * d + c];
-        gCh[(pi * d + a) * d + b] = gC[a * d + b] + cfg->dt * s;
-      }
-  }
+  /* (A), (B) */
+  for (int pi = 0; pi < cfg->n; ++pi) stepAB_particle(cfg, st, gin, gvh, gCh, pi);
   /* (C) P:515-521: scatter to dL/dv_i */
   memset(dvi, 0, sizeof(double) * nn * d);
-  for (int pi = 0; pi < cfg->n; ++pi) {
-    const double* x = st + (size_t)pi * S;
-    for (int s = 0; s < ns; ++s) {
-      int o[MAXD], i[MAXD];
-      stencil_offset(d, s, o);
-      double W = 1.0, dpos[MAXD];
-      for (int a = 0; a < d; ++a) {
-        i[a] = pq[pi].base[a] + o[a];
-        W *= orc_N(x[a] / dx - (double)i[a]);
-        dpos[a] = (double)i[a] * dx - x[a];
-      }
-      int ni = node_index(cfg, i);
-      for (int a = 0; a < d; ++a) {
-        double cd = 0.0;
-        for (int b = 0; b < d; ++b) cd += gCh[(pi * d + a) * d + b] * dpos[b];
-        dvi[ni * d + a] += gvh[pi * d + a] * W + 4.0 / (dx * dx) * W * cd;
-      }
-    }
-  }
+  for (int pi = 0; pi < cfg->n; ++pi) g2pT_particle(cfg, st, pq, gvh, gCh, dvi, 0, pi);
   /* (L) P:609-635, then (D) P:525-530 and (E) P:534-540 per node */
-  int node[MAXD];
-  for (int ni = 0; ni < nn; ++ni) {
-    int r = ni;
-    for (int a = d - 1; a >= 0; --a) { node[a] = r % cfg->res; r /= cfg->res; }
-    orc_grid_node_adj(cfg, node, g->m[ni], g->p + ni * d, dvi + ni * d, dpi + ni * d, &dmi[ni]);
-  }
+  for (int ni = 0; ni < nn; ++ni) grid_node_adj_at(cfg, g, dvi, dpi, dmi, ni);
   /* (F)-(K) P:543-605 per particle */
-  for (int pi = 0; pi < cfg->n; ++pi) {
+  for (int pi = 0; pi < cfg->n; ++pi)
+    p2gT_particle(cfg, st, st_next, mass, vol, E, nu, act_id, gin, gout, gE, gnu, ga_t, gm, g, pq, gvh,
+                  gCh, dpi, dmi, pi);
+  free(gvh);
+  free(gCh);
+  return ORC_OK;
+}
+
+/* (F)-(K) P:543-605 of particle pi; adds its actuation gradient to ga_t (step K) */
+static void p2gT_particle(const orc_cfg* cfg, const double* st, const double* st_next,
+                          const double* mass, const double* vol, const double* E, const double* nu,
+                          const int* act_id, const double* gin, double* gout, double* gE, double* gnu,
+                          double* ga_t, double* gm, const grid_t* g, const pq_t* pq, const double* gvh,
+                          const double* gCh, const double* dpi, const double* dmi, int pi) {
+  int d = cfg->dim, S = S_of(d), ns = n_stencil(d);
+  double dx = 1.0 / (double)cfg->res, res = (double)cfg->res;
+  {
     const double* rec = st + (size_t)pi * S;
     const double* x = rec;
     const double* v = rec + d;
@@ -861,9 +913,6 @@ static int step_backward(const orc_cfg* cfg, const double* st, const double* st_
     gE[pi] += dmu * dmu_dE + dlam * dlam_dE;
     gnu[pi] += dmu * dmu_dnu + dlam * dlam_dnu;
   }
-  free(gvh);
-  free(gCh);
-  return ORC_OK;
 }
 
 int orc_backward_ex(const orc_cfg* cfg, int n_steps, const double* traj, const double* mass,

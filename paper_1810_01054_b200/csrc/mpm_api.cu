@@ -91,6 +91,7 @@ struct mpm_ctx_s {
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
   std::string last_error;
   int64_t launches = 0;
+  int latch_step = -1;  // step of the last latched device error (check_latch)
   // tape
   float* tape_state = nullptr;
   int* tape_perm = nullptr;
@@ -170,6 +171,9 @@ struct mpm_ctx_s {
 };
 
 namespace {
+
+// the reason the calling thread's last mpm_create failed (read by mpm_last_error(NULL))
+thread_local std::string g_create_error;
 
 mpm_status fail(mpm_ctx c, mpm_status s, const std::string& msg) {
   if (c) c->last_error = msg;
@@ -289,6 +293,7 @@ mpm_status check_latch(mpm_ctx c) {
   cudaError_t e = cudaMemcpy(&h, c->err, sizeof(h), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return cuda_fail(c, e, "error latch readback");
   if (h.code == 0) return MPM_OK;
+  c->latch_step = h.step;
   char buf[256];
   if (h.code == E_DOMAIN) {
     snprintf(buf, sizeof buf, "particle %d left the domain (base index outside [0, res-3]) at step %d", h.particle, h.step);
@@ -683,6 +688,46 @@ mpm_status ctrl_masses(mpm_ctx c) {
   return MPM_OK;
 }
 
+// (Re)allocate the tape's grid-slot arena for `per` slots per step (and the two per-step
+// adjoint grids).  keep: copy the current arena's contents (the steps already on the tape keep
+// their absolute slot numbers).  The old buffers are freed only once the new ones exist.
+mpm_status alloc_arena(mpm_ctx c, long per, bool keep) {
+  const size_t slots = (size_t)per * (size_t)(c->tape_cap + 1);
+  float4 *na = nullptr, *ng0 = nullptr, *ng1 = nullptr;
+  auto release = [&] {
+    cudaFree(na);
+    cudaFree(ng0);
+    cudaFree(ng1);
+    cudaGetLastError();
+  };
+  if (cudaMalloc(&na, slots * kCPB * sizeof(float4)) != cudaSuccess ||
+      cudaMalloc(&ng0, (size_t)per * kCPB * sizeof(float4)) != cudaSuccess ||
+      cudaMalloc(&ng1, (size_t)per * kCPB * sizeof(float4)) != cudaSuccess) {
+    release();
+    return fail(c, MPM_ERR_OOM, "grid-slot arena of " + std::to_string(slots * kCPB * sizeof(float4)) +
+                                    " bytes: cudaMalloc failed");
+  }
+  drop_graphs(c);  // captured loops hold the old pointers
+  if (c->arena) {
+    if (keep) {
+      CK(cudaMemcpyAsync(na, c->arena, c->arena_slots * kCPB * sizeof(float4), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (void* old : {(void*)c->arena, (void*)c->agrid, (void*)c->agrid1}) {
+      c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), old), c->allocs.end());
+      cudaFree(old);
+    }
+  }
+  for (void* q : {(void*)na, (void*)ng0, (void*)ng1}) c->allocs.push_back(q);
+  c->arena = na;
+  c->agrid = ng0;
+  c->agrid1 = ng1;
+  c->P.slots_per_step = (int)per;
+  c->arena_slots = slots;
+  c->P.arena_slots = (int)std::min<size_t>(slots, (size_t)0x7fffffff);
+  return MPM_OK;
+}
+
 template <int D>
 mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* F, const float* C,
                         const float* mass, const float* vol, const float* E, const float* nu,
@@ -723,8 +768,10 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
     CK(cudaMemcpyAsync(ck_orig_of(c, 0), orig_at(c, 0), NT * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
     c->ck_valid = 1;
   }
-  // automatic grid-slot capacity from the touched blocks of the initial state
-  if (c->arena == nullptr) {
+  // grid-slot capacity per step: config.grid_slots, or automatic -- twice the touched blocks
+  // of this initial state (re-sized on every set_state whose body needs more; grown during a
+  // rollout that spreads beyond it, see mpm_forward)
+  if (c->arena == nullptr || c->cfg.grid_slots <= 0) {
     launch(c, KI_MISC, [&] {
       if (c->cfg.fuse_g2p2g) kx(c, k_scan_a<D, true>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums);
       else kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums);
@@ -734,17 +781,12 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
     CK(cudaStreamSynchronize(c->stream));
     long touched = 0;
     for (auto& q : ts) touched += q.z;
-    long per = c->cfg.grid_slots > 0 ? c->cfg.grid_slots
-                                      : std::min<long>(P.NBT, 2 * touched + 64L * P.B + 64);
-    c->P.slots_per_step = (int)per;
-    c->arena_slots = (size_t)per * (size_t)(c->tape_cap + 1);
-    c->P.arena_slots = (int)std::min<size_t>(c->arena_slots, (size_t)0x7fffffff);
-    mpm_status s = dalloc(c, &c->arena, c->arena_slots * kCPB);
-    if (s) return s;
-    s = dalloc(c, &c->agrid, (size_t)per * kCPB);
-    if (s) return s;
-    s = dalloc(c, &c->agrid1, (size_t)per * kCPB);
-    if (s) return s;
+    const long per = c->cfg.grid_slots > 0 ? c->cfg.grid_slots
+                                            : std::min<long>(P.NBT, 2 * touched + 64L * P.B + 64);
+    if (c->arena == nullptr || per > c->P.slots_per_step) {
+      mpm_status s = alloc_arena(c, per, false);
+      if (s) return s;
+    }
   }
   CK(cudaMemsetAsync(c->dmu, 0, NT * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->dlam, 0, NT * sizeof(float), c->stream));
@@ -772,6 +814,8 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
 // no per-launch profiling events, a non-legacy stream.  At least two steps: the binning scan's
 // tile flags carry the epoch of the last scan, and a graph whose first and last scan are the
 // same launch could read its own stale flags on the next replay.
+constexpr size_t kGraphCache = 16;  // CUDA-graph executables kept per context (LRU)
+
 bool graphs_ok(mpm_ctx c, int n) {
   return c->graphs && c->stream && !c->profiling && !has_nbr(c) && !c->comm && c->ck == 0 && n >= 2;
 }
@@ -783,8 +827,10 @@ bool graphs_ok(mpm_ctx c, int n) {
 template <class F, class G>
 mpm_status run_graphed(mpm_ctx c, int dir, int t0, int n, F&& body, G&& after) {
   if (!graphs_ok(c, n)) return body();
-  for (auto& g : c->gcache)
-    if (g.dir == dir && g.t0 == t0 && g.n == n) {
+  for (size_t i = 0; i < c->gcache.size(); ++i)
+    if (c->gcache[i].dir == dir && c->gcache[i].t0 == t0 && c->gcache[i].n == n) {
+      std::rotate(c->gcache.begin() + i, c->gcache.begin() + i + 1, c->gcache.end());  // most recent last
+      const auto& g = c->gcache.back();
       c->launches += g.launches;
       c->scan_epoch += g.epochs;
       after();
@@ -797,15 +843,25 @@ mpm_status run_graphed(mpm_ctx c, int dir, int t0, int n, F&& body, G&& after) {
   mpm_status s = body();
   cudaGraph_t graph = nullptr;
   cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
-  if (s) {
-    if (graph) cudaGraphDestroy(graph);
-    return s;
-  }
-  if (e != cudaSuccess) return cuda_fail(c, e, "graph capture");
   cudaGraphExec_t exec = nullptr;
-  e = cudaGraphInstantiate(&exec, graph, 0);
-  cudaGraphDestroy(graph);
-  if (e != cudaSuccess) return cuda_fail(c, e, "graph instantiate");
+  if (!s && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (s || e != cudaSuccess) {
+    // body() advanced the host state (tape end, fused-grid step, adjoint buffers, counters)
+    // for launches that never ran: undo the counters and refuse further steps until
+    // mpm_set_state rebuilds a consistent context
+    cudaGetLastError();
+    c->launches = l0;
+    c->scan_epoch = e0;
+    c->poisoned = true;
+    return s ? s : cuda_fail(c, e, "graph capture / instantiate (context reset required: mpm_set_state)");
+  }
+  // bounded cache: keep the kGraphCache most recent (direction, start, length) executables
+  if (c->gcache.size() >= kGraphCache) {
+    cudaStreamSynchronize(c->stream);
+    cudaGraphExecDestroy(c->gcache.front().exec);
+    c->gcache.erase(c->gcache.begin());
+  }
   c->gcache.push_back({dir, t0, n, exec, c->launches - l0, c->scan_epoch - e0});
   CK(cudaGraphLaunch(exec, c->stream));
   return MPM_OK;
@@ -1138,13 +1194,17 @@ mpm_status group_backward(mpm_ctx* cs, int32_t n, const float* const* gx, const 
 extern "C" {
 
 mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
-  if (!cfg || !out) return MPM_ERR_INVALID_ARG;
+  g_create_error.clear();
+  if (!cfg || !out) {
+    g_create_error = "mpm_create: null config or output pointer";
+    return MPM_ERR_INVALID_ARG;
+  }
   *out = nullptr;
   mpm_ctx c = new mpm_ctx_s();
   c->cfg = *cfg;
   const mpm_config& k = *cfg;
   auto bad = [&](const char* why) {
-    c->last_error = why;
+    g_create_error = why;
     delete c;
     return MPM_ERR_INVALID_ARG;
   };
@@ -1165,7 +1225,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   if (nb * k.batch >= (1LL << 31) / kCPB) return bad("too many grid blocks (batch * (res/Bb)^dim)");
   cudaError_t e = cudaSetDevice(k.device);
   if (e != cudaSuccess) {
-    c->last_error = cudaGetErrorString(e);
+    g_create_error = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
     delete c;
     return MPM_ERR_CUDA;
   }
@@ -1288,7 +1348,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   AL(stage, NT * (2 * D + 2 * D * D + 2));
 #undef AL
   if (s) {
-    std::string why = c->last_error;
+    g_create_error = c->last_error;
     mpm_destroy(c);
     return s;
   }
@@ -1300,7 +1360,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   cudaMemset(c->info, 0, (TC + 1) * kInfo * sizeof(int));
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
-    c->last_error = cudaGetErrorString(e);
+    g_create_error = std::string("device initialisation: ") + cudaGetErrorString(e);
     mpm_destroy(c);
     return MPM_ERR_CUDA;
   }
@@ -1358,7 +1418,25 @@ mpm_status mpm_forward(mpm_ctx c, int32_t n) {
     mpm_status s = c->D == 3 ? bring_to_tape<3>(c, c->tape_len) : bring_to_tape<2>(c, c->tape_len);
     if (s) return s;
   }
-  return c->D == 3 ? do_forward<3>(c, n) : do_forward<2>(c, n);
+  const int t_end = c->tape_len + n;
+  for (;;) {
+    mpm_status s = c->D == 3 ? do_forward<3>(c, t_end - c->tape_len) : do_forward<2>(c, t_end - c->tape_len);
+    // automatic capacity (config.grid_slots = 0): a body that spread beyond the grid-slot arena
+    // sized at set_state.  Steps before the latched one are intact (the overflow is detected by
+    // the binning scan of the grid being built, before anything is written into it); grow the
+    // arena x2 keeping them, rewind to that step and carry on.  Not in slab mode with a
+    // communicator (the ranks would diverge) nor with checkpoints (the step may not be resident).
+    const bool growable = s == MPM_ERR_TAPE_FULL && c->cfg.grid_slots <= 0 && !c->comm && c->ck == 0 &&
+                          c->P.slots_per_step < c->P.NBT && c->latch_step >= c->seg0 && c->latch_step < t_end;
+    if (!growable) return s;
+    const int t_fail = c->latch_step;
+    s = alloc_arena(c, std::min<long>(c->P.NBT, 2L * c->P.slots_per_step), true);
+    if (s) return s;
+    c->poisoned = false;
+    c->tape_len = std::max(c->tape_len, t_fail);  // do_forward advanced nothing on failure
+    s = c->D == 3 ? do_rewind<3>(c, t_fail) : do_rewind<2>(c, t_fail);
+    if (s) return s;
+  }
 }
 
 int32_t mpm_tape_length(mpm_ctx c) { return c ? c->tape_len : -1; }
@@ -1403,7 +1481,10 @@ mpm_status mpm_grad(mpm_ctx c, float* dx0, float* dv0, float* dF0, float* dC0, f
   return c->D == 3 ? do_grad<3>(c, dx0, dv0, dF0, dC0, dE, dnu, da) : do_grad<2>(c, dx0, dv0, dF0, dC0, dE, dnu, da);
 }
 
-const char* mpm_last_error(mpm_ctx c) { return c ? c->last_error.c_str() : "null context"; }
+const char* mpm_last_error(mpm_ctx c) {
+  if (c) return c->last_error.c_str();
+  return g_create_error.empty() ? "null context" : g_create_error.c_str();
+}
 
 mpm_status mpm_get_binning(mpm_ctx c, int32_t t, float* x_store, int32_t* orig, int32_t* keyo, int32_t* perm,
                            int32_t* block_start) {

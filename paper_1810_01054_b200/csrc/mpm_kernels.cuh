@@ -1050,6 +1050,39 @@ __device__ __forceinline__ void cell_scan(const int* s_hist, int* s_cstart, int*
   }
 }
 
+// In-place ascending sort of a[0, m) (distinct ints) by the whole CTA: a bitonic network in the
+// mirrored form, where every compare-exchange puts the smaller key at the lower index, so the
+// virtual +inf padding up to the next power of two never moves and out-of-range partners are
+// simply skipped.  O(m log^2 m) work; contains barriers (call uniformly).
+__device__ __forceinline__ void cta_sort_ints(int* a, int m, int tid, int nthr) {
+  int P2 = 1;
+  while (P2 < m) P2 <<= 1;
+  auto cx = [&](int lo, int hi) {
+    if (hi < m) {
+      const int x = a[lo], y = a[hi];
+      if (y < x) { a[lo] = y; a[hi] = x; }
+    }
+  };
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int i = tid; i < P2 / 2; i += nthr) {  // mirrored merge step of the size-k blocks
+      const int h = k / 2, blk = i / h, off = i - blk * h;
+      cx(blk * k + off, blk * k + k - 1 - off);
+    }
+    __syncthreads();
+    for (int j = k / 4; j > 0; j >>= 1) {
+      for (int i = tid; i < P2 / 2; i += nthr) {
+        const int blk = i / j, off = i - blk * j;
+        cx(blk * 2 * j + off, blk * 2 * j + off + j);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// cells with more particles than this are ordered by cta_sort_ints instead of per-particle
+// ranks (O(count) each): a compressed pile-up stays O(n log^2 n) instead of O(n^2)
+constexpr int kRankMax = 32;
+
 // Forward in-block sort (P2G prologue): the block's particles, grouped by k_scatter in
 // (storage index, key) pairs, are sorted by (cell, storage index) (stable, R18) into
 // perm[s .. s+n); s_cstart gets the cells' ranges.  CTA-wide (contains barriers).
@@ -1104,9 +1137,16 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
     for (int step = kCPB / 2; step > 0; step >>= 1)
       if (s_cstart[c + step] <= i) c += step;
     const int lo = s_cstart[c], hi = s_cstart[c + 1];
+    if (hi - lo > kRankMax) continue;  // a crowded cell: sorted below
     int rank = 0;
     for (int q = lo; q < hi; ++q) rank += buf[q] < j;
     A.perm[s + lo + rank] = j;  // stable: ties by storage index (R18)
+  }
+  for (int c = 0; c < kCPB; ++c) {  // uniform: s_cstart is shared
+    const int lo = s_cstart[c], hi = s_cstart[c + 1];
+    if (hi - lo <= kRankMax) continue;
+    cta_sort_ints(buf + lo, hi - lo, tid, kThreads);  // storage indices ascending = stable order
+    for (int i = tid; i < hi - lo; i += kThreads) A.perm[s + lo + i] = buf[lo + i];
   }
   __syncthreads();
 }

@@ -112,15 +112,54 @@ def _ptr(a):
     raise TypeError(f"unsupported array type {type(a)}")
 
 
-def _in(a, dtype, shape):
+def _check_tensor(a, dtype, n, device, name):
+    """A torch tensor passed as a raw pointer: its element type, size, layout and device must
+    be what the ABI reads or writes (the library cannot see any of them)."""
+    import torch
+    want = {np.float32: torch.float32, np.int32: torch.int32}[dtype]
+    if a.dtype != want:
+        raise TypeError(f"{name}: dtype {a.dtype}, the ABI needs {want}")
+    if a.numel() != n:
+        raise ValueError(f"{name}: {a.numel()} elements, the ABI needs {n}")
+    if not a.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if a.device.type == "cuda" and device is not None and a.device.index != device:
+        raise ValueError(f"{name}: on cuda:{a.device.index}, the context is on cuda:{device}")
+    if a.device.type not in ("cpu", "cuda"):
+        raise ValueError(f"{name}: unsupported device {a.device}")
+
+
+def _in(a, dtype, shape, device=None, name="input"):
+    """An input array: numpy (converted to dtype, made contiguous) or a torch tensor (checked)."""
     if a is None:
         return None
+    n = int(np.prod(shape))
     if isinstance(a, np.ndarray):
         a = np.ascontiguousarray(a, dtype=dtype)
-        assert a.size == int(np.prod(shape)), (a.shape, shape)
+        if a.size != n:
+            raise ValueError(f"{name}: shape {a.shape}, the ABI needs {n} elements {tuple(shape)}")
         return a
-    assert a.is_contiguous() and a.numel() == int(np.prod(shape)), (tuple(a.shape), shape)
-    return a
+    if hasattr(a, "data_ptr"):
+        _check_tensor(a, dtype, n, device, name)
+        return a
+    raise TypeError(f"{name}: unsupported array type {type(a)}")
+
+
+def _out(a, dtype, shape, device=None, name="output"):
+    """An output buffer the library writes into: numpy (exact dtype, C-contiguous, writeable)
+    or a torch tensor (checked)."""
+    if a is None:
+        return None
+    n = int(np.prod(shape))
+    if isinstance(a, np.ndarray):
+        if a.dtype != dtype or not a.flags.c_contiguous or not a.flags.writeable or a.size != n:
+            raise ValueError(f"{name}: needs a writeable C-contiguous {np.dtype(dtype)} array of {n} elements, "
+                             f"got {a.dtype} {a.shape}")
+        return a
+    if hasattr(a, "data_ptr"):
+        _check_tensor(a, dtype, n, device, name)
+        return a
+    raise TypeError(f"{name}: unsupported array type {type(a)}")
 
 
 @dataclass
@@ -175,7 +214,7 @@ class MPM:
     def _check(self, rc, h=None):
         if rc != 0:
             hh = h if h is not None else self.h
-            msg = self.L.mpm_last_error(hh).decode() if hh and hh.value else "create failed"
+            msg = self.L.mpm_last_error(hh if hh and hh.value else None).decode()
             raise MPMError(rc, msg)
 
     def close(self):
@@ -196,12 +235,12 @@ class MPM:
     # -- the path -----------------------------------------------------------------------
     def set_state(self, x, v=None, F=None, C_=None, mass=None, vol=None, E=None, nu=None,
                   actuator_id=None):
-        d, NT = self.cfg.dim, self.NT
-        arrs = [_in(x, np.float32, (NT, d)), _in(v, np.float32, (NT, d)),
-                _in(F, np.float32, (NT, d, d)), _in(C_, np.float32, (NT, d, d)),
-                _in(mass, np.float32, (NT,)), _in(vol, np.float32, (NT,)),
-                _in(E, np.float32, (NT,)), _in(nu, np.float32, (NT,)),
-                _in(actuator_id, np.int32, (NT,))]
+        d, NT, dev = self.cfg.dim, self.NT, self.cfg.device
+        arrs = [_in(x, np.float32, (NT, d), dev, "x"), _in(v, np.float32, (NT, d), dev, "v"),
+                _in(F, np.float32, (NT, d, d), dev, "F"), _in(C_, np.float32, (NT, d, d), dev, "C"),
+                _in(mass, np.float32, (NT,), dev, "mass"), _in(vol, np.float32, (NT,), dev, "vol"),
+                _in(E, np.float32, (NT,), dev, "E"), _in(nu, np.float32, (NT,), dev, "nu"),
+                _in(actuator_id, np.int32, (NT,), dev, "actuator_id")]
         self._check(self.L.mpm_set_state(self.h, *[_ptr(a) for a in arrs]))
 
     def set_scene(self, sc):
@@ -214,7 +253,7 @@ class MPM:
 
     def set_actuation(self, a):
         cfg = self.cfg
-        a = _in(a, np.float32, (cfg.batch, cfg.max_steps, cfg.n_actuators, cfg.dim))
+        a = _in(a, np.float32, (cfg.batch, cfg.max_steps, cfg.n_actuators, cfg.dim), cfg.device, "actuation")
         self._check(self.L.mpm_set_actuation(self.h, _ptr(a)))
 
     def forward(self, n_steps: int):
@@ -232,13 +271,15 @@ class MPM:
         if out is None:
             out = (np.empty((NT, d), np.float32), np.empty((NT, d), np.float32),
                    np.empty((NT, d, d), np.float32), np.empty((NT, d, d), np.float32))
+        shapes = ((NT, d), (NT, d), (NT, d, d), (NT, d, d))
+        out = tuple(_out(a, np.float32, sh, self.cfg.device, nm) for a, sh, nm in zip(out, shapes, "xvFC"))
         self._check(self.L.mpm_get_state(self.h, int(t), *[_ptr(a) for a in out]))
         return out
 
     def backward(self, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
-        d, NT = self.cfg.dim, self.NT
-        arrs = [_in(dLdx, np.float32, (NT, d)), _in(dLdv, np.float32, (NT, d)),
-                _in(dLdF, np.float32, (NT, d, d)), _in(dLdC, np.float32, (NT, d, d))]
+        d, NT, dev = self.cfg.dim, self.NT, self.cfg.device
+        arrs = [_in(dLdx, np.float32, (NT, d), dev, "dLdx"), _in(dLdv, np.float32, (NT, d), dev, "dLdv"),
+                _in(dLdF, np.float32, (NT, d, d), dev, "dLdF"), _in(dLdC, np.float32, (NT, d, d), dev, "dLdC")]
         self._check(self.L.mpm_backward(self.h, *[_ptr(a) for a in arrs]))
 
     def grad(self, out=None):
@@ -250,7 +291,13 @@ class MPM:
                        dE=np.empty(NT, np.float32), dnu=np.empty(NT, np.float32),
                        da=np.empty((cfg.batch, cfg.max_steps, max(cfg.n_actuators, 0), d), np.float32))
         keys = ("dx0", "dv0", "dF0", "dC0", "dE", "dnu", "da")
-        self._check(self.L.mpm_grad(self.h, *[_ptr(out.get(k)) for k in keys]))
+        shapes = dict(dx0=(NT, d), dv0=(NT, d), dF0=(NT, d, d), dC0=(NT, d, d), dE=(NT,), dnu=(NT,),
+                      da=(cfg.batch, cfg.max_steps, max(cfg.n_actuators, 0), d))
+        unknown = set(out) - set(keys)
+        if unknown:
+            raise KeyError(f"grad(out=): unknown keys {sorted(unknown)}")
+        ptrs = [_ptr(_out(out.get(k), np.float32, shapes[k], cfg.device, k)) for k in keys]
+        self._check(self.L.mpm_grad(self.h, *ptrs))
         return out
 
     def enable_mass_grad(self, on: bool = True):
@@ -260,14 +307,15 @@ class MPM:
         """dL/dm_p (NEXT N3) from the last backward, user order [B*N]."""
         if out is None:
             out = np.empty(self.NT, np.float32)
+        out = _out(out, np.float32, (self.NT,), self.cfg.device, "dmass")
         self._check(self.L.mpm_grad_mass(self.h, _ptr(out)))
         return out
 
     def add_seed(self, t, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
         """Additive seed dL/dstate_t for a running loss (NEXT N4)."""
-        d, NT = self.cfg.dim, self.NT
-        arrs = [_in(dLdx, np.float32, (NT, d)), _in(dLdv, np.float32, (NT, d)),
-                _in(dLdF, np.float32, (NT, d, d)), _in(dLdC, np.float32, (NT, d, d))]
+        d, NT, dev = self.cfg.dim, self.NT, self.cfg.device
+        arrs = [_in(dLdx, np.float32, (NT, d), dev, "dLdx"), _in(dLdv, np.float32, (NT, d), dev, "dLdv"),
+                _in(dLdF, np.float32, (NT, d, d), dev, "dLdF"), _in(dLdC, np.float32, (NT, d, d), dev, "dLdC")]
         self._check(self.L.mpm_add_seed(self.h, int(t), *[_ptr(a) for a in arrs]))
 
     def clear_seeds(self):
@@ -284,8 +332,9 @@ class MPM:
             self._check(self.L.mpm_set_controller(self.h, None, None, None))
             return
         KD = self.cfg.n_actuators * self.cfg.dim
-        arrs = [_in(W, np.float32, (KD, self.n_obs)), _in(b, np.float32, (KD,)),
-                _in(target, np.float32, (self.cfg.dim,))]
+        dev = self.cfg.device
+        arrs = [_in(W, np.float32, (KD, self.n_obs), dev, "W"), _in(b, np.float32, (KD,), dev, "b"),
+                _in(target, np.float32, (self.cfg.dim,), dev, "target")]
         self._check(self.L.mpm_set_controller(self.h, *[_ptr(a) for a in arrs]))
 
     def grad_controller(self):
@@ -397,7 +446,7 @@ def group_backward(sims, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
             return None
         ptrs = []
         for s, a in zip(sims, seeds):
-            a = _in(a, np.float32, shape_of(s))
+            a = _in(a, np.float32, shape_of(s), s.cfg.device, "seed")
             keep.append(a)
             ptrs.append(_ptr(a))
         return (C.c_void_p * len(sims))(*ptrs)

@@ -39,6 +39,9 @@ def test_config_validation_is_host_side(bad):
     with pytest.raises(mpm.MPMError) as e:
         mpm.MPM(cfg)
     assert e.value.status == "MPM_ERR_INVALID_ARG"
+    # the reason survives the failed create (mpm_last_error(NULL), thread-local)
+    msg = str(e.value)
+    assert "create failed" not in msg and "null context" not in msg and len(msg) > 30, msg
 
 
 def test_no_cpu_fallback(monkeypatch, tmp_path):
@@ -57,3 +60,34 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "mpm_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_binding_checks_dtype_size_layout_and_device():
+    """The binding passes raw pointers, so it must reject what the ABI would misread: a torch
+    tensor of the wrong dtype (an int64 actuator id read as int32, an fp64 x read as fp32), the
+    wrong size, a non-contiguous view, a tensor on another GPU; and output buffers that numpy
+    would have to convert (the library would write into a temporary)."""
+    import numpy as np
+    import torch
+    from paper_1810_01054_b200.mpm import _in, _out
+    assert _in(np.zeros((3, 2), np.float64), np.float32, (3, 2)).dtype == np.float32  # numpy: converted
+    with pytest.raises(TypeError):
+        _in(torch.zeros(6, dtype=torch.float64), np.float32, (3, 2))
+    with pytest.raises(TypeError):
+        _in(torch.zeros(3, dtype=torch.int64), np.int32, (3,))
+    with pytest.raises(ValueError):
+        _in(torch.zeros(5, dtype=torch.float32), np.float32, (3, 2))
+    with pytest.raises(ValueError):
+        _in(torch.zeros(6, 2, dtype=torch.float32)[:, 0], np.float32, (6,))
+    with pytest.raises(ValueError):
+        _in(np.zeros(4, np.float32), np.float32, (3,))
+    assert _in(torch.zeros(6, dtype=torch.float32), np.float32, (3, 2)) is not None
+    with pytest.raises(ValueError):
+        _out(np.zeros((3, 2), np.float64), np.float32, (3, 2))
+    with pytest.raises(ValueError):
+        _out(np.zeros((2, 3), np.float32).T, np.float32, (3, 2))
+    with pytest.raises(TypeError):
+        _out(torch.zeros(6, dtype=torch.float64), np.float32, (3, 2))
+    assert _out(np.zeros((3, 2), np.float32), np.float32, (3, 2)) is not None
+    with pytest.raises(TypeError):
+        _in([1.0, 2.0], np.float32, (2,))

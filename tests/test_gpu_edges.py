@@ -182,3 +182,93 @@ def test_zero_step_trajectory(d, fuse):
         np.testing.assert_array_equal(g[k], s)
     assert not np.any(g["dE"]) and not np.any(g["dnu"]) and not np.any(g["da"])
 
+
+
+@pytest.mark.parametrize("fuse", [0, 1])
+def test_spreading_body_grows_the_grid_arena(fuse):
+    """A cloud that spreads during the rollout to many times the grid blocks it touched at
+    set_state (automatic grid_slots): 64 particles on a 3-cell lattice (their stencils never
+    overlap, so each flies ballistically) moving radially apart.  The arena is grown x2 (keeping
+    the steps already on the tape) and the forward resumes from the step that overflowed: state
+    and gradients as the oracle's, no MPM_ERR_TAPE_FULL."""
+    d, T, res = 3, 40, 64
+    off = np.array([-4.5, -1.5, 1.5, 4.5])
+    lat = np.stack(np.meshgrid(off, off, off, indexing="ij"), -1).reshape(-1, d)  # cells from the centre
+    x = ((32.0 + lat) / res).astype(np.float32)
+    dt = 1e-3
+    v = (lat * (0.5 / 4.5) / res / dt).astype(np.float32)  # outermost: 0.5 cells per step
+    sc = _scene_from(scenes.tiny(d, seed=80, res=res, steps=T, K=0, gravity=(0.0, 0.0, 0.0)), x, v)
+    sc.dt = dt
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, fuse_g2p2g=fuse))
+    sim.set_scene(sc)
+    sim.forward(T)
+    touched = [sim.step_info(t)[1] for t in range(T)]
+    assert touched[-1] > 2 * touched[0] + 128, touched  # beyond the capacity sized at set_state
+    _check_against_oracle(sim, sc, T)
+
+
+def test_set_state_with_a_wider_body_resizes_the_arena():
+    """The same particle count re-set over a much wider region (many more touched blocks than
+    the first set_state sized the arena for): the arena is re-sized at set_state."""
+    d, T = 3, 4
+    sc = scenes.tiny(d, seed=82, res=64, n_cells=(3, 3, 3), steps=T, K=0)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T))
+    sim.set_scene(sc)
+    sim.forward(T)
+    rng = np.random.default_rng(83)
+    x = (rng.uniform(4.0, 58.0, sc.x[0].shape) / 64).astype(np.float32)  # the same 216 particles, scattered
+    wide = _scene_from(sc, x)
+    sim.set_scene(wide)
+    sim.forward(T)
+    assert sim.step_info(0)[1] > 4 * 27
+    _check_against_oracle(sim, wide, T)
+
+
+def _check_against_oracle(sim, sc, T):
+    cfg = oracle_cfg(sc)
+    m, vol, E, nu, aid, act = oracle_params(sc)
+    traj = oracle.forward(cfg, oracle_state(sc), m, vol, E, nu, aid, act[:T], T)
+    x, v, F, Cm = sim.get_state(T)
+    ox, ov, oC, oF = oracle.unpack(traj[T], sc.dim)
+    vmax = max(np.abs(ov).max(), 1e-6)
+    for k, a, b, scale in (("x", x, ox, 1.0), ("v", v, ov, vmax), ("F", F, oF, np.abs(oF).max()),
+                           ("C", Cm, oC, 4 * sc.res * vmax)):
+        assert np.abs(a - b).max() / scale < 1e-4, k
+    w = np.random.default_rng(84).standard_normal(traj[T].shape)
+    wx, wv, wC, wF = oracle.unpack(w, sc.dim)
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)
+    sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
+    g = sim.grad()
+    g0, gE, gnu, ga = oracle.backward(cfg, traj, m, vol, E, nu, aid, act[:T], w)
+    gx, gv, gC, gF = oracle.unpack(g0, sc.dim)
+    assert_grads([("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF), ("dC0", g["dC0"], gC),
+                  ("dE", g["dE"], gE)])
+
+
+def test_crowded_cell_binning_is_bit_exact_and_fast():
+    """A compressed pile-up: 20,000 particles in one grid cell (a block far beyond the in-smem
+    sort capacity) next to an ordinary body: the in-cell order falls back from per-particle ranks
+    (O(count^2) per cell) to a CTA sort; binning bit-exact with the oracle at every step, and
+    the step stays fast."""
+    import time
+    d, T = 3, 3
+    rng = np.random.default_rng(85)
+    body = scenes.tiny(d, seed=86, res=32, n_cells=(6, 6, 6), steps=T, K=0)
+    pile = ((np.array([20.0, 20.0, 20.0]) + 0.6 + 0.3 * rng.random((20000, 3))) / 32).astype(np.float32)
+    x = np.concatenate([body.x[0], pile]).astype(np.float32)
+    v = np.zeros_like(x)
+    sc = _scene_from(body, x, v)
+    sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, fuse_g2p2g=1))
+    sim.set_scene(sc)
+    sim.forward(1)  # warm-up (module load, arena)
+    sim.rewind(0)
+    t0 = time.perf_counter()
+    sim.forward(T)
+    elapsed = time.perf_counter() - t0
+    for t in range(T):
+        xs, orig, key, perm, bs = sim.get_binning(t)
+        okey, operm, obs = oracle.bin_particles(d, sc.res, xs.reshape(1, -1, d))
+        np.testing.assert_array_equal(key, okey)
+        np.testing.assert_array_equal(perm, operm)
+        np.testing.assert_array_equal(bs, obs)
+    assert elapsed < 0.5, elapsed  # O(n^2) ranks on the 20,000-particle cell took seconds
