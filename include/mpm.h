@@ -39,6 +39,7 @@
 #ifndef MPM_H
 #define MPM_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -58,8 +59,11 @@ typedef enum {
   MPM_ERR_CALL_ORDER = 7,    /* e.g. backward before forward, grad before backward   */
   MPM_ERR_COMM = 8,          /* NCCL failure (slab mode)                             */
   MPM_ERR_OUT_OF_SLAB = 9,   /* particle left its slab's halo (slab mode, see below) */
-  MPM_ERR_CFL = 10           /* fuse_g2p2g: a particle moved too far in one step for the
+  MPM_ERR_CFL = 10,          /* fuse_g2p2g: a particle moved too far in one step for the
                                 dilated grid of the next step (needs |v| dt < dx)          */
+  MPM_ERR_MIGRATE = 11       /* migrating slab mode: more leavers per side and step than
+                                mig_cap, more particles than the storage capacity, or a
+                                particle that crossed a whole slab in one step              */
 } mpm_status;
 
 typedef struct {
@@ -76,7 +80,11 @@ typedef struct {
   float act_strength;   /* s in sigma_pa = s * Diag(a[t][k])  (R4)                    */
   int32_t device;       /* CUDA device ordinal                                        */
   void* stream;         /* cudaStream_t or NULL                                       */
-  int32_t grid_slots;   /* grid-block slots per step in the tape arena; 0 = automatic */
+  int32_t grid_slots;   /* grid-block slots per step in the tape arena; 0 = automatic: sized at
+                           every mpm_set_state (twice the touched blocks of the state) and
+                           doubled by mpm_forward when a spreading body overflows it (the steps
+                           on the tape are kept and the forward resumes from the overflowing
+                           step); with grid_slots > 0 an overflow is MPM_ERR_TAPE_FULL         */
   int32_t checkpoint_every; /* NEXT N2: 0 = the memo keeps every step (max_steps of tape);
                            k > 0 = the tape keeps one k-step segment and full states every
                            k steps (max_steps/k + 1 checkpoints); mpm_backward recomputes
@@ -201,6 +209,49 @@ mpm_status mpm_grad_controller(mpm_ctx ctx, float* dW, float* db, float* dtarget
  *   used by the parity tests; no kernel waits on another.  Seeds: arrays of n pointers
  *   (user order of each context) or NULL.                                                 */
 mpm_status mpm_set_slab(mpm_ctx ctx, int32_t x_lo, int32_t x_hi, int32_t halo_blocks);
+
+/* ---- migrating slab mode ("halo exchange of ghost grid nodes and migrating
+ * particles") ----
+ * As mpm_set_slab, but ownership is Eulerian: at EVERY step a particle belongs to the slab
+ * whose [x_lo, x_hi) holds its base_x (the first slab also takes base_x < x_lo, the last
+ * base_x >= x_hi), so a body may travel across any number of slab boundaries (no drift bound).
+ * After the G2P of each step the particles whose base_x left the slab are packed (state + user
+ * index) and exchanged with the x-neighbour (one grouped exchange per step; fixed-size buffers
+ * of mig_cap records per side), and the arrivals are appended to the next state.  The window
+ * sums of mpm_set_slab stay.  The send / receive buffers of every step stay on the tape: the
+ * backward returns the adjoint of every arrival to the rank it came from and fills the slots of
+ * the particles that left with the adjoints coming back (reverse migration), so each rank's
+ * reverse pass sees exactly the particles it simulated at that step.
+ *   - config.n_particles is this context's STORAGE capacity (live particles at any step;
+ *     MPM_ERR_MIGRATE beyond it); n_global is the whole body's particle count: every array in
+ *     user order (mpm_set_state, mpm_get_state, seeds, mpm_grad, mpm_grad_mass) spans the whole
+ *     body, [n_global] leading.  mpm_set_state keeps the particles the slab owns at t = 0.
+ *     mpm_get_state(t) and mpm_grad's dx0, dv0, dF0, dC0 write this slab's particles (owned at
+ *     t, resp. at 0) and zeros elsewhere: the sum over the slabs is the whole body.  dE, dnu,
+ *     dmass and da are the whole-body gradients on every slab (summed over the slabs by the
+ *     backward: NCCL all-reduce, or in-process for mpm_group_backward).
+ *   - mig_cap: records per side and step (0 = max(1024, capacity / 64)).
+ *   - batch 1; checkpoint_every 0; no controller; no CUDA graphs; fuse_g2p2g is ignored.
+ *   - mpm_group_forward / mpm_group_backward drive adjacent migrating contexts of one process
+ *     (the same kernels, device copies in place of the exchanges).                           */
+mpm_status mpm_set_slab_migrating(mpm_ctx ctx, int32_t x_lo, int32_t x_hi, int32_t halo_blocks,
+                                  int32_t n_global, int32_t mig_cap);
+
+/* Host-staged transport for the slab exchanges (an alternative to mpm_comm_init's NCCL, e.g.
+ * gloo through torch.distributed for multi-process tests where the ranks share a GPU or have
+ * none for NCCL): at every exchange the library synchronises its stream, copies the send
+ * buffers to pinned host memory and calls fn(user, kind, send_left, send_right, recv_left,
+ * recv_right, bytes) with host pointers (NULL on a side without a neighbour); fn must send
+ * send_left to the left neighbour's recv_right (and send_right to the right neighbour's
+ * recv_left), fill recv_left / recv_right, and return 0.  kind: MPM_XCHG_WINDOW (grid windows),
+ * MPM_XCHG_MIGRATE (migrant records), MPM_XCHG_MIGRATE_ADJ (their adjoints, backward),
+ * MPM_XCHG_REDUCE (fn must overwrite send_left with the elementwise sum over all ranks; the
+ * right pointers are NULL: the da / dmu / dlam / dmass sums of the backward).  With a transport
+ * set, forward/backward/get_state are collective over the ranks as with NCCL.  fn = NULL unsets. */
+enum { MPM_XCHG_WINDOW = 0, MPM_XCHG_MIGRATE = 1, MPM_XCHG_MIGRATE_ADJ = 2, MPM_XCHG_REDUCE = 3 };
+typedef int (*mpm_transport_fn)(void* user, int32_t kind, const float* send_left, const float* send_right,
+                                float* recv_left, float* recv_right, size_t bytes);
+mpm_status mpm_set_transport(mpm_ctx ctx, mpm_transport_fn fn, void* user);
 mpm_status mpm_comm_unique_id(char out[128]);
 mpm_status mpm_comm_init(mpm_ctx ctx, int32_t rank, int32_t world, const char id[128]);
 mpm_status mpm_group_forward(mpm_ctx* ctxs, int32_t n_ctx, int32_t n_steps);

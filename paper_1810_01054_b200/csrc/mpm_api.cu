@@ -22,11 +22,11 @@ namespace {
 
 enum KernelId {
   KI_SCAN, KI_SCATTER, KI_P2G, KI_G2P, KI_ZERO, KI_G2PT, KI_GRIDT, KI_P2GT, KI_MISC,
-  KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_FUSE, KI_COUNT
+  KI_BANDP, KI_BANDU, KI_CTRL, KI_CTRLT, KI_FUSE, KI_MIG, KI_COUNT
 };
 const char* kKernelNames[KI_COUNT] = {"scan",  "scatter", "p2g",       "g2p",         "zero_adj", "g2p_T", "grid_T",
                                       "p2g_T", "misc",    "band_pack", "band_unpack", "ctrl",     "ctrl_T",
-                                      "g2p2g"};
+                                      "g2p2g", "migrate"};
 
 struct PendingEvent {
   cudaEvent_t a, b;
@@ -86,6 +86,8 @@ struct mpm_ctx_s {
   int res_end = 0;  // the states of steps [seg0, res_end] on the tape are valid
   int fused_grid = -1;  // fused forward: the step whose grid the previous G2P2G already built
   int occ_fuse = 2;
+  int occ_frt = 2;      // fused reverse kernel k_p2g2p_adj
+  bool bfuse = false;   // fused reverse step (MPM_FUSE_BWD=1 enables; follows config.fuse_g2p2g)
   float* ck_state = nullptr;
   int* ck_orig = nullptr;
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
@@ -139,6 +141,20 @@ struct mpm_ctx_s {
   float4 *send_lo = nullptr, *send_hi = nullptr, *recv_lo = nullptr, *recv_hi = nullptr;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  // migrating slab mode (mpm_set_slab_migrating): ownership by base_x at every step; user arrays
+  // span the whole body (NU particles), storage holds up to P.NT (the capacity)
+  bool mig = false;
+  size_t NU = 0;                 // user-array length (= P.NT outside migrating mode)
+  size_t mig_floats = 0;         // floats per migrant buffer (header + mig_cap records)
+  float* mig_send_tape = nullptr;  // [tape_cap][2][mig_floats]: leavers of step t (kept for the backward)
+  float* mig_recv_tape = nullptr;  // [tape_cap][2][mig_floats]: arrivals of step t
+  float *rev_send[2] = {nullptr, nullptr}, *rev_recv[2] = {nullptr, nullptr};  // [mig_cap][S] adjoints
+  int* members = nullptr;        // set_state: this slab's user indices (storage order 0)
+  // host-staged transport (mpm_set_transport): the exchanges go through a caller callback
+  mpm_transport_fn transport = nullptr;
+  void* transport_user = nullptr;
+  float* host_stage = nullptr;   // pinned: send_l | send_r | recv_l | recv_r
+  size_t host_stage_floats = 0;
   // NEXT N1 controller: a_t = tanh(W z_t + b)
   bool ctrl = false, ctrl_grad_valid = false;
   float *ctrl_W = nullptr, *ctrl_b = nullptr, *ctrl_target = nullptr, *ctrl_Minv = nullptr, *ctrl_acc = nullptr;
@@ -281,6 +297,12 @@ int* slot_at(mpm_ctx c, int t) { return c->tape_slot + ti(c, t) * c->P.NBT; }
 int* occ_at(mpm_ctx c, int t) { return c->tape_occ + ti(c, t) * c->P.NBT; }
 int* touch_at(mpm_ctx c, int t) { return c->tape_touch + ti(c, t) * c->P.NBT; }
 int* info_at(mpm_ctx c, int t) { return c->info + ti(c, t) * kInfo; }
+// migrating slab mode: buffers of step t
+float* mig_send_at(mpm_ctx c, int t, int side) { return c->mig_send_tape + ((size_t)ti(c, t) * 2 + side) * c->mig_floats; }
+float* mig_recv_at(mpm_ctx c, int t, int side) { return c->mig_recv_tape + ((size_t)ti(c, t) * 2 + side) * c->mig_floats; }
+const int* nslot_at(mpm_ctx c, int t) { return c->mig ? info_at(c, t) + I_NSLOT : nullptr; }
+size_t rev_floats(mpm_ctx c) { return (size_t)c->P.mig_cap * c->S; }
+
 bool on_tape(mpm_ctx c, int t) { return t >= c->seg0 && t <= c->res_end && t <= c->tape_len; }
 float* ck_state_of(mpm_ctx c, int i) { return c->ck_state + (size_t)i * c->S * NTs(c); }
 int* ck_orig_of(mpm_ctx c, int i) { return c->ck_orig + (size_t)i * NTs(c); }
@@ -323,6 +345,13 @@ mpm_status check_latch(mpm_ctx c) {
     c->poisoned = true;
     return fail(c, MPM_ERR_OUT_OF_SLAB, buf);
   }
+  if (h.code == E_MIGRATE) {
+    snprintf(buf, sizeof buf, "migrating slab mode at step %d: more leavers per side than mig_cap (%d), more "
+             "particles than the storage capacity, or a particle that crossed a whole slab (%d)", h.step,
+             c->P.mig_cap, h.particle);
+    c->poisoned = true;
+    return fail(c, MPM_ERR_MIGRATE, buf);
+  }
   snprintf(buf, sizeof buf, "device error code %d", h.code);
   return fail(c, MPM_ERR_CUDA, buf);
 }
@@ -338,9 +367,12 @@ mpm_status sync_and_check(mpm_ctx c, const char* where) {
 template <int D>
 void launch_keys(mpm_ctx c, int t) {
   const KParams& P = c->P;
+  // storage order 0 = user order (identity orig) outside migrating mode; there set_state wrote
+  // the members' user indices
+  int* orig0 = (t == 0 && !c->mig) ? orig_at(c, 0) : nullptr;
   launch(c, KI_MISC, [&] {
-    k_init_keys<D><<<grid1d(P.NT), 256, 0, c->stream>>>(P, state_at(c, t), c->key, c->cnt,
-                                                         t == 0 ? orig_at(c, 0) : c->scratch, c->err);
+    k_init_keys<D><<<grid1d(P.NT), 256, 0, c->stream>>>(P, state_at(c, t), c->key, c->cnt, orig0, c->err,
+                                                         nslot_at(c, t));
   });
 }
 
@@ -396,7 +428,7 @@ void launch_scatter(mpm_ctx c, int t, const int* za, const int* zb) {
   const KParams& P = c->P;
   launch(c, KI_SCATTER, [&] {
     kx(c, k_scatter, dim3(std::max(1, std::min(grid1d(P.NT), c->n_sm * 8))), dim3(256), 0, P.NT, c->key, bs_at(c, t),
-       c->cnt, c->tmp_pk, za, zb, c->arena);
+       c->cnt, c->tmp_pk, za, zb, c->arena, nslot_at(c, t));
   });
 }
 
@@ -433,20 +465,76 @@ void launch_band_unpack(mpm_ctx c, int t, bool adj, float4* g) {
 }
 size_t band_floats(mpm_ctx c) { return (size_t)c->band_blocks * kCPB * 4; }
 
-// NCCL transport: grouped send/recv with the x-neighbours (ranks ordered by slab)
-mpm_status exchange_nccl(mpm_ctx c) {
-  const size_t n = band_floats(c);
+// Exchange with the x-neighbours (ranks ordered by slab): send_l -> left, send_r -> right,
+// recv_l <- left, recv_r <- right, n floats each (sides without a neighbour are skipped).
+// NCCL: grouped send/recv on the library stream.  With a transport callback (mpm_set_transport):
+// the stream is synchronised, the send buffers staged in pinned host memory, the callback does
+// the exchange, and the receive buffers are copied back -- no kernel waits on another rank.
+mpm_status exchange_pair(mpm_ctx c, int kind, const float* send_l, const float* send_r, float* recv_l, float* recv_r,
+                         size_t n) {
+  if (c->transport) {
+    if (c->host_stage_floats < 4 * n) {
+      if (c->host_stage) cudaFreeHost(c->host_stage);
+      c->host_stage = nullptr;
+      c->host_stage_floats = 0;
+      CK(cudaMallocHost(&c->host_stage, 4 * n * sizeof(float)));
+      c->host_stage_floats = 4 * n;
+    }
+    float* h = c->host_stage;
+    if (c->left) CK(cudaMemcpyAsync(h, send_l, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    if (c->right) CK(cudaMemcpyAsync(h + n, send_r, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int rc = c->transport(c->transport_user, kind, c->left ? h : nullptr, c->right ? h + n : nullptr,
+                                c->left ? h + 2 * n : nullptr, c->right ? h + 3 * n : nullptr, n * sizeof(float));
+    if (rc != 0) return fail(c, MPM_ERR_COMM, "transport callback failed (" + std::to_string(rc) + ")");
+    if (c->left) CK(cudaMemcpyAsync(recv_l, h + 2 * n, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    if (c->right) CK(cudaMemcpyAsync(recv_r, h + 3 * n, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    return MPM_OK;
+  }
   const NcclApi* N = nccl_api();  // non-null: the communicator exists
   ncclResult_t r = N->GroupStart();
-  if (r == ncclSuccess && c->left) r = N->Send(c->send_lo, n, ncclFloat, c->rank - 1, c->comm, c->stream);
-  if (r == ncclSuccess && c->left) r = N->Recv(c->recv_lo, n, ncclFloat, c->rank - 1, c->comm, c->stream);
-  if (r == ncclSuccess && c->right) r = N->Send(c->send_hi, n, ncclFloat, c->rank + 1, c->comm, c->stream);
-  if (r == ncclSuccess && c->right) r = N->Recv(c->recv_hi, n, ncclFloat, c->rank + 1, c->comm, c->stream);
+  if (r == ncclSuccess && c->left) r = N->Send(send_l, n, ncclFloat, c->rank - 1, c->comm, c->stream);
+  if (r == ncclSuccess && c->left) r = N->Recv(recv_l, n, ncclFloat, c->rank - 1, c->comm, c->stream);
+  if (r == ncclSuccess && c->right) r = N->Send(send_r, n, ncclFloat, c->rank + 1, c->comm, c->stream);
+  if (r == ncclSuccess && c->right) r = N->Recv(recv_r, n, ncclFloat, c->rank + 1, c->comm, c->stream);
   ncclResult_t r2 = N->GroupEnd();
   if (r == ncclSuccess) r = r2;
-  if (r != ncclSuccess) return fail(c, MPM_ERR_COMM, std::string("halo exchange: ") + N->GetErrorString(r));
+  if (r != ncclSuccess) return fail(c, MPM_ERR_COMM, std::string("slab exchange: ") + N->GetErrorString(r));
   return MPM_OK;
 }
+
+// the grid windows (forward after P2G, backward after G2P^T)
+mpm_status exchange_nccl(mpm_ctx c) {
+  return exchange_pair(c, MPM_XCHG_WINDOW, (const float*)c->send_lo, (const float*)c->send_hi, (float*)c->recv_lo,
+                       (float*)c->recv_hi, band_floats(c));
+}
+
+// in-place sum over the slab ranks of n floats (NCCL all-reduce, or the transport's REDUCE)
+mpm_status allreduce_sum(mpm_ctx c, float* d, size_t n) {
+  if (n == 0) return MPM_OK;
+  if (c->transport) {
+    if (c->host_stage_floats < n) {
+      if (c->host_stage) cudaFreeHost(c->host_stage);
+      c->host_stage = nullptr;
+      c->host_stage_floats = 0;
+      CK(cudaMallocHost(&c->host_stage, n * sizeof(float)));
+      c->host_stage_floats = n;
+    }
+    CK(cudaMemcpyAsync(c->host_stage, d, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const int rc = c->transport(c->transport_user, MPM_XCHG_REDUCE, c->host_stage, nullptr, nullptr, nullptr,
+                                n * sizeof(float));
+    if (rc != 0) return fail(c, MPM_ERR_COMM, "transport callback failed (" + std::to_string(rc) + ")");
+    CK(cudaMemcpyAsync(d, c->host_stage, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    return MPM_OK;
+  }
+  const NcclApi* N = nccl_api();
+  ncclResult_t r = N->AllReduce(d, d, n, ncclFloat, ncclSum, c->comm, c->stream);
+  if (r != ncclSuccess) return fail(c, MPM_ERR_COMM, std::string("all-reduce: ") + N->GetErrorString(r));
+  return MPM_OK;
+}
+
+bool has_xchg(mpm_ctx c) { return c->comm != nullptr || c->transport != nullptr; }
 
 // in-process transport (mpm_group_*): contexts in slab order on one stream
 mpm_status exchange_local(mpm_ctx* cs, int n) {
@@ -456,6 +544,30 @@ mpm_status exchange_local(mpm_ctx* cs, int n) {
     const size_t bytes = band_floats(a) * sizeof(float);
     CK(cudaMemcpyAsync(b->recv_lo, a->send_hi, bytes, cudaMemcpyDeviceToDevice, a->stream));
     CK(cudaMemcpyAsync(a->recv_hi, b->send_lo, bytes, cudaMemcpyDeviceToDevice, a->stream));
+  }
+  return MPM_OK;
+}
+
+// migrating slab mode, in process: the migrant records of step t (forward) ...
+mpm_status exchange_local_mig(mpm_ctx* cs, int n, int t) {
+  for (int i = 0; i + 1 < n; ++i) {
+    mpm_ctx a = cs[i], b = cs[i + 1];
+    mpm_ctx c = a;
+    const size_t bytes = a->mig_floats * sizeof(float);
+    CK(cudaMemcpyAsync(mig_recv_at(b, t, 0), mig_send_at(a, t, 1), bytes, cudaMemcpyDeviceToDevice, a->stream));
+    CK(cudaMemcpyAsync(mig_recv_at(a, t, 1), mig_send_at(b, t, 0), bytes, cudaMemcpyDeviceToDevice, a->stream));
+  }
+  return MPM_OK;
+}
+
+// ... and the adjoints of the arrivals going back (backward)
+mpm_status exchange_local_rev(mpm_ctx* cs, int n) {
+  for (int i = 0; i + 1 < n; ++i) {
+    mpm_ctx a = cs[i], b = cs[i + 1];
+    mpm_ctx c = a;
+    const size_t bytes = rev_floats(a) * sizeof(float);
+    CK(cudaMemcpyAsync(b->rev_recv[0], a->rev_send[1], bytes, cudaMemcpyDeviceToDevice, a->stream));
+    CK(cudaMemcpyAsync(a->rev_recv[1], b->rev_send[0], bytes, cudaMemcpyDeviceToDevice, a->stream));
   }
   return MPM_OK;
 }
@@ -507,6 +619,42 @@ void forward_phase_b(mpm_ctx c, int t) {
     if (c->split) kx(c, k_g2p<D, true>, dim3(ng), dim3(kThreads), 0, P, A);  // small problems: blocks split
     else kx(c, k_g2p<D>, dim3(ng), dim3(kThreads), 0, P, A);
   });
+  if (c->mig) {  // migrating slab mode: the particles of state t+1 that left the slab
+    for (int side = 0; side < 2; ++side) cudaMemsetAsync(mig_send_at(c, t, side), 0, Mig<D>::HDR * sizeof(float), c->stream);
+    launch(c, KI_MIG, [&] {
+      kx(c, k_mig_leavers<D>, dim3(c->n_sm * 4), dim3(256), 0, P, (const int*)bs_at(c, t), (const float*)state_at(c, t + 1),
+         (const int*)orig_at(c, t + 1), c->key, c->cnt, mig_send_at(c, t, 0), mig_send_at(c, t, 1), c->err, t);
+    });
+  }
+}
+
+// migrating slab mode, after the migrant exchange of step t: append the arrivals to state t+1
+template <int D>
+void forward_phase_c(mpm_ctx c, int t) {
+  const KParams& P = c->P;
+  launch(c, KI_MIG, [&] {
+    kx(c, k_mig_append<D>, dim3(c->n_sm), dim3(256), 0, P, c->left ? (const float*)mig_recv_at(c, t, 0) : nullptr,
+       c->right ? (const float*)mig_recv_at(c, t, 1) : nullptr, (const int*)bs_at(c, t), state_at(c, t + 1),
+       orig_at(c, t + 1), c->key, c->cnt, info_at(c, t + 1), c->err, t);
+  });
+}
+
+// migrating slab mode, before G2P^T of step t: arrivals' adjoints out, leavers' adjoints in
+template <int D>
+void backward_mig_pack(mpm_ctx c, int t) {
+  launch(c, KI_MIG, [&] {
+    kx(c, k_mig_rev_pack<D>, dim3(c->n_sm), dim3(256), 0, c->P, c->left ? (const float*)mig_recv_at(c, t, 0) : nullptr,
+       c->right ? (const float*)mig_recv_at(c, t, 1) : nullptr, (const int*)bs_at(c, t), (const float*)c->bcur,
+       c->rev_send[0], c->rev_send[1]);
+  });
+}
+template <int D>
+void backward_mig_unpack(mpm_ctx c, int t) {
+  launch(c, KI_MIG, [&] {
+    kx(c, k_mig_rev_unpack<D>, dim3(c->n_sm), dim3(256), 0, c->P, c->left ? (const float*)mig_send_at(c, t, 0) : nullptr,
+       c->right ? (const float*)mig_send_at(c, t, 1) : nullptr, (const float*)c->rev_recv[0],
+       (const float*)c->rev_recv[1], c->bcur);
+  });
 }
 
 // NEXT N2 fused forward (config.fuse_g2p2g): step t's G2P also scatters step t+1's P2G
@@ -517,7 +665,7 @@ void forward_phase_b(mpm_ctx c, int t) {
 // of a range or of a segment) runs the unfused P2G first.
 // (a slab with neighbours exchanges its windows between P2G and G2P: not fusable; a slab
 // without neighbours -- the whole domain, bench.py's C5a at N = 1 -- is)
-bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !has_nbr(c) && !c->ctrl; }
+bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !has_nbr(c) && !c->ctrl && !c->mig; }
 
 template <int D, bool SORT, bool SCAT>
 void launch_fused(mpm_ctx c, const StepArgs& A) {
@@ -590,6 +738,14 @@ mpm_status forward_range(mpm_ctx c, int t0, int t1) {
       if (s) return s;
     }
     forward_phase_b<D>(c, t);
+    if (c->mig) {
+      if (has_nbr(c)) {
+        mpm_status s = exchange_pair(c, MPM_XCHG_MIGRATE, mig_send_at(c, t, 0), mig_send_at(c, t, 1),
+                                     mig_recv_at(c, t, 0), mig_recv_at(c, t, 1), c->mig_floats);
+        if (s) return s;
+      }
+      forward_phase_c<D>(c, t);
+    }
   }
   return MPM_OK;
 }
@@ -616,6 +772,14 @@ void launch_p2gT(mpm_ctx c, const KParams& P, const StepArgs& A, int na) {
 
 // backward step t = phase A ([zero,] G2P^T [, window pack]) | exchange | phase B ([unpack,]
 // grid^T, P2G^T); the particle adjoint flows c->bcur -> c->bnxt
+// The reverse step t runs fused with G2P^T of step t-1 (k_p2g2p_adj) when the fused mode is
+// on and nothing has to happen between P2G^T(t) and G2P^T(t-1): no controller adjoint (it
+// needs all of dL/da_t), no slab neighbours (window exchange), no migration, step t-1 in the
+// same tape segment; small problems keep the split kernels.
+bool bwd_fuse_at(mpm_ctx c, int t) {
+  return c->cfg.fuse_g2p2g && c->bfuse && !c->ctrl && !has_nbr(c) && !c->mig && !c->split && t - 1 >= c->seg0;
+}
+
 template <int D>
 void backward_phase_a(mpm_ctx c, int t) {
   const KParams& P = c->P;
@@ -625,6 +789,7 @@ void backward_phase_a(mpm_ctx c, int t) {
   A.gout = c->bnxt;
   if (t == c->seg_end - 1)  // first backward step of a segment: prepare its buffer (later: by grid_T)
     launch(c, KI_ZERO, [&] { kx(c, k_zero_slots, dim3(c->n_sm * 4), dim3(256), 0, info_at(c, t), A.grid); });
+  if (t + 1 < c->seg_end && bwd_fuse_at(c, t + 1)) return;  // G2P^T(t) ran inside k_p2g2p_adj of step t+1
   const int nbla = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter_adj));
   launch(c, KI_G2PT, [&] {
     if (c->split) kx(c, k_block_scatter<D, true, 0, true>, dim3(nbla), dim3(kThreads), scatter_dyn_smem<D, true>(), P, A);
@@ -645,8 +810,31 @@ void backward_phase_b(mpm_ctx c, int t) {
     kx(c, k_grid_adj<D>, dim3(c->n_sm * 8), dim3(256), 0, P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
                                                        t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
-  const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
-  launch(c, KI_P2GT, [&] { launch_p2gT<D>(c, P, A, na); });
+  if (bwd_fuse_at(c, t)) {
+    // fused reverse step: P2G^T of step t + G2P^T of step t-1 (k_p2g2p_adj); the adjoint grid
+    // of step t-1 was prepared by the grid^T above
+    A.st_prev = state_at(c, t - 1);
+    A.perm_prev = perm_at(c, t - 1);
+    A.slot_prev = slot_at(c, t - 1);
+    A.info_gprev = info_at(c, t - 1);
+    A.agrid_t1 = agrid_of(c, t - 1);
+    auto it = c->seeds.find(t);
+    A.seed_t = it == c->seeds.end() ? nullptr : it->second;
+    A.NU = (int)c->NU;
+    const int nf = std::max(1, std::min(P.NBT, c->n_sm * c->occ_frt));
+    launch(c, KI_P2GT, [&] {
+      if (c->mass_grad) {
+        if (P.material == 1) kx(c, k_p2g2p_adj<D, true, 1>, dim3(nf), dim3(kFRT), 0, P, A);
+        else kx(c, k_p2g2p_adj<D, true, 0>, dim3(nf), dim3(kFRT), 0, P, A);
+      } else {
+        if (P.material == 1) kx(c, k_p2g2p_adj<D, false, 1>, dim3(nf), dim3(kFRT), 0, P, A);
+        else kx(c, k_p2g2p_adj<D, false, 0>, dim3(nf), dim3(kFRT), 0, P, A);
+      }
+    });
+  } else {
+    const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
+    launch(c, KI_P2GT, [&] { launch_p2gT<D>(c, P, A, na); });
+  }
   if (c->ctrl) {  // N1: controller adjoint of step t (needs this step's complete dL/da)
     const int KD = P.K * D;
     launch(c, KI_CTRLT, [&] {
@@ -733,33 +921,55 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
                         const float* mass, const float* vol, const float* E, const float* nu,
                         const int32_t* aid) {
   const KParams& P = c->P;
-  const size_t NT = P.NT;
+  const size_t NT = P.NT, NU = c->NU;  // storage capacity, user-array length (equal outside migrating mode)
   c->seg0 = 0;  // a new rollout starts in tape slot 0
   c->res_end = 0;
   c->ck_valid = 0;
   // stage user arrays on the device (host or device pointers, UVA)
   float* sx = c->stage;
-  float* sv = sx + NT * D;
-  float* sF = sv + NT * D;
-  float* sC = sF + NT * D * D;
-  CK(cudaMemcpyAsync(sx, x, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (v) CK(cudaMemcpyAsync(sv, v, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (F) CK(cudaMemcpyAsync(sF, F, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (C) CK(cudaMemcpyAsync(sC, C, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  float* sv = sx + NU * D;
+  float* sF = sv + NU * D;
+  float* sC = sF + NU * D * D;
+  CK(cudaMemcpyAsync(sx, x, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (v) CK(cudaMemcpyAsync(sv, v, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (F) CK(cudaMemcpyAsync(sF, F, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (C) CK(cudaMemcpyAsync(sC, C, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  int n0 = (int)NT;
+  if (c->mig) {
+    // migrating slab mode: storage order 0 = the particles whose base_x the slab owns, in user
+    // order (the binning decision of R17: fp32 x * res - 0.5, floor)
+    std::vector<float> hx(NU * D);
+    CK(cudaMemcpyAsync(hx.data(), sx, NU * D * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int> mem;
+    for (size_t u = 0; u < NU; ++u) {
+      const int bx = (int)floorf(hx[u * D] * P.fres - 0.5f);
+      if (bx >= P.own_lo && bx < P.own_hi) mem.push_back((int)u);
+    }
+    if (mem.size() > NT)
+      return fail(c, MPM_ERR_MIGRATE, "slab owns " + std::to_string(mem.size()) + " particles at t = 0, capacity " +
+                                          std::to_string(NT) + " (config.n_particles)");
+    n0 = (int)mem.size();
+    CK(cudaMemcpyAsync(c->members, mem.data(), mem.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(orig_at(c, 0), c->members, mem.size() * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(info_at(c, 0) + I_NSLOT, &n0, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));  // n0, mem are host locals
+  }
   launch(c, KI_MISC, [&] {
-    k_user_to_soa<D><<<grid1d(NT), 256, 0, c->stream>>>(P, sx, v ? sv : nullptr, F ? sF : nullptr,
-                                                         C ? sC : nullptr, state_at(c, 0));
+    k_user_to_soa<D><<<grid1d(std::max(n0, 1)), 256, 0, c->stream>>>(P, sx, v ? sv : nullptr, F ? sF : nullptr,
+                                                                       C ? sC : nullptr, state_at(c, 0),
+                                                                       c->mig ? c->members : nullptr, n0);
   });
-  float* pm = sC + NT * D * D;
-  float* pv = pm + NT;
-  CK(cudaMemcpyAsync(pm, mass, NT * sizeof(float), cudaMemcpyDefault, c->stream));
-  CK(cudaMemcpyAsync(pv, vol, NT * sizeof(float), cudaMemcpyDefault, c->stream));
-  CK(cudaMemcpyAsync(c->E, E, NT * sizeof(float), cudaMemcpyDefault, c->stream));
-  CK(cudaMemcpyAsync(c->nu, nu, NT * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (aid) CK(cudaMemcpyAsync(c->aid, aid, NT * sizeof(int), cudaMemcpyDefault, c->stream));
-  else CK(cudaMemsetAsync(c->aid, 0xff, NT * sizeof(int), c->stream));
+  float* pm = sC + NU * D * D;
+  float* pv = pm + NU;
+  CK(cudaMemcpyAsync(pm, mass, NU * sizeof(float), cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpyAsync(pv, vol, NU * sizeof(float), cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpyAsync(c->E, E, NU * sizeof(float), cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpyAsync(c->nu, nu, NU * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (aid) CK(cudaMemcpyAsync(c->aid, aid, NU * sizeof(int), cudaMemcpyDefault, c->stream));
+  else CK(cudaMemsetAsync(c->aid, 0xff, NU * sizeof(int), c->stream));
   CK(cudaMemsetAsync(c->dbad, 0, sizeof(int), c->stream));
-  launch(c, KI_MISC, [&] { k_params<<<grid1d(NT), 256, 0, c->stream>>>((int)NT, pm, pv, c->E, c->nu, c->prm, c->dbad); });
+  launch(c, KI_MISC, [&] { k_params<<<grid1d(NU), 256, 0, c->stream>>>((int)NU, pm, pv, c->E, c->nu, c->prm, c->dbad); });
   CK(cudaMemsetAsync(c->err, 0, sizeof(ErrLatch), c->stream));
   CK(cudaMemsetAsync(c->cnt, 0, (size_t)P.NBT * sizeof(int), c->stream));
   launch_keys<D>(c, 0);
@@ -788,8 +998,8 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
       if (s) return s;
     }
   }
-  CK(cudaMemsetAsync(c->dmu, 0, NT * sizeof(float), c->stream));
-  CK(cudaMemsetAsync(c->dlam, 0, NT * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->dmu, 0, NU * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->dlam, 0, NU * sizeof(float), c->stream));
   mpm_status s = sync_and_check(c, "set_state");
   int bad = 0;
   CK(cudaMemcpy(&bad, c->dbad, sizeof(int), cudaMemcpyDeviceToHost));
@@ -817,7 +1027,7 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
 constexpr size_t kGraphCache = 16;  // CUDA-graph executables kept per context (LRU)
 
 bool graphs_ok(mpm_ctx c, int n) {
-  return c->graphs && c->stream && !c->profiling && !has_nbr(c) && !c->comm && c->ck == 0 && n >= 2;
+  return c->graphs && c->stream && !c->profiling && !has_nbr(c) && !has_xchg(c) && !c->mig && c->ck == 0 && n >= 2;
 }
 
 // Run body() -- which launches a step loop and advances the host state -- directly, or
@@ -890,9 +1100,10 @@ void add_step_seed(mpm_ctx c, int t, float* g) {
   if (it == c->seeds.end()) return;
   const size_t NT = c->P.NT;
   const float* b = it->second;
+  const size_t NU = c->NU;  // seeds are user arrays
   launch(c, KI_MISC, [&] {
-    kx(c, k_seed<D>, dim3(grid1d(NT)), dim3(256), 0, c->P, orig_at(c, t), b, b + NT * D, b + 2 * NT * D,
-                                                  b + 2 * NT * D + NT * D * D, g, 1);
+    kx(c, k_seed<D>, dim3(grid1d(NT)), dim3(256), 0, c->P, orig_at(c, t), b, b + NU * D, b + 2 * NU * D,
+                                                  b + 2 * NU * D + NU * D * D, g, 1, nslot_at(c, t));
   });
 }
 
@@ -900,26 +1111,26 @@ void add_step_seed(mpm_ctx c, int t, float* g) {
 template <int D>
 mpm_status backward_begin(mpm_ctx c, const float* gx, const float* gv, const float* gF, const float* gC) {
   const KParams& P = c->P;
-  const size_t NT = P.NT;
+  const size_t NT = P.NT, NU = c->NU;
   const int T = c->tape_len;
   float* sx = c->stage;
-  float* sv = sx + NT * D;
-  float* sF = sv + NT * D;
-  float* sC = sF + NT * D * D;
-  if (gx) CK(cudaMemcpyAsync(sx, gx, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (gv) CK(cudaMemcpyAsync(sv, gv, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (gF) CK(cudaMemcpyAsync(sF, gF, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (gC) CK(cudaMemcpyAsync(sC, gC, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  float* sv = sx + NU * D;
+  float* sF = sv + NU * D;
+  float* sC = sF + NU * D * D;
+  if (gx) CK(cudaMemcpyAsync(sx, gx, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (gv) CK(cudaMemcpyAsync(sv, gv, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (gF) CK(cudaMemcpyAsync(sF, gF, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (gC) CK(cudaMemcpyAsync(sC, gC, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
   c->bcur = c->gA;
   c->bnxt = c->gB;
   launch(c, KI_MISC, [&] {
     kx(c, k_seed<D>, dim3(grid1d(NT)), dim3(256), 0, P, orig_at(c, T), gx ? sx : nullptr, gv ? sv : nullptr,
-                                                  gF ? sF : nullptr, gC ? sC : nullptr, c->bcur, 0);
+                                                  gF ? sF : nullptr, gC ? sC : nullptr, c->bcur, 0, nslot_at(c, T));
   });
   add_step_seed<D>(c, T, c->bcur);
-  CK(cudaMemsetAsync(c->dmu, 0, NT * sizeof(float), c->stream));
-  CK(cudaMemsetAsync(c->dlam, 0, NT * sizeof(float), c->stream));
-  CK(cudaMemsetAsync(c->dmass, 0, NT * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->dmu, 0, NU * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->dlam, 0, NU * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->dmass, 0, NU * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->da, 0, (size_t)P.B * P.T * std::max(P.K, 1) * D * sizeof(float), c->stream));
   return MPM_OK;
 }
@@ -976,6 +1187,13 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
         c, 1, c->seg0, steps,
         [&]() -> mpm_status {
           for (int t = c->seg_end - 1; t >= c->seg0; --t) {
+            if (c->mig && has_nbr(c)) {  // reverse migration of the adjoint of state t+1
+              backward_mig_pack<D>(c, t);
+              mpm_status q = exchange_pair(c, MPM_XCHG_MIGRATE_ADJ, c->rev_send[0], c->rev_send[1], c->rev_recv[0],
+                                           c->rev_recv[1], rev_floats(c));
+              if (q) return q;
+              backward_mig_unpack<D>(c, t);
+            }
             backward_phase_a<D>(c, t);
             if (has_nbr(c)) {
               mpm_status q = exchange_nccl(c);
@@ -1010,10 +1228,15 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
   }
   s = backward_finish(c);
   if (s) return s;
-  if (c->slab && c->comm && c->P.K > 0) {  // slab mode: the actuation is shared by all slabs
-    const NcclApi* N = nccl_api();
-    ncclResult_t r = N->AllReduce(c->da, c->da, da_count(c), ncclFloat, ncclSum, c->comm, c->stream);
-    if (r != ncclSuccess) return fail(c, MPM_ERR_COMM, std::string("actuation-gradient all-reduce: ") + N->GetErrorString(r));
+  if (c->slab && has_xchg(c)) {
+    // slab mode: the actuation is shared by all slabs; migrating mode: a particle's dL/dmu,
+    // dL/dlam, dL/dm collect on whichever slab simulated each step
+    if (c->P.K > 0 && (s = allreduce_sum(c, c->da, da_count(c)))) return s;
+    if (c->mig) {
+      if ((s = allreduce_sum(c, c->dmu, c->NU))) return s;
+      if ((s = allreduce_sum(c, c->dlam, c->NU))) return s;
+      if (c->mass_grad && (s = allreduce_sum(c, c->dmass, c->NU))) return s;
+    }
   }
   s = sync_and_check(c, "backward");
   if (s) return s;
@@ -1025,39 +1248,49 @@ mpm_status do_backward(mpm_ctx c, const float* gx, const float* gv, const float*
 
 template <int D>
 mpm_status do_get_state(mpm_ctx c, int t, float* x, float* v, float* F, float* C) {
-  const size_t NT = c->P.NT;
+  const size_t NT = c->P.NT, NU = c->NU;
   float* sx = c->stage;
-  float* sv = sx + NT * D;
-  float* sF = sv + NT * D;
-  float* sC = sF + NT * D * D;
+  float* sv = sx + NU * D;
+  float* sF = sv + NU * D;
+  float* sC = sF + NU * D * D;
+  if (c->mig)  // this slab writes its own particles; zeros elsewhere (the sum over slabs is the body)
+    CK(cudaMemsetAsync(sx, 0, NU * (2 * D + 2 * D * D) * sizeof(float), c->stream));
   launch(c, KI_MISC, [&] {
-    k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(c->P, orig_at(c, t), state_at(c, t), sx, sv, sF, sC, 1);
+    k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(c->P, orig_at(c, t), state_at(c, t), sx, sv, sF, sC, 1,
+                                                         nslot_at(c, t), c->mig ? state_at(c, t) : nullptr);
   });
-  if (x) CK(cudaMemcpyAsync(x, sx, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (v) CK(cudaMemcpyAsync(v, sv, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (F) CK(cudaMemcpyAsync(F, sF, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (C) CK(cudaMemcpyAsync(C, sC, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (x) CK(cudaMemcpyAsync(x, sx, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (v) CK(cudaMemcpyAsync(v, sv, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (F) CK(cudaMemcpyAsync(F, sF, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (C) CK(cudaMemcpyAsync(C, sC, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
   return sync_and_check(c, "get_state");
 }
 
 template <int D>
 mpm_status do_grad(mpm_ctx c, float* dx0, float* dv0, float* dF0, float* dC0, float* dE, float* dnu, float* da) {
   const KParams& P = c->P;
-  const size_t NT = P.NT;
+  const size_t NT = P.NT, NU = c->NU;
   float* sx = c->stage;
-  float* sv = sx + NT * D;
-  float* sF = sv + NT * D;
-  float* sC = sF + NT * D * D;
-  float* sE = sC + NT * D * D;
-  float* sn = sE + NT;
-  launch(c, KI_MISC, [&] { k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(P, nullptr, c->gA, sx, sv, sF, sC, 0); });
-  launch(c, KI_MISC, [&] { k_finalize_params<<<grid1d(NT), 256, 0, c->stream>>>((int)NT, c->E, c->nu, c->dmu, c->dlam, sE, sn); });
-  if (dx0) CK(cudaMemcpyAsync(dx0, sx, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (dv0) CK(cudaMemcpyAsync(dv0, sv, NT * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (dF0) CK(cudaMemcpyAsync(dF0, sF, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (dC0) CK(cudaMemcpyAsync(dC0, sC, NT * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (dE) CK(cudaMemcpyAsync(dE, sE, NT * sizeof(float), cudaMemcpyDefault, c->stream));
-  if (dnu) CK(cudaMemcpyAsync(dnu, sn, NT * sizeof(float), cudaMemcpyDefault, c->stream));
+  float* sv = sx + NU * D;
+  float* sF = sv + NU * D;
+  float* sC = sF + NU * D * D;
+  float* sE = sC + NU * D * D;
+  float* sn = sE + NU;
+  if (c->mig) {  // storage order 0 = the members; zeros for the other slabs' particles
+    CK(cudaMemsetAsync(sx, 0, NU * (2 * D + 2 * D * D) * sizeof(float), c->stream));
+    launch(c, KI_MISC, [&] {
+      k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(P, orig_at(c, 0), c->gA, sx, sv, sF, sC, 0, nslot_at(c, 0));
+    });
+  } else {
+    launch(c, KI_MISC, [&] { k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(P, nullptr, c->gA, sx, sv, sF, sC, 0); });
+  }
+  launch(c, KI_MISC, [&] { k_finalize_params<<<grid1d(NU), 256, 0, c->stream>>>((int)NU, c->E, c->nu, c->dmu, c->dlam, sE, sn); });
+  if (dx0) CK(cudaMemcpyAsync(dx0, sx, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (dv0) CK(cudaMemcpyAsync(dv0, sv, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (dF0) CK(cudaMemcpyAsync(dF0, sF, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (dC0) CK(cudaMemcpyAsync(dC0, sC, NU * D * D * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (dE) CK(cudaMemcpyAsync(dE, sE, NU * sizeof(float), cudaMemcpyDefault, c->stream));
+  if (dnu) CK(cudaMemcpyAsync(dnu, sn, NU * sizeof(float), cudaMemcpyDefault, c->stream));
   if (da && P.K > 0)
     CK(cudaMemcpyAsync(da, c->da, (size_t)P.B * P.T * P.K * D * sizeof(float), cudaMemcpyDefault, c->stream));
   return sync_and_check(c, "grad");
@@ -1106,8 +1339,11 @@ mpm_status group_check(mpm_ctx* cs, int32_t n) {
     if (c->poisoned) return fail(c, MPM_ERR_CALL_ORDER, "context poisoned by an earlier error; call mpm_set_state");
     if (c->comm) return fail(c, MPM_ERR_CALL_ORDER, "context has a communicator; use mpm_forward/mpm_backward");
     if (c->cfg.device != c0->cfg.device || c->stream != c0->stream || c->D != c0->D || c->P.res != c0->P.res ||
-        c->tape_len != c0->tape_len)
-      return fail(c, MPM_ERR_INVALID_ARG, "group contexts need one device, one stream, equal dim/res/tape length");
+        c->tape_len != c0->tape_len || c->mig != c0->mig ||
+        (c->mig && (c->NU != c0->NU || c->P.mig_cap != c0->P.mig_cap)))
+      return fail(c, MPM_ERR_INVALID_ARG, "group contexts need one device, one stream, equal dim/res/tape length "
+                                          "and the same slab mode");
+    if (c->transport) return fail(c, MPM_ERR_CALL_ORDER, "context has a transport; use mpm_forward/mpm_backward");
     if (n > 1 && !c->slab) return fail(c, MPM_ERR_INVALID_ARG, "group contexts need mpm_set_slab");
     if (c->ck) return fail(c, MPM_ERR_INVALID_ARG, "group calls do not support checkpoint_every");
     if (c->slab) {
@@ -1130,6 +1366,13 @@ mpm_status group_forward(mpm_ctx* cs, int32_t n, int32_t steps) {
       if (s) return s;
     }
     for (int i = 0; i < n; ++i) forward_phase_b<D>(cs[i], t);
+    if (cs[0]->mig) {
+      if (n > 1) {
+        mpm_status s = exchange_local_mig(cs, n, t);
+        if (s) return s;
+      }
+      for (int i = 0; i < n; ++i) forward_phase_c<D>(cs[i], t);
+    }
   }
   mpm_status first = MPM_OK;
   for (int i = 0; i < n; ++i) {
@@ -1151,6 +1394,12 @@ mpm_status group_backward(mpm_ctx* cs, int32_t n, const float* const* gx, const 
   }
   for (int i = 0; i < n; ++i) cs[i]->seg_end = cs[i]->tape_len;
   for (int t = cs[0]->tape_len - 1; t >= 0; --t) {
+    if (cs[0]->mig && n > 1) {  // reverse migration of the adjoint of state t+1
+      for (int i = 0; i < n; ++i) backward_mig_pack<D>(cs[i], t);
+      mpm_status s = exchange_local_rev(cs, n);
+      if (s) return s;
+      for (int i = 0; i < n; ++i) backward_mig_unpack<D>(cs[i], t);
+    }
     for (int i = 0; i < n; ++i) backward_phase_a<D>(cs[i], t);
     if (n > 1) {
       mpm_status s = exchange_local(cs, n);
@@ -1166,12 +1415,23 @@ mpm_status group_backward(mpm_ctx* cs, int32_t n, const float* const* gx, const 
     if (s) return s;
   }
   mpm_ctx c = cs[0];
-  if (n > 1 && c->P.K > 0) {  // the actuation is shared by all slabs: every context gets the sum
-    const size_t m = da_count(c);
+  // the actuation is shared by all slabs; in migrating mode a particle's dL/dmu, dL/dlam, dL/dm
+  // collect on whichever slab simulated each step: every context gets the sums
+  auto sum_all = [&](float* mpm_ctx_s::*field, size_t m) -> mpm_status {
     for (int i = 1; i < n; ++i)
-      launch(c, KI_MISC, [&] { k_add_inplace<<<c->n_sm, 256, 0, c->stream>>>(m, c->da, cs[i]->da); });
+      launch(c, KI_MISC, [&] { k_add_inplace<<<c->n_sm, 256, 0, c->stream>>>(m, c->*field, cs[i]->*field); });
     for (int i = 1; i < n; ++i)
-      CK(cudaMemcpyAsync(cs[i]->da, c->da, m * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(cs[i]->*field, c->*field, m * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    return MPM_OK;
+  };
+  if (n > 1) {
+    mpm_status s = MPM_OK;
+    if (c->P.K > 0 && (s = sum_all(&mpm_ctx_s::da, da_count(c)))) return s;
+    if (c->mig) {
+      if ((s = sum_all(&mpm_ctx_s::dmu, c->NU))) return s;
+      if ((s = sum_all(&mpm_ctx_s::dlam, c->NU))) return s;
+      if (c->mass_grad && (s = sum_all(&mpm_ctx_s::dmass, c->NU))) return s;
+    }
   }
   mpm_status first = MPM_OK;
   for (int i = 0; i < n; ++i) {
@@ -1232,6 +1492,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, k.device);
   c->stream = (cudaStream_t)k.stream;
   if (const char* e = getenv("MPM_PDL")) c->pdl = atoi(e) != 0;
+  if (const char* e = getenv("MPM_FUSE_BWD")) c->bfuse = atoi(e) != 0;
   c->D = k.dim;
   c->S = 2 * k.dim + 2 * k.dim * k.dim;
   KParams& P = c->P;
@@ -1253,6 +1514,11 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   P.act_s = k.act_strength;
   P.slab_lo = 0;
   P.slab_hi = k.res - 3;
+  P.migrate = 0;
+  P.own_lo = INT32_MIN;
+  P.own_hi = INT32_MAX;
+  P.mig_cap = 0;
+  c->NU = (size_t)k.batch * k.n_particles;
   P.material = k.material;
   c->n_tiles = (P.NBT + kScanTile - 1) / kScanTile;
   // fewer than ~400 particles per gather CTA slot: too few occupied blocks to fill the GPU
@@ -1288,6 +1554,9 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<2, 0, true, true>, kThreads, fuse_dyn_smem<2>());
     c->occ_fuse = std::max(1, occ);
   }
+  if (k.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g2p_adj<3, false, 0>, kFRT, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g2p_adj<2, false, 0>, kFRT, 0);
+  c->occ_frt = std::max(1, occ);
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<3>, kThreads, 0);
     c->occ_g2p = std::max(1, occ);
@@ -1373,6 +1642,7 @@ void mpm_destroy(mpm_ctx c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   else cudaDeviceSynchronize();
   if (c->comm) nccl_api()->CommDestroy(c->comm);
+  if (c->host_stage) cudaFreeHost(c->host_stage);
   for (void* p : c->allocs) cudaFree(p);
   for (auto& kv : c->seeds) cudaFree(kv.second);
   for (auto& p : c->pending) {
@@ -1410,8 +1680,8 @@ mpm_status mpm_forward(mpm_ctx c, int32_t n) {
   if (!c->has_state) return fail(c, MPM_ERR_CALL_ORDER, "mpm_forward before mpm_set_state");
   if (c->poisoned) return fail(c, MPM_ERR_CALL_ORDER, "context poisoned by an earlier error; call mpm_set_state");
   if (c->tape_len + n > c->cfg.max_steps) return fail(c, MPM_ERR_TAPE_FULL, "forward beyond max_steps");
-  if (has_nbr(c) && !c->comm)
-    return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init, or use mpm_group_forward");
+  if (has_nbr(c) && !has_xchg(c))
+    return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init / mpm_set_transport, or use mpm_group_forward");
   cudaSetDevice(c->cfg.device);
   c->has_grad = false;
   if (!on_tape(c, c->tape_len)) {  // N2: the tape end was evicted by a checkpointed backward
@@ -1464,8 +1734,8 @@ mpm_status mpm_backward(mpm_ctx c, const float* gx, const float* gv, const float
   if (!c) return MPM_ERR_INVALID_ARG;
   if (!c->has_state) return fail(c, MPM_ERR_CALL_ORDER, "mpm_backward before mpm_set_state");
   if (c->poisoned) return fail(c, MPM_ERR_CALL_ORDER, "context poisoned by an earlier error; call mpm_set_state");
-  if (has_nbr(c) && !c->comm)
-    return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init, or use mpm_group_backward");
+  if (has_nbr(c) && !has_xchg(c))
+    return fail(c, MPM_ERR_CALL_ORDER, "slab context with neighbours: call mpm_comm_init / mpm_set_transport, or use mpm_group_backward");
   cudaSetDevice(c->cfg.device);
   if (!on_tape(c, c->tape_len)) {  // N2: bring the last segment back
     mpm_status s = c->D == 3 ? bring_to_tape<3>(c, c->tape_len) : bring_to_tape<2>(c, c->tape_len);
@@ -1512,9 +1782,9 @@ mpm_status mpm_get_binning(mpm_ctx c, int32_t t, float* x_store, int32_t* orig, 
     // keys of storage order t: recompute from the stored positions (same device code as the step)
     int* tmp = c->scratch;
     if (D == 3)
-      k_init_keys<3><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, reinterpret_cast<int*>(c->tmp_pk), c->err);
+      k_init_keys<3><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, nullptr, c->err, nslot_at(c, t));
     else
-      k_init_keys<2><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, reinterpret_cast<int*>(c->tmp_pk), c->err);
+      k_init_keys<2><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, nullptr, c->err, nslot_at(c, t));
     CK(cudaMemcpyAsync(keyo, tmp, NT * sizeof(int), cudaMemcpyDefault, c->stream));
   }
   return sync_and_check(c, "get_binning");
@@ -1618,7 +1888,7 @@ mpm_status mpm_add_seed(mpm_ctx c, int32_t t, const float* dLdx, const float* dL
                         const float* dLdC) {
   if (!c || t < 0 || t > c->cfg.max_steps) return MPM_ERR_INVALID_ARG;
   cudaSetDevice(c->cfg.device);
-  const size_t NT = c->P.NT, D = c->D;
+  const size_t NT = c->NU, D = c->D;  // a seed is a user array
   const size_t n = NT * (2 * D + 2 * D * D);
   float*& b = c->seeds[t];
   if (!b) {
@@ -1663,7 +1933,7 @@ mpm_status mpm_grad_mass(mpm_ctx c, float* dmass) {
   if (!c->has_grad || !c->mass_grad_valid)
     return fail(c, MPM_ERR_CALL_ORDER, "mpm_grad_mass needs mpm_enable_mass_grad(1) before mpm_backward");
   cudaSetDevice(c->cfg.device);
-  CK(cudaMemcpyAsync(dmass, c->dmass, (size_t)c->P.NT * sizeof(float), cudaMemcpyDefault, c->stream));
+  CK(cudaMemcpyAsync(dmass, c->dmass, c->NU * sizeof(float), cudaMemcpyDefault, c->stream));
   return sync_and_check(c, "grad_mass");
 }
 
@@ -1709,6 +1979,67 @@ mpm_status mpm_set_slab(mpm_ctx c, int32_t x_lo, int32_t x_hi, int32_t halo) {
   return MPM_OK;
 }
 
+mpm_status mpm_set_slab_migrating(mpm_ctx c, int32_t x_lo, int32_t x_hi, int32_t halo, int32_t n_global,
+                                  int32_t mig_cap) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  if (c->cfg.checkpoint_every) return fail(c, MPM_ERR_INVALID_ARG, "migrating slab mode needs checkpoint_every = 0");
+  if (c->ctrl) return fail(c, MPM_ERR_INVALID_ARG, "migrating slab mode does not support the controller");
+  if (n_global < 1) return fail(c, MPM_ERR_INVALID_ARG, "n_global >= 1 required");
+  if (mig_cap < 0) return fail(c, MPM_ERR_INVALID_ARG, "mig_cap >= 0 required");
+  mpm_status s = mpm_set_slab(c, x_lo, x_hi, halo);
+  if (s) return s;
+  KParams& P = c->P;
+  const int D = c->D;
+  // ownership: base_x in [x_lo, x_hi) (the outer slabs also take what lies beyond; the domain
+  // check rejects it); no drift bound
+  P.slab_lo = 0;
+  P.slab_hi = P.res - 3;
+  P.migrate = 1;
+  P.own_lo = c->left ? x_lo : INT32_MIN;
+  P.own_hi = c->right ? x_hi : INT32_MAX;
+  P.mig_cap = mig_cap > 0 ? mig_cap : std::max(1024, P.NT / 64);
+  c->mig = true;
+  c->NU = (size_t)n_global;
+  c->mig_floats = Mig<3>::HDR + (size_t)P.mig_cap * (D == 3 ? Mig<3>::R : Mig<2>::R);
+  // user-indexed arrays span the whole body now (the storage ones keep the capacity P.NT)
+  auto realloc_user = [&](auto*& ptr, size_t count) -> mpm_status {
+    c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)ptr), c->allocs.end());
+    cudaFree(ptr);
+    ptr = nullptr;
+    return dalloc(c, &ptr, count);
+  };
+  const size_t NU = c->NU, TC = c->tape_cap;
+  if (!s) s = realloc_user(c->prm, NU);
+  if (!s) s = realloc_user(c->aid, NU);
+  if (!s) s = realloc_user(c->E, NU);
+  if (!s) s = realloc_user(c->nu, NU);
+  if (!s) s = realloc_user(c->dmu, NU);
+  if (!s) s = realloc_user(c->dlam, NU);
+  if (!s) s = realloc_user(c->dmass, NU);
+  if (!s) s = realloc_user(c->stage, NU * (2 * D + 2 * D * D + 2));
+  if (!s) s = dalloc(c, &c->members, (size_t)P.NT);
+  if (!s) s = dalloc(c, &c->mig_send_tape, TC * 2 * c->mig_floats);
+  if (!s) s = dalloc(c, &c->mig_recv_tape, TC * 2 * c->mig_floats);
+  for (int side = 0; side < 2 && !s; ++side) {
+    s = dalloc(c, &c->rev_send[side], rev_floats(c));
+    if (!s) s = dalloc(c, &c->rev_recv[side], rev_floats(c));
+  }
+  if (s) return s;
+  CK(cudaMemset(c->mig_recv_tape, 0, TC * 2 * c->mig_floats * sizeof(float)));
+  CK(cudaMemset(c->mig_send_tape, 0, TC * 2 * c->mig_floats * sizeof(float)));
+  return MPM_OK;
+}
+
+mpm_status mpm_set_transport(mpm_ctx c, mpm_transport_fn fn, void* user) {
+  if (!c) return MPM_ERR_INVALID_ARG;
+  if (c->comm && fn) return fail(c, MPM_ERR_CALL_ORDER, "context already has an NCCL communicator");
+  if (fn && !c->slab) return fail(c, MPM_ERR_CALL_ORDER, "mpm_set_transport needs mpm_set_slab first");
+  drop_graphs(c);
+  c->transport = fn;
+  c->transport_user = user;
+  return MPM_OK;
+}
+
 mpm_status mpm_comm_unique_id(char out[128]) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
   if (!out) return MPM_ERR_INVALID_ARG;
@@ -1724,6 +2055,7 @@ mpm_status mpm_comm_init(mpm_ctx c, int32_t rank, int32_t world, const char id[1
   if (!c || !id || world < 1 || rank < 0 || rank >= world) return MPM_ERR_INVALID_ARG;
   if (!c->slab) return fail(c, MPM_ERR_CALL_ORDER, "mpm_comm_init needs mpm_set_slab first");
   if (c->comm) return fail(c, MPM_ERR_CALL_ORDER, "communicator already initialised");
+  if (c->transport) return fail(c, MPM_ERR_CALL_ORDER, "context has a transport callback");
   if ((c->left && rank == 0) || (c->right && rank == world - 1))
     return fail(c, MPM_ERR_INVALID_ARG, "ranks must be ordered by slab (left neighbour = rank - 1)");
   const NcclApi* N = nccl_api();
@@ -1778,7 +2110,7 @@ mpm_status mpm_set_controller(mpm_ctx c, const float* W, const float* b, const f
   KParams& P = c->P;
   const int D = c->D;
   if (P.K < 1) return fail(c, MPM_ERR_INVALID_ARG, "the controller needs n_actuators >= 1");
-  if (has_nbr(c)) return fail(c, MPM_ERR_INVALID_ARG, "the controller is not supported across slabs");
+  if (has_nbr(c) || c->mig) return fail(c, MPM_ERR_INVALID_ARG, "the controller is not supported across slabs");
   const int KD = P.K * D, nz = D * (1 + 2 * P.K);
   const size_t T = c->cfg.max_steps;
   if (!c->ctrl_W) {

@@ -110,7 +110,7 @@ constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
   } while (0)
 #endif
 
-enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6, E_SLAB = 9, E_FUSE = 10 };
+enum ErrCode { E_OK = 0, E_DOMAIN = 4, E_INVERTED = 5, E_TAPE_FULL = 6, E_SLAB = 9, E_FUSE = 10, E_MIGRATE = 11 };
 
 template <int D> struct Dim;
 template <> struct Dim<3> {
@@ -133,11 +133,23 @@ struct KParams {
   int slab_lo, slab_hi;                     // allowed base_x range (inclusive); slab mode
   int material;                             // 0 = neo-Hookean (R1), 1 = fixed-corotated (R21)
   int nz;                                   // controller observation length d (1 + 2K) (NEXT N1)
+  int migrate;                              // migrating slab mode: a particle is owned by the slab
+  int own_lo, own_hi;                       //   whose [own_lo, own_hi) holds its base_x, every step
+  int mig_cap;                              //   migrant records per side and step
 };
 
 // Per-step bookkeeping record, info[t * kInfo + field]
-constexpr int kInfo = 8;
-enum { I_NOCC = 0, I_NTOUCH = 1, I_BASE = 2, I_WORK = 3, I_WORK2 = 4, I_OK = 5, I_WORK3 = 6, I_WORK4 = 7 };
+constexpr int kInfo = 12;
+enum { I_NOCC = 0, I_NTOUCH = 1, I_BASE = 2, I_WORK = 3, I_WORK2 = 4, I_OK = 5, I_WORK3 = 6, I_WORK4 = 7,
+       I_NSLOT = 8 };  // I_NSLOT: storage slots of state t (migrating slab mode; live + left-behind holes)
+
+// Migrating slab mode: a particle whose base_x leaves the slab after G2P gets this key (it is
+// not binned, gathered or scattered on this rank at the next step -- a hole in the storage)
+constexpr int kDeadKey = -2;
+// migrant record in a send / receive buffer: the new state (S floats, H = F - I), the user index
+// and the sender's storage slot (bit-cast into floats); buffer = int count (padded to 4 floats)
+// followed by mig_cap records
+template <int D> struct Mig { static constexpr int S = Dim<D>::S, U = S, K = S + 1, R = S + 2, HDR = 4; };
 
 struct ErrLatch { int code, step, particle, pad; };
 
@@ -555,22 +567,24 @@ __device__ __forceinline__ int key_of(const float* x, int r, const KParams& P, i
 // ------------------------------------------------------------------------------------
 // set_state helpers
 // ------------------------------------------------------------------------------------
-// user AoS [NT][D], [NT][D][D] -> SoA state; params -> {m, V, mu, lam}
+// user AoS [N][D], [N][D][D] -> SoA state of n storage slots; slot j takes user particle
+// idx[j] (migrating slab mode: this slab's members) or j; params -> {m, V, mu, lam}
 template <int D>
 __global__ void k_user_to_soa(KParams P, const float* __restrict__ x, const float* __restrict__ v,
                               const float* __restrict__ F, const float* __restrict__ C,
-                              float* __restrict__ st) {
+                              float* __restrict__ st, const int* __restrict__ idx, int n) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.NT) return;
+  if (j >= n) return;
   const size_t NT = P.NT;
+  const size_t u = idx ? idx[j] : j;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    st[comp_x<D>(a) * NT + j] = x[j * D + a];
-    st[comp_v<D>(a) * NT + j] = v ? v[j * D + a] : 0.f;
+    st[comp_x<D>(a) * NT + j] = x[u * D + a];
+    st[comp_v<D>(a) * NT + j] = v ? v[u * D + a] : 0.f;
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      st[comp_C<D>(a, b) * NT + j] = C ? C[(j * D + a) * D + b] : 0.f;
-      st[comp_F<D>(a, b) * NT + j] = F ? F[(j * D + a) * D + b] - (a == b ? 1.f : 0.f) : 0.f;  // H = F - I
+      st[comp_C<D>(a, b) * NT + j] = C ? C[(u * D + a) * D + b] : 0.f;
+      st[comp_F<D>(a, b) * NT + j] = F ? F[(u * D + a) * D + b] - (a == b ? 1.f : 0.f) : 0.f;  // H = F - I
     }
   }
 }
@@ -588,20 +602,32 @@ __global__ void k_params(int NT, const float* __restrict__ m, const float* __res
   prm[j] = make_float4(m[j], V[j], mu, lam);
 }
 
-// keys, histogram and orig for t = 0 (storage order 0 = user order)
+// keys and block histogram of a stored state (storage slots [0, *nslot), or all NT); orig (if
+// given) = identity, for t = 0 where storage order 0 = user order.  Migrating slab mode: a slot
+// whose base_x is outside the slab (a particle that left at the previous step) is a hole.
 template <int D>
 __global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __restrict__ key,
-                            int* __restrict__ cnt, int* __restrict__ orig, ErrLatch* err) {
+                            int* __restrict__ cnt, int* __restrict__ orig, ErrLatch* err,
+                            const int* __restrict__ nslot) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  bool valid = j < P.NT;
+  bool valid = j < (nslot ? *nslot : P.NT);
   int gb = 0, k = 0;
   if (valid) {
     float x[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = st[(size_t)comp_x<D>(a) * P.NT + j];
-    if (const int e = key_of<D>(x, j / P.N, P, gb, k)) latch(err, e, 0, j);
-    key[j] = k;
-    orig[j] = j;
+    if (P.migrate) {
+      const int bx = base_of(x[0], P.fres);
+      if (bx < P.own_lo || bx >= P.own_hi) {
+        key[j] = kDeadKey;
+        valid = false;
+      }
+    }
+    if (valid) {
+      if (const int e = key_of<D>(x, j / P.N, P, gb, k)) latch(err, e, 0, j);
+      key[j] = k;
+    }
+    if (orig) orig[j] = j;
   }
   warp_hist_add(cnt, gb, valid);
 }
@@ -800,18 +826,21 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
       if (fits) touched_list[sl] = gb;
     }
   }
-  if (info_bin && gb == P.NBT - 1) block_start[P.NBT] = P.NT;
+  if (info_bin && gb == P.NBT - 1) block_start[P.NBT] = ex.x + pre.x + c;  // the binned (live) particles
   if (tile == n_tiles - 1 && threadIdx.x == 0) {
     const int ntouch = pre.z + tot.z;
     const int ok = ntouch <= cap;
     if (info_grid) {
+      // arena overflow: latched (the forward grows the arena and re-runs from this step); the
+      // step still runs on the blocks that got a slot so that every later launch of this call
+      // sees consistent tables (its results are discarded)
       if (!ok) latch(err, E_TAPE_FULL, DIL ? t + 1 : t, ntouch);
-      info_grid[I_NTOUCH] = ok ? ntouch : 0;
+      info_grid[I_NTOUCH] = ok ? ntouch : max(cap, 0);
       info_grid[I_BASE] = base;
       info_grid[I_OK] = ok;
     }
     if (info_bin) {
-      info_bin[I_NOCC] = (ok || info_grid != info_bin) ? pre.y + tot.y : 0;
+      info_bin[I_NOCC] = pre.y + tot.y;
       info_bin[I_WORK] = 0;
       info_bin[I_WORK2] = 0;
       info_bin[I_WORK3] = 0;
@@ -824,8 +853,9 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
 // also zeroes the grid slots of step t (the P2G flush accumulates into them)
 __global__ void k_scatter(int NT, const int* __restrict__ key, const int* __restrict__ block_start,
                           int* __restrict__ cnt, int2* __restrict__ tmp_pk, const int* __restrict__ zero_a,
-                          const int* __restrict__ zero_b, float4* __restrict__ arena) {
+                          const int* __restrict__ zero_b, float4* __restrict__ arena, const int* __restrict__ nslot) {
   MPM_PDL_ENTRY();
+  if (nslot) NT = *nslot;  // migrating slab mode: the storage slots of this step (holes have kDeadKey)
   // the grid slots the next scatter accumulates into (zero_a, zero_b: step records or null)
   for (const int* zi : {zero_a, zero_b}) {
     if (!zi) continue;
@@ -944,9 +974,18 @@ struct StepArgs {
   float* dlam;
   float* dmass;           // [NT] user order (NEXT N3)
   float* da;              // [B][T][K][D]
+  // fused reverse step (k_p2g2p_adj): G2P^T of step t-1 from the adjoint P2G^T of step t produced
+  const float* st_prev;   // state t-1 (storage order t-1)
+  const int* perm_prev;   // sorted slot of step t-1 (= storage index of state t) -> storage index t-1
+  const int* slot_prev;   // grid-slot map of step t-1
+  const int* info_gprev;  // step record of t-1 (base slot of its adjoint grid)
+  float4* agrid_t1;       // adjoint grid of step t-1
+  const float* seed_t;    // running-loss seed of state t (user-order AoS x|v|F|C, NU rows) or null
+  int NU;                 // rows of seed_t
   ErrLatch* err;
   int t;
 };
+
 
 // L2 prefetch of one particle's SoA record (ncomp components at index j) -- issued for a
 // block's particles before its tile is staged, so the particle loop's loads hit L2
@@ -1054,7 +1093,7 @@ __device__ __forceinline__ void cell_scan(const int* s_hist, int* s_cstart, int*
 // mirrored form, where every compare-exchange puts the smaller key at the lower index, so the
 // virtual +inf padding up to the next power of two never moves and out-of-range partners are
 // simply skipped.  O(m log^2 m) work; contains barriers (call uniformly).
-__device__ __forceinline__ void cta_sort_ints(int* a, int m, int tid, int nthr) {
+__device__ __noinline__ void cta_sort_ints(int* a, int m, int tid, int nthr) {
   int P2 = 1;
   while (P2 < m) P2 <<= 1;
   auto cx = [&](int lo, int hi) {
@@ -1082,6 +1121,17 @@ __device__ __forceinline__ void cta_sort_ints(int* a, int m, int tid, int nthr) 
 // cells with more particles than this are ordered by cta_sort_ints instead of per-particle
 // ranks (O(count) each): a compressed pile-up stays O(n log^2 n) instead of O(n^2)
 constexpr int kRankMax = 32;
+
+// the crowded cells of a block: buf (cell-grouped storage indices) sorted per cell into perm
+// (out of line: the common path only tests a flag)
+__device__ __noinline__ void sort_crowded_cells(int* perm, int* buf, const int* s_cstart, int tid) {
+  for (int c = 0; c < kCPB; ++c) {  // uniform: s_cstart is shared
+    const int lo = s_cstart[c], hi = s_cstart[c + 1];
+    if (hi - lo <= kRankMax) continue;
+    cta_sort_ints(buf + lo, hi - lo, tid, kThreads);  // storage indices ascending = stable order
+    for (int i = tid; i < hi - lo; i += kThreads) perm[lo + i] = buf[lo + i];
+  }
+}
 
 // Forward in-block sort (P2G prologue): the block's particles, grouped by k_scatter in
 // (storage index, key) pairs, are sorted by (cell, storage index) (stable, R18) into
@@ -1115,8 +1165,14 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
   }
   for (int i = tid + 2 * kThreads; i < n; i += kThreads) atomicAdd(&s_hist[A.tmp_pk[s + i].y & (kCPB - 1)], 1);
   __syncthreads();
+  __shared__ int s_crowd;  // some cell holds more than kRankMax particles (a pile-up)
   cell_scan(s_hist, s_cstart, s_cursor, tid);
+  if (tid < 32) {
+    const bool cr = __any_sync(0xffffffffu, (s_hist[tid] > kRankMax) | (s_hist[tid + 32] > kRankMax));
+    if (tid == 0) s_crowd = cr;
+  }
   __syncthreads();
+  const bool crowd = s_crowd;
   int* buf = (n <= kSortCap) ? s_sort : (A.scratch + s);
 #pragma unroll
   for (int q = 0; q < 2; ++q)
@@ -1137,17 +1193,12 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
     for (int step = kCPB / 2; step > 0; step >>= 1)
       if (s_cstart[c + step] <= i) c += step;
     const int lo = s_cstart[c], hi = s_cstart[c + 1];
-    if (hi - lo > kRankMax) continue;  // a crowded cell: sorted below
+    if (crowd && hi - lo > kRankMax) continue;  // a crowded cell: sorted below
     int rank = 0;
     for (int q = lo; q < hi; ++q) rank += buf[q] < j;
     A.perm[s + lo + rank] = j;  // stable: ties by storage index (R18)
   }
-  for (int c = 0; c < kCPB; ++c) {  // uniform: s_cstart is shared
-    const int lo = s_cstart[c], hi = s_cstart[c + 1];
-    if (hi - lo <= kRankMax) continue;
-    cta_sort_ints(buf + lo, hi - lo, tid, kThreads);  // storage indices ascending = stable order
-    for (int i = tid; i < hi - lo; i += kThreads) A.perm[s + lo + i] = buf[lo + i];
-  }
+  if (crowd) sort_crowded_cells(A.perm + s, buf, s_cstart, tid);
   __syncthreads();
 }
 
@@ -2501,6 +2552,246 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
 }
 
 // ------------------------------------------------------------------------------------
+// Fused reverse step (the mirror of the forward's G2P2G): k_p2g2p_adj runs P2G^T of step t
+// (as k_p2g_adj) and, with the adjoint of state t just computed for the particle, the G2P^T of
+// step t-1 -- steps A, B with x^{t-1}, F^{t-1}, the payload
+// u(o) = g_v + 4 res g_C (o - fx^{t-1}) and the scatter into the adjoint grid of step t-1
+// (step C) through an in-CTA counting sort by the step-(t-1) cell, the tile consumer
+// and one RED flush per tile node; a particle whose step-(t-1) cell lies outside the CTA's block
+// (it changed block between t-1 and t) adds its nodes with direct REDs.  Saves G2P^T's re-read
+// of the particle adjoint (96 B per particle) and one launch per reverse step.  The running-loss
+// seed of state t (N4) is added in registers before the payload; the controller (N1), slab
+// windows, migration and checkpoint boundaries keep the unfused order.
+// ------------------------------------------------------------------------------------
+constexpr int kFRT = 256;  // threads of the fused reverse kernel (the consumer needs 3 x 64)
+
+template <int D>
+__device__ __forceinline__ void scatter_escapees_adj(const StepArgs& A, int r, const int* bc,
+                                                     const float (*s_pay)[kFRT], const short* s_cell,
+                                                     const short* s_ord, int nesc, int it, int nthr, int nb,
+                                                     int nbpa, int base_prev) {
+  using DD = Dim<D>;
+  using PY = PayFA<D>;
+  constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
+  for (int idx = it; idx < nesc * DD::NS; idx += nthr) {
+    const int e = idx / DD::NS;
+    int q = idx - e * DD::NS;
+    const int pi = s_ord[kFRT - 1 - e];
+    const int pk = -2 - (int)s_cell[pi];
+    const int ps = pay_slot(pi);
+    int o[D], nb_[D], loc[D];
+    float W = 1.f;
+#pragma unroll
+    for (int a = D - 1; a >= 0; --a) {
+      o[a] = q % 3;
+      q /= 3;
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int lb = ((pk >> (EB * (D - 1 - a))) & (2 * EO - 1)) - EO;
+      const int node = bc[a] * DD::BB + lb + o[a];
+      W *= bspl(s_pay[PY::W + a][ps], o[a]);
+      nb_[a] = node >> DD::LOG_BB;
+      loc[a] = node & (DD::BB - 1);
+    }
+    const int slot = __ldg(&A.slot_prev[r * nb + block_lin<D>(nb_, nbpa)]);
+    if (slot < 0) continue;  // cannot happen: the node is in a touched block of step t-1
+    float val[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      float acc = s_pay[PY::A + a][ps];
+#pragma unroll
+      for (int b = 0; b < D; ++b) acc = fmaf((float)o[b], s_pay[PY::B + a * D + b][ps], acc);
+      val[a] = W * acc;
+    }
+    atomicAdd(A.agrid_t1 + (size_t)(slot - base_prev) * kCPB + cell_lin<D>(loc), make_float4(val[0], val[1], val[2], 0.f));
+  }
+}
+
+template <int D, bool MG, int MAT>
+__global__ __launch_bounds__(kFRT, 2) void k_p2g2p_adj(KParams P, StepArgs A) {
+  MPM_PDL_ENTRY();
+  using DD = Dim<D>;
+  using PY = PayFA<D>;
+  constexpr int NW = kFRT / 32, BB = DD::BB, TN = DD::TN;
+  constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
+  __shared__ float4 s_v[TN];
+  __shared__ float4 s_a[TN];
+  __shared__ float4 s_tile[3][TN];
+  __shared__ float s_pay[PY::N][kFRT];
+  __shared__ short s_cell[kFRT], s_ord[kFRT];
+  __shared__ int s_hist[kCPB], s_cstart[kCPB + 1], s_cursor[kCPB];
+  __shared__ int s_blk, s_nesc;
+  __shared__ float s_da[NW][kMaxAct * D];
+  __shared__ int s_da_r;
+  const int tid = threadIdx.x;
+  const int n_occ = A.info_t[I_NOCC];
+  const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
+  const int base_prev = A.info_gprev[I_BASE];
+  const size_t NT = P.NT;
+  const int KD = P.K * D;
+  const int ox = tid / kCPB;
+  const int c = D == 3 ? ((((tid >> 2) & 3) * 4 + ((tid >> 4) & 3)) * 4 + (tid & 3)) : tid % kCPB;
+  for (int q = tid; q < NW * kMaxAct * D; q += kFRT) (&s_da[0][0])[q] = 0.f;
+  if (tid == 0) s_da_r = -1;
+  auto flush_da = [&](int rr) {
+    for (int q = tid; q < KD; q += kFRT) {
+      float v = 0.f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        v += s_da[w][q];
+        s_da[w][q] = 0.f;
+      }
+      if (v != 0.f) atomicAdd(&A.da[((size_t)rr * P.T + A.t) * KD + q], v);
+    }
+  };
+  for (;;) {
+    if (tid == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
+    __syncthreads();
+    int gb, s, n;
+    if (!work_item<false>(A, s_blk, n_occ, 1, gb, s, n)) break;
+    int r, bc[D];
+    block_coords<D>(P, gb, r, bc);
+    if (KD > 0 && r != s_da_r) {
+      if (s_da_r >= 0) flush_da(s_da_r);
+      __syncthreads();
+      if (tid == 0) s_da_r = r;
+    }
+    int myslot = -1;  // adjoint grid t-1 slots of the tile's blocks bc + {0, 1}^D (flush)
+    {
+      const int lane = tid & 31;
+      if (lane < (1 << D)) {
+        int nb_[D];
+        bool inside = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          nb_[a] = bc[a] + ((lane >> (D - 1 - a)) & 1);
+          inside &= nb_[a] < P.nbpa;
+        }
+        if (inside) myslot = __ldg(&A.slot_prev[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
+      }
+    }
+    for (int i = tid; i < 3 * TN; i += kFRT) (&s_tile[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 vref, aref;
+    stage_tile<D, true, kFRT>(P, A, r, bc, s_v, s_a, abase, vref, aref);
+    __syncthreads();
+    for (int i0 = 0; i0 < n; i0 += kFRT) {  // rounds of kFRT particles: uniform trip count
+      if (tid < kCPB) s_hist[tid] = 0;
+      if (tid == 0) s_nesc = 0;
+      const int i = i0 + tid;
+      int ai = -1;
+      float dsig[D] = {};
+      if (i < n) p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
+      __syncwarp();
+      if (P.K > 0) reduce_actuation<D>(s_da[tid >> 5], ai, dsig);
+      __syncthreads();  // s_hist, s_nesc reset
+      // ---- G2P^T of step t-1 for this particle: its adjoint of state t is at storage index
+      //      j (written just above by this thread) ----
+      int cell = -1;
+      if (i < n) {
+        const int k = s + i;
+        const int j = __ldg(&A.perm[k]);
+        const int jp = __ldg(&A.perm_prev[j]);  // its storage index in state t-1
+        const float* g = A.gout;
+        float gx[D], gv[D], gC[D][D], gF[D][D], x[D], Fp[D][D];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          gx[a] = __ldcg(&g[(size_t)comp_x<D>(a) * NT + j]);
+          gv[a] = __ldcg(&g[(size_t)comp_v<D>(a) * NT + j]);
+          x[a] = __ldg(&A.st_prev[(size_t)comp_x<D>(a) * NT + jp]);
+#pragma unroll
+          for (int b = 0; b < D; ++b) {
+            gC[a][b] = __ldcg(&g[(size_t)comp_C<D>(a, b) * NT + j]);
+            gF[a][b] = __ldcg(&g[(size_t)comp_F<D>(a, b) * NT + j]);
+            Fp[a][b] = __ldg(&A.st_prev[(size_t)comp_F<D>(a, b) * NT + jp]) + (a == b ? 1.f : 0.f);
+          }
+        }
+        if (A.seed_t) {  // N4: the running-loss seed of state t, before it flows into step t-1
+          const int u = __ldg(&A.orig_next[k]);
+          const size_t NU = A.NU;
+          const float* sd = A.seed_t;
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            gx[a] += sd[(size_t)u * D + a];
+            gv[a] += sd[NU * D + (size_t)u * D + a];
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+              gF[a][b] += sd[2 * NU * D + ((size_t)u * D + a) * D + b];
+              gC[a][b] += sd[2 * NU * D + NU * D * D + ((size_t)u * D + a) * D + b];
+            }
+          }
+        }
+        Stencil<D> sc;
+        make_stencil<D>(x, P.fres, sc);
+        // steps A and B: g_v = gv + dt gx ; g_C = gC + dt gF F^T ; payload A = g_v - B fx, B = 4 res g_C
+        float Bm[D][D], Av[D];
+        const float s4 = 4.f * P.fres;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+          for (int b = 0; b < D; ++b) {
+            float acc = gC[a][b];
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) acc = fmaf(P.dt * gF[a][cc], Fp[b][cc], acc);
+            Bm[a][b] = s4 * acc;
+          }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          float acc = fmaf(P.dt, gx[a], gv[a]);
+#pragma unroll
+          for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], sc.fx[b], acc);
+          Av[a] = acc;
+        }
+        const int ps = pay_slot(tid);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          s_pay[PY::W + a][ps] = sc.fx[a];
+          s_pay[PY::A + a][ps] = Av[a];
+#pragma unroll
+          for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][ps] = Bm[a][b];
+        }
+        int lb[D];
+        bool inb = true;
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+          lb[a] = sc.base[a] - bc[a] * BB;
+          inb &= (lb[a] >= 0) & (lb[a] < BB);
+        }
+        if (inb) {
+          cell = cell_lin<D>(lb);
+          atomicAdd(&s_hist[cell], 1);
+        } else {  // the particle changed block between t-1 and t (CFL: within a few cells)
+          int pk = 0;
+#pragma unroll
+          for (int a = 0; a < D; ++a) pk = (pk << EB) | ((lb[a] + EO) & (2 * EO - 1));
+          cell = -2 - pk;
+          s_ord[kFRT - 1 - atomicAdd(&s_nesc, 1)] = (short)tid;
+        }
+      }
+      s_cell[tid] = (short)cell;
+      __syncthreads();
+      cell_scan(s_hist, s_cstart, s_cursor, tid);
+      __syncthreads();
+      {
+        const int cl = s_cell[tid];
+        if (cl >= 0) s_ord[atomicAdd(&s_cursor[cl], 1)] = (short)tid;
+      }
+      __syncthreads();
+      const int c0 = tid < 3 * kCPB ? s_cstart[c] : 0;
+      const int c1 = tid < 3 * kCPB ? s_cstart[c + 1] : 0;
+      scatter_consume<D, true, true, kFRT, true>(s_pay, s_tile, c0, c1, s_ord, ox, c, tid);
+      if (tid >= 3 * kCPB)
+        scatter_escapees_adj<D>(A, r, bc, s_pay, s_cell, s_ord, s_nesc, tid - 3 * kCPB, kFRT - 3 * kCPB, P.nb,
+                                P.nbpa, base_prev);
+      __syncthreads();  // payload consumed before the next round overwrites it
+    }
+    scatter_flush<D, true>(P, A.agrid_t1, s_tile, bc, myslot, base_prev, tid);
+    __syncthreads();
+  }
+  if (KD > 0 && s_da_r >= 0) flush_da(s_da_r);
+}
+
+// ------------------------------------------------------------------------------------
 // NEXT N1: closed-loop controller embedded in P2G (Fig. 2 caption P:84):
 //   z_t = [target, CoM_k, V_k (k < K)] per rollout, CoM_k / V_k = mass-weighted means over the
 //   particles of actuator group k (DESIGN R20);  a_t = tanh(W z_t + b) -> act[r][t][k][:].
@@ -2733,6 +3024,121 @@ __global__ void k_band_unpack(int nblk, int gb_lo, int gb_hi, const int* __restr
   }
 }
 
+// ------------------------------------------------------------------------------------
+// Migrating slab mode (SURVEY 8e "migrating particles"): a particle is owned, at every step, by
+// the slab whose [own_lo, own_hi) holds its base_x.  After G2P of step t the particles that left
+// (mig_pack, in g2p_particle) sit in the send buffers; the neighbours' buffers are received and
+// appended behind the n_t particles G2P wrote (storage slots [n_t, n_t + a_L + a_R) of state
+// t+1, left arrivals first).  The send buffers stay on the tape: the backward sends the adjoint
+// of every arrival slot back to the rank it came from and writes the adjoints coming back into
+// the slots the leavers left (their sorted slots k, recorded in the records).
+// ------------------------------------------------------------------------------------
+// after G2P of step t: the particles of state t+1 (slots [0, n_t)) whose base_x left the slab
+// become holes (kDeadKey, taken out of the block histogram G2P built) and their records go to
+// the send buffer of that side (record order = arrival order at the neighbour)
+template <int D>
+__global__ void k_mig_leavers(KParams P, const int* __restrict__ block_start_t, const float* __restrict__ st_next,
+                              const int* __restrict__ orig_next, int* __restrict__ key, int* __restrict__ cnt,
+                              float* __restrict__ send_l, float* __restrict__ send_r, ErrLatch* err, int t) {
+  MPM_PDL_ENTRY();
+  using MG = Mig<D>;
+  const int nt = block_start_t[P.NBT];
+  const size_t NT = P.NT;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nt; j += gridDim.x * blockDim.x) {
+    const int bx = base_of(st_next[(size_t)comp_x<D>(0) * NT + j], P.fres);
+    if (bx >= P.own_lo && bx < P.own_hi) continue;
+    const int kj = key[j];
+    if (kj >= 0) atomicSub(&cnt[kj / kCPB], 1);
+    key[j] = kDeadKey;
+    float* buf = bx < P.own_lo ? send_l : send_r;
+    const int pos = atomicAdd(reinterpret_cast<int*>(buf), 1);
+    if (pos >= P.mig_cap) {
+      latch(err, E_MIGRATE, t + 1, orig_next[j]);
+      continue;
+    }
+    float* rec = buf + MG::HDR + (size_t)pos * MG::R;
+    for (int c = 0; c < MG::S; ++c) rec[c] = st_next[(size_t)c * NT + j];
+    rec[MG::U] = __int_as_float(orig_next[j]);
+    rec[MG::K] = __int_as_float(j);
+  }
+}
+
+template <int D>
+__global__ void k_mig_append(KParams P, const float* __restrict__ recv_l, const float* __restrict__ recv_r,
+                             const int* __restrict__ block_start_t, float* __restrict__ st_next,
+                             int* __restrict__ orig_next, int* __restrict__ key, int* __restrict__ cnt,
+                             int* __restrict__ info_next, ErrLatch* err, int t) {
+  MPM_PDL_ENTRY();
+  using MG = Mig<D>;
+  const int nt = block_start_t[P.NBT];  // particles G2P wrote (live at step t)
+  const int al = recv_l ? min(*reinterpret_cast<const int*>(recv_l), P.mig_cap) : 0;
+  const int ar = recv_r ? min(*reinterpret_cast<const int*>(recv_r), P.mig_cap) : 0;
+  const size_t NT = P.NT;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (nt + al + ar > P.NT) latch(err, E_MIGRATE, t + 1, nt + al + ar);
+    info_next[I_NSLOT] = min(nt + al + ar, P.NT);
+  }
+  for (int i0 = blockIdx.x * blockDim.x; i0 < al + ar; i0 += gridDim.x * blockDim.x) {  // warp-uniform trips
+    const int i = i0 + threadIdx.x;
+    const int j = nt + i;
+    bool valid = i < al + ar && j < P.NT;
+    int gb = 0;
+    if (valid) {
+      const float* rec = (i < al ? recv_l + MG::HDR + (size_t)i * MG::R : recv_r + MG::HDR + (size_t)(i - al) * MG::R);
+      for (int c = 0; c < MG::S; ++c) st_next[(size_t)c * NT + j] = rec[c];
+      orig_next[j] = __float_as_int(rec[MG::U]);
+      float x[D];
+#pragma unroll
+      for (int a = 0; a < D; ++a) x[a] = rec[comp_x<D>(a)];
+      int k;
+      if (const int e = key_of<D>(x, 0, P, gb, k)) latch(err, e, t + 1, orig_next[j]);
+      const int bx = base_of(x[0], P.fres);
+      if (bx < P.own_lo || bx >= P.own_hi) latch(err, E_MIGRATE, t + 1, orig_next[j]);  // crossed a whole slab
+      key[j] = k;
+    }
+    warp_hist_add(cnt, gb, valid);
+  }
+}
+
+// backward, before G2P^T of step t: the adjoint of state t+1 at this rank's arrival slots goes
+// back to the sender (left arrivals to the left, right ones to the right, in arrival order)
+template <int D>
+__global__ void k_mig_rev_pack(KParams P, const float* __restrict__ recv_l, const float* __restrict__ recv_r,
+                               const int* __restrict__ block_start_t, const float* __restrict__ g,
+                               float* __restrict__ out_l, float* __restrict__ out_r) {
+  MPM_PDL_ENTRY();
+  using MG = Mig<D>;
+  const int nt = block_start_t[P.NBT];
+  const int al = recv_l ? min(*reinterpret_cast<const int*>(recv_l), P.mig_cap) : 0;
+  const int ar = recv_r ? min(*reinterpret_cast<const int*>(recv_r), P.mig_cap) : 0;
+  const size_t NT = P.NT;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (al + ar) * MG::S; q += gridDim.x * blockDim.x) {
+    const int i = q / MG::S, c = q - i * MG::S;
+    const int j = nt + i;
+    if (j >= P.NT) continue;
+    float* out = i < al ? out_l + (size_t)i * MG::S : out_r + (size_t)(i - al) * MG::S;
+    out[c] = g[(size_t)c * NT + j];
+  }
+}
+
+// ... and the adjoints coming back from the neighbours fill the slots of this rank's leavers
+template <int D>
+__global__ void k_mig_rev_unpack(KParams P, const float* __restrict__ sent_l, const float* __restrict__ sent_r,
+                                 const float* __restrict__ in_l, const float* __restrict__ in_r, float* __restrict__ g) {
+  MPM_PDL_ENTRY();
+  using MG = Mig<D>;
+  const int nl = sent_l ? min(*reinterpret_cast<const int*>(sent_l), P.mig_cap) : 0;
+  const int nr = sent_r ? min(*reinterpret_cast<const int*>(sent_r), P.mig_cap) : 0;
+  const size_t NT = P.NT;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (nl + nr) * MG::S; q += gridDim.x * blockDim.x) {
+    const int i = q / MG::S, c = q - i * MG::S;
+    const float* rec = i < nl ? sent_l + MG::HDR + (size_t)i * MG::R : sent_r + MG::HDR + (size_t)(i - nl) * MG::R;
+    const float* in = i < nl ? in_l + (size_t)i * MG::S : in_r + (size_t)(i - nl) * MG::S;
+    const int k = __float_as_int(rec[MG::K]);
+    g[(size_t)c * NT + k] = in[c];
+  }
+}
+
 __global__ void k_add_inplace(size_t n, float* __restrict__ a, const float* __restrict__ b) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     a[i] += b[i];
@@ -2795,10 +3201,11 @@ __global__ void k_grid_adj(KParams P, const int* __restrict__ info_t, const int*
 template <int D>
 __global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __restrict__ gx,
                        const float* __restrict__ gv, const float* __restrict__ gF,
-                       const float* __restrict__ gC, float* __restrict__ g, int accumulate) {
+                       const float* __restrict__ gC, float* __restrict__ g, int accumulate,
+                       const int* __restrict__ nslot) {
   MPM_PDL_ENTRY();
   int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= P.NT) return;
+  if (k >= (nslot ? *nslot : P.NT)) return;  // migrating slab mode: the state's storage slots
   const size_t NT = P.NT;
   int u = orig[k];
   auto put = [&](int comp, float val) {
@@ -2817,13 +3224,19 @@ __global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __r
   }
 }
 
-// SoA storage order -> user AoS (x, v, F, C), any may be null
+// SoA storage order -> user AoS (x, v, F, C), any may be null.  Migrating slab mode: only the
+// slots [0, *nslot) whose particle this slab owns in `owner` (the state's positions) are written.
 template <int D>
 __global__ void k_soa_to_user(KParams P, const int* __restrict__ orig, const float* __restrict__ st,
-                              float* x, float* v, float* F, float* C, int state) {
+                              float* x, float* v, float* F, float* C, int state,
+                              const int* __restrict__ nslot = nullptr, const float* __restrict__ owner = nullptr) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.NT) return;
+  if (j >= (nslot ? *nslot : P.NT)) return;
   const size_t NT = P.NT;
+  if (owner) {
+    const int bx = base_of(owner[(size_t)comp_x<D>(0) * NT + j], P.fres);
+    if (bx < P.own_lo || bx >= P.own_hi) return;  // a hole: the particle is the neighbour's now
+  }
   int u = orig ? orig[j] : j;
 #pragma unroll
   for (int a = 0; a < D; ++a) {

@@ -22,7 +22,7 @@ LIB_PATH = os.path.join(_HERE, "libmpm.so")
 STATUS = {0: "MPM_OK", 1: "MPM_ERR_INVALID_ARG", 2: "MPM_ERR_OOM", 3: "MPM_ERR_CUDA",
           4: "MPM_ERR_OUT_OF_DOMAIN", 5: "MPM_ERR_INVERTED", 6: "MPM_ERR_TAPE_FULL",
           7: "MPM_ERR_CALL_ORDER", 8: "MPM_ERR_COMM", 9: "MPM_ERR_OUT_OF_SLAB",
-          10: "MPM_ERR_CFL"}
+          10: "MPM_ERR_CFL", 11: "MPM_ERR_MIGRATE"}
 
 # every symbol include/mpm.h declares
 EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "mpm_forward",
@@ -31,7 +31,14 @@ EXPORTS = ("mpm_create", "mpm_destroy", "mpm_set_state", "mpm_set_actuation", "m
            "mpm_get_profile", "mpm_launch_count", "mpm_get_step_info", "mpm_grad_mass",
            "mpm_add_seed", "mpm_clear_seeds", "mpm_enable_mass_grad", "mpm_set_slab",
            "mpm_comm_unique_id", "mpm_comm_init", "mpm_group_forward", "mpm_group_backward",
-           "mpm_set_controller", "mpm_grad_controller", "mpm_set_graphs")
+           "mpm_set_controller", "mpm_grad_controller", "mpm_set_graphs", "mpm_set_slab_migrating",
+           "mpm_set_transport")
+
+
+# int fn(void* user, int32 kind, const float* send_l, const float* send_r, float* recv_l,
+#        float* recv_r, size_t bytes)   (include/mpm.h mpm_transport_fn)
+_TRANSPORT_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                            C.c_size_t)
 
 
 class MPMError(RuntimeError):
@@ -91,6 +98,8 @@ def load():
     L.mpm_set_controller.argtypes = [vp, vp, vp, vp]
     L.mpm_grad_controller.argtypes = [vp, vp, vp, vp]
     L.mpm_set_slab.argtypes = [vp, i32, i32, i32]
+    L.mpm_set_slab_migrating.argtypes = [vp, i32, i32, i32, i32, i32]
+    L.mpm_set_transport.argtypes = [vp, _TRANSPORT_FN, vp]
     L.mpm_comm_unique_id.argtypes = [C.c_char_p]
     L.mpm_comm_init.argtypes = [vp, i32, i32, C.c_char_p]
     L.mpm_group_forward.argtypes = [C.POINTER(vp), i32, i32]
@@ -230,12 +239,18 @@ class MPM:
 
     @property
     def NT(self):
+        """Storage capacity (batch x n_particles)."""
         return self.cfg.batch * self.cfg.n_particles
+
+    @property
+    def NU(self):
+        """Length of the user-order arrays: NT, or the whole body's count in migrating slab mode."""
+        return getattr(self, "_nu", None) or self.NT
 
     # -- the path -----------------------------------------------------------------------
     def set_state(self, x, v=None, F=None, C_=None, mass=None, vol=None, E=None, nu=None,
                   actuator_id=None):
-        d, NT, dev = self.cfg.dim, self.NT, self.cfg.device
+        d, NT, dev = self.cfg.dim, self.NU, self.cfg.device
         arrs = [_in(x, np.float32, (NT, d), dev, "x"), _in(v, np.float32, (NT, d), dev, "v"),
                 _in(F, np.float32, (NT, d, d), dev, "F"), _in(C_, np.float32, (NT, d, d), dev, "C"),
                 _in(mass, np.float32, (NT,), dev, "mass"), _in(vol, np.float32, (NT,), dev, "vol"),
@@ -267,7 +282,7 @@ class MPM:
         return self.L.mpm_tape_length(self.h)
 
     def get_state(self, t: int, out=None):
-        d, NT = self.cfg.dim, self.NT
+        d, NT = self.cfg.dim, self.NU
         if out is None:
             out = (np.empty((NT, d), np.float32), np.empty((NT, d), np.float32),
                    np.empty((NT, d, d), np.float32), np.empty((NT, d, d), np.float32))
@@ -277,14 +292,14 @@ class MPM:
         return out
 
     def backward(self, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
-        d, NT, dev = self.cfg.dim, self.NT, self.cfg.device
+        d, NT, dev = self.cfg.dim, self.NU, self.cfg.device
         arrs = [_in(dLdx, np.float32, (NT, d), dev, "dLdx"), _in(dLdv, np.float32, (NT, d), dev, "dLdv"),
                 _in(dLdF, np.float32, (NT, d, d), dev, "dLdF"), _in(dLdC, np.float32, (NT, d, d), dev, "dLdC")]
         self._check(self.L.mpm_backward(self.h, *[_ptr(a) for a in arrs]))
 
     def grad(self, out=None):
         cfg = self.cfg
-        d, NT = cfg.dim, self.NT
+        d, NT = cfg.dim, self.NU
         if out is None:
             out = dict(dx0=np.empty((NT, d), np.float32), dv0=np.empty((NT, d), np.float32),
                        dF0=np.empty((NT, d, d), np.float32), dC0=np.empty((NT, d, d), np.float32),
@@ -306,14 +321,14 @@ class MPM:
     def grad_mass(self, out=None):
         """dL/dm_p (NEXT N3) from the last backward, user order [B*N]."""
         if out is None:
-            out = np.empty(self.NT, np.float32)
-        out = _out(out, np.float32, (self.NT,), self.cfg.device, "dmass")
+            out = np.empty(self.NU, np.float32)
+        out = _out(out, np.float32, (self.NU,), self.cfg.device, "dmass")
         self._check(self.L.mpm_grad_mass(self.h, _ptr(out)))
         return out
 
     def add_seed(self, t, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
         """Additive seed dL/dstate_t for a running loss (NEXT N4)."""
-        d, NT, dev = self.cfg.dim, self.NT, self.cfg.device
+        d, NT, dev = self.cfg.dim, self.NU, self.cfg.device
         arrs = [_in(dLdx, np.float32, (NT, d), dev, "dLdx"), _in(dLdv, np.float32, (NT, d), dev, "dLdv"),
                 _in(dLdF, np.float32, (NT, d, d), dev, "dLdF"), _in(dLdC, np.float32, (NT, d, d), dev, "dLdC")]
         self._check(self.L.mpm_add_seed(self.h, int(t), *[_ptr(a) for a in arrs]))
@@ -346,6 +361,36 @@ class MPM:
         return out
 
     # -- slab mode -----------------------------------------------------------
+    def set_slab_migrating(self, x_lo: int, x_hi: int, halo_blocks: int, n_global: int, mig_cap: int = 0):
+        """Migrating slab mode (include/mpm.h): ownership by base_x at every step, particles
+        migrate between neighbouring slabs; user arrays span the whole body (n_global)."""
+        self._check(self.L.mpm_set_slab_migrating(self.h, int(x_lo), int(x_hi), int(halo_blocks), int(n_global),
+                                                  int(mig_cap)))
+        self._nu = int(n_global)
+
+    def set_transport(self, fn):
+        """Host-staged slab exchanges through fn(kind, send_l, send_r, recv_l, recv_r) with numpy
+        float32 views (None on a side without a neighbour); kind "reduce": overwrite send_l with
+        the sum over ranks.  fn=None unsets."""
+        if fn is None:
+            self._transport = None
+            self._check(self.L.mpm_set_transport(self.h, None, None))
+            return
+        kinds = {0: "window", 1: "migrate", 2: "migrate_adj", 3: "reduce"}
+
+        def cb(user, kind, sl, sr, rl, rr, nbytes):
+            try:
+                n = nbytes // 4
+                view = lambda p: None if not p else np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_float)), (n,))
+                fn(kinds[kind], view(sl), view(sr), view(rl), view(rr))
+                return 0
+            except Exception as e:  # noqa: BLE001 -- reported through the status code
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._transport = _TRANSPORT_FN(cb)  # keep alive while set
+        self._check(self.L.mpm_set_transport(self.h, self._transport, None))
+
     def set_slab(self, x_lo: int, x_hi: int, halo_blocks: int = 1):
         """This context simulates the x-slab [x_lo, x_hi) of node planes (before set_state)."""
         self._check(self.L.mpm_set_slab(self.h, int(x_lo), int(x_hi), int(halo_blocks)))
@@ -451,7 +496,7 @@ def group_backward(sims, dLdx=None, dLdv=None, dLdF=None, dLdC=None):
             ptrs.append(_ptr(a))
         return (C.c_void_p * len(sims))(*ptrs)
 
-    vec = lambda s: (s.NT, s.cfg.dim)
-    mat = lambda s: (s.NT, s.cfg.dim, s.cfg.dim)
+    vec = lambda s: (s.NU, s.cfg.dim)
+    mat = lambda s: (s.NU, s.cfg.dim, s.cfg.dim)
     args = [arr(dLdx, vec), arr(dLdv, vec), arr(dLdF, mat), arr(dLdC, mat)]
     _group_check(sims, L.mpm_group_backward(_handles(sims), len(sims), *args))
