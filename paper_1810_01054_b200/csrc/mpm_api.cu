@@ -86,8 +86,6 @@ struct mpm_ctx_s {
   int res_end = 0;  // the states of steps [seg0, res_end] on the tape are valid
   int fused_grid = -1;  // fused forward: the step whose grid the previous G2P2G already built
   int occ_fuse = 2;
-  int occ_frt = 2;      // fused reverse kernel k_p2g2p_adj
-  bool bfuse = false;   // fused reverse step (MPM_FUSE_BWD=1 enables; follows config.fuse_g2p2g)
   float* ck_state = nullptr;
   int* ck_orig = nullptr;
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
@@ -772,14 +770,6 @@ void launch_p2gT(mpm_ctx c, const KParams& P, const StepArgs& A, int na) {
 
 // backward step t = phase A ([zero,] G2P^T [, window pack]) | exchange | phase B ([unpack,]
 // grid^T, P2G^T); the particle adjoint flows c->bcur -> c->bnxt
-// The reverse step t runs fused with G2P^T of step t-1 (k_p2g2p_adj) when the fused mode is
-// on and nothing has to happen between P2G^T(t) and G2P^T(t-1): no controller adjoint (it
-// needs all of dL/da_t), no slab neighbours (window exchange), no migration, step t-1 in the
-// same tape segment; small problems keep the split kernels.
-bool bwd_fuse_at(mpm_ctx c, int t) {
-  return c->cfg.fuse_g2p2g && c->bfuse && !c->ctrl && !has_nbr(c) && !c->mig && !c->split && t - 1 >= c->seg0;
-}
-
 template <int D>
 void backward_phase_a(mpm_ctx c, int t) {
   const KParams& P = c->P;
@@ -789,7 +779,6 @@ void backward_phase_a(mpm_ctx c, int t) {
   A.gout = c->bnxt;
   if (t == c->seg_end - 1)  // first backward step of a segment: prepare its buffer (later: by grid_T)
     launch(c, KI_ZERO, [&] { kx(c, k_zero_slots, dim3(c->n_sm * 4), dim3(256), 0, info_at(c, t), A.grid); });
-  if (t + 1 < c->seg_end && bwd_fuse_at(c, t + 1)) return;  // G2P^T(t) ran inside k_p2g2p_adj of step t+1
   const int nbla = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter_adj));
   launch(c, KI_G2PT, [&] {
     if (c->split) kx(c, k_block_scatter<D, true, 0, true>, dim3(nbla), dim3(kThreads), scatter_dyn_smem<D, true>(), P, A);
@@ -810,31 +799,8 @@ void backward_phase_b(mpm_ctx c, int t) {
     kx(c, k_grid_adj<D>, dim3(c->n_sm * 8), dim3(256), 0, P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
                                                        t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
   });
-  if (bwd_fuse_at(c, t)) {
-    // fused reverse step: P2G^T of step t + G2P^T of step t-1 (k_p2g2p_adj); the adjoint grid
-    // of step t-1 was prepared by the grid^T above
-    A.st_prev = state_at(c, t - 1);
-    A.perm_prev = perm_at(c, t - 1);
-    A.slot_prev = slot_at(c, t - 1);
-    A.info_gprev = info_at(c, t - 1);
-    A.agrid_t1 = agrid_of(c, t - 1);
-    auto it = c->seeds.find(t);
-    A.seed_t = it == c->seeds.end() ? nullptr : it->second;
-    A.NU = (int)c->NU;
-    const int nf = std::max(1, std::min(P.NBT, c->n_sm * c->occ_frt));
-    launch(c, KI_P2GT, [&] {
-      if (c->mass_grad) {
-        if (P.material == 1) kx(c, k_p2g2p_adj<D, true, 1>, dim3(nf), dim3(kFRT), 0, P, A);
-        else kx(c, k_p2g2p_adj<D, true, 0>, dim3(nf), dim3(kFRT), 0, P, A);
-      } else {
-        if (P.material == 1) kx(c, k_p2g2p_adj<D, false, 1>, dim3(nf), dim3(kFRT), 0, P, A);
-        else kx(c, k_p2g2p_adj<D, false, 0>, dim3(nf), dim3(kFRT), 0, P, A);
-      }
-    });
-  } else {
-    const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
-    launch(c, KI_P2GT, [&] { launch_p2gT<D>(c, P, A, na); });
-  }
+  const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
+  launch(c, KI_P2GT, [&] { launch_p2gT<D>(c, P, A, na); });
   if (c->ctrl) {  // N1: controller adjoint of step t (needs this step's complete dL/da)
     const int KD = P.K * D;
     launch(c, KI_CTRLT, [&] {
@@ -1492,7 +1458,6 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   cudaDeviceGetAttribute(&c->n_sm, cudaDevAttrMultiProcessorCount, k.device);
   c->stream = (cudaStream_t)k.stream;
   if (const char* e = getenv("MPM_PDL")) c->pdl = atoi(e) != 0;
-  if (const char* e = getenv("MPM_FUSE_BWD")) c->bfuse = atoi(e) != 0;
   c->D = k.dim;
   c->S = 2 * k.dim + 2 * k.dim * k.dim;
   KParams& P = c->P;
@@ -1554,9 +1519,6 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p2g<2, 0, true, true>, kThreads, fuse_dyn_smem<2>());
     c->occ_fuse = std::max(1, occ);
   }
-  if (k.dim == 3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g2p_adj<3, false, 0>, kFRT, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_p2g2p_adj<2, false, 0>, kFRT, 0);
-  c->occ_frt = std::max(1, occ);
   if (k.dim == 3) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_g2p<3>, kThreads, 0);
     c->occ_g2p = std::max(1, occ);

@@ -974,14 +974,6 @@ struct StepArgs {
   float* dlam;
   float* dmass;           // [NT] user order (NEXT N3)
   float* da;              // [B][T][K][D]
-  // fused reverse step (k_p2g2p_adj): G2P^T of step t-1 from the adjoint P2G^T of step t produced
-  const float* st_prev;   // state t-1 (storage order t-1)
-  const int* perm_prev;   // sorted slot of step t-1 (= storage index of state t) -> storage index t-1
-  const int* slot_prev;   // grid-slot map of step t-1
-  const int* info_gprev;  // step record of t-1 (base slot of its adjoint grid)
-  float4* agrid_t1;       // adjoint grid of step t-1
-  const float* seed_t;    // running-loss seed of state t (user-order AoS x|v|F|C, NU rows) or null
-  int NU;                 // rows of seed_t
   ErrLatch* err;
   int t;
 };
@@ -2546,246 +2538,6 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       __syncwarp();
       if (P.K > 0) reduce_actuation<D>(s_da[threadIdx.x >> 5], ai, dsig);
     }
-    __syncthreads();
-  }
-  if (KD > 0 && s_da_r >= 0) flush_da(s_da_r);
-}
-
-// ------------------------------------------------------------------------------------
-// Fused reverse step (the mirror of the forward's G2P2G): k_p2g2p_adj runs P2G^T of step t
-// (as k_p2g_adj) and, with the adjoint of state t just computed for the particle, the G2P^T of
-// step t-1 -- steps A, B with x^{t-1}, F^{t-1}, the payload
-// u(o) = g_v + 4 res g_C (o - fx^{t-1}) and the scatter into the adjoint grid of step t-1
-// (step C) through an in-CTA counting sort by the step-(t-1) cell, the tile consumer
-// and one RED flush per tile node; a particle whose step-(t-1) cell lies outside the CTA's block
-// (it changed block between t-1 and t) adds its nodes with direct REDs.  Saves G2P^T's re-read
-// of the particle adjoint (96 B per particle) and one launch per reverse step.  The running-loss
-// seed of state t (N4) is added in registers before the payload; the controller (N1), slab
-// windows, migration and checkpoint boundaries keep the unfused order.
-// ------------------------------------------------------------------------------------
-constexpr int kFRT = 256;  // threads of the fused reverse kernel (the consumer needs 3 x 64)
-
-template <int D>
-__device__ __forceinline__ void scatter_escapees_adj(const StepArgs& A, int r, const int* bc,
-                                                     const float (*s_pay)[kFRT], const short* s_cell,
-                                                     const short* s_ord, int nesc, int it, int nthr, int nb,
-                                                     int nbpa, int base_prev) {
-  using DD = Dim<D>;
-  using PY = PayFA<D>;
-  constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
-  for (int idx = it; idx < nesc * DD::NS; idx += nthr) {
-    const int e = idx / DD::NS;
-    int q = idx - e * DD::NS;
-    const int pi = s_ord[kFRT - 1 - e];
-    const int pk = -2 - (int)s_cell[pi];
-    const int ps = pay_slot(pi);
-    int o[D], nb_[D], loc[D];
-    float W = 1.f;
-#pragma unroll
-    for (int a = D - 1; a >= 0; --a) {
-      o[a] = q % 3;
-      q /= 3;
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      const int lb = ((pk >> (EB * (D - 1 - a))) & (2 * EO - 1)) - EO;
-      const int node = bc[a] * DD::BB + lb + o[a];
-      W *= bspl(s_pay[PY::W + a][ps], o[a]);
-      nb_[a] = node >> DD::LOG_BB;
-      loc[a] = node & (DD::BB - 1);
-    }
-    const int slot = __ldg(&A.slot_prev[r * nb + block_lin<D>(nb_, nbpa)]);
-    if (slot < 0) continue;  // cannot happen: the node is in a touched block of step t-1
-    float val[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      float acc = s_pay[PY::A + a][ps];
-#pragma unroll
-      for (int b = 0; b < D; ++b) acc = fmaf((float)o[b], s_pay[PY::B + a * D + b][ps], acc);
-      val[a] = W * acc;
-    }
-    atomicAdd(A.agrid_t1 + (size_t)(slot - base_prev) * kCPB + cell_lin<D>(loc), make_float4(val[0], val[1], val[2], 0.f));
-  }
-}
-
-template <int D, bool MG, int MAT>
-__global__ __launch_bounds__(kFRT, 2) void k_p2g2p_adj(KParams P, StepArgs A) {
-  MPM_PDL_ENTRY();
-  using DD = Dim<D>;
-  using PY = PayFA<D>;
-  constexpr int NW = kFRT / 32, BB = DD::BB, TN = DD::TN;
-  constexpr int EB = Esc<D>::EB, EO = Esc<D>::EO;
-  __shared__ float4 s_v[TN];
-  __shared__ float4 s_a[TN];
-  __shared__ float4 s_tile[3][TN];
-  __shared__ float s_pay[PY::N][kFRT];
-  __shared__ short s_cell[kFRT], s_ord[kFRT];
-  __shared__ int s_hist[kCPB], s_cstart[kCPB + 1], s_cursor[kCPB];
-  __shared__ int s_blk, s_nesc;
-  __shared__ float s_da[NW][kMaxAct * D];
-  __shared__ int s_da_r;
-  const int tid = threadIdx.x;
-  const int n_occ = A.info_t[I_NOCC];
-  const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
-  const int base_prev = A.info_gprev[I_BASE];
-  const size_t NT = P.NT;
-  const int KD = P.K * D;
-  const int ox = tid / kCPB;
-  const int c = D == 3 ? ((((tid >> 2) & 3) * 4 + ((tid >> 4) & 3)) * 4 + (tid & 3)) : tid % kCPB;
-  for (int q = tid; q < NW * kMaxAct * D; q += kFRT) (&s_da[0][0])[q] = 0.f;
-  if (tid == 0) s_da_r = -1;
-  auto flush_da = [&](int rr) {
-    for (int q = tid; q < KD; q += kFRT) {
-      float v = 0.f;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        v += s_da[w][q];
-        s_da[w][q] = 0.f;
-      }
-      if (v != 0.f) atomicAdd(&A.da[((size_t)rr * P.T + A.t) * KD + q], v);
-    }
-  };
-  for (;;) {
-    if (tid == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
-    __syncthreads();
-    int gb, s, n;
-    if (!work_item<false>(A, s_blk, n_occ, 1, gb, s, n)) break;
-    int r, bc[D];
-    block_coords<D>(P, gb, r, bc);
-    if (KD > 0 && r != s_da_r) {
-      if (s_da_r >= 0) flush_da(s_da_r);
-      __syncthreads();
-      if (tid == 0) s_da_r = r;
-    }
-    int myslot = -1;  // adjoint grid t-1 slots of the tile's blocks bc + {0, 1}^D (flush)
-    {
-      const int lane = tid & 31;
-      if (lane < (1 << D)) {
-        int nb_[D];
-        bool inside = true;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          nb_[a] = bc[a] + ((lane >> (D - 1 - a)) & 1);
-          inside &= nb_[a] < P.nbpa;
-        }
-        if (inside) myslot = __ldg(&A.slot_prev[r * P.nb + block_lin<D>(nb_, P.nbpa)]);
-      }
-    }
-    for (int i = tid; i < 3 * TN; i += kFRT) (&s_tile[0][0])[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 vref, aref;
-    stage_tile<D, true, kFRT>(P, A, r, bc, s_v, s_a, abase, vref, aref);
-    __syncthreads();
-    for (int i0 = 0; i0 < n; i0 += kFRT) {  // rounds of kFRT particles: uniform trip count
-      if (tid < kCPB) s_hist[tid] = 0;
-      if (tid == 0) s_nesc = 0;
-      const int i = i0 + tid;
-      int ai = -1;
-      float dsig[D] = {};
-      if (i < n) p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
-      __syncwarp();
-      if (P.K > 0) reduce_actuation<D>(s_da[tid >> 5], ai, dsig);
-      __syncthreads();  // s_hist, s_nesc reset
-      // ---- G2P^T of step t-1 for this particle: its adjoint of state t is at storage index
-      //      j (written just above by this thread) ----
-      int cell = -1;
-      if (i < n) {
-        const int k = s + i;
-        const int j = __ldg(&A.perm[k]);
-        const int jp = __ldg(&A.perm_prev[j]);  // its storage index in state t-1
-        const float* g = A.gout;
-        float gx[D], gv[D], gC[D][D], gF[D][D], x[D], Fp[D][D];
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          gx[a] = __ldcg(&g[(size_t)comp_x<D>(a) * NT + j]);
-          gv[a] = __ldcg(&g[(size_t)comp_v<D>(a) * NT + j]);
-          x[a] = __ldg(&A.st_prev[(size_t)comp_x<D>(a) * NT + jp]);
-#pragma unroll
-          for (int b = 0; b < D; ++b) {
-            gC[a][b] = __ldcg(&g[(size_t)comp_C<D>(a, b) * NT + j]);
-            gF[a][b] = __ldcg(&g[(size_t)comp_F<D>(a, b) * NT + j]);
-            Fp[a][b] = __ldg(&A.st_prev[(size_t)comp_F<D>(a, b) * NT + jp]) + (a == b ? 1.f : 0.f);
-          }
-        }
-        if (A.seed_t) {  // N4: the running-loss seed of state t, before it flows into step t-1
-          const int u = __ldg(&A.orig_next[k]);
-          const size_t NU = A.NU;
-          const float* sd = A.seed_t;
-#pragma unroll
-          for (int a = 0; a < D; ++a) {
-            gx[a] += sd[(size_t)u * D + a];
-            gv[a] += sd[NU * D + (size_t)u * D + a];
-#pragma unroll
-            for (int b = 0; b < D; ++b) {
-              gF[a][b] += sd[2 * NU * D + ((size_t)u * D + a) * D + b];
-              gC[a][b] += sd[2 * NU * D + NU * D * D + ((size_t)u * D + a) * D + b];
-            }
-          }
-        }
-        Stencil<D> sc;
-        make_stencil<D>(x, P.fres, sc);
-        // steps A and B: g_v = gv + dt gx ; g_C = gC + dt gF F^T ; payload A = g_v - B fx, B = 4 res g_C
-        float Bm[D][D], Av[D];
-        const float s4 = 4.f * P.fres;
-#pragma unroll
-        for (int a = 0; a < D; ++a)
-#pragma unroll
-          for (int b = 0; b < D; ++b) {
-            float acc = gC[a][b];
-#pragma unroll
-            for (int cc = 0; cc < D; ++cc) acc = fmaf(P.dt * gF[a][cc], Fp[b][cc], acc);
-            Bm[a][b] = s4 * acc;
-          }
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          float acc = fmaf(P.dt, gx[a], gv[a]);
-#pragma unroll
-          for (int b = 0; b < D; ++b) acc = fmaf(-Bm[a][b], sc.fx[b], acc);
-          Av[a] = acc;
-        }
-        const int ps = pay_slot(tid);
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          s_pay[PY::W + a][ps] = sc.fx[a];
-          s_pay[PY::A + a][ps] = Av[a];
-#pragma unroll
-          for (int b = 0; b < D; ++b) s_pay[PY::B + a * D + b][ps] = Bm[a][b];
-        }
-        int lb[D];
-        bool inb = true;
-#pragma unroll
-        for (int a = 0; a < D; ++a) {
-          lb[a] = sc.base[a] - bc[a] * BB;
-          inb &= (lb[a] >= 0) & (lb[a] < BB);
-        }
-        if (inb) {
-          cell = cell_lin<D>(lb);
-          atomicAdd(&s_hist[cell], 1);
-        } else {  // the particle changed block between t-1 and t (CFL: within a few cells)
-          int pk = 0;
-#pragma unroll
-          for (int a = 0; a < D; ++a) pk = (pk << EB) | ((lb[a] + EO) & (2 * EO - 1));
-          cell = -2 - pk;
-          s_ord[kFRT - 1 - atomicAdd(&s_nesc, 1)] = (short)tid;
-        }
-      }
-      s_cell[tid] = (short)cell;
-      __syncthreads();
-      cell_scan(s_hist, s_cstart, s_cursor, tid);
-      __syncthreads();
-      {
-        const int cl = s_cell[tid];
-        if (cl >= 0) s_ord[atomicAdd(&s_cursor[cl], 1)] = (short)tid;
-      }
-      __syncthreads();
-      const int c0 = tid < 3 * kCPB ? s_cstart[c] : 0;
-      const int c1 = tid < 3 * kCPB ? s_cstart[c + 1] : 0;
-      scatter_consume<D, true, true, kFRT, true>(s_pay, s_tile, c0, c1, s_ord, ox, c, tid);
-      if (tid >= 3 * kCPB)
-        scatter_escapees_adj<D>(A, r, bc, s_pay, s_cell, s_ord, s_nesc, tid - 3 * kCPB, kFRT - 3 * kCPB, P.nb,
-                                P.nbpa, base_prev);
-      __syncthreads();  // payload consumed before the next round overwrites it
-    }
-    scatter_flush<D, true>(P, A.agrid_t1, s_tile, bc, myslot, base_prev, tid);
     __syncthreads();
   }
   if (KD > 0 && s_da_r >= 0) flush_da(s_da_r);
