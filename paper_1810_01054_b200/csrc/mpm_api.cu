@@ -91,6 +91,7 @@ struct mpm_ctx_s {
   bool has_state = false, has_act = false, has_grad = false, poisoned = false;
   std::string last_error;
   int64_t launches = 0;
+  MigParams M{0, INT32_MIN, INT32_MAX, 0};  // migrating slab mode
   int latch_step = -1;  // step of the last latched device error (check_latch)
   // tape
   float* tape_state = nullptr;
@@ -299,7 +300,7 @@ int* info_at(mpm_ctx c, int t) { return c->info + ti(c, t) * kInfo; }
 float* mig_send_at(mpm_ctx c, int t, int side) { return c->mig_send_tape + ((size_t)ti(c, t) * 2 + side) * c->mig_floats; }
 float* mig_recv_at(mpm_ctx c, int t, int side) { return c->mig_recv_tape + ((size_t)ti(c, t) * 2 + side) * c->mig_floats; }
 const int* nslot_at(mpm_ctx c, int t) { return c->mig ? info_at(c, t) + I_NSLOT : nullptr; }
-size_t rev_floats(mpm_ctx c) { return (size_t)c->P.mig_cap * c->S; }
+size_t rev_floats(mpm_ctx c) { return (size_t)c->M.mig_cap * c->S; }
 
 bool on_tape(mpm_ctx c, int t) { return t >= c->seg0 && t <= c->res_end && t <= c->tape_len; }
 float* ck_state_of(mpm_ctx c, int i) { return c->ck_state + (size_t)i * c->S * NTs(c); }
@@ -346,7 +347,7 @@ mpm_status check_latch(mpm_ctx c) {
   if (h.code == E_MIGRATE) {
     snprintf(buf, sizeof buf, "migrating slab mode at step %d: more leavers per side than mig_cap (%d), more "
              "particles than the storage capacity, or a particle that crossed a whole slab (%d)", h.step,
-             c->P.mig_cap, h.particle);
+             c->M.mig_cap, h.particle);
     c->poisoned = true;
     return fail(c, MPM_ERR_MIGRATE, buf);
   }
@@ -370,7 +371,7 @@ void launch_keys(mpm_ctx c, int t) {
   int* orig0 = (t == 0 && !c->mig) ? orig_at(c, 0) : nullptr;
   launch(c, KI_MISC, [&] {
     k_init_keys<D><<<grid1d(P.NT), 256, 0, c->stream>>>(P, state_at(c, t), c->key, c->cnt, orig0, c->err,
-                                                         nslot_at(c, t));
+                                                         nslot_at(c, t), c->M);
   });
 }
 
@@ -620,7 +621,7 @@ void forward_phase_b(mpm_ctx c, int t) {
   if (c->mig) {  // migrating slab mode: the particles of state t+1 that left the slab
     for (int side = 0; side < 2; ++side) cudaMemsetAsync(mig_send_at(c, t, side), 0, Mig<D>::HDR * sizeof(float), c->stream);
     launch(c, KI_MIG, [&] {
-      kx(c, k_mig_leavers<D>, dim3(c->n_sm * 4), dim3(256), 0, P, (const int*)bs_at(c, t), (const float*)state_at(c, t + 1),
+      kx(c, k_mig_leavers<D>, dim3(c->n_sm * 4), dim3(256), 0, P, c->M, (const int*)bs_at(c, t), (const float*)state_at(c, t + 1),
          (const int*)orig_at(c, t + 1), c->key, c->cnt, mig_send_at(c, t, 0), mig_send_at(c, t, 1), c->err, t);
     });
   }
@@ -631,7 +632,7 @@ template <int D>
 void forward_phase_c(mpm_ctx c, int t) {
   const KParams& P = c->P;
   launch(c, KI_MIG, [&] {
-    kx(c, k_mig_append<D>, dim3(c->n_sm), dim3(256), 0, P, c->left ? (const float*)mig_recv_at(c, t, 0) : nullptr,
+    kx(c, k_mig_append<D>, dim3(c->n_sm), dim3(256), 0, P, c->M, c->left ? (const float*)mig_recv_at(c, t, 0) : nullptr,
        c->right ? (const float*)mig_recv_at(c, t, 1) : nullptr, (const int*)bs_at(c, t), state_at(c, t + 1),
        orig_at(c, t + 1), c->key, c->cnt, info_at(c, t + 1), c->err, t);
   });
@@ -641,7 +642,7 @@ void forward_phase_c(mpm_ctx c, int t) {
 template <int D>
 void backward_mig_pack(mpm_ctx c, int t) {
   launch(c, KI_MIG, [&] {
-    kx(c, k_mig_rev_pack<D>, dim3(c->n_sm), dim3(256), 0, c->P, c->left ? (const float*)mig_recv_at(c, t, 0) : nullptr,
+    kx(c, k_mig_rev_pack<D>, dim3(c->n_sm), dim3(256), 0, c->P, c->M, c->left ? (const float*)mig_recv_at(c, t, 0) : nullptr,
        c->right ? (const float*)mig_recv_at(c, t, 1) : nullptr, (const int*)bs_at(c, t), (const float*)c->bcur,
        c->rev_send[0], c->rev_send[1]);
   });
@@ -649,7 +650,7 @@ void backward_mig_pack(mpm_ctx c, int t) {
 template <int D>
 void backward_mig_unpack(mpm_ctx c, int t) {
   launch(c, KI_MIG, [&] {
-    kx(c, k_mig_rev_unpack<D>, dim3(c->n_sm), dim3(256), 0, c->P, c->left ? (const float*)mig_send_at(c, t, 0) : nullptr,
+    kx(c, k_mig_rev_unpack<D>, dim3(c->n_sm), dim3(256), 0, c->P, c->M, c->left ? (const float*)mig_send_at(c, t, 0) : nullptr,
        c->right ? (const float*)mig_send_at(c, t, 1) : nullptr, (const float*)c->rev_recv[0],
        (const float*)c->rev_recv[1], c->bcur);
   });
@@ -910,7 +911,7 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
     std::vector<int> mem;
     for (size_t u = 0; u < NU; ++u) {
       const int bx = (int)floorf(hx[u * D] * P.fres - 0.5f);
-      if (bx >= P.own_lo && bx < P.own_hi) mem.push_back((int)u);
+      if (bx >= c->M.own_lo && bx < c->M.own_hi) mem.push_back((int)u);
     }
     if (mem.size() > NT)
       return fail(c, MPM_ERR_MIGRATE, "slab owns " + std::to_string(mem.size()) + " particles at t = 0, capacity " +
@@ -1223,7 +1224,7 @@ mpm_status do_get_state(mpm_ctx c, int t, float* x, float* v, float* F, float* C
     CK(cudaMemsetAsync(sx, 0, NU * (2 * D + 2 * D * D) * sizeof(float), c->stream));
   launch(c, KI_MISC, [&] {
     k_soa_to_user<D><<<grid1d(NT), 256, 0, c->stream>>>(c->P, orig_at(c, t), state_at(c, t), sx, sv, sF, sC, 1,
-                                                         nslot_at(c, t), c->mig ? state_at(c, t) : nullptr);
+                                                         nslot_at(c, t), c->mig ? state_at(c, t) : nullptr, c->M);
   });
   if (x) CK(cudaMemcpyAsync(x, sx, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
   if (v) CK(cudaMemcpyAsync(v, sv, NU * D * sizeof(float), cudaMemcpyDefault, c->stream));
@@ -1306,7 +1307,7 @@ mpm_status group_check(mpm_ctx* cs, int32_t n) {
     if (c->comm) return fail(c, MPM_ERR_CALL_ORDER, "context has a communicator; use mpm_forward/mpm_backward");
     if (c->cfg.device != c0->cfg.device || c->stream != c0->stream || c->D != c0->D || c->P.res != c0->P.res ||
         c->tape_len != c0->tape_len || c->mig != c0->mig ||
-        (c->mig && (c->NU != c0->NU || c->P.mig_cap != c0->P.mig_cap)))
+        (c->mig && (c->NU != c0->NU || c->M.mig_cap != c0->M.mig_cap)))
       return fail(c, MPM_ERR_INVALID_ARG, "group contexts need one device, one stream, equal dim/res/tape length "
                                           "and the same slab mode");
     if (c->transport) return fail(c, MPM_ERR_CALL_ORDER, "context has a transport; use mpm_forward/mpm_backward");
@@ -1479,10 +1480,6 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   P.act_s = k.act_strength;
   P.slab_lo = 0;
   P.slab_hi = k.res - 3;
-  P.migrate = 0;
-  P.own_lo = INT32_MIN;
-  P.own_hi = INT32_MAX;
-  P.mig_cap = 0;
   c->NU = (size_t)k.batch * k.n_particles;
   P.material = k.material;
   c->n_tiles = (P.NBT + kScanTile - 1) / kScanTile;
@@ -1744,9 +1741,9 @@ mpm_status mpm_get_binning(mpm_ctx c, int32_t t, float* x_store, int32_t* orig, 
     // keys of storage order t: recompute from the stored positions (same device code as the step)
     int* tmp = c->scratch;
     if (D == 3)
-      k_init_keys<3><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, nullptr, c->err, nslot_at(c, t));
+      k_init_keys<3><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, nullptr, c->err, nslot_at(c, t), c->M);
     else
-      k_init_keys<2><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, nullptr, c->err, nslot_at(c, t));
+      k_init_keys<2><<<grid1d(NT), 256, 0, c->stream>>>(P, state_at(c, t), tmp, c->hist2, nullptr, c->err, nslot_at(c, t), c->M);
     CK(cudaMemcpyAsync(keyo, tmp, NT * sizeof(int), cudaMemcpyDefault, c->stream));
   }
   return sync_and_check(c, "get_binning");
@@ -1956,13 +1953,13 @@ mpm_status mpm_set_slab_migrating(mpm_ctx c, int32_t x_lo, int32_t x_hi, int32_t
   // check rejects it); no drift bound
   P.slab_lo = 0;
   P.slab_hi = P.res - 3;
-  P.migrate = 1;
-  P.own_lo = c->left ? x_lo : INT32_MIN;
-  P.own_hi = c->right ? x_hi : INT32_MAX;
-  P.mig_cap = mig_cap > 0 ? mig_cap : std::max(1024, P.NT / 64);
+  c->M.migrate = 1;
+  c->M.own_lo = c->left ? x_lo : INT32_MIN;
+  c->M.own_hi = c->right ? x_hi : INT32_MAX;
+  c->M.mig_cap = mig_cap > 0 ? mig_cap : std::max(1024, P.NT / 64);
   c->mig = true;
   c->NU = (size_t)n_global;
-  c->mig_floats = Mig<3>::HDR + (size_t)P.mig_cap * (D == 3 ? Mig<3>::R : Mig<2>::R);
+  c->mig_floats = Mig<3>::HDR + (size_t)c->M.mig_cap * (D == 3 ? Mig<3>::R : Mig<2>::R);
   // user-indexed arrays span the whole body now (the storage ones keep the capacity P.NT)
   auto realloc_user = [&](auto*& ptr, size_t count) -> mpm_status {
     c->allocs.erase(std::remove(c->allocs.begin(), c->allocs.end(), (void*)ptr), c->allocs.end());

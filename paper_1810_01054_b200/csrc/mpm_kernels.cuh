@@ -55,6 +55,7 @@
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
 #endif
+
 #ifndef MPM_SCAT_FX
 #define MPM_SCAT_FX 1
 #endif
@@ -133,9 +134,14 @@ struct KParams {
   int slab_lo, slab_hi;                     // allowed base_x range (inclusive); slab mode
   int material;                             // 0 = neo-Hookean (R1), 1 = fixed-corotated (R21)
   int nz;                                   // controller observation length d (1 + 2K) (NEXT N1)
-  int migrate;                              // migrating slab mode: a particle is owned by the slab
-  int own_lo, own_hi;                       //   whose [own_lo, own_hi) holds its base_x, every step
-  int mig_cap;                              //   migrant records per side and step
+};
+
+// Migrating slab mode (separate from KParams so the step kernels' parameters are unchanged): a
+// particle is owned by the slab whose [own_lo, own_hi) holds its base_x, at every step.
+struct MigParams {
+  int migrate;
+  int own_lo, own_hi;
+  int mig_cap;  // migrant records per side and step
 };
 
 // Per-step bookkeeping record, info[t * kInfo + field]
@@ -608,7 +614,7 @@ __global__ void k_params(int NT, const float* __restrict__ m, const float* __res
 template <int D>
 __global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __restrict__ key,
                             int* __restrict__ cnt, int* __restrict__ orig, ErrLatch* err,
-                            const int* __restrict__ nslot) {
+                            const int* __restrict__ nslot, MigParams M) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   bool valid = j < (nslot ? *nslot : P.NT);
   int gb = 0, k = 0;
@@ -616,9 +622,9 @@ __global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __rest
     float x[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) x[a] = st[(size_t)comp_x<D>(a) * P.NT + j];
-    if (P.migrate) {
+    if (M.migrate) {
       const int bx = base_of(x[0], P.fres);
-      if (bx < P.own_lo || bx >= P.own_hi) {
+      if (bx < M.own_lo || bx >= M.own_hi) {
         key[j] = kDeadKey;
         valid = false;
       }
@@ -2789,7 +2795,7 @@ __global__ void k_band_unpack(int nblk, int gb_lo, int gb_hi, const int* __restr
 // become holes (kDeadKey, taken out of the block histogram G2P built) and their records go to
 // the send buffer of that side (record order = arrival order at the neighbour)
 template <int D>
-__global__ void k_mig_leavers(KParams P, const int* __restrict__ block_start_t, const float* __restrict__ st_next,
+__global__ void k_mig_leavers(KParams P, MigParams M, const int* __restrict__ block_start_t, const float* __restrict__ st_next,
                               const int* __restrict__ orig_next, int* __restrict__ key, int* __restrict__ cnt,
                               float* __restrict__ send_l, float* __restrict__ send_r, ErrLatch* err, int t) {
   MPM_PDL_ENTRY();
@@ -2798,13 +2804,13 @@ __global__ void k_mig_leavers(KParams P, const int* __restrict__ block_start_t, 
   const size_t NT = P.NT;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nt; j += gridDim.x * blockDim.x) {
     const int bx = base_of(st_next[(size_t)comp_x<D>(0) * NT + j], P.fres);
-    if (bx >= P.own_lo && bx < P.own_hi) continue;
+    if (bx >= M.own_lo && bx < M.own_hi) continue;
     const int kj = key[j];
     if (kj >= 0) atomicSub(&cnt[kj / kCPB], 1);
     key[j] = kDeadKey;
-    float* buf = bx < P.own_lo ? send_l : send_r;
+    float* buf = bx < M.own_lo ? send_l : send_r;
     const int pos = atomicAdd(reinterpret_cast<int*>(buf), 1);
-    if (pos >= P.mig_cap) {
+    if (pos >= M.mig_cap) {
       latch(err, E_MIGRATE, t + 1, orig_next[j]);
       continue;
     }
@@ -2816,15 +2822,15 @@ __global__ void k_mig_leavers(KParams P, const int* __restrict__ block_start_t, 
 }
 
 template <int D>
-__global__ void k_mig_append(KParams P, const float* __restrict__ recv_l, const float* __restrict__ recv_r,
+__global__ void k_mig_append(KParams P, MigParams M, const float* __restrict__ recv_l, const float* __restrict__ recv_r,
                              const int* __restrict__ block_start_t, float* __restrict__ st_next,
                              int* __restrict__ orig_next, int* __restrict__ key, int* __restrict__ cnt,
                              int* __restrict__ info_next, ErrLatch* err, int t) {
   MPM_PDL_ENTRY();
   using MG = Mig<D>;
   const int nt = block_start_t[P.NBT];  // particles G2P wrote (live at step t)
-  const int al = recv_l ? min(*reinterpret_cast<const int*>(recv_l), P.mig_cap) : 0;
-  const int ar = recv_r ? min(*reinterpret_cast<const int*>(recv_r), P.mig_cap) : 0;
+  const int al = recv_l ? min(*reinterpret_cast<const int*>(recv_l), M.mig_cap) : 0;
+  const int ar = recv_r ? min(*reinterpret_cast<const int*>(recv_r), M.mig_cap) : 0;
   const size_t NT = P.NT;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (nt + al + ar > P.NT) latch(err, E_MIGRATE, t + 1, nt + al + ar);
@@ -2845,7 +2851,7 @@ __global__ void k_mig_append(KParams P, const float* __restrict__ recv_l, const 
       int k;
       if (const int e = key_of<D>(x, 0, P, gb, k)) latch(err, e, t + 1, orig_next[j]);
       const int bx = base_of(x[0], P.fres);
-      if (bx < P.own_lo || bx >= P.own_hi) latch(err, E_MIGRATE, t + 1, orig_next[j]);  // crossed a whole slab
+      if (bx < M.own_lo || bx >= M.own_hi) latch(err, E_MIGRATE, t + 1, orig_next[j]);  // crossed a whole slab
       key[j] = k;
     }
     warp_hist_add(cnt, gb, valid);
@@ -2855,14 +2861,14 @@ __global__ void k_mig_append(KParams P, const float* __restrict__ recv_l, const 
 // backward, before G2P^T of step t: the adjoint of state t+1 at this rank's arrival slots goes
 // back to the sender (left arrivals to the left, right ones to the right, in arrival order)
 template <int D>
-__global__ void k_mig_rev_pack(KParams P, const float* __restrict__ recv_l, const float* __restrict__ recv_r,
+__global__ void k_mig_rev_pack(KParams P, MigParams M, const float* __restrict__ recv_l, const float* __restrict__ recv_r,
                                const int* __restrict__ block_start_t, const float* __restrict__ g,
                                float* __restrict__ out_l, float* __restrict__ out_r) {
   MPM_PDL_ENTRY();
   using MG = Mig<D>;
   const int nt = block_start_t[P.NBT];
-  const int al = recv_l ? min(*reinterpret_cast<const int*>(recv_l), P.mig_cap) : 0;
-  const int ar = recv_r ? min(*reinterpret_cast<const int*>(recv_r), P.mig_cap) : 0;
+  const int al = recv_l ? min(*reinterpret_cast<const int*>(recv_l), M.mig_cap) : 0;
+  const int ar = recv_r ? min(*reinterpret_cast<const int*>(recv_r), M.mig_cap) : 0;
   const size_t NT = P.NT;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (al + ar) * MG::S; q += gridDim.x * blockDim.x) {
     const int i = q / MG::S, c = q - i * MG::S;
@@ -2875,12 +2881,12 @@ __global__ void k_mig_rev_pack(KParams P, const float* __restrict__ recv_l, cons
 
 // ... and the adjoints coming back from the neighbours fill the slots of this rank's leavers
 template <int D>
-__global__ void k_mig_rev_unpack(KParams P, const float* __restrict__ sent_l, const float* __restrict__ sent_r,
+__global__ void k_mig_rev_unpack(KParams P, MigParams M, const float* __restrict__ sent_l, const float* __restrict__ sent_r,
                                  const float* __restrict__ in_l, const float* __restrict__ in_r, float* __restrict__ g) {
   MPM_PDL_ENTRY();
   using MG = Mig<D>;
-  const int nl = sent_l ? min(*reinterpret_cast<const int*>(sent_l), P.mig_cap) : 0;
-  const int nr = sent_r ? min(*reinterpret_cast<const int*>(sent_r), P.mig_cap) : 0;
+  const int nl = sent_l ? min(*reinterpret_cast<const int*>(sent_l), M.mig_cap) : 0;
+  const int nr = sent_r ? min(*reinterpret_cast<const int*>(sent_r), M.mig_cap) : 0;
   const size_t NT = P.NT;
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (nl + nr) * MG::S; q += gridDim.x * blockDim.x) {
     const int i = q / MG::S, c = q - i * MG::S;
@@ -2981,13 +2987,14 @@ __global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __r
 template <int D>
 __global__ void k_soa_to_user(KParams P, const int* __restrict__ orig, const float* __restrict__ st,
                               float* x, float* v, float* F, float* C, int state,
-                              const int* __restrict__ nslot = nullptr, const float* __restrict__ owner = nullptr) {
+                              const int* __restrict__ nslot = nullptr, const float* __restrict__ owner = nullptr,
+                              MigParams M = MigParams{}) {
   int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= (nslot ? *nslot : P.NT)) return;
   const size_t NT = P.NT;
   if (owner) {
     const int bx = base_of(owner[(size_t)comp_x<D>(0) * NT + j], P.fres);
-    if (bx < P.own_lo || bx >= P.own_hi) return;  // a hole: the particle is the neighbour's now
+    if (bx < M.own_lo || bx >= M.own_hi) return;  // a hole: the particle is the neighbour's now
   }
   int u = orig ? orig[j] : j;
 #pragma unroll
