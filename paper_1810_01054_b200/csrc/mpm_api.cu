@@ -288,7 +288,8 @@ void drop_graphs(mpm_ctx c) {
 
 // tape slot of global step t (segment-local; the caller guarantees seg0 <= t <= seg0 + tape_cap)
 size_t ti(mpm_ctx c, int t) { return (size_t)(t - c->seg0); }
-float* state_at(mpm_ctx c, int t) { return c->tape_state + ti(c, t) * c->S * NTs(c); }
+size_t recf(mpm_ctx c) { return rec_floats(c->S, NTs(c)); }  // floats of one particle-record buffer
+float* state_at(mpm_ctx c, int t) { return c->tape_state + ti(c, t) * recf(c); }
 int* perm_at(mpm_ctx c, int t) { return c->tape_perm + ti(c, t) * NTs(c); }
 int* orig_at(mpm_ctx c, int t) { return c->tape_orig + ti(c, t) * NTs(c); }
 int* bs_at(mpm_ctx c, int t) { return c->tape_bs + ti(c, t) * (c->P.NBT + 1); }
@@ -303,7 +304,7 @@ const int* nslot_at(mpm_ctx c, int t) { return c->mig ? info_at(c, t) + I_NSLOT 
 size_t rev_floats(mpm_ctx c) { return (size_t)c->M.mig_cap * c->S; }
 
 bool on_tape(mpm_ctx c, int t) { return t >= c->seg0 && t <= c->res_end && t <= c->tape_len; }
-float* ck_state_of(mpm_ctx c, int i) { return c->ck_state + (size_t)i * c->S * NTs(c); }
+float* ck_state_of(mpm_ctx c, int i) { return c->ck_state + (size_t)i * recf(c); }
 int* ck_orig_of(mpm_ctx c, int i) { return c->ck_orig + (size_t)i * NTs(c); }
 
 int grid1d(size_t n, int bs = 256) { return (int)((n + bs - 1) / bs); }
@@ -575,7 +576,7 @@ mpm_status exchange_local_rev(mpm_ctx* cs, int n) {
 // N2: the tape is full at step t (t - seg0 == tape_cap): state t becomes checkpoint t / k and
 // the first slot of a new segment (its keys / histogram are already in the work buffers)
 void roll_segment(mpm_ctx c, int t) {
-  const size_t bs = (size_t)c->S * NTs(c) * sizeof(float), bo = NTs(c) * sizeof(int);
+  const size_t bs = recf(c) * sizeof(float), bo = NTs(c) * sizeof(int);
   const int i = t / c->ck;
   cudaMemcpyAsync(ck_state_of(c, i), state_at(c, t), bs, cudaMemcpyDeviceToDevice, c->stream);
   cudaMemcpyAsync(ck_orig_of(c, i), orig_at(c, t), bo, cudaMemcpyDeviceToDevice, c->stream);
@@ -941,7 +942,7 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   CK(cudaMemsetAsync(c->cnt, 0, (size_t)P.NBT * sizeof(int), c->stream));
   launch_keys<D>(c, 0);
   if (c->ck) {  // N2: checkpoint 0 = the initial state
-    CK(cudaMemcpyAsync(ck_state_of(c, 0), state_at(c, 0), (size_t)c->S * NT * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(ck_state_of(c, 0), state_at(c, 0), recf(c) * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
     CK(cudaMemcpyAsync(ck_orig_of(c, 0), orig_at(c, 0), NT * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
     c->ck_valid = 1;
   }
@@ -1112,7 +1113,7 @@ void backward_step_end(mpm_ctx c, int t) {
 // gradients reduced over steps and rollouts
 mpm_status backward_finish(mpm_ctx c) {
   if (c->bcur != c->gA)
-    CK(cudaMemcpyAsync(c->gA, c->bcur, (size_t)c->S * c->P.NT * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->gA, c->bcur, recf(c) * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
   if (c->ctrl) {
     const int T = c->tape_len;
     launch(c, KI_CTRLT, [&] {
@@ -1132,7 +1133,7 @@ size_t da_count(mpm_ctx c) { return (size_t)c->P.B * c->P.T * std::max(c->P.K, 1
 // N2: make checkpoint i (step i k) the first slot of the tape and recompute the keys of its state
 template <int D>
 void restore_checkpoint(mpm_ctx c, int i) {
-  const size_t bs = (size_t)c->S * NTs(c) * sizeof(float), bo = NTs(c) * sizeof(int);
+  const size_t bs = recf(c) * sizeof(float), bo = NTs(c) * sizeof(int);
   c->seg0 = i * c->ck;
   c->res_end = c->seg0;
   cudaMemcpyAsync(c->tape_state, ck_state_of(c, i), bs, cudaMemcpyDeviceToDevice, c->stream);
@@ -1537,7 +1538,8 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   mpm_status s = MPM_OK;
 #define AL(ptr, n) \
   if (!s) s = dalloc(c, &c->ptr, (n))
-  AL(tape_state, (TC + 1) * S * NT);
+  const size_t RF = rec_floats((int)S, NT);  // one particle-record buffer (AoSoA: padded)
+  AL(tape_state, (TC + 1) * RF);
   AL(tape_perm, TC * NT);
   AL(tape_orig, (TC + 1) * NT);
   AL(tape_bs, TC * (size_t)(P.NBT + 1));
@@ -1546,7 +1548,7 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   AL(tape_touch, TC * (size_t)P.NBT);
   AL(info, (TC + 1) * kInfo);
   if (c->ck) {
-    AL(ck_state, (size_t)c->n_ck * S * NT);
+    AL(ck_state, (size_t)c->n_ck * RF);
     AL(ck_orig, (size_t)c->n_ck * NT);
   }
   AL(key, NT);
@@ -1567,8 +1569,8 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
   AL(E, NT);
   AL(nu, NT);
   AL(act, (size_t)P.B * T * std::max(P.K, 1) * D);
-  AL(gA, S * NT);
-  AL(gB, S * NT);
+  AL(gA, RF);
+  AL(gB, RF);
   AL(dmu, NT);
   AL(dlam, NT);
   AL(dmass, NT);
@@ -1725,13 +1727,13 @@ mpm_status mpm_get_binning(mpm_ctx c, int32_t t, float* x_store, int32_t* orig, 
   const size_t NT = P.NT;
   const int D = c->D;
   if (x_store) {
-    // SoA -> [NT][D] storage order
-    std::vector<float> h((size_t)D * NT);
+    // record buffer -> [NT][D] storage order
+    std::vector<float> h(recf(c));
     CK(cudaMemcpyAsync(h.data(), state_at(c, t), h.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     std::vector<float> o((size_t)D * NT);
     for (size_t j = 0; j < NT; ++j)
-      for (int a = 0; a < D; ++a) o[j * D + a] = h[a * NT + j];
+      for (int a = 0; a < D; ++a) o[j * D + a] = h[rixs(c->S, a, (int)j, NT)];
     CK(cudaMemcpy(x_store, o.data(), o.size() * sizeof(float), cudaMemcpyDefault));
   }
   if (orig) CK(cudaMemcpyAsync(orig, orig_at(c, t), NT * sizeof(int), cudaMemcpyDefault, c->stream));

@@ -4,9 +4,9 @@
 // Citations: P:<line> = PAPER.md line; R<k> = DESIGN.md reading k.
 //
 // Layout:
-//   particle state, tape step t: SoA, component-major, "storage order t"
+//   particle state, tape step t: AoSoA, "storage order t" -- groups of 32 particles, component-
+//   major inside a group (rix below; MPM_AOSOA=0: plain SoA, comp * NT + j)
 //       comp(x_a) = a, comp(v_a) = D + a, comp(C_ab) = 2D + aD + b, comp(F_ab) = 2D + D^2 + aD + b
-//       value of particle j = state[comp * NT + j]
 //     storage order t+1 == the sorted (block, cell, index) order of step t.
 //   grid: sparse, one 64-node slot (1 KiB, float4 per node) per touched block of Bb^D
 //     nodes (Bb = 4 in 3D, 8 in 2D); node float4 = (p_x, p_y, p_z, m) after P2G,
@@ -169,10 +169,37 @@ __device__ __forceinline__ void latch(ErrLatch* e, int code, int step, int parti
 // ------------------------------------------------------------------------------------
 // index helpers
 // ------------------------------------------------------------------------------------
+// Particle records (states on the tape, adjoints): component comp of particle j.  AoSoA: a
+// particle's 32-lane group holds its S components as 32-float rows, so after the per-particle
+// group base every component is an immediate offset (the SoA form needs a 64-bit comp * NT
+// multiply-add per access); warps reading 32 consecutive particles stay fully coalesced.
+#ifndef MPM_AOSOA
+#define MPM_AOSOA 1
+#endif
+__host__ __device__ __forceinline__ size_t rixs(int S, int comp, int j, size_t NT) {
+#if MPM_AOSOA
+  (void)NT;
+  return ((size_t)(j >> 5) * S + comp) * 32 + (j & 31);
+#else
+  return (size_t)comp * NT + j;
+#endif
+}
+// floats of a record buffer of NT particles (AoSoA pads to a whole group)
+__host__ __device__ __forceinline__ size_t rec_floats(int S, size_t NT) {
+#if MPM_AOSOA
+  return (size_t)S * ((NT + 31) / 32 * 32);
+#else
+  return (size_t)S * NT;
+#endif
+}
+
 template <int D> __device__ __forceinline__ int comp_x(int a) { return a; }
 template <int D> __device__ __forceinline__ int comp_v(int a) { return D + a; }
 template <int D> __device__ __forceinline__ int comp_C(int a, int b) { return 2 * D + a * D + b; }
 template <int D> __device__ __forceinline__ int comp_F(int a, int b) { return 2 * D + D * D + a * D + b; }
+template <int D> __device__ __forceinline__ size_t rix(int comp, int j, size_t NT) {
+  return rixs(2 * D + 2 * D * D, comp, j, NT);
+}
 
 // block linear index inside one rollout from block coords (row-major, axis 0 slowest)
 template <int D> __device__ __forceinline__ int block_lin(const int* b, int nbpa) {
@@ -301,7 +328,7 @@ __device__ __forceinline__ void load_H(const float* st, size_t NT, int j, float 
 #pragma unroll
   for (int a = 0; a < D; ++a)
 #pragma unroll
-    for (int b = 0; b < D; ++b) H[a][b] = __ldg(&st[(size_t)comp_F<D>(a, b) * NT + j]);
+    for (int b = 0; b < D; ++b) H[a][b] = __ldg(&st[rix<D>(comp_F<D>(a, b), j, NT)]);
 }
 
 template <int D>
@@ -585,12 +612,12 @@ __global__ void k_user_to_soa(KParams P, const float* __restrict__ x, const floa
   const size_t u = idx ? idx[j] : j;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    st[comp_x<D>(a) * NT + j] = x[u * D + a];
-    st[comp_v<D>(a) * NT + j] = v ? v[u * D + a] : 0.f;
+    st[rix<D>(comp_x<D>(a), j, NT)] = x[u * D + a];
+    st[rix<D>(comp_v<D>(a), j, NT)] = v ? v[u * D + a] : 0.f;
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      st[comp_C<D>(a, b) * NT + j] = C ? C[(u * D + a) * D + b] : 0.f;
-      st[comp_F<D>(a, b) * NT + j] = F ? F[(u * D + a) * D + b] - (a == b ? 1.f : 0.f) : 0.f;  // H = F - I
+      st[rix<D>(comp_C<D>(a, b), j, NT)] = C ? C[(u * D + a) * D + b] : 0.f;
+      st[rix<D>(comp_F<D>(a, b), j, NT)] = F ? F[(u * D + a) * D + b] - (a == b ? 1.f : 0.f) : 0.f;  // H = F - I
     }
   }
 }
@@ -621,7 +648,7 @@ __global__ void k_init_keys(KParams P, const float* __restrict__ st, int* __rest
   if (valid) {
     float x[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) x[a] = st[(size_t)comp_x<D>(a) * P.NT + j];
+    for (int a = 0; a < D; ++a) x[a] = st[rix<D>(comp_x<D>(a), j, P.NT)];
     if (M.migrate) {
       const int bx = base_of(x[0], P.fres);
       if (bx < M.own_lo || bx >= M.own_hi) {
@@ -990,8 +1017,9 @@ struct StepArgs {
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+template <int D>
 __device__ __forceinline__ void prefetch_record(const float* base, size_t NT, int j, int c0, int ncomp) {
-  for (int c = c0; c < c0 + ncomp; ++c) prefetch_l2(base + (size_t)c * NT + j);
+  for (int c = c0; c < c0 + ncomp; ++c) prefetch_l2(base + rix<D>(c, j, NT));
 }
 
 // G2P^T's payload carries fx instead of the stencil weights (MPM_SCATA_FX; 15 rows in 3D)
@@ -1152,10 +1180,10 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
       // the producer reads this particle's record after the sort: start fetching it now
       // (PF_XF: the fused G2P2G reads x and F only)
       if (PF_XF) {
-        prefetch_record(A.st, NT, e.x, 0, D);
-        prefetch_record(A.st, NT, e.x, comp_F<D>(0, 0), D * D);
+        prefetch_record<D>(A.st, NT, e.x, 0, D);
+        prefetch_record<D>(A.st, NT, e.x, comp_F<D>(0, 0), D * D);
       } else {
-        prefetch_record(A.st, NT, e.x, 0, Dim<D>::S);
+        prefetch_record<D>(A.st, NT, e.x, 0, Dim<D>::S);
       }
       prefetch_l2(&A.orig[e.x]);
 #endif
@@ -1416,7 +1444,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
         float x[D], f[D];
         Stencil<D> sc;
 #pragma unroll
-        for (int a = 0; a < D; ++a) x[a] = A.st[(size_t)comp_x<D>(a) * NT + j];
+        for (int a = 0; a < D; ++a) x[a] = A.st[rix<D>(comp_x<D>(a), j, NT)];
         make_stencil<D>(x, P.fres, sc);
         const int ps = pay_slot(pi);
         MPM_CHECK(ps >= 0 && ps < kCap);
@@ -1444,11 +1472,11 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
           float H[D][D], Cm[D][D], v[D];
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            v[a] = A.st[(size_t)comp_v<D>(a) * NT + j];
+            v[a] = A.st[rix<D>(comp_v<D>(a), j, NT)];
 #pragma unroll
             for (int b = 0; b < D; ++b) {
-              H[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j];
-              Cm[a][b] = A.st[(size_t)comp_C<D>(a, b) * NT + j];
+              H[a][b] = A.st[rix<D>(comp_F<D>(a, b), j, NT)];
+              Cm[a][b] = A.st[rix<D>(comp_C<D>(a, b), j, NT)];
             }
           }
           p2g_payload<D, MAT>(P, A, r, A.t, u, pr, A.aid[u], v, H, Cm, f, Av, Bm);
@@ -1459,12 +1487,12 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
           float F[D][D], gF[D][D], gC[D][D], gv[D];
 #pragma unroll
           for (int a = 0; a < D; ++a) {
-            gv[a] = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
+            gv[a] = fmaf(P.dt, gi[rix<D>(comp_x<D>(a), k, NT)], gi[rix<D>(comp_v<D>(a), k, NT)]);
 #pragma unroll
             for (int b = 0; b < D; ++b) {
-              F[a][b] = A.st[(size_t)comp_F<D>(a, b) * NT + j] + (a == b ? 1.f : 0.f);  // F = I + H
-              gF[a][b] = gi[(size_t)comp_F<D>(a, b) * NT + k];
-              gC[a][b] = gi[(size_t)comp_C<D>(a, b) * NT + k];
+              F[a][b] = A.st[rix<D>(comp_F<D>(a, b), j, NT)] + (a == b ? 1.f : 0.f);  // F = I + H
+              gF[a][b] = gi[rix<D>(comp_F<D>(a, b), k, NT)];
+              gC[a][b] = gi[rix<D>(comp_C<D>(a, b), k, NT)];
             }
           }
           const float s4 = 4.f * P.fres;
@@ -1737,9 +1765,9 @@ __device__ __forceinline__ bool g2p_particle(const KParams& P, const StepArgs& A
   float H[D][D];  // H = F - I
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
+    x[a] = __ldg(&A.st[rix<D>(comp_x<D>(a), j, NT)]);
 #pragma unroll
-    for (int b = 0; b < D; ++b) H[a][b] = __ldg(&A.st[(size_t)comp_F<D>(a, b) * NT + j]);
+    for (int b = 0; b < D; ++b) H[a][b] = __ldg(&A.st[rix<D>(comp_F<D>(a, b), j, NT)]);
   }
   u = __ldg(&A.orig[j]);
   if (PRM) {  // the fused P2G's parameters: issued now, consumed after the gather
@@ -1773,13 +1801,13 @@ __device__ __forceinline__ bool g2p_particle(const KParams& P, const StepArgs& A
 #pragma unroll
       for (int c = 0; c < D; ++c) acc = fmaf(P.dt * Cn[a][c], H[c][b], acc);
       Hn[a][b] = acc;
-      out[(size_t)comp_F<D>(a, b) * NT + k] = acc;
-      out[(size_t)comp_C<D>(a, b) * NT + k] = Cn[a][b];
+      out[rix<D>(comp_F<D>(a, b), k, NT)] = acc;
+      out[rix<D>(comp_C<D>(a, b), k, NT)] = Cn[a][b];
     }
     vn[a] = S[a] + (&vref.x)[a];
-    out[(size_t)comp_v<D>(a) * NT + k] = vn[a];
+    out[rix<D>(comp_v<D>(a), k, NT)] = vn[a];
     x[a] = fmaf(P.dt, vn[a], x[a]);
-    out[(size_t)comp_x<D>(a) * NT + k] = x[a];
+    out[rix<D>(comp_x<D>(a), k, NT)] = x[a];
   }
   A.orig_next[k] = u;
   int gbn, key;
@@ -1816,8 +1844,8 @@ __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepA
 #if MPM_G2P_PF
     for (int i = threadIdx.x; i < n; i += kThreads) {  // this block's x, F -> L2
       const int j = __ldg(&A.perm[s + i]);
-      prefetch_record(A.st, NT, j, 0, D);
-      prefetch_record(A.st, NT, j, comp_F<D>(0, 0), D * D);
+      prefetch_record<D>(A.st, NT, j, 0, D);
+      prefetch_record<D>(A.st, NT, j, comp_F<D>(0, 0), D * D);
     }
 #endif
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
@@ -2260,7 +2288,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
   float x[D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) x[a] = __ldg(&A.st[(size_t)comp_x<D>(a) * NT + j]);
+  for (int a = 0; a < D; ++a) x[a] = __ldg(&A.st[rix<D>(comp_x<D>(a), j, NT)]);
   Stencil<D> sc;
   make_stencil<D>(x, P.fres, sc);
   float dw[D][3];
@@ -2282,14 +2310,14 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     float u0[D], U[D][D];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      u0[a] = fmaf(P.dt, gi[(size_t)comp_x<D>(a) * NT + k], gi[(size_t)comp_v<D>(a) * NT + k]);
+      u0[a] = fmaf(P.dt, gi[rix<D>(comp_x<D>(a), k, NT)], gi[rix<D>(comp_v<D>(a), k, NT)]);
 #pragma unroll
       for (int b = 0; b < D; ++b) {
         // g_C = gC + dt gF F^T with F = I + H
-        float gc = fmaf(P.dt, gi[(size_t)comp_F<D>(a, b) * NT + k], gi[(size_t)comp_C<D>(a, b) * NT + k]);
+        float gc = fmaf(P.dt, gi[rix<D>(comp_F<D>(a, b), k, NT)], gi[rix<D>(comp_C<D>(a, b), k, NT)]);
 #pragma unroll
         for (int c = 0; c < D; ++c)
-          gc = fmaf(P.dt * gi[(size_t)comp_F<D>(a, c) * NT + k], __ldg(&A.st[(size_t)comp_F<D>(b, c) * NT + j]), gc);
+          gc = fmaf(P.dt * gi[rix<D>(comp_F<D>(a, c), k, NT)], __ldg(&A.st[rix<D>(comp_F<D>(b, c), j, NT)]), gc);
         U[a][b] = 4.f * P.fres * gc;
         u0[a] = fmaf(-U[a][b], sc.fx[b], u0[a]);
       }
@@ -2320,10 +2348,10 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     else kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, log1pf(det1m<D>(H)));
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      q0[a] = pr.x * __ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]);
+      q0[a] = pr.x * __ldg(&A.st[rix<D>(comp_v<D>(a), j, NT)]);
 #pragma unroll
       for (int b = 0; b < D; ++b) {
-        Gm[a][b] = P.dx * fmaf(-kk, tau[a][b], pr.x * __ldg(&A.st[(size_t)comp_C<D>(a, b) * NT + j]));
+        Gm[a][b] = P.dx * fmaf(-kk, tau[a][b], pr.x * __ldg(&A.st[rix<D>(comp_C<D>(a, b), j, NT)]));
         q0[a] = fmaf(-Gm[a][b], sc.fx[b], q0[a]);
       }
     }
@@ -2338,17 +2366,17 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     for (int b = 0; b < D; ++b) {
       Q[a][b] = P.dx * fmaf(-Rd.S[a], sc.fx[b], Rd.M[a][b]);
       T[a][b] = -kk * Q[a][b];
-      go[(size_t)comp_C<D>(a, b) * NT + j] = m * Q[a][b];  // (I)
+      go[rix<D>(comp_C<D>(a, b), j, NT)] = m * Q[a][b];  // (I)
     }
-    go[(size_t)comp_v<D>(a) * NT + j] = m * (Rd.S[a] + (&aref.x)[a]);  // (F): sum W dp = S' + dp_ref
+    go[rix<D>(comp_v<D>(a), j, NT)] = m * (Rd.S[a] + (&aref.x)[a]);  // (F): sum W dp = S' + dp_ref
   }
   // (J): dx = gx + sum dW s - 4res^2 g_C^T S_v - G^T S_d
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    float acc = gi[(size_t)comp_x<D>(a) * NT + k] + gxv[a] + Rd.g[a];
+    float acc = gi[rix<D>(comp_x<D>(a), k, NT)] + gxv[a] + Rd.g[a];
 #pragma unroll
     for (int b = 0; b < D; ++b) acc = fmaf(-P.fres * Gm[b][a], Rd.S[b], acc);
-    go[(size_t)comp_x<D>(a) * NT + j] = acc;
+    go[rix<D>(comp_x<D>(a), j, NT)] = acc;
   }
   // (H), (K), material parameters
   float H[D][D], F[D][D];
@@ -2408,11 +2436,11 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   for (int a = 0; a < D; ++a)
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      float acc = gi[(size_t)comp_F<D>(a, b) * NT + k];
+      float acc = gi[rix<D>(comp_F<D>(a, b), k, NT)];
       float tf = 0.f;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        acc = fmaf(P.dt * Cn[c][a], gi[(size_t)comp_F<D>(c, b) * NT + k], acc);
+        acc = fmaf(P.dt * Cn[c][a], gi[rix<D>(comp_F<D>(c, b), k, NT)], acc);
         tf = fmaf(T[a][c] + T[c][a], F[c][b], tf);
       }
       if constexpr (MAT == 1) {
@@ -2423,7 +2451,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         acc = fmaf(pr.z + sig[b], tf, acc);  // mu (T+T^T) F + (T+T^T) F sigma
         acc = fmaf(pr.w * trT, FiT[a][b], acc);
       }
-      go[(size_t)comp_F<D>(a, b) * NT + j] = acc;
+      go[rix<D>(comp_F<D>(a, b), j, NT)] = acc;
     }
   float dmu = 0.f;
 #pragma unroll
@@ -2447,9 +2475,9 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     float gmass = Rd.Se + aref.w;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      gmass = fmaf(__ldg(&A.st[(size_t)comp_v<D>(a) * NT + j]), Rd.S[a] + (&aref.x)[a], gmass);
+      gmass = fmaf(__ldg(&A.st[rix<D>(comp_v<D>(a), j, NT)]), Rd.S[a] + (&aref.x)[a], gmass);
 #pragma unroll
-      for (int b = 0; b < D; ++b) gmass = fmaf(__ldg(&A.st[(size_t)comp_C<D>(a, b) * NT + j]), Q[a][b], gmass);
+      for (int b = 0; b < D; ++b) gmass = fmaf(__ldg(&A.st[rix<D>(comp_C<D>(a, b), j, NT)]), Q[a][b], gmass);
     }
     A.dmass[u] = dm0 + gmass;
   }
@@ -2529,8 +2557,8 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
 #if MPM_P2GT_PF
     for (int i = threadIdx.x; i < n; i += MPM_P2GT_THREADS) {  // this block's particle records -> L2
       const int k = s + i, j = __ldg(&A.perm[k]), u = __ldg(&A.orig_next[k]);
-      prefetch_record(A.st, NT, j, 0, Dim<D>::S);
-      prefetch_record(A.gin, NT, k, 0, Dim<D>::S);
+      prefetch_record<D>(A.st, NT, j, 0, Dim<D>::S);
+      prefetch_record<D>(A.gin, NT, k, 0, Dim<D>::S);
       prefetch_l2(&A.prm[u]);
     }
 #endif
@@ -2614,8 +2642,8 @@ __global__ __launch_bounds__(256) void k_ctrl_observe(KParams P, const float* __
         const float m = prm[u].x;
 #pragma unroll
         for (int a = 0; a < D; ++a) {
-          val[a] = m * st[(size_t)comp_x<D>(a) * NT + j];
-          val[D + a] = m * st[(size_t)comp_v<D>(a) * NT + j];
+          val[a] = m * st[rix<D>(comp_x<D>(a), j, NT)];
+          val[D + a] = m * st[rix<D>(comp_v<D>(a), j, NT)];
         }
       }
     }
@@ -2680,8 +2708,8 @@ __global__ void k_ctrl_adj_state(KParams P, const float* __restrict__ gz, const 
     const float* z = gz + (size_t)r * P.nz + D;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      g[(size_t)comp_x<D>(a) * NT + j] += w * z[k * D + a];
-      g[(size_t)comp_v<D>(a) * NT + j] += w * z[P.K * D + k * D + a];
+      g[rix<D>(comp_x<D>(a), j, NT)] += w * z[k * D + a];
+      g[rix<D>(comp_v<D>(a), j, NT)] += w * z[P.K * D + k * D + a];
     }
   }
 }
@@ -2732,7 +2760,7 @@ __global__ void k_remap_adjoint(int NT, int S, const int* __restrict__ old_orig,
                                 const float* __restrict__ src, float* __restrict__ dst) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < NT; j += gridDim.x * blockDim.x) {
     const int jn = inv_new[old_orig[j]];
-    for (int c = 0; c < S; ++c) dst[(size_t)c * NT + jn] = src[(size_t)c * NT + j];
+    for (int c = 0; c < S; ++c) dst[rixs(S, c, jn, NT)] = src[rixs(S, c, j, NT)];
   }
 }
 
@@ -2803,7 +2831,7 @@ __global__ void k_mig_leavers(KParams P, MigParams M, const int* __restrict__ bl
   const int nt = block_start_t[P.NBT];
   const size_t NT = P.NT;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nt; j += gridDim.x * blockDim.x) {
-    const int bx = base_of(st_next[(size_t)comp_x<D>(0) * NT + j], P.fres);
+    const int bx = base_of(st_next[rix<D>(comp_x<D>(0), j, NT)], P.fres);
     if (bx >= M.own_lo && bx < M.own_hi) continue;
     const int kj = key[j];
     if (kj >= 0) atomicSub(&cnt[kj / kCPB], 1);
@@ -2815,7 +2843,7 @@ __global__ void k_mig_leavers(KParams P, MigParams M, const int* __restrict__ bl
       continue;
     }
     float* rec = buf + MG::HDR + (size_t)pos * MG::R;
-    for (int c = 0; c < MG::S; ++c) rec[c] = st_next[(size_t)c * NT + j];
+    for (int c = 0; c < MG::S; ++c) rec[c] = st_next[rix<D>(c, j, NT)];
     rec[MG::U] = __int_as_float(orig_next[j]);
     rec[MG::K] = __int_as_float(j);
   }
@@ -2843,7 +2871,7 @@ __global__ void k_mig_append(KParams P, MigParams M, const float* __restrict__ r
     int gb = 0;
     if (valid) {
       const float* rec = (i < al ? recv_l + MG::HDR + (size_t)i * MG::R : recv_r + MG::HDR + (size_t)(i - al) * MG::R);
-      for (int c = 0; c < MG::S; ++c) st_next[(size_t)c * NT + j] = rec[c];
+      for (int c = 0; c < MG::S; ++c) st_next[rix<D>(c, j, NT)] = rec[c];
       orig_next[j] = __float_as_int(rec[MG::U]);
       float x[D];
 #pragma unroll
@@ -2875,7 +2903,7 @@ __global__ void k_mig_rev_pack(KParams P, MigParams M, const float* __restrict__
     const int j = nt + i;
     if (j >= P.NT) continue;
     float* out = i < al ? out_l + (size_t)i * MG::S : out_r + (size_t)(i - al) * MG::S;
-    out[c] = g[(size_t)c * NT + j];
+    out[c] = g[rix<D>(c, j, NT)];
   }
 }
 
@@ -2893,7 +2921,7 @@ __global__ void k_mig_rev_unpack(KParams P, MigParams M, const float* __restrict
     const float* rec = i < nl ? sent_l + MG::HDR + (size_t)i * MG::R : sent_r + MG::HDR + (size_t)(i - nl) * MG::R;
     const float* in = i < nl ? in_l + (size_t)i * MG::S : in_r + (size_t)(i - nl) * MG::S;
     const int k = __float_as_int(rec[MG::K]);
-    g[(size_t)c * NT + k] = in[c];
+    g[rix<D>(c, k, NT)] = in[c];
   }
 }
 
@@ -2967,7 +2995,7 @@ __global__ void k_seed(KParams P, const int* __restrict__ orig, const float* __r
   const size_t NT = P.NT;
   int u = orig[k];
   auto put = [&](int comp, float val) {
-    float* q = &g[(size_t)comp * NT + k];
+    float* q = &g[rix<D>(comp, k, NT)];
     *q = accumulate ? *q + val : val;
   };
 #pragma unroll
@@ -2993,19 +3021,19 @@ __global__ void k_soa_to_user(KParams P, const int* __restrict__ orig, const flo
   if (j >= (nslot ? *nslot : P.NT)) return;
   const size_t NT = P.NT;
   if (owner) {
-    const int bx = base_of(owner[(size_t)comp_x<D>(0) * NT + j], P.fres);
+    const int bx = base_of(owner[rix<D>(comp_x<D>(0), j, NT)], P.fres);
     if (bx < M.own_lo || bx >= M.own_hi) return;  // a hole: the particle is the neighbour's now
   }
   int u = orig ? orig[j] : j;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    if (x) x[u * D + a] = st[(size_t)comp_x<D>(a) * NT + j];
-    if (v) v[u * D + a] = st[(size_t)comp_v<D>(a) * NT + j];
+    if (x) x[u * D + a] = st[rix<D>(comp_x<D>(a), j, NT)];
+    if (v) v[u * D + a] = st[rix<D>(comp_v<D>(a), j, NT)];
 #pragma unroll
     for (int b = 0; b < D; ++b) {
       // states store H = F - I; adjoints (dL/dF = dL/dH) are returned as they are
-      if (F) F[(u * D + a) * D + b] = st[(size_t)comp_F<D>(a, b) * NT + j] + ((state && a == b) ? 1.f : 0.f);
-      if (C) C[(u * D + a) * D + b] = st[(size_t)comp_C<D>(a, b) * NT + j];
+      if (F) F[(u * D + a) * D + b] = st[rix<D>(comp_F<D>(a, b), j, NT)] + ((state && a == b) ? 1.f : 0.f);
+      if (C) C[(u * D + a) * D + b] = st[rix<D>(comp_C<D>(a, b), j, NT)];
     }
   }
 }
