@@ -55,6 +55,9 @@
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
 #endif
+#ifndef MPM_P2GT_CLAIM
+#define MPM_P2GT_CLAIM 1  // P2G^T work items claimed and decoded by thread 0 (claim_item)
+#endif
 
 #ifndef MPM_SCAT_FX
 #define MPM_SCAT_FX 1
@@ -1061,6 +1064,34 @@ __device__ __forceinline__ bool work_item(const StepArgs& A, int wi, int n_occ, 
   return true;
 }
 
+template <int D>
+__device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, int* bc) {
+  r = gb / P.nb;
+  int t = gb - r * P.nb;
+#pragma unroll
+  for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
+}
+
+// A CTA's next work item, claimed and decoded by thread 0 alone (the block id, particle range,
+// rollout and block coordinates, with their runtime divisions) and broadcast through shared
+// memory at the claim barrier: the per-item set-up is not repeated by every thread (a block's
+// ~512 particles give each thread only ~2 of them, so per-item work is a visible share).
+template <int D> struct WorkSh { int gb, s, n, r, bc[D]; };  // n < 0: no work left
+template <int D, bool SPLIT>
+__device__ __forceinline__ void claim_item(const KParams& P, const StepArgs& A, int field, int n_occ, int parts,
+                                           WorkSh<D>& w) {
+  const int wi = atomicAdd(&A.info_t[field], 1);
+  int gb, s, n;
+  if (!work_item<SPLIT>(A, wi, n_occ, parts, gb, s, n)) {
+    w.n = -1;
+    return;
+  }
+  w.gb = gb;
+  w.s = s;
+  w.n = n;
+  block_coords<D>(P, gb, w.r, w.bc);
+}
+
 // P2G payload of one particle (Eq. 4 with P_total F^T = tau, R1/R21 + actuation S1):
 //   B = dx G = -4 res dt V tau + m dx C,  A = m v - B fx   (node value w_o (A + B o))
 // t = the step whose actuation applies; latches an inverted element (det F <= 0).
@@ -1212,17 +1243,23 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
     buf[atomicAdd(&s_cursor[e.y & (kCPB - 1)], 1)] = e.x;
   }
   __syncthreads();
-  for (int i = tid; i < n; i += kThreads) {
-    const int j = buf[i];
-    int c = 0;  // cell of position i: the last c with cstart[c] <= i (binary search)
-#pragma unroll
-    for (int step = kCPB / 2; step > 0; step >>= 1)
-      if (s_cstart[c + step] <= i) c += step;
+  // rank of each particle among its cell's (stable: ties by storage index, R18), per input
+  // element: the first two of a thread still hold (storage index, cell) in registers, the
+  // others re-read their (storage index, key) pair -- no search for the cell of a position
+  auto place = [&](int j, int c) {
     const int lo = s_cstart[c], hi = s_cstart[c + 1];
-    if (crowd && hi - lo > kRankMax) continue;  // a crowded cell: sorted below
+    if (crowd && hi - lo > kRankMax) return;  // a crowded cell: sorted below
     int rank = 0;
+#pragma unroll 4
     for (int q = lo; q < hi; ++q) rank += buf[q] < j;
-    A.perm[s + lo + rank] = j;  // stable: ties by storage index (R18)
+    A.perm[s + lo + rank] = j;
+  };
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (tid + q * kThreads < n) place(pj[q], pc[q]);
+  for (int i = tid + 2 * kThreads; i < n; i += kThreads) {
+    const int2 e = A.tmp_pk[s + i];
+    place(e.x, e.y & (kCPB - 1));
   }
   if (crowd) sort_crowded_cells(A.perm + s, buf, s_cstart, tid);
   __syncthreads();
@@ -1376,7 +1413,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
   float (*s_pay)[kCap] = reinterpret_cast<float (*)[kCap]>(s_dyn);  // [PY::N][kCap], dynamic
   int* s_sort = scat_fx(ADJ) ? reinterpret_cast<int*>(s_dyn) : s_sort_st;  // done before the payload is written
   __shared__ float4 s_tile[3][TN];
-  __shared__ int s_blk;
+  __shared__ WorkSh<D> s_w;
   const int tid = threadIdx.x;
   const size_t NT = P.NT;
   const int work_field = ADJ ? I_WORK2 : I_WORK;
@@ -1388,21 +1425,18 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
   static_assert(!SPLIT || ADJ, "only the adjoint scatter splits blocks");
   const int parts = work_parts<SPLIT>(n_occ);
   for (;;) {
-    if (tid == 0) s_blk = atomicAdd(&A.info_t[work_field], 1);
+    if (tid == 0) claim_item<D, SPLIT>(P, A, work_field, n_occ, parts, s_w);
     __syncthreads();
-    int gb, s, n;
-    if (!work_item<SPLIT>(A, s_blk, n_occ, parts, gb, s, n)) break;
-    if (SPLIT && n == 0) {  // uniform; every thread has read s_blk before thread 0 claims again
+    const int n = s_w.n;
+    if (n < 0) break;
+    if (SPLIT && n == 0) {  // uniform; every thread has read s_w before thread 0 claims again
       __syncthreads();
       continue;
     }
-    const int r = gb / P.nb;
+    const int gb = s_w.gb, s = s_w.s, r = s_w.r;
     int bc[D];
-    {
-      int t = gb - r * P.nb;
 #pragma unroll
-      for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
-    }
+    for (int a = 0; a < D; ++a) bc[a] = s_w.bc[a];
     // the tile's 2^D block slots (flush): looked up now, used at the end
     int myslot = -1;
     {
@@ -1554,13 +1588,6 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 // Weights are separable, W = wx(ox) wy(oy) wz(oz); oz-sums are formed first and folded
 // per (ox, oy), so the moments sum_i W v_i o_b cost O(1) per node.
 // ------------------------------------------------------------------------------------
-template <int D>
-__device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, int* bc) {
-  r = gb / P.nb;
-  int t = gb - r * P.nb;
-#pragma unroll
-  for (int a = D - 1; a >= 0; --a) { bc[a] = t % P.nbpa; t /= P.nbpa; }
-}
 
 template <int D, bool TWO>
 __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs& A, const int* node, int slot,
@@ -1825,21 +1852,23 @@ template <int D, bool SPLIT = false>
 __global__ __launch_bounds__(kThreads, MPM_G2P_MINB) void k_g2p(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   __shared__ float4 s_v[Dim<D>::TN];
-  __shared__ int s_blk;
+  __shared__ WorkSh<D> s_w;
   const size_t NT = P.NT;
   const int n_occ = A.info_t[I_NOCC];
   const int parts = work_parts<SPLIT>(n_occ);
   for (;;) {
-    if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK3], 1);
+    if (threadIdx.x == 0) claim_item<D, SPLIT>(P, A, I_WORK3, n_occ, parts, s_w);
     __syncthreads();
-    int gb, s, n;
-    if (!work_item<SPLIT>(A, s_blk, n_occ, parts, gb, s, n)) break;
-    if (SPLIT && n == 0) {  // uniform; every thread has read s_blk before thread 0 claims again
+    const int n = s_w.n;
+    if (n < 0) break;
+    if (SPLIT && n == 0) {  // uniform; every thread has read s_w before thread 0 claims again
       __syncthreads();
       continue;
     }
-    int r, bc[D];
-    block_coords<D>(P, gb, r, bc);
+    const int s = s_w.s, r = s_w.r;
+    int bc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) bc[a] = s_w.bc[a];
     float4 vref, aref_unused;
 #if MPM_G2P_PF
     for (int i = threadIdx.x; i < n; i += kThreads) {  // this block's x, F -> L2
@@ -1950,18 +1979,21 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
   extern __shared__ __align__(16) unsigned char s_dyn[];
   float (*s_pay)[kCapF] = reinterpret_cast<float (*)[kCapF]>(s_dyn);  // [PY::N][kCapF], dynamic (SCAT)
   int* s_sort = SCAT ? reinterpret_cast<int*>(s_dyn) : s_sort_st;  // the sort is done before the payload is written
-  __shared__ int s_blk, s_nesc;
+  __shared__ WorkSh<D> s_w;
+  __shared__ int s_nesc;
   const int tid = threadIdx.x;
   const int n_occ = A.info_t[I_NOCC];
   const int ox = tid / kCPB;
   const int c = D == 3 ? ((((tid >> 2) & 3) * 4 + ((tid >> 4) & 3)) * 4 + (tid & 3)) : tid % kCPB;
   for (;;) {
-    if (tid == 0) s_blk = atomicAdd(&A.info_t[I_WORK3], 1);
+    if (tid == 0) claim_item<D, false>(P, A, I_WORK3, n_occ, 1, s_w);
     __syncthreads();
-    int gb, s, n;
-    if (!work_item<false>(A, s_blk, n_occ, 1, gb, s, n)) break;
-    int r, bc[D];
-    block_coords<D>(P, gb, r, bc);
+    const int n = s_w.n;
+    if (n < 0) break;
+    const int s = s_w.s, r = s_w.r;
+    int bc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) bc[a] = s_w.bc[a];
     int myslot = -1;  // grid t+1 slots of the tile's blocks bc + {0, 1}^D (flush)
     if (SCAT) {
       const int lane = tid & 31;
@@ -2516,7 +2548,11 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
   constexpr int NW = MPM_P2GT_THREADS / 32;
   __shared__ float4 s_v[Dim<D>::TN];
   __shared__ float4 s_a[Dim<D>::TN];
+#if MPM_P2GT_CLAIM
+  __shared__ WorkSh<D> s_w;
+#else
   __shared__ int s_blk;
+#endif
   __shared__ float s_da[NW][kMaxAct * D];  // per-warp dL/da[r][t][:][:] partial sums
   __shared__ int s_da_r;                   // the rollout they belong to (-1: none)
   const int n_occ = A.info_t[I_NOCC];
@@ -2538,6 +2574,20 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
   };
   const int parts = work_parts<SPLIT>(n_occ);
   for (;;) {
+#if MPM_P2GT_CLAIM
+    if (threadIdx.x == 0) claim_item<D, SPLIT>(P, A, I_WORK4, n_occ, parts, s_w);
+    __syncthreads();
+    const int n = s_w.n;
+    if (n < 0) break;
+    if (SPLIT && n == 0) {  // uniform; every thread has read s_w before thread 0 claims again
+      __syncthreads();
+      continue;
+    }
+    const int s = s_w.s, r = s_w.r;
+    int bc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) bc[a] = s_w.bc[a];
+#else
     if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
     __syncthreads();
     int gb, s, n;
@@ -2548,6 +2598,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
     }
     int r, bc[D];
     block_coords<D>(P, gb, r, bc);
+#endif
     if (KD > 0 && r != s_da_r) {  // uniform: a new rollout -> flush the previous one's sums
       if (s_da_r >= 0) flush_da(s_da_r);
       __syncthreads();
