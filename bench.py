@@ -56,8 +56,9 @@ def _cfg_dict(K, W, n_gpus, sc, workload="C4", slabs=None, fuse=0):
     return {"workload": WORKLOADS[workload], "particles_per_rank": int(sc.batch * sc.n),
             "rollouts_per_rank": int(sc.batch), "grid": f"{sc.res}^3", "dim": 3, "dt": sc.dt,
             "steps_per_pass": K, "warmup": W, "parallelism": par,
-            "forward": ("fused G2P2G, one particle pass per step (NEXT N2)" if fuse and not (workload == "C5a" and n_gpus > 1)
-                        else "P2G + G2P passes"),
+            "forward": ("fused G2P2G, one particle pass per step (NEXT N2)"
+                        + ("; slab windows of grid t+1 summed between launches" if workload == "C5a" and n_gpus > 1 else "")
+                        if fuse else "P2G + G2P passes"),
             "l2": (f"inputs larger than L2: per-step state {sc.batch * sc.n * 96 / 2**20:.0f} MiB read + written, "
                    f"tape of K states")}
 
@@ -448,7 +449,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--fuse", type=int, default=1, choices=[0, 1],
-                    help="fused G2P2G forward (NEXT N2); C5a split over GPUs runs P2G + G2P (window exchange between them)")
+                    help="fused G2P2G forward (NEXT N2; C5a split over GPUs sums grid t+1's windows between launches)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -96,10 +96,12 @@ typedef struct {
                            step: the G2P of step t also scatters step t+1's P2G into a
                            grid allocated as the one-block dilation of step t's occupied
                            blocks (results equal the unfused path up to fp32 summation
-                           order).  Requires |v| dt < dx (else MPM_ERR_CFL); ignored for
-                           a slab with neighbours (its window exchange sits between P2G and
-                           G2P) and with a controller (N1 needs state t+1 before step
-                           t+1's P2G).  0 = P2G and G2P as separate passes.              */
+                           order).  Requires |v| dt < dx (else MPM_ERR_CFL).  A slab with
+                           neighbours sums the windows of grid t+1 between two fused launches;
+                           ignored in the migrating slab mode (arrivals join state t+1 after
+                           its G2P) and with a controller (N1 needs state t+1 before step
+                           t+1's P2G).  Group calls need the same value in every context.
+                           0 = P2G and G2P as separate passes.                           */
 } mpm_config;
 
 /* Create a context on config->device.  Validates the config (MPM_ERR_INVALID_ARG) and
@@ -203,6 +205,9 @@ mpm_status mpm_grad_controller(mpm_ctx ctx, float* dW, float* db, float* dtarget
  *   left neighbour is rank r-1 (ranks ordered by slab).  The exchange is a grouped NCCL
  *   send/recv with the two neighbours on config.stream; the da sum an NCCL all-reduce.
  *   mpm_comm_init is collective over the world (blocks until all ranks call it).
+ *   libnccl.so.2 is loaded at the first NCCL call: one already in the process if any, else the
+ *   file named by the environment variable MPM_NCCL_LIB (the Python binding sets it to the
+ *   NCCL that torch bundles), else the loader's search path; none -> MPM_ERR_COMM.
  * mpm_group_forward / mpm_group_backward: the same exchange between n contexts of ONE
  *   process (adjacent slabs in x order, one device, one stream), done as device-to-device
  *   copies between the phases of every step -- a single-GPU emulation of the sharded run

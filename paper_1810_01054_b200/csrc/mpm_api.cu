@@ -52,7 +52,12 @@ const NcclApi* nccl_api() {
   // function-local static: initialised once, thread-safe (C++11)
   static const NcclApi* const api = []() -> const NcclApi* {
     static NcclApi a{};
+    // an NCCL already in the process (e.g. torch's) first; else MPM_NCCL_LIB (the Python binding
+    // points it at the NCCL torch bundles, so that a later `import torch` finds the NCCL it
+    // was built against under the shared soname); else the loader's search path
     void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h)
+      if (const char* p = getenv("MPM_NCCL_LIB"); p && *p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     bool ok = h != nullptr;
@@ -663,9 +668,10 @@ void backward_mig_unpack(mpm_ctx c, int t) {
 // table) -> k_scatter (block grouping, zero grid t+1) -> k_g2p2g (cell sort of t, G2P, P2G
 // of t+1): 3 launches, one particle pass.  A step whose grid is not yet built (the first
 // of a range or of a segment) runs the unfused P2G first.
-// (a slab with neighbours exchanges its windows between P2G and G2P: not fusable; a slab
-// without neighbours -- the whole domain, bench.py's C5a at N = 1 -- is)
-bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !has_nbr(c) && !c->ctrl && !c->mig; }
+// A slab with neighbours (Lagrangian ownership) sums its windows of grid t+1 between two
+// G2P2G launches: grid t+1 is complete before the G2P of step t+1 reads it.  Not fused: the
+// migrating slab mode (arrivals are appended to state t+1 after its G2P) and the controller.
+bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !c->ctrl && !c->mig; }
 
 template <int D, bool SORT, bool SCAT>
 void launch_fused(mpm_ctx c, const StepArgs& A) {
@@ -676,32 +682,47 @@ void launch_fused(mpm_ctx c, const StepArgs& A) {
   else kx(c, k_g2p2g<D, 0, SORT, SCAT>, dim3(ng), dim3(kThreads), dyn, P, A);
 }
 
+// A fused step in two halves around the slab-window exchanges (a slab with neighbours sums its
+// windows of grid t after the unfused P2G that starts a range, and of grid t+1 after each
+// G2P2G).  Part a: start of a range or segment -- binning of t and the unfused P2G of step t
+// (returns true: grid t was just built and, in slab mode, its windows are packed).
 template <int D>
-void forward_fused_step(mpm_ctx c, int t, int t_end) {
+bool fused_part_a(mpm_ctx c, int t, int t_end) {
   const KParams& P = c->P;
   if (c->ck && t - c->seg0 == c->tape_cap) {
     roll_segment(c, t);
     c->fused_grid = -1;
   }
-  const bool have = c->fused_grid == t;
+  if (c->fused_grid == t) return false;
+  const bool next = t + 1 < t_end && (int)ti(c, t + 1) < c->tape_cap;
+  StepArgs A = step_args(c, t);
+  const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
+  launch(c, KI_SCAN, [&] {
+    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
+       info_at(c, t), bs_at(c, t), occ_at(c, t), info_at(c, t), ti(c, t) ? info_at(c, t - 1) : nullptr,
+       slot_at(c, t), touch_at(c, t), c->err, t);
+  });
+  if (next) launch_bin_fused<D>(c, t, false, true);
+  launch_scatter(c, t, info_at(c, t), next ? info_at(c, t + 1) : nullptr);
+  const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
+  launch(c, KI_P2G, [&] {
+    if (P.material == 1) kx(c, k_block_scatter<D, false, 1>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A);
+    else kx(c, k_block_scatter<D, false>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A);
+  });
+  if (has_nbr(c)) launch_band_pack(c, t, false, c->arena);
+  return true;
+}
+
+// Part b: the G2P of step t, fused with step t+1's P2G when t+1 is in the range and segment
+// (returns true: grid t+1 was built and, in slab mode, its windows are packed).
+template <int D>
+bool fused_part_b(mpm_ctx c, int t, int t_end, bool built) {
+  const KParams& P = c->P;
   const bool next = t + 1 < t_end && (int)ti(c, t + 1) < c->tape_cap;
   StepArgs A = step_args(c, t);
   A.slot_next = next ? slot_at(c, t + 1) : nullptr;
-  if (!have) {
-    // the unfused P2G of step t builds grid t (with its own, undilated slot map)
-    const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
-    launch(c, KI_SCAN, [&] {
-      kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
-         info_at(c, t), bs_at(c, t), occ_at(c, t), info_at(c, t), ti(c, t) ? info_at(c, t - 1) : nullptr,
-         slot_at(c, t), touch_at(c, t), c->err, t);
-    });
-    if (next) launch_bin_fused<D>(c, t, false, true);
-    launch_scatter(c, t, info_at(c, t), next ? info_at(c, t + 1) : nullptr);
-    const int nblk = std::max(1, std::min(P.NBT, c->n_sm * c->occ_scatter));
-    launch(c, KI_P2G, [&] {
-      if (P.material == 1) kx(c, k_block_scatter<D, false, 1>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A);
-      else kx(c, k_block_scatter<D, false>, dim3(nblk), dim3(kThreads), scatter_dyn_smem<D, false>(), P, A);
-    });
+  if (built) {
+    if (has_nbr(c)) launch_band_unpack(c, t, false, c->arena);
     if (next) {
       launch(c, KI_FUSE, [&] { launch_fused<D, false, true>(c, A); });
     } else {
@@ -721,6 +742,8 @@ void forward_fused_step(mpm_ctx c, int t, int t_end) {
   }
   c->res_end = t + 1;
   c->fused_grid = next ? t + 1 : -1;
+  if (next && has_nbr(c)) launch_band_pack(c, t + 1, false, c->arena);
+  return next;
 }
 
 // forward steps [t0, t1) (slab mode: with the window exchange between the phases)
@@ -728,7 +751,19 @@ template <int D>
 mpm_status forward_range(mpm_ctx c, int t0, int t1) {
   c->fused_grid = -1;
   if (fuse_on(c)) {
-    for (int t = t0; t < t1; ++t) forward_fused_step<D>(c, t, t1);
+    for (int t = t0; t < t1; ++t) {
+      const bool built = fused_part_a<D>(c, t, t1);
+      if (built && has_nbr(c)) {
+        mpm_status s = exchange_nccl(c);
+        if (s) return s;
+      }
+      const bool next = fused_part_b<D>(c, t, t1, built);
+      if (next && has_nbr(c)) {
+        mpm_status s = exchange_nccl(c);
+        if (s) return s;
+        launch_band_unpack(c, t + 1, false, c->arena);
+      }
+    }
     return MPM_OK;
   }
   for (int t = t0; t < t1; ++t) {
@@ -1307,10 +1342,11 @@ mpm_status group_check(mpm_ctx* cs, int32_t n) {
     if (c->poisoned) return fail(c, MPM_ERR_CALL_ORDER, "context poisoned by an earlier error; call mpm_set_state");
     if (c->comm) return fail(c, MPM_ERR_CALL_ORDER, "context has a communicator; use mpm_forward/mpm_backward");
     if (c->cfg.device != c0->cfg.device || c->stream != c0->stream || c->D != c0->D || c->P.res != c0->P.res ||
-        c->tape_len != c0->tape_len || c->mig != c0->mig ||
+        c->tape_len != c0->tape_len || c->mig != c0->mig || c->cfg.fuse_g2p2g != c0->cfg.fuse_g2p2g ||
+        c->ctrl != c0->ctrl ||
         (c->mig && (c->NU != c0->NU || c->M.mig_cap != c0->M.mig_cap)))
-      return fail(c, MPM_ERR_INVALID_ARG, "group contexts need one device, one stream, equal dim/res/tape length "
-                                          "and the same slab mode");
+      return fail(c, MPM_ERR_INVALID_ARG, "group contexts need one device, one stream, equal dim/res/tape length, "
+                                          "the same slab mode and the same fuse_g2p2g / controller setting");
     if (c->transport) return fail(c, MPM_ERR_CALL_ORDER, "context has a transport; use mpm_forward/mpm_backward");
     if (n > 1 && !c->slab) return fail(c, MPM_ERR_INVALID_ARG, "group contexts need mpm_set_slab");
     if (c->ck) return fail(c, MPM_ERR_INVALID_ARG, "group calls do not support checkpoint_every");
@@ -1326,7 +1362,24 @@ mpm_status group_check(mpm_ctx* cs, int32_t n) {
 
 template <int D>
 mpm_status group_forward(mpm_ctx* cs, int32_t n, int32_t steps) {
-  for (int k = 0; k < steps; ++k) {
+  const int t_end = cs[0]->tape_len + steps;
+  for (int i = 0; i < n; ++i) cs[i]->fused_grid = -1;
+  for (int k = 0; k < steps && fuse_on(cs[0]); ++k) {  // fused forward, windows summed between launches
+    const int t = cs[0]->tape_len + k;
+    bool built = false, next = false;
+    for (int i = 0; i < n; ++i) built = fused_part_a<D>(cs[i], t, t_end);
+    if (built && n > 1) {
+      mpm_status s = exchange_local(cs, n);
+      if (s) return s;
+    }
+    for (int i = 0; i < n; ++i) next = fused_part_b<D>(cs[i], t, t_end, built);
+    if (next && n > 1) {
+      mpm_status s = exchange_local(cs, n);
+      if (s) return s;
+      for (int i = 0; i < n; ++i) launch_band_unpack(cs[i], t + 1, false, cs[i]->arena);
+    }
+  }
+  for (int k = 0; k < steps && !fuse_on(cs[0]); ++k) {
     const int t = cs[0]->tape_len + k;
     for (int i = 0; i < n; ++i) forward_phase_a<D>(cs[i], t);
     if (n > 1) {

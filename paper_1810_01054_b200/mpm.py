@@ -60,6 +60,22 @@ class _Config(C.Structure):
 _lib = None
 
 
+def _bundled_nccl():
+    """Path of the libnccl.so.2 of the nvidia-nccl wheel torch links against, or None (found
+    without importing torch).  libmpm dlopens NCCL lazily; loading this one keeps a later
+    `import torch` from resolving its libnccl.so.2 to an older system copy."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
+
+
 def load():
     """Load libmpm.so (raises if it was not built: there is no fallback)."""
     global _lib
@@ -67,6 +83,10 @@ def load():
         return _lib
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+    if "MPM_NCCL_LIB" not in os.environ:  # the NCCL torch bundles (see nccl_api in mpm_api.cu)
+        nccl = _bundled_nccl()
+        if nccl:
+            os.environ["MPM_NCCL_LIB"] = nccl
     L = C.CDLL(LIB_PATH)
     vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
     L.mpm_create.argtypes = [C.POINTER(_Config), C.POINTER(vp)]

@@ -16,12 +16,12 @@ from tests.helpers import assert_grads, oracle_cfg, rel_err
 pytestmark = pytest.mark.gpu
 
 
-def _slab_sims(sc, T, G, halo=1):
+def _slab_sims(sc, T, G, halo=1, fuse=0):
     bounds = parallel.slab_partition(sc.x[0], sc.res, sc.dim, G, halo)
     sims, idxs = [], []
     for lo, hi in bounds:
         s2, idx = parallel.shard_slab(sc, lo, hi)
-        sim = mpm.MPM(mpm.Config.from_scene(s2, max_steps=T))
+        sim = mpm.MPM(mpm.Config.from_scene(s2, max_steps=T, fuse_g2p2g=fuse))
         sim.set_slab(lo, hi, halo)
         sim.set_scene(s2)
         sims.append(sim)
@@ -51,9 +51,16 @@ def _oracle(sc, T, seed):
     return traj, w, g
 
 
-def _check_slab_run(sc, T, G, halo=1, seed=5, tol=1e-3, orc=None):
-    sims, idxs, bounds = _slab_sims(sc, T, G, halo)
+def _check_slab_run(sc, T, G, halo=1, seed=5, tol=1e-3, orc=None, fuse=0):
+    sims, idxs, bounds = _slab_sims(sc, T, G, halo, fuse)
+    if fuse:
+        for sim in sims:
+            sim.set_profiling(True)
     mpm.group_forward(sims, T)
+    if fuse:  # the fused forward really ran: one unfused P2G, then G2P2G with window sums between
+        for sim in sims:
+            pf = sim.profile()
+            assert pf["p2g"][1] == 1 and pf["g2p2g"][1] == T and pf["band_pack"][1] == T, pf
     x, v, F, Cm = _gather_state(sims, idxs, sc, T)
     traj, w, (g0, gE, gnu, ga) = orc if orc is not None else _oracle(sc, T, seed)
     ox, ov, oC, oF = oracle.unpack(traj[T], sc.dim)
@@ -91,11 +98,13 @@ def _drift_scene(dim):
     return scenes.tiny(3, seed=12, res=64, n_cells=(24, 8, 8), steps=40, v0=(6.0, 0.0, 0.0), K=2, s=40.0)
 
 
+@pytest.mark.parametrize("fuse", [0, 1])
 @pytest.mark.parametrize("dim,G,halo", [(2, 2, 1), (2, 3, 1), (3, 2, 1), (3, 3, 1), (3, 2, 2)])
-def test_slab_drift_across_boundaries_vs_oracle(dim, G, halo):
+def test_slab_drift_across_boundaries_vs_oracle(dim, G, halo, fuse):
     """Particles stream in +x across the slab boundaries (ownership stays with the t = 0
     slab; their stencils move into the neighbour's window): state and every gradient family
-    of the whole body vs the oracle, 40 steps with random F0/C0, actuation, floor friction."""
+    of the whole body vs the oracle, 40 steps with random F0/C0, actuation, floor friction.
+    fuse = 1: the fused G2P2G forward, grid t+1's windows summed between two launches."""
     sc = _drift_scene(dim)
     bounds = parallel.slab_partition(sc.x[0], sc.res, sc.dim, G, halo)
     # the scene really crosses: some particle's base_x ends beyond its slab
@@ -104,7 +113,7 @@ def test_slab_drift_across_boundaries_vs_oracle(dim, G, halo):
     bxT = np.floor(traj[40][:, 0] * sc.res - 0.5)
     crossed = sum(int(np.sum((bx0 < hi) & (bxT >= hi))) for _, hi in bounds[:-1])
     assert crossed > 0
-    _check_slab_run(sc, 40, G, halo, orc=(traj, w, g))
+    _check_slab_run(sc, 40, G, halo, orc=(traj, w, g), fuse=fuse)
 
 
 @pytest.fixture(scope="module")
@@ -113,12 +122,12 @@ def c3_oracle():
     return sc, _oracle(sc, 100, 9)
 
 
-@pytest.mark.parametrize("G", [2, 3])
-def test_slab_quadruped_c3_vs_oracle(c3_oracle, G):
+@pytest.mark.parametrize("G,fuse", [(2, 0), (3, 0), (2, 1), (3, 1)])
+def test_slab_quadruped_c3_vs_oracle(c3_oracle, G, fuse):
     """configs[2] quadruped (29,952 particles, 16 actuators) split into G x-slabs: whole-body
-    state and gradients after 100 steps within the north_star's 1e-3."""
+    state and gradients after 100 steps within the north_star's 1e-3 (unfused and fused forward)."""
     sc, orc = c3_oracle
-    _check_slab_run(sc, 100, G, orc=orc)
+    _check_slab_run(sc, 100, G, orc=orc, fuse=fuse)
 
 
 def test_slab_single_context_equals_plain():

@@ -142,7 +142,7 @@ def test_migrate_capacity_errors():
 
 
 # ---- two processes on one GPU, host-staged exchanges through gloo --------------------------------
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, mode="migrate"):
     try:
         os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         import torch
@@ -154,10 +154,18 @@ def _rank_main(rank, world, port, q):
         cut = 32  # two slabs of the 64^3 quadruped (block-aligned)
         bounds = [(0, cut), (cut, sc.res)]
         lo, hi = bounds[rank]
-        cfg = mpm.Config.from_scene(sc, max_steps=T)
-        cfg.n_particles = int(0.9 * sc.n)
-        sim = mpm.MPM(cfg)
-        sim.set_slab_migrating(lo, hi, 1, sc.n, 0)
+        idx = None
+        if mode == "migrate":
+            cfg = mpm.Config.from_scene(sc, max_steps=T)
+            cfg.n_particles = int(0.9 * sc.n)
+            sim = mpm.MPM(cfg)
+            sim.set_slab_migrating(lo, hi, 1, sc.n, 0)
+        else:  # Lagrangian ownership, fused forward (windows of grid t+1 summed between launches)
+            sc_full = sc
+            sc, idx = parallel.shard_slab(sc_full, lo, hi)
+            sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=T, fuse_g2p2g=1))
+            sim.set_slab(lo, hi, 1)
+            sim.set_profiling(True)
 
         def xchg(kind, sl, sr, rl, rr):
             if kind == "reduce":
@@ -177,27 +185,35 @@ def _rank_main(rank, world, port, q):
         sim.set_transport(xchg)
         sim.set_scene(sc)
         sim.forward(T)
+        if idx is not None:
+            pf = sim.profile()
+            assert pf["p2g"][1] == 1 and pf["g2p2g"][1] == T and pf["band_pack"][1] == T, pf
         st = [a.copy() for a in sim.get_state(T)]
         rng = np.random.default_rng(51)
-        w = rng.standard_normal((sc.n, oracle.S_of(3)))
+        w = rng.standard_normal((scenes.quadruped_3d(steps=40).n, oracle.S_of(3)))
+        if idx is not None:
+            w = w[idx]
         wx, wv, wC, wF = oracle.unpack(w, 3)
         f32 = lambda a: np.ascontiguousarray(a, np.float32)
         sim.backward(f32(wx), f32(wv), f32(wF), f32(wC))
         g = sim.grad()
-        q.put((rank, st, {k: np.asarray(v).copy() for k, v in g.items()}, int(np.sum(bx >= cut))))
+        q.put((rank, st, {k: np.asarray(v).copy() for k, v in g.items()}, int(np.sum(bx >= cut)), idx))
         sim.close()
         dist.barrier()
         dist.destroy_process_group()
     except Exception as e:  # noqa: BLE001
         import traceback
-        q.put((rank, "error", traceback.format_exc(), None))
+        q.put((rank, "error", traceback.format_exc(), None, None))
 
 
-def test_two_processes_gloo_transport_vs_oracle():
+@pytest.mark.parametrize("mode", ["migrate", "lagrangian_fused"])
+def test_two_processes_gloo_transport_vs_oracle(mode):
     """configs[2]'s quadruped (29,952 particles) split at x = 32 between two PROCESSES on cuda:0,
-    exchanging windows, migrants and adjoints through gloo (mpm_set_transport); summed state
-    and gradients vs the whole-body oracle -- the collective call order of forward / get_state
-    / backward / grad and the gradient reductions across processes."""
+    exchanging through gloo (mpm_set_transport); summed / gathered state and gradients vs the
+    whole-body oracle -- the collective call order of forward / get_state / backward / grad and
+    the gradient reductions across processes.  migrate: Eulerian ownership with migrants and
+    reverse-migrated adjoints; lagrangian_fused: fixed ownership with the fused forward (the
+    windows of grid t+1 summed between two G2P2G launches)."""
     import multiprocessing as mp
     import socket
     with socket.socket() as s_:
@@ -205,7 +221,7 @@ def test_two_processes_gloo_transport_vs_oracle():
         port = s_.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q, mode)) for r in range(2)]
     for p in procs:
         p.start()
     res = {}
@@ -219,15 +235,30 @@ def test_two_processes_gloo_transport_vs_oracle():
     sc = scenes.quadruped_3d(steps=40)
     T = 40
     traj, w, (g0, gE, gnu, ga) = _oracle_run(sc, T, 51)
-    st = [res[0][1][i].astype(np.float64) + res[1][1][i] for i in range(4)]
+    if mode == "migrate":
+        st = [res[0][1][i].astype(np.float64) + res[1][1][i] for i in range(4)]
+        g = {k: res[0][2][k].astype(np.float64) + res[1][2][k] for k in ("dx0", "dv0", "dF0", "dC0", "dE", "dnu")}
+    else:  # each process holds its shard (parallel.shard_slab indices)
+        st = [np.zeros((sc.n,) + a.shape[1:]) for a in res[0][1]]
+        g = {k: np.zeros((sc.n,) + np.asarray(res[0][2][k]).shape[1:]) for k in ("dx0", "dv0", "dF0", "dC0", "dE", "dnu")}
+        for r in (0, 1):
+            idx = res[r][4]
+            for i in range(4):
+                st[i][idx] = res[r][1][i]
+            for k in g:
+                g[k][idx] = res[r][2][k]
     ox, ov, oC, oF = oracle.unpack(traj[T], 3)
     vmax = np.abs(ov).max()
     for k, a, b, scale in (("x", st[0], ox, 1.0), ("v", st[1], ov, vmax), ("F", st[2], oF, np.abs(oF).max()),
                            ("C", st[3], oC, 4 * sc.res * vmax)):
         assert np.abs(a - b).max() / scale < 1e-4, k
-    g = {k: res[0][2][k].astype(np.float64) + res[1][2][k] for k in ("dx0", "dv0", "dF0", "dC0")}
-    np.testing.assert_array_equal(res[0][2]["dE"], res[1][2]["dE"])
+    if mode == "migrate":
+        np.testing.assert_array_equal(res[0][2]["dE"], res[1][2]["dE"])
+        gE_gpu, gnu_gpu = res[0][2]["dE"], res[0][2]["dnu"]
+    else:
+        gE_gpu, gnu_gpu = g["dE"], g["dnu"]
+    np.testing.assert_array_equal(res[0][2]["da"], res[1][2]["da"])  # the shared actuation gradient
     gx, gv, gC, gF = oracle.unpack(g0, 3)
     assert_grads([("dx0", g["dx0"], gx), ("dv0", g["dv0"], gv), ("dF0", g["dF0"], gF), ("dC0", g["dC0"], gC),
-                  ("dE", res[0][2]["dE"], gE), ("dnu", res[0][2]["dnu"], gnu), ("da", res[0][2]["da"][0, :T], ga)])
+                  ("dE", gE_gpu, gE), ("dnu", gnu_gpu, gnu), ("da", res[0][2]["da"][0, :T], ga)], ctx=mode)
     assert 0 < res[0][3] < sc.n  # both slabs own particles
