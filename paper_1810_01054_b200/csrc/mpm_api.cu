@@ -676,8 +676,14 @@ bool fuse_on(mpm_ctx c) { return c->cfg.fuse_g2p2g && !c->ctrl && !c->mig; }
 template <int D, bool SORT, bool SCAT>
 void launch_fused(mpm_ctx c, const StepArgs& A) {
   const KParams& P = c->P;
-  const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_fuse));
   const size_t dyn = SCAT ? fuse_dyn_smem<D>() : 0;
+  if (c->split) {  // small problems: blocks shared by several CTAs (work_parts)
+    const int ng = std::max(1, std::min(8 * P.NBT, c->n_sm * c->occ_fuse));
+    if (P.material == 1) kx(c, k_g2p2g<D, 1, SORT, SCAT, true>, dim3(ng), dim3(kThreads), dyn, P, A);
+    else kx(c, k_g2p2g<D, 0, SORT, SCAT, true>, dim3(ng), dim3(kThreads), dyn, P, A);
+    return;
+  }
+  const int ng = std::max(1, std::min(P.NBT, c->n_sm * c->occ_fuse));
   if (P.material == 1) kx(c, k_g2p2g<D, 1, SORT, SCAT>, dim3(ng), dim3(kThreads), dyn, P, A);
   else kx(c, k_g2p2g<D, 0, SORT, SCAT>, dim3(ng), dim3(kThreads), dyn, P, A);
 }
@@ -1561,8 +1567,9 @@ mpm_status mpm_create(const mpm_config* cfg, mpm_ctx* out) {
     c->occ_scatter_adj = std::max(1, occ);
   }
   {  // NEXT N2 fused forward: payload buffer in dynamic shared memory
-#define FA(D, MAT, SORT) \
-  cudaFuncSetAttribute(k_g2p2g<D, MAT, SORT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fuse_dyn_smem<D>())
+#define FA(D, MAT, SORT)                                                                                         \
+  cudaFuncSetAttribute(k_g2p2g<D, MAT, SORT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fuse_dyn_smem<D>()); \
+  cudaFuncSetAttribute(k_g2p2g<D, MAT, SORT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fuse_dyn_smem<D>())
     FA(3, 0, false); FA(3, 0, true); FA(3, 1, false); FA(3, 1, true);
     FA(2, 0, false); FA(2, 0, true); FA(2, 1, false); FA(2, 1, true);
 #undef FA

@@ -1076,7 +1076,7 @@ __device__ __forceinline__ void block_coords(const KParams& P, int gb, int& r, i
 // rollout and block coordinates, with their runtime divisions) and broadcast through shared
 // memory at the claim barrier: the per-item set-up is not repeated by every thread (a block's
 // ~512 particles give each thread only ~2 of them, so per-item work is a visible share).
-template <int D> struct WorkSh { int gb, s, n, r, bc[D]; };  // n < 0: no work left
+template <int D> struct WorkSh { int gb, s, n, r, bc[D], s0, n0; };  // n < 0: no work left; s0, n0: the whole block
 template <int D, bool SPLIT>
 __device__ __forceinline__ void claim_item(const KParams& P, const StepArgs& A, int field, int n_occ, int parts,
                                            WorkSh<D>& w) {
@@ -1089,6 +1089,8 @@ __device__ __forceinline__ void claim_item(const KParams& P, const StepArgs& A, 
   w.gb = gb;
   w.s = s;
   w.n = n;
+  w.s0 = SPLIT ? A.block_start[gb] : s;
+  w.n0 = SPLIT ? A.block_start[gb + 1] - w.s0 : n;
   block_coords<D>(P, gb, w.r, w.bc);
 }
 
@@ -1961,7 +1963,7 @@ __device__ __forceinline__ void scatter_escapees(const KParams& P, const StepArg
   }
 }
 
-template <int D, int MAT, bool SORT, bool SCAT>
+template <int D, int MAT, bool SORT, bool SCAT, bool SPLIT = false>
 __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, StepArgs A) {
   MPM_PDL_ENTRY();
   using DD = Dim<D>;
@@ -1985,12 +1987,26 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
   const int n_occ = A.info_t[I_NOCC];
   const int ox = tid / kCPB;
   const int c = D == 3 ? ((((tid >> 2) & 3) * 4 + ((tid >> 4) & 3)) * 4 + (tid & 3)) : tid % kCPB;
+  // SPLIT (small problems, fewer occupied blocks than CTAs): a block's particles are shared by
+  // up to 8 CTAs; each sorts the whole block (identical perm values; a block beyond kSortCap,
+  // whose sort needs the global scratch, goes to its first part alone) and runs G2P and the
+  // step-(t+1) scatter on its range of the sorted order, flushing a partial tile with REDs
+  const int parts = work_parts<SPLIT>(n_occ);
   for (;;) {
-    if (tid == 0) claim_item<D, false>(P, A, I_WORK3, n_occ, 1, s_w);
+    if (tid == 0) claim_item<D, SPLIT>(P, A, I_WORK3, n_occ, parts, s_w);
     __syncthreads();
-    const int n = s_w.n;
+    int n = s_w.n, s = s_w.s;
     if (n < 0) break;
-    const int s = s_w.s, r = s_w.r;
+    const int s0 = s_w.s0, n0 = s_w.n0;
+    if (SPLIT && n0 > kSortCap) {  // uniform: the whole block to the part that starts it
+      n = s == s0 ? n0 : 0;
+      s = s0;
+    }
+    if (SPLIT && n == 0) {  // uniform; every thread has read s_w before thread 0 claims again
+      __syncthreads();
+      continue;
+    }
+    const int r = s_w.r;
     int bc[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) bc[a] = s_w.bc[a];
@@ -2017,7 +2033,7 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
     if (SORT) {
       if (tid < kCPB) s_hist[tid] = 0;
       __syncthreads();
-      block_cell_sort<D, true>(P, A, s, n, tid, s_hist, s_cstart, s_cursor, s_sort);
+      block_cell_sort<D, true>(P, A, s0, n0, tid, s_hist, s_cstart, s_cursor, s_sort);
     }
 #if !MPM_FUSE_STAGE_FIRST
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
@@ -2139,7 +2155,7 @@ template <int D> struct PassAcc {
 };
 
 // one pass; F4 = tile of float4 (f = .xyz, e = em * .w), c(o) = c0 + Cm o
-template <int D, int OX, int OY, bool WS>
+template <int D, int OX, int OY, bool WS, bool EM = true>
 __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, const float (&w)[D][3],
                                          const float (&dw)[D][3], const float* c0, const float (&Cm)[D][D],
                                          float em, const float4& ref, PassAcc<D>& R) {
@@ -2158,7 +2174,7 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
     for (int oz = 0; oz < 3; ++oz) {
       const float4 q = tile[tile_idx<D, OX, OY, 0>(lb) + oz];
       const float f[3] = {q.x - ref.x, q.y - ref.y, q.z - ref.z};
-      float sv = em * (q.w - ref.w);
+      float sv = EM ? em * (q.w - ref.w) : 0.f;  // EM = false: no e_i term (v-pass; 0 * q.w is not foldable)
 #pragma unroll
       for (int a = 0; a < 3; ++a) sv = fmaf(f[a], oz == 0 ? cxy[a] : fmaf((float)oz, Cm[a][2], cxy[a]), sv);
       const float wz = w[2][oz];
@@ -2186,7 +2202,7 @@ __device__ __forceinline__ void pass_row(const float4* tile, const int* lb, cons
   } else {
     const float4 q = tile[tile_idx<D, OX, OY, 0>(lb)];
     const float f[2] = {q.x - ref.x, q.y - ref.y};
-    float sv = em * (q.w - ref.w);
+    float sv = EM ? em * (q.w - ref.w) : 0.f;
 #pragma unroll
     for (int a = 0; a < 2; ++a) sv = fmaf(f[a], cxy[a], sv);
     const float wx = w[0][OX], wy = w[1][OY], wxy = wx * wy;
@@ -2282,7 +2298,7 @@ __device__ __forceinline__ void stencil_pass2(const float4* tile, const int* lb,
   Ro.Se = R.Se;
 }
 
-template <int D, bool WS, bool F2 = false>
+template <int D, bool WS, bool F2 = false, bool EM = true>
 __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, const float (&w)[D][3],
                                              const float (&dw)[D][3], const float* c0,
                                              const float (&Cm)[D][D], float em, const float4& ref,
@@ -2298,11 +2314,11 @@ __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, 
     stencil_pass2<WS>(tile, lb, w, dw, c0, Cm, em, R);  // ref is zero at every call site
     return;
   }
-  pass_row<D, 0, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 0, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 0, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 1, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 2, 0, WS>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 2, 1, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
-  pass_row<D, 2, 2, WS>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 0, 0, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 0, 1, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 0, 2, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 0, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 1, 1, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 1, 2, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 2, 0, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R); pass_row<D, 2, 1, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R);
+  pass_row<D, 2, 2, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R);
 }
 
 template <int D, bool MG, int MAT>
@@ -2354,7 +2370,7 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
         u0[a] = fmaf(-U[a][b], sc.fx[b], u0[a]);
       }
     }
-    stencil_pass<D, false, (MPM_FFMA2_P2GT & 1) != 0>(s_v, lb, sc.w, dw, u0, U, 0.f, make_float4(0.f, 0.f, 0.f, 0.f), Rv);
+    stencil_pass<D, false, (MPM_FFMA2_P2GT & 1) != 0, false>(s_v, lb, sc.w, dw, u0, U, 0.f, make_float4(0.f, 0.f, 0.f, 0.f), Rv);
     // dx term -4 res^2 g_C^T v^{t+1} = -res U^T S_v
 #pragma unroll
     for (int a = 0; a < D; ++a) {

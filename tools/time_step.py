@@ -1,6 +1,7 @@
 """Per-kernel device time of the C4 forward + backward step (CUDA events around every
 launch inside libmpm).  Usage: python tools/time_step.py [steps] [lib_path]
-(MPM_FUSE=1 in the environment: the fused G2P2G forward, NEXT N2)"""
+(MPM_FUSE=1 in the environment: the fused G2P2G forward, NEXT N2; MPM_SCENE=c1|c2|c3 times a
+small BASELINE config over K steps instead of C4)"""
 import json
 import os
 import sys
@@ -17,12 +18,14 @@ def main():
     K = int(sys.argv[1]) if len(sys.argv) > 1 else 20
     if len(sys.argv) > 2:
         mpm.LIB_PATH = sys.argv[2]
-    sc = scenes.slab_3d(steps=K)
+    make = {"c4": scenes.slab_3d, "c1": scenes.block_2d, "c2": scenes.walker_2d,
+            "c3": scenes.quadruped_3d}[os.environ.get("MPM_SCENE", "c4")]
+    sc = make(steps=K)
     fuse = int(os.environ.get("MPM_FUSE", "0"))
     sim = mpm.MPM(mpm.Config.from_scene(sc, max_steps=K, fuse_g2p2g=fuse))
     sim.set_scene(sc)
     m = sc.mass.reshape(-1).astype(np.float64)
-    seed = np.zeros((sc.n, 3), np.float32)
+    seed = np.zeros((sc.n, sc.dim), np.float32)
     seed[:, 0] = m / m.sum()
     for _ in range(2):
         sim.rewind(0)
