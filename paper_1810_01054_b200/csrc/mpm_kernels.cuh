@@ -150,7 +150,10 @@ struct MigParams {
 // Per-step bookkeeping record, info[t * kInfo + field]
 constexpr int kInfo = 12;
 enum { I_NOCC = 0, I_NTOUCH = 1, I_BASE = 2, I_WORK = 3, I_WORK2 = 4, I_OK = 5, I_WORK3 = 6, I_WORK4 = 7,
-       I_NSLOT = 8 };  // I_NSLOT: storage slots of state t (migrating slab mode; live + left-behind holes)
+       I_NSLOT = 8,    // storage slots of state t (migrating slab mode; live + left-behind holes)
+       I_NBIG = 9 };   // occupied blocks with >= kBigBlock particles: occ_list[0, I_NBIG); the others
+                       // fill occ_list from its end (occ_list[NBT - 1 - i], i < I_NOCC - I_NBIG)
+constexpr int kBigBlock = 256;  // particles: the "long" work items claimed first (k_scan_lookback)
 
 // Migrating slab mode: a particle whose base_x leaves the slab after G2P gets this key (it is
 // not binned, gathered or scattered on this rank at the next step -- a hole in the storage)
@@ -732,6 +735,37 @@ __device__ __forceinline__ int3 warp_incl_scan3(int3 v) {
   return v;
 }
 
+__device__ __forceinline__ int4 warp_incl_scan4(int4 v) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int a = __shfl_up_sync(0xffffffffu, v.x, o);
+    int b = __shfl_up_sync(0xffffffffu, v.y, o);
+    int c = __shfl_up_sync(0xffffffffu, v.z, o);
+    int d = __shfl_up_sync(0xffffffffu, v.w, o);
+    if (lane >= o) { v.x += a; v.y += b; v.z += c; v.w += d; }
+  }
+  return v;
+}
+
+// CTA-wide exclusive scan of an int4 (kThreads threads)
+__device__ __forceinline__ int4 cta_excl_scan4(int4 v, int4* s_warp, int4& total) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int4 inc = warp_incl_scan4(v);
+  if (lane == 31) s_warp[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int4 t = lane < kThreads / 32 ? s_warp[lane] : make_int4(0, 0, 0, 0);
+    int4 ti = warp_incl_scan4(t);
+    if (lane < kThreads / 32) s_warp[lane] = make_int4(ti.x - t.x, ti.y - t.y, ti.z - t.z, ti.w - t.w);
+    if (lane == kThreads / 32 - 1) s_warp[kThreads / 32] = ti;
+  }
+  __syncthreads();
+  int4 wo = s_warp[w];
+  total = s_warp[kThreads / 32];
+  return make_int4(wo.x + inc.x - v.x, wo.y + inc.y - v.y, wo.z + inc.z - v.z, wo.w + inc.w - v.w);
+}
+
 // CTA-wide exclusive scan of an int3 (kThreads threads)
 __device__ __forceinline__ int3 cta_excl_scan3(int3 v, int3* s_warp, int3& total) {
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -777,8 +811,8 @@ __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __res
 // last tile writes the step record (counts, arena base, zeroed work counters).
 struct ScanTileState {
   unsigned* flag;          // [n_tiles]: epoch << 2 | status (1 = aggregate, 2 = inclusive prefix)
-  int3* agg;               // [n_tiles]
-  int3* incl;              // [n_tiles]
+  int4* agg;               // [n_tiles] (count, big occupied, touched, small occupied)
+  int4* incl;              // [n_tiles]
   unsigned long long* ticket;
 };
 
@@ -795,17 +829,22 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
                                                            int* __restrict__ slot_of, int* __restrict__ touched_list,
                                                            ErrLatch* err, int t) {
   MPM_PDL_ENTRY();
-  __shared__ int3 s_warp[kThreads / 32 + 1];
+  __shared__ int4 s_warp[kThreads / 32 + 1];
   __shared__ int s_tile;
-  __shared__ int3 s_pre;
+  __shared__ int4 s_pre;
   if (threadIdx.x == 0) s_tile = (int)(atomicAdd(ts.ticket, 1ull) % (unsigned long long)n_tiles);
   __syncthreads();
   const int tile = s_tile;
   const int gb = tile * kScanTile + threadIdx.x;
   int c = 0, o = 0, tc = 0;
   if (gb < P.NBT) block_flags<D, DIL>(P, cnt, gb, c, o, tc);
-  int3 tot;
-  const int3 ex = cta_excl_scan3(make_int3(c, o, tc), s_warp, tot);
+  // occupied blocks in two classes for the work lists of the block kernels: big ones (at least
+  // kBigBlock particles) from the front of occ_list, small ones from its back, so that the CTAs
+  // that claim items dynamically take the long items first and the short ones last (a shorter
+  // tail when the last items run out)
+  const int ob = o && c >= kBigBlock, os = o && c < kBigBlock;
+  int4 tot;
+  const int4 ex = cta_excl_scan4(make_int4(c, ob, tc, os), s_warp, tot);
   const unsigned ep = epoch << 2;
   if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 tiles at a time
     const int lane = threadIdx.x;
@@ -814,32 +853,33 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
       __threadfence();
       atomicExch(&ts.flag[tile], ep | (tile == 0 ? 2u : 1u));
     }
-    int3 pre = make_int3(0, 0, 0);
+    int4 pre = make_int4(0, 0, 0, 0);
     for (int i = tile - 1; i >= 0; i -= 32) {
       const int idx = i - lane;
       unsigned f = ep | 2u;  // before tile 0: an empty inclusive prefix
-      int3 v = make_int3(0, 0, 0);
+      int4 v = make_int4(0, 0, 0, 0);
       if (idx >= 0) {
         do { f = *((volatile unsigned*)&ts.flag[idx]); } while ((f & ~3u) != ep || (f & 3u) == 0u);
         __threadfence();
         const volatile int* q = (const volatile int*)((f & 3u) == 2u ? &ts.incl[idx] : &ts.agg[idx]);
-        v = make_int3(q[0], q[1], q[2]);
+        v = make_int4(q[0], q[1], q[2], q[3]);
       }
       const unsigned pm = __ballot_sync(0xffffffffu, (f & 3u) == 2u);
       const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix (lowest lane)
-      if (lane > stop) v = make_int3(0, 0, 0);
+      if (lane > stop) v = make_int4(0, 0, 0, 0);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
         v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
         v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
+        v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
       }
-      pre.x += v.x; pre.y += v.y; pre.z += v.z;
+      pre.x += v.x; pre.y += v.y; pre.z += v.z; pre.w += v.w;
       if (pm) break;
     }
     if (lane == 0) {
       if (tile > 0) {
-        ts.incl[tile] = make_int3(pre.x + tot.x, pre.y + tot.y, pre.z + tot.z);
+        ts.incl[tile] = make_int4(pre.x + tot.x, pre.y + tot.y, pre.z + tot.z, pre.w + tot.w);
         __threadfence();
         atomicExch(&ts.flag[tile], ep | 2u);
       }
@@ -847,13 +887,14 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
     }
   }
   __syncthreads();
-  const int3 pre = s_pre;
+  const int4 pre = s_pre;
   const int base = info_gprev ? info_gprev[I_BASE] + info_gprev[I_NTOUCH] : 0;
   const int cap = min(P.slots_per_step, P.arena_slots - base);
   if (gb < P.NBT) {
     if (info_bin) {
       block_start[gb] = ex.x + pre.x;
-      if (o) occ_list[ex.y + pre.y] = gb;
+      if (ob) occ_list[ex.y + pre.y] = gb;
+      if (os) occ_list[P.NBT - 1 - (ex.w + pre.w)] = gb;
     }
     if (info_grid) {
       const int sl = ex.z + pre.z;
@@ -876,7 +917,8 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
       info_grid[I_OK] = ok;
     }
     if (info_bin) {
-      info_bin[I_NOCC] = pre.y + tot.y;
+      info_bin[I_NOCC] = pre.y + tot.y + pre.w + tot.w;
+      info_bin[I_NBIG] = pre.y + tot.y;
       info_bin[I_WORK] = 0;
       info_bin[I_WORK2] = 0;
       info_bin[I_WORK3] = 0;
@@ -1041,22 +1083,28 @@ __device__ __forceinline__ int pay_slot(int p) { return p ^ (((p >> 5) ^ (p >> 7
 // Work items of the gathers: (occupied block, part of its particles).  Small problems (fewer
 // occupied blocks than CTAs) split each block into up to 8 particle ranges so that more CTAs
 // work (each stages its block's tile); large ones keep one item per block.
+// i-th occupied block in claim order: the big ones, then the small ones (k_scan_lookback)
+__device__ __forceinline__ int occ_item(const KParams& P, const StepArgs& A, int i) {
+  const int nbig = A.info_t[I_NBIG];
+  return i < nbig ? A.occ_list[i] : A.occ_list[P.NBT - 1 - (i - nbig)];
+}
+
 template <bool SPLIT>
 __device__ __forceinline__ int work_parts(int n_occ) {
   return SPLIT ? max(1, min(8, (int)gridDim.x / max(n_occ, 1))) : 1;
 }
 template <bool SPLIT>
-__device__ __forceinline__ bool work_item(const StepArgs& A, int wi, int n_occ, int parts, int& gb, int& s, int& n) {
+__device__ __forceinline__ bool work_item(const KParams& P, const StepArgs& A, int wi, int n_occ, int parts, int& gb, int& s, int& n) {
   if (!SPLIT) {
     if (wi >= n_occ) return false;
-    gb = A.occ_list[wi];
+    gb = occ_item(P, A, wi);
     s = A.block_start[gb];
     n = A.block_start[gb + 1] - s;
     return true;
   }
   if (wi >= n_occ * parts) return false;
   const int bi = wi / parts, part = wi - bi * parts;
-  gb = A.occ_list[bi];
+  gb = occ_item(P, A, bi);
   const int s0 = A.block_start[gb], n0 = A.block_start[gb + 1] - s0;
   const int lo = n0 * part / parts, hi = n0 * (part + 1) / parts;
   s = s0 + lo;
@@ -1082,7 +1130,7 @@ __device__ __forceinline__ void claim_item(const KParams& P, const StepArgs& A, 
                                            WorkSh<D>& w) {
   const int wi = atomicAdd(&A.info_t[field], 1);
   int gb, s, n;
-  if (!work_item<SPLIT>(A, wi, n_occ, parts, gb, s, n)) {
+  if (!work_item<SPLIT>(P, A, wi, n_occ, parts, gb, s, n)) {
     w.n = -1;
     return;
   }
@@ -2607,7 +2655,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
     if (threadIdx.x == 0) s_blk = atomicAdd(&A.info_t[I_WORK4], 1);
     __syncthreads();
     int gb, s, n;
-    if (!work_item<SPLIT>(A, s_blk, n_occ, parts, gb, s, n)) break;
+    if (!work_item<SPLIT>(P, A, s_blk, n_occ, parts, gb, s, n)) break;
     if (SPLIT && n == 0) {  // uniform; every thread has read s_blk before thread 0 claims again
       __syncthreads();
       continue;
