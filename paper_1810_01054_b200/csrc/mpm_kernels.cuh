@@ -55,6 +55,9 @@
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
 #endif
+#ifndef MPM_P2GT_SIG_EARLY
+#define MPM_P2GT_SIG_EARLY 1  // the actuation load issued before the v-pass: measured -2 us (P2G^T 136.0 -> 134.0)
+#endif
 #ifndef MPM_P2GT_CLAIM
 #define MPM_P2GT_CLAIM 1  // P2G^T work items claimed and decoded by thread 0 (claim_item)
 #endif
@@ -2382,6 +2385,14 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   const float dmu0 = A.dmu[u], dlam0 = A.dlam[u];  // accumulators: loaded early, stored at the end
   const float dm0 = MG ? A.dmass[u] : 0.f;
   const float kk = 4.f * P.fres * P.fres * P.dt * pr.y;
+#if MPM_P2GT_SIG_EARLY
+  // the actuation of this particle (third load of the chain orig -> aid -> act), issued before
+  // the v-pass so that its latency overlaps the pass
+  float sig[D];
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+    sig[a] = ai >= 0 ? P.act_s * __ldg(&A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a]) : 0.f;
+#endif
   float x[D];
 #pragma unroll
   for (int a = 0; a < D; ++a) x[a] = __ldg(&A.st[rix<D>(comp_x<D>(a), j, NT)]);
@@ -2431,10 +2442,12 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
     }
   }
   // ---- dp-pass: c(o) = q(o) = m v + dx G (o - fx), e_i = m dm_i   (Eqs. 4-5) ----
+#if !MPM_P2GT_SIG_EARLY
   float sig[D];
 #pragma unroll
   for (int a = 0; a < D; ++a)
     sig[a] = ai >= 0 ? P.act_s * __ldg(&A.act[(((size_t)r * P.T + A.t) * P.K + ai) * D + a]) : 0.f;
+#endif
   PassAcc<D> Rd;
   float Gm[D][D];  // dx G
   {
