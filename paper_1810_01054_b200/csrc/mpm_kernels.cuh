@@ -58,6 +58,9 @@
 #ifndef MPM_P2GT_SIG_EARLY
 #define MPM_P2GT_SIG_EARLY 1  // the actuation load issued before the v-pass: measured -2 us (P2G^T 136.0 -> 134.0)
 #endif
+#ifndef MPM_P2GT_PARK
+#define MPM_P2GT_PARK 3  // record rows parked in shared memory (1: dL/dx, dL/dF; 2: + H; 3: + v, C): -9.5 us
+#endif
 #ifndef MPM_P2GT_CLAIM
 #define MPM_P2GT_CLAIM 1  // P2G^T work items claimed and decoded by thread 0 (claim_item)
 #endif
@@ -2372,10 +2375,28 @@ __device__ __forceinline__ void stencil_pass(const float4* tile, const int* lb, 
   pass_row<D, 2, 2, WS, EM>(tile, lb, w, dw, c0, Cm, em, ref, R);
 }
 
+// P2G^T's shared-memory park of one particle (rows of MPM_P2GT_THREADS floats): incoming
+// dL/dx, dL/dF; the state's H; v; C
+template <int D> constexpr int kParkH = D + D * D;
+template <int D> constexpr int kParkV = kParkH<D> + D * D;
+template <int D> constexpr int kParkC = kParkV<D> + D;
+template <int D> constexpr int kParkN = MPM_P2GT_PARK >= 3 ? kParkC<D> + D * D : MPM_P2GT_PARK >= 2 ? kParkV<D> : MPM_P2GT_PARK ? kParkH<D> : 1;
+template <int D>
+__device__ __forceinline__ void park_H(const StepArgs& A, size_t NT, int j, const float* park, float (&H)[D][D]) {
+#if MPM_P2GT_PARK >= 2
+#pragma unroll
+  for (int a = 0; a < D; ++a)
+#pragma unroll
+    for (int b = 0; b < D; ++b) H[a][b] = park[(kParkH<D> + a * D + b) * MPM_P2GT_THREADS];
+#else
+  load_H<D>(A.st, NT, j, H);
+#endif
+}
+
 template <int D, bool MG, int MAT>
 __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArgs& A, const float4* s_v,
                                                  const float4* s_a, const float4& aref, const int* bc,
-                                                 int r, int k, int& aid_out, float* dsig_out) {
+                                                 int r, int k, int& aid_out, float* dsig_out, float* park) {
   const size_t NT = P.NT;
   const float* gi = A.gin;
   const int j = __ldg(&A.perm[k]);
@@ -2415,6 +2436,33 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   float gxv[D];
   {
     float u0[D], U[D][D];
+#if MPM_P2GT_PARK
+    // the incoming dL/dx and dL/dF of this particle, parked in shared memory for the epilogue
+    // ((J), (H)) instead of re-read from global memory there (a stride of the CTA size:
+    // conflict-free)
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      park[a * MPM_P2GT_THREADS] = gi[rix<D>(comp_x<D>(a), k, NT)];
+#pragma unroll
+      for (int b = 0; b < D; ++b) park[(D + a * D + b) * MPM_P2GT_THREADS] = gi[rix<D>(comp_F<D>(a, b), k, NT)];
+    }
+#endif
+#if MPM_P2GT_PARK >= 2  // and the state's H (read by the stress and by (H), (K))
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        park[(kParkH<D> + a * D + b) * MPM_P2GT_THREADS] = __ldg(&A.st[rix<D>(comp_F<D>(a, b), j, NT)]);
+#endif
+#if MPM_P2GT_PARK >= 3  // and the state's v, C (the dp-pass payload)
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      park[(kParkV<D> + a) * MPM_P2GT_THREADS] = __ldg(&A.st[rix<D>(comp_v<D>(a), j, NT)]);
+#pragma unroll
+      for (int b = 0; b < D; ++b)
+        park[(kParkC<D> + a * D + b) * MPM_P2GT_THREADS] = __ldg(&A.st[rix<D>(comp_C<D>(a, b), j, NT)]);
+    }
+#endif
 #pragma unroll
     for (int a = 0; a < D; ++a) {
       u0[a] = fmaf(P.dt, gi[rix<D>(comp_x<D>(a), k, NT)], gi[rix<D>(comp_v<D>(a), k, NT)]);
@@ -2452,15 +2500,17 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   float Gm[D][D];  // dx G
   {
     float H[D][D], tau[D][D], q0[D];
-    load_H<D>(A.st, NT, j, H);
+    park_H<D>(A, NT, j, park, H);
     if constexpr (MAT == 1) kirchhoff_fcr<D>(H, pr.z, pr.w, sig, tau, det1m<D>(H));
     else kirchhoff_h<D>(H, pr.z, pr.w, sig, tau, log1pf(det1m<D>(H)));
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-      q0[a] = pr.x * __ldg(&A.st[rix<D>(comp_v<D>(a), j, NT)]);
+      q0[a] = pr.x * (MPM_P2GT_PARK >= 3 ? park[(kParkV<D> + a) * MPM_P2GT_THREADS] : __ldg(&A.st[rix<D>(comp_v<D>(a), j, NT)]));
 #pragma unroll
       for (int b = 0; b < D; ++b) {
-        Gm[a][b] = P.dx * fmaf(-kk, tau[a][b], pr.x * __ldg(&A.st[rix<D>(comp_C<D>(a, b), j, NT)]));
+        Gm[a][b] = P.dx * fmaf(-kk, tau[a][b],
+                               pr.x * (MPM_P2GT_PARK >= 3 ? park[(kParkC<D> + a * D + b) * MPM_P2GT_THREADS]
+                                                          : __ldg(&A.st[rix<D>(comp_C<D>(a, b), j, NT)])));
         q0[a] = fmaf(-Gm[a][b], sc.fx[b], q0[a]);
       }
     }
@@ -2482,14 +2532,14 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   // (J): dx = gx + sum dW s - 4res^2 g_C^T S_v - G^T S_d
 #pragma unroll
   for (int a = 0; a < D; ++a) {
-    float acc = gi[rix<D>(comp_x<D>(a), k, NT)] + gxv[a] + Rd.g[a];
+    float acc = (MPM_P2GT_PARK ? park[a * MPM_P2GT_THREADS] : gi[rix<D>(comp_x<D>(a), k, NT)]) + gxv[a] + Rd.g[a];
 #pragma unroll
     for (int b = 0; b < D; ++b) acc = fmaf(-P.fres * Gm[b][a], Rd.S[b], acc);
     go[rix<D>(comp_x<D>(a), j, NT)] = acc;
   }
   // (H), (K), material parameters
   float H[D][D], F[D][D];
-  load_H<D>(A.st, NT, j, H);
+  park_H<D>(A, NT, j, park, H);
   F_of_H<D>(H, F);
   const float jm1 = det1m<D>(H);
   const float J = 1.f + jm1;
@@ -2545,11 +2595,12 @@ __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArg
   for (int a = 0; a < D; ++a)
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      float acc = gi[rix<D>(comp_F<D>(a, b), k, NT)];
+      float acc = MPM_P2GT_PARK ? park[(D + a * D + b) * MPM_P2GT_THREADS] : gi[rix<D>(comp_F<D>(a, b), k, NT)];
       float tf = 0.f;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        acc = fmaf(P.dt * Cn[c][a], gi[rix<D>(comp_F<D>(c, b), k, NT)], acc);
+        acc = fmaf(P.dt * Cn[c][a],
+                   MPM_P2GT_PARK ? park[(D + c * D + b) * MPM_P2GT_THREADS] : gi[rix<D>(comp_F<D>(c, b), k, NT)], acc);
         tf = fmaf(T[a][c] + T[c][a], F[c][b], tf);
       }
       if constexpr (MAT == 1) {
@@ -2631,6 +2682,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
   __shared__ int s_blk;
 #endif
   __shared__ float s_da[NW][kMaxAct * D];  // per-warp dL/da[r][t][:][:] partial sums
+  __shared__ float s_park[kParkN<D> * MPM_P2GT_THREADS];  // p2g_adj_particle's parked record
   __shared__ int s_da_r;                   // the rollout they belong to (-1: none)
   const int n_occ = A.info_t[I_NOCC];
   const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
@@ -2696,7 +2748,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       const int i = i0 + threadIdx.x;
       int ai = -1;
       float dsig[D] = {};
-      if (i < n) p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig);
+      if (i < n) p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig, s_park + threadIdx.x);
       __syncwarp();
       if (P.K > 0) reduce_actuation<D>(s_da[threadIdx.x >> 5], ai, dsig);
     }
