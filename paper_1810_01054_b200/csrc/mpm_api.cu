@@ -838,10 +838,15 @@ void backward_phase_b(mpm_ctx c, int t) {
   A.gin = c->bcur;
   A.gout = c->bnxt;
   if (has_nbr(c)) launch_band_unpack(c, t, true, A.grid);
-  launch(c, KI_GRIDT, [&] {
-    kx(c, k_grid_adj<D>, dim3(c->n_sm * 8), dim3(256), 0, P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
-                                                       t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
-  });
+  if (MPM_GRIDT_FUSED && c->split) {  // small problems: gridT inside P2G^T's tile staging; P2G^T
+    A.info_prev = t > c->seg0 ? info_at(c, t - 1) : nullptr;  // also prepares step t-1's adjoint grid
+    A.agrid_prev = agrid_of(c, t - 1);
+  } else {
+    launch(c, KI_GRIDT, [&] {
+      kx(c, k_grid_adj<D>, dim3(c->n_sm * 8), dim3(256), 0, P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
+                                                         t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
+    });
+  }
   const int na = std::max(1, std::min(P.NBT, c->n_sm * c->occ_p2gT));
   launch(c, KI_P2GT, [&] { launch_p2gT<D>(c, P, A, na); });
   if (c->ctrl) {  // N1: controller adjoint of step t (needs this step's complete dL/da)

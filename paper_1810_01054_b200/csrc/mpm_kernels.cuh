@@ -61,6 +61,9 @@
 #ifndef MPM_P2GT_PARK
 #define MPM_P2GT_PARK 3  // record rows parked in shared memory (1: dL/dx, dL/dF; 2: + H; 3: + v, C): -9.5 us
 #endif
+#ifndef MPM_GRIDT_FUSED
+#define MPM_GRIDT_FUSED 1  // small problems: gridT folded into P2G^T's tile staging (no k_grid_adj launch)
+#endif
 #ifndef MPM_P2GT_CLAIM
 #define MPM_P2GT_CLAIM 1  // P2G^T work items claimed and decoded by thread 0 (claim_item)
 #endif
@@ -576,6 +579,13 @@ __device__ __forceinline__ void project_node_adj(const float* vbar, float* g, co
     }
   }
   for (int w = nw - 1; w >= 0; --w) project_wall_adj<D>(vin[w], g, wax[w], wsg[w], wc[w]);
+}
+
+// the wall-band nodes' projection adjoint out of line (rare; keeps its replay arrays out of
+// the register allocation of the kernels that stage tiles)
+template <int D>
+__device__ __noinline__ void band_node_adj(const float* vbar, float* g, const int* node, const KParams& P) {
+  project_node_adj<D>(vbar, g, node, P);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1645,7 +1655,7 @@ __global__ __launch_bounds__(kThreads, ADJ ? MPM_SCATA_MINB : MPM_SCAT_MINB) voi
 // per (ox, oy), so the moments sum_i W v_i o_b cost O(1) per node.
 // ------------------------------------------------------------------------------------
 
-template <int D, bool TWO>
+template <int D, bool TWO, bool RAW = false>
 __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs& A, const int* node, int slot,
                                                 size_t abase, float4& v, float4& ad);
 
@@ -1670,7 +1680,7 @@ __device__ __forceinline__ void fetch_node(const KParams& P, const StepArgs& A, 
 }
 
 // the same with the node's grid slot already known (-1: untouched block)
-template <int D, bool TWO>
+template <int D, bool TWO, bool RAW>
 __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs& A, const int* node, int slot,
                                                 size_t abase, float4& v, float4& ad) {
   using DD = Dim<D>;
@@ -1693,7 +1703,24 @@ __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs
   for (int a = 0; a < D; ++a) vv[a] = vb[a];
   if (in_band<D>(node, P.res, P.bound)) project_node<D>(vv, node, P);
   v = make_float4(vv[0], vv[1], D == 3 ? vv[D - 1] : 0.f, pm.w);
-  if (TWO) ad = A.grid[addr - abase];  // (dL/dp_i, dL/dm_i) from k_grid_adj
+  if (TWO) {
+    ad = A.grid[addr - abase];
+    if constexpr (RAW) {
+    // gridT (steps L, D, E; what k_grid_adj computes in place) on the raw dL/dvbar that G2P^T
+    // accumulated: the wall projection's adjoint, then vbar = p/m + dt g -> dL/dp = gv / m,
+    // dL/dm = -(p/m . gv) / m
+    const float im = 1.f / pm.w;
+    float vg[D], gv[D];
+    vg[0] = fmaf(pm.x, im, P.dt * P.g[0]); vg[1] = fmaf(pm.y, im, P.dt * P.g[1]);
+    gv[0] = ad.x; gv[1] = ad.y;
+    if constexpr (D == 3) { vg[2] = fmaf(pm.z, im, P.dt * P.g[2]); gv[2] = ad.z; }
+    if (in_band<D>(node, P.res, P.bound)) band_node_adj<D>(vg, gv, node, P);
+    float pg = 0.f;
+#pragma unroll
+    for (int d = 0; d < D; ++d) pg = fmaf(vg[d] - P.dt * P.g[d], gv[d], pg);
+    ad = make_float4(gv[0] * im, gv[1] * im, D == 3 ? gv[D - 1] * im : 0.f, -pg * im);
+    }
+  }
 }
 
 // Stage the block's node tile: s_v = v_i - vref, s_a = a_i - aref, with (vref, aref) the
@@ -1702,7 +1729,7 @@ __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs
 // the quadratic B-spline); the shift removes the common-mode velocity / adjoint so the fp32
 // cancellations in C' (Eq. 8) and in step J shrink to |v_i - vref|.  Callers add the
 // references back where an unshifted sum is needed (v' = S + vref, sum W dp = S_d + aref).
-template <int D, bool TWO, int NTH = kThreads>
+template <int D, bool TWO, int NTH = kThreads, bool RAW = false>
 __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, int r, const int* bc,
                                            float4* s_v, float4* s_a, size_t abase, float4& vref,
                                            float4& aref) {
@@ -1726,7 +1753,7 @@ __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, 
     int node[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) node[a] = bc[a] * DD::BB + DD::BB / 2;
-    fetch_node_slot<D, TWO>(P, A, node, __shfl_sync(0xffffffffu, myslot, 0), abase, vref, aref);
+    fetch_node_slot<D, TWO, RAW>(P, A, node, __shfl_sync(0xffffffffu, myslot, 0), abase, vref, aref);
   }
   for (int t0 = 0; t0 < DD::TN; t0 += NTH) {  // uniform trip count: whole warps reach the shuffle
     const int tn = t0 + (int)threadIdx.x;
@@ -1742,7 +1769,7 @@ __device__ __forceinline__ void stage_tile(const KParams& P, const StepArgs& A, 
     const int slot = __shfl_sync(0xffffffffu, myslot, sb);
     if (tn < DD::TN) {
       float4 v, ad;
-      fetch_node_slot<D, TWO>(P, A, node, slot, abase, v, ad);
+      fetch_node_slot<D, TWO, RAW>(P, A, node, slot, abase, v, ad);
       s_v[tn] = make_float4(v.x - vref.x, v.y - vref.y, v.z - vref.z, v.w);
       if (TWO) s_a[tn] = make_float4(ad.x - aref.x, ad.y - aref.y, ad.z - aref.z, ad.w - aref.w);
     }
@@ -2702,6 +2729,12 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
     }
   };
   const int parts = work_parts<SPLIT>(n_occ);
+  // small problems (SPLIT): gridT of this step runs in the tile staging (a launch fewer on a
+  // latency-bound chain; at C4 scale it costs more inside the staging than the k_grid_adj launch
+  // it saves: P2G^T +18 us for gridT's 10); its other job moves here: zero the adjoint grid of
+  // step t-1 (G2P^T of t-1 accumulates into it) and reset that step's work counters
+  constexpr bool RAW = SPLIT && MPM_GRIDT_FUSED;
+  if (RAW && A.info_prev) adj_prepare(A.info_prev, A.agrid_prev, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   for (;;) {
 #if MPM_P2GT_CLAIM
     if (threadIdx.x == 0) claim_item<D, SPLIT>(P, A, I_WORK4, n_occ, parts, s_w);
@@ -2742,7 +2775,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       prefetch_l2(&A.prm[u]);
     }
 #endif
-    stage_tile<D, true, MPM_P2GT_THREADS>(P, A, r, bc, s_v, s_a, abase, vref, aref);
+    stage_tile<D, true, MPM_P2GT_THREADS, RAW>(P, A, r, bc, s_v, s_a, abase, vref, aref);
     __syncthreads();
     for (int i0 = 0; i0 < n; i0 += MPM_P2GT_THREADS) {  // uniform trip count: whole warps reach the reduction
       const int i = i0 + threadIdx.x;
