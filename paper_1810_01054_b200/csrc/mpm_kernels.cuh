@@ -50,7 +50,7 @@
 #define MPM_FFMA2_SCAT 1
 #endif
 #ifndef MPM_FFMA2_P2GT
-#define MPM_FFMA2_P2GT 0  // ... in P2G^T (bit 0: v-pass, bit 1: dp-pass): both measured 3 us slower (128-register cliff)
+#define MPM_FFMA2_P2GT 3  // packed FFMA2 in both P2G^T passes: -6.9 us once the park freed registers (round 1: +3 us at the register cliff)
 #endif
 #ifndef MPM_P2GT_THREADS
 #define MPM_P2GT_THREADS 128
