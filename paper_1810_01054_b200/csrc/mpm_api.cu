@@ -104,7 +104,7 @@ struct mpm_ctx_s {
   int* tape_orig = nullptr;
   int* tape_bs = nullptr;
   int* tape_slot = nullptr;
-  int* tape_occ = nullptr;
+  int4* tape_occ = nullptr;  // per step: occupied-block work items {block, first, count, 0}
   int* tape_touch = nullptr;
   int* info = nullptr;
   float4* arena = nullptr;
@@ -299,7 +299,7 @@ int* perm_at(mpm_ctx c, int t) { return c->tape_perm + ti(c, t) * NTs(c); }
 int* orig_at(mpm_ctx c, int t) { return c->tape_orig + ti(c, t) * NTs(c); }
 int* bs_at(mpm_ctx c, int t) { return c->tape_bs + ti(c, t) * (c->P.NBT + 1); }
 int* slot_at(mpm_ctx c, int t) { return c->tape_slot + ti(c, t) * c->P.NBT; }
-int* occ_at(mpm_ctx c, int t) { return c->tape_occ + ti(c, t) * c->P.NBT; }
+int4* occ_at(mpm_ctx c, int t) { return c->tape_occ + ti(c, t) * c->P.NBT; }
 int* touch_at(mpm_ctx c, int t) { return c->tape_touch + ti(c, t) * c->P.NBT; }
 int* info_at(mpm_ctx c, int t) { return c->info + ti(c, t) * kInfo; }
 // migrating slab mode: buffers of step t

@@ -840,7 +840,7 @@ struct ScanTileState {
 template <int D, bool DIL = false>
 __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int* __restrict__ cnt, ScanTileState ts,
                                                            unsigned epoch, int n_tiles, int* __restrict__ info_bin,
-                                                           int* __restrict__ block_start, int* __restrict__ occ_list,
+                                                           int* __restrict__ block_start, int4* __restrict__ occ_list,
                                                            int* __restrict__ info_grid, const int* __restrict__ info_gprev,
                                                            int* __restrict__ slot_of, int* __restrict__ touched_list,
                                                            ErrLatch* err, int t) {
@@ -909,8 +909,8 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
   if (gb < P.NBT) {
     if (info_bin) {
       block_start[gb] = ex.x + pre.x;
-      if (ob) occ_list[ex.y + pre.y] = gb;
-      if (os) occ_list[P.NBT - 1 - (ex.w + pre.w)] = gb;
+      if (ob) occ_list[ex.y + pre.y] = make_int4(gb, ex.x + pre.x, c, 0);
+      if (os) occ_list[P.NBT - 1 - (ex.w + pre.w)] = make_int4(gb, ex.x + pre.x, c, 0);
     }
     if (info_grid) {
       const int sl = ex.z + pre.z;
@@ -1049,7 +1049,7 @@ struct StepArgs {
   const int* aid;         // actuator id, user order
   const float* act;       // [B][T][K][D]
   const int* block_start;
-  const int* occ_list;
+  const int4* occ_list;   // occupied-block items {block, first, count, 0} (k_scan_lookback)
   const int* slot_of;
   const int* slot_next;   // fused G2P2G: slot map of grid t+1
   const int* touched_list;
@@ -1100,7 +1100,8 @@ __device__ __forceinline__ int pay_slot(int p) { return p ^ (((p >> 5) ^ (p >> 7
 // occupied blocks than CTAs) split each block into up to 8 particle ranges so that more CTAs
 // work (each stages its block's tile); large ones keep one item per block.
 // i-th occupied block in claim order: the big ones, then the small ones (k_scan_lookback)
-__device__ __forceinline__ int occ_item(const KParams& P, const StepArgs& A, int i) {
+// (a record {block, first particle, count, 0}: a claimed item costs one dependent load)
+__device__ __forceinline__ int4 occ_item(const KParams& P, const StepArgs& A, int i) {
   const int nbig = A.info_t[I_NBIG];
   return i < nbig ? A.occ_list[i] : A.occ_list[P.NBT - 1 - (i - nbig)];
 }
@@ -1113,15 +1114,17 @@ template <bool SPLIT>
 __device__ __forceinline__ bool work_item(const KParams& P, const StepArgs& A, int wi, int n_occ, int parts, int& gb, int& s, int& n) {
   if (!SPLIT) {
     if (wi >= n_occ) return false;
-    gb = occ_item(P, A, wi);
-    s = A.block_start[gb];
-    n = A.block_start[gb + 1] - s;
+    const int4 it = occ_item(P, A, wi);
+    gb = it.x;
+    s = it.y;
+    n = it.z;
     return true;
   }
   if (wi >= n_occ * parts) return false;
   const int bi = wi / parts, part = wi - bi * parts;
-  gb = occ_item(P, A, bi);
-  const int s0 = A.block_start[gb], n0 = A.block_start[gb + 1] - s0;
+  const int4 it = occ_item(P, A, bi);
+  gb = it.x;
+  const int s0 = it.y, n0 = it.z;
   const int lo = n0 * part / parts, hi = n0 * (part + 1) / parts;
   s = s0 + lo;
   n = hi - lo;
@@ -1153,8 +1156,14 @@ __device__ __forceinline__ void claim_item(const KParams& P, const StepArgs& A, 
   w.gb = gb;
   w.s = s;
   w.n = n;
-  w.s0 = SPLIT ? A.block_start[gb] : s;
-  w.n0 = SPLIT ? A.block_start[gb + 1] - w.s0 : n;
+  if (SPLIT) {  // the whole block (its item record again: an L1/L2 hit)
+    const int4 it = occ_item(P, A, wi / parts);
+    w.s0 = it.y;
+    w.n0 = it.z;
+  } else {
+    w.s0 = s;
+    w.n0 = n;
+  }
   block_coords<D>(P, gb, w.r, w.bc);
 }
 
