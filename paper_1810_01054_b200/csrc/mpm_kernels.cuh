@@ -64,6 +64,9 @@
 #ifndef MPM_GRIDT_FUSED
 #define MPM_GRIDT_FUSED 1  // small problems: gridT folded into P2G^T's tile staging (no k_grid_adj launch)
 #endif
+#ifndef MPM_P2GT_IDXSM
+#define MPM_P2GT_IDXSM 1
+#endif
 #ifndef MPM_P2GT_CLAIM
 #define MPM_P2GT_CLAIM 1  // P2G^T work items claimed and decoded by thread 0 (claim_item)
 #endif
@@ -89,6 +92,7 @@ constexpr int kCap = 512;        // particles per producer chunk
 constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks use scratch)
 constexpr int kScanTile = kThreads;
 constexpr int kScatQ = 4;        // particles per thread in k_scatter
+constexpr int kIdxCap = 512;     // P2G^T: an item's perm / orig entries held in shared memory
 constexpr int kMaxAct = 64;      // n_actuators cap (mpm_create validates)  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
 
@@ -2432,11 +2436,13 @@ __device__ __forceinline__ void park_H(const StepArgs& A, size_t NT, int j, cons
 template <int D, bool MG, int MAT>
 __device__ __forceinline__ void p2g_adj_particle(const KParams& P, const StepArgs& A, const float4* s_v,
                                                  const float4* s_a, const float4& aref, const int* bc,
-                                                 int r, int k, int& aid_out, float* dsig_out, float* park) {
+                                                 int r, int k, int& aid_out, float* dsig_out, float* park,
+                                                 int j_in = -1, int u_in = -1) {
   const size_t NT = P.NT;
   const float* gi = A.gin;
-  const int j = __ldg(&A.perm[k]);
-  const int u = __ldg(&A.orig_next[k]);  // = orig_t[perm[k]] (written by G2P of this step)
+  // (j, u) from the caller's shared copy of the item's perm / orig (MPM_P2GT_IDXSM), else loaded
+  const int j = j_in >= 0 ? j_in : __ldg(&A.perm[k]);
+  const int u = u_in >= 0 ? u_in : __ldg(&A.orig_next[k]);  // = orig_t[perm[k]] (written by G2P of this step)
   const float4 pr = __ldg(&A.prm[u]);
   const int ai = __ldg(&A.aid[u]);
   const float dmu0 = A.dmu[u], dlam0 = A.dlam[u];  // accumulators: loaded early, stored at the end
@@ -2719,6 +2725,9 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
 #endif
   __shared__ float s_da[NW][kMaxAct * D];  // per-warp dL/da[r][t][:][:] partial sums
   __shared__ float s_park[kParkN<D> * MPM_P2GT_THREADS];  // p2g_adj_particle's parked record
+#if MPM_P2GT_IDXSM
+  __shared__ int s_pj[kIdxCap], s_pu[kIdxCap];  // the item's perm / orig (first kIdxCap particles)
+#endif
   __shared__ int s_da_r;                   // the rollout they belong to (-1: none)
   const int n_occ = A.info_t[I_NOCC];
   const size_t abase = (size_t)A.info_t[I_BASE] * kCPB;
@@ -2784,13 +2793,27 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
       prefetch_l2(&A.prm[u]);
     }
 #endif
+#if MPM_P2GT_IDXSM
+    // the item's (perm, orig) entries, read coalesced into shared memory while the tile is
+    // staged: a particle's record loads then wait on one global round trip instead of two
+    for (int q = threadIdx.x; q < min(n, kIdxCap); q += MPM_P2GT_THREADS) {
+      s_pj[q] = __ldg(&A.perm[s + q]);
+      s_pu[q] = __ldg(&A.orig_next[s + q]);
+    }
+#endif
     stage_tile<D, true, MPM_P2GT_THREADS, RAW>(P, A, r, bc, s_v, s_a, abase, vref, aref);
     __syncthreads();
     for (int i0 = 0; i0 < n; i0 += MPM_P2GT_THREADS) {  // uniform trip count: whole warps reach the reduction
       const int i = i0 + threadIdx.x;
       int ai = -1;
       float dsig[D] = {};
+#if MPM_P2GT_IDXSM
+      if (i < n)
+        p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig, s_park + threadIdx.x,
+                                     i < kIdxCap ? s_pj[i] : -1, i < kIdxCap ? s_pu[i] : -1);
+#else
       if (i < n) p2g_adj_particle<D, MG, MAT>(P, A, s_v, s_a, aref, bc, r, s + i, ai, dsig, s_park + threadIdx.x);
+#endif
       __syncwarp();
       if (P.K > 0) reduce_actuation<D>(s_da[threadIdx.x >> 5], ai, dsig);
     }
