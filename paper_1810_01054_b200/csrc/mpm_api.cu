@@ -421,7 +421,7 @@ void launch_bin(mpm_ctx c, int t) {
   const KParams& P = c->P;
   const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
   launch(c, KI_SCAN, [&] {
-    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
+    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kScanTile), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
        info_at(c, t), bs_at(c, t), occ_at(c, t), info_at(c, t), ti(c, t) ? info_at(c, t - 1) : nullptr,
        slot_at(c, t), touch_at(c, t), c->err, t);
   });
@@ -444,7 +444,7 @@ void launch_bin_fused(mpm_ctx c, int t, bool bin, bool grid) {
   const KParams& P = c->P;
   const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
   launch(c, KI_SCAN, [&] {
-    kx(c, k_scan_lookback<D, true>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
+    kx(c, k_scan_lookback<D, true>, dim3(c->n_tiles), dim3(kScanTile), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
        bin ? info_at(c, t) : nullptr, bs_at(c, t), occ_at(c, t), grid ? info_at(c, t + 1) : nullptr, info_at(c, t),
        grid ? slot_at(c, t + 1) : nullptr, grid ? touch_at(c, t + 1) : nullptr, c->err, t);
   });
@@ -704,7 +704,7 @@ bool fused_part_a(mpm_ctx c, int t, int t_end) {
   StepArgs A = step_args(c, t);
   const unsigned epoch = (++c->scan_epoch) & 0x3fffffffu;
   launch(c, KI_SCAN, [&] {
-    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
+    kx(c, k_scan_lookback<D>, dim3(c->n_tiles), dim3(kScanTile), 0, P, c->cnt, c->scan, epoch, c->n_tiles,
        info_at(c, t), bs_at(c, t), occ_at(c, t), info_at(c, t), ti(c, t) ? info_at(c, t - 1) : nullptr,
        slot_at(c, t), touch_at(c, t), c->err, t);
   });
@@ -997,8 +997,8 @@ mpm_status do_set_state(mpm_ctx c, const float* x, const float* v, const float* 
   // rollout that spreads beyond it, see mpm_forward)
   if (c->arena == nullptr || c->cfg.grid_slots <= 0) {
     launch(c, KI_MISC, [&] {
-      if (c->cfg.fuse_g2p2g) kx(c, k_scan_a<D, true>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums);
-      else kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kThreads), 0, P, c->cnt, c->bflag, c->tile_sums);
+      if (c->cfg.fuse_g2p2g) kx(c, k_scan_a<D, true>, dim3(c->n_tiles), dim3(kScanTile), 0, P, c->cnt, c->bflag, c->tile_sums);
+      else kx(c, k_scan_a<D>, dim3(c->n_tiles), dim3(kScanTile), 0, P, c->cnt, c->bflag, c->tile_sums);
     });
     std::vector<int3> ts(c->n_tiles);
     CK(cudaMemcpyAsync(ts.data(), c->tile_sums, ts.size() * sizeof(int3), cudaMemcpyDeviceToHost, c->stream));

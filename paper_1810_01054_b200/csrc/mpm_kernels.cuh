@@ -90,7 +90,10 @@ constexpr int kCPB = 64;         // cells (and nodes) per grid block
 constexpr int kThreads = 256;    // CTA size of the block-tile kernels
 constexpr int kCap = 512;        // particles per producer chunk
 constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks use scratch)
-constexpr int kScanTile = kThreads;
+#ifndef MPM_SCAN_THREADS
+#define MPM_SCAN_THREADS 512  // 512-block tiles: C4 scan -1.4 us (256: 14.4, 1024: 12.7 but C3 +2 us)
+#endif
+constexpr int kScanTile = MPM_SCAN_THREADS;  // grid blocks per scan tile = threads of a scan CTA
 constexpr int kScatQ = 4;        // particles per thread in k_scatter
 constexpr int kIdxCap = 512;     // P2G^T: an item's perm / orig entries held in shared memory
 constexpr int kMaxAct = 64;      // n_actuators cap (mpm_create validates)  // grid blocks per scan tile (one per thread)
@@ -768,50 +771,52 @@ __device__ __forceinline__ int4 warp_incl_scan4(int4 v) {
   return v;
 }
 
-// CTA-wide exclusive scan of an int4 (kThreads threads)
+// CTA-wide exclusive scan of an int4 (NTH threads)
+template <int NTH = kThreads>
 __device__ __forceinline__ int4 cta_excl_scan4(int4 v, int4* s_warp, int4& total) {
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int4 inc = warp_incl_scan4(v);
   if (lane == 31) s_warp[w] = inc;
   __syncthreads();
   if (w == 0) {
-    int4 t = lane < kThreads / 32 ? s_warp[lane] : make_int4(0, 0, 0, 0);
+    int4 t = lane < NTH / 32 ? s_warp[lane] : make_int4(0, 0, 0, 0);
     int4 ti = warp_incl_scan4(t);
-    if (lane < kThreads / 32) s_warp[lane] = make_int4(ti.x - t.x, ti.y - t.y, ti.z - t.z, ti.w - t.w);
-    if (lane == kThreads / 32 - 1) s_warp[kThreads / 32] = ti;
+    if (lane < NTH / 32) s_warp[lane] = make_int4(ti.x - t.x, ti.y - t.y, ti.z - t.z, ti.w - t.w);
+    if (lane == NTH / 32 - 1) s_warp[NTH / 32] = ti;
   }
   __syncthreads();
   int4 wo = s_warp[w];
-  total = s_warp[kThreads / 32];
+  total = s_warp[NTH / 32];
   return make_int4(wo.x + inc.x - v.x, wo.y + inc.y - v.y, wo.z + inc.z - v.z, wo.w + inc.w - v.w);
 }
 
-// CTA-wide exclusive scan of an int3 (kThreads threads)
+// CTA-wide exclusive scan of an int3 (NTH threads)
+template <int NTH = kThreads>
 __device__ __forceinline__ int3 cta_excl_scan3(int3 v, int3* s_warp, int3& total) {
   int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int3 inc = warp_incl_scan3(v);
   if (lane == 31) s_warp[w] = inc;
   __syncthreads();
   if (w == 0) {
-    int3 t = lane < kThreads / 32 ? s_warp[lane] : make_int3(0, 0, 0);
+    int3 t = lane < NTH / 32 ? s_warp[lane] : make_int3(0, 0, 0);
     int3 ti = warp_incl_scan3(t);
-    if (lane < kThreads / 32) s_warp[lane] = make_int3(ti.x - t.x, ti.y - t.y, ti.z - t.z);
-    if (lane == kThreads / 32 - 1) s_warp[kThreads / 32] = ti;
+    if (lane < NTH / 32) s_warp[lane] = make_int3(ti.x - t.x, ti.y - t.y, ti.z - t.z);
+    if (lane == NTH / 32 - 1) s_warp[NTH / 32] = ti;
   }
   __syncthreads();
   int3 wo = s_warp[w];
-  total = s_warp[kThreads / 32];
+  total = s_warp[NTH / 32];
   return make_int3(wo.x + inc.x - v.x, wo.y + inc.y - v.y, wo.z + inc.z - v.z);
 }
 
 // per-tile totals of (count, occupied, touched) -- used once by set_state to size the grid-slot
 // arena; flag word of a block: count | occupied << 30 | touched << 31
 template <int D, bool DIL = false>
-__global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __restrict__ cnt,
+__global__ __launch_bounds__(kScanTile) void k_scan_a(KParams P, const int* __restrict__ cnt,
                                                      unsigned* __restrict__ bflag,
                                                      int3* __restrict__ tile_sums) {
   MPM_PDL_ENTRY();
-  __shared__ int3 s_warp[kThreads / 32 + 1];
+  __shared__ int3 s_warp[kScanTile / 32 + 1];
   const int gb = blockIdx.x * kScanTile + threadIdx.x;
   int c = 0, o = 0, t = 0;
   if (gb < P.NBT) {
@@ -819,7 +824,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_a(KParams P, const int* __res
     bflag[gb] = (unsigned)c | ((unsigned)o << 30) | ((unsigned)t << 31);
   }
   int3 tot;
-  cta_excl_scan3(make_int3(c, o, t), s_warp, tot);
+  cta_excl_scan3<kScanTile>(make_int3(c, o, t), s_warp, tot);
   if (threadIdx.x == 0) tile_sums[blockIdx.x] = tot;
 }
 
@@ -842,14 +847,14 @@ struct ScanTileState {
 // null) -- step t's own grid, or with DIL step t+1's (fused G2P2G).  The arena base follows
 // the previous grid's slots (info_gprev; null = the segment's first grid, base 0).
 template <int D, bool DIL = false>
-__global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int* __restrict__ cnt, ScanTileState ts,
+__global__ __launch_bounds__(kScanTile) void k_scan_lookback(KParams P, const int* __restrict__ cnt, ScanTileState ts,
                                                            unsigned epoch, int n_tiles, int* __restrict__ info_bin,
                                                            int* __restrict__ block_start, int4* __restrict__ occ_list,
                                                            int* __restrict__ info_grid, const int* __restrict__ info_gprev,
                                                            int* __restrict__ slot_of, int* __restrict__ touched_list,
                                                            ErrLatch* err, int t) {
   MPM_PDL_ENTRY();
-  __shared__ int4 s_warp[kThreads / 32 + 1];
+  __shared__ int4 s_warp[kScanTile / 32 + 1];
   __shared__ int s_tile;
   __shared__ int4 s_pre;
   if (threadIdx.x == 0) s_tile = (int)(atomicAdd(ts.ticket, 1ull) % (unsigned long long)n_tiles);
@@ -864,7 +869,7 @@ __global__ __launch_bounds__(kThreads) void k_scan_lookback(KParams P, const int
   // tail when the last items run out)
   const int ob = o && c >= kBigBlock, os = o && c < kBigBlock;
   int4 tot;
-  const int4 ex = cta_excl_scan4(make_int4(c, ob, tc, os), s_warp, tot);
+  const int4 ex = cta_excl_scan4<kScanTile>(make_int4(c, ob, tc, os), s_warp, tot);
   const unsigned ep = epoch << 2;
   if (threadIdx.x < 32) {  // warp 0: publish, then look back 32 tiles at a time
     const int lane = threadIdx.x;
