@@ -432,7 +432,7 @@ void launch_bin(mpm_ctx c, int t) {
 void launch_scatter(mpm_ctx c, int t, const int* za, const int* zb) {
   const KParams& P = c->P;
   launch(c, KI_SCATTER, [&] {
-    kx(c, k_scatter, dim3(std::max(1, std::min(grid1d(P.NT), c->n_sm * 8))), dim3(256), 0, P.NT, c->key, bs_at(c, t),
+    kx(c, k_scatter, dim3(std::max(1, std::min(grid1d(P.NT), c->n_sm * MPM_SCAT_CTAS))), dim3(256), 0, P.NT, c->key, bs_at(c, t),
        c->cnt, c->tmp_pk, za, zb, c->arena, nslot_at(c, t));
   });
 }
@@ -843,7 +843,7 @@ void backward_phase_b(mpm_ctx c, int t) {
     A.agrid_prev = agrid_of(c, t - 1);
   } else {
     launch(c, KI_GRIDT, [&] {
-      kx(c, k_grid_adj<D>, dim3(c->n_sm * 8), dim3(256), 0, P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
+      kx(c, k_grid_adj<D>, dim3(c->n_sm * MPM_GRIDT_CTAS), dim3(256), 0, P, info_at(c, t), touch_at(c, t), c->arena, A.grid,
                                                          t > c->seg0 ? info_at(c, t - 1) : nullptr, agrid_of(c, t - 1));
     });
   }

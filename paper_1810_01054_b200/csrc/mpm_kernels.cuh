@@ -94,7 +94,16 @@ constexpr int kSortCap = 2048;   // in-smem cell sort capacity (larger blocks us
 #define MPM_SCAN_THREADS 512  // 512-block tiles: C4 scan -1.4 us (256: 14.4, 1024: 12.7 but C3 +2 us)
 #endif
 constexpr int kScanTile = MPM_SCAN_THREADS;  // grid blocks per scan tile = threads of a scan CTA
-constexpr int kScatQ = 4;        // particles per thread in k_scatter
+#ifndef MPM_SCAT_CTAS
+#define MPM_SCAT_CTAS 8  // k_scatter CTAs per SM (256 threads)
+#endif
+#ifndef MPM_GRIDT_CTAS
+#define MPM_GRIDT_CTAS 8  // k_grid_adj CTAs per SM (256 threads)
+#endif
+#ifndef MPM_SCATQ
+#define MPM_SCATQ 4
+#endif
+constexpr int kScatQ = MPM_SCATQ;  // particles per thread in k_scatter
 constexpr int kIdxCap = 512;     // P2G^T: an item's perm / orig entries held in shared memory
 constexpr int kMaxAct = 64;      // n_actuators cap (mpm_create validates)  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
