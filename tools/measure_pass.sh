@@ -1,6 +1,6 @@
 # measurement pass (run on the GPU box from the repo root; outputs under gpurun_out/): ncu full capture first
-# this build's counters), then bench lines, reference arm, small configs, paper cubes, parity
-# margins, ncu launch list
+# (so the bench line's traffic and issue view use this build's counters), then bench lines, reference arm,
+# small configs, paper cubes, ncu launch list
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt
 EXTRA=$(python tools/ncu_summary.py --metrics)
