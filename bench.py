@@ -182,9 +182,13 @@ def run_ours(args):
 
     from paper_1810_01054_b200 import mpm
 
-    D = parallel.init_from_env("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else None)
+    # MPM_BENCH_SHARED_GPU=1 (tests only): the ranks share cuda:0 and talk through gloo (slab
+    # exchanges through a host-staged transport) -- checks the N > 1 harness on a 1-GPU box;
+    # its timings mean nothing
+    shared = os.environ.get("MPM_BENCH_SHARED_GPU") == "1"
+    D = parallel.init_from_env("gloo" if shared else ("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else None))
     world, rank, local = D.world, D.rank, D.local_rank
-    dev = torch.device("cuda", local if world > 1 else 0)
+    dev = torch.device("cuda", local if world > 1 and not shared else 0)
     torch.cuda.set_device(dev)
     K, W = args.steps, args.warmup
     seg = min(K, SEG)
@@ -196,7 +200,10 @@ def run_ours(args):
     if slabs is not None:
         sim.set_slab(*slabs[rank], 1)
         if world > 1:
-            parallel.init_slab_comm(sim, D)
+            if shared:
+                sim.set_transport(parallel.gloo_transport(D))
+            else:
+                parallel.init_slab_comm(sim, D)
     NT = sc.batch * sc.n
     m = torch.tensor(sc.mass, device=dev, dtype=torch.float64)  # [B][N]
     seed = torch.zeros((NT, 3), device=dev, dtype=torch.float32)
@@ -403,10 +410,14 @@ def run_reference(args):
     metric / config / unit.  Each step is one forward + one backward step of the FULL C4 state
     (1,048,576 particles, the bench workload) when K steps fit REF_BUDGET_S; otherwise of a
     sub-slab of the same slab at the same density, sized to fit."""
-    import oracle
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # torchrun sets OMP_NUM_THREADS=1 per rank; rank 0 runs the oracle alone here, on all
+        # the cores it may use (set before the OpenMP runtime is loaded)
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
+    import oracle
     K, W = args.steps, args.warmup
     full = scenes.slab_3d(seed=0, steps=2)
     f, fb = _oracle_fb(full, 1, "omp64")  # first warm-up step, on the full state

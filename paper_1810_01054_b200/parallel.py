@@ -76,6 +76,8 @@ def max_over_ranks(x: float, d: Dist, device=None) -> float:
         return float(x)
     import torch
     import torch.distributed as dist
+    if dist.get_backend() == "gloo":
+        device = None  # host tensors for gloo
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -162,6 +164,30 @@ def shard_slab(sc, lo: int, hi: int):
         setattr(out, name, np.ascontiguousarray(getattr(sc, name)[:, idx]))
     out.meta = dict(sc.meta, slab=(lo, hi))
     return out, idx
+
+
+def gloo_transport(d: Dist):
+    """A host-staged slab-exchange callback for `MPM.set_transport` over the default
+    torch.distributed process group (e.g. gloo, ranks sharing one GPU): neighbour windows /
+    migrants / adjoints with isend/irecv to rank -+ 1, the gradient sums with all_reduce."""
+    import torch
+    import torch.distributed as dist
+
+    def xchg(kind, sl, sr, rl, rr):
+        if kind == "reduce":
+            t = torch.from_numpy(sl)
+            dist.all_reduce(t)
+            return
+        reqs = []
+        if sl is not None:
+            reqs.append(dist.isend(torch.from_numpy(sl.copy()), d.rank - 1))
+            reqs.append(dist.irecv(torch.from_numpy(rl), d.rank - 1))
+        if sr is not None:
+            reqs.append(dist.isend(torch.from_numpy(sr.copy()), d.rank + 1))
+            reqs.append(dist.irecv(torch.from_numpy(rr), d.rank + 1))
+        for r in reqs:
+            r.wait()
+    return xchg
 
 
 def init_slab_comm(sim, d: Dist):
