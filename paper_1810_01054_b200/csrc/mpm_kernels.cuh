@@ -67,6 +67,9 @@
 #ifndef MPM_P2GT_IDXSM
 #define MPM_P2GT_IDXSM 1
 #endif
+#ifndef MPM_FUSE_SPERM
+#define MPM_FUSE_SPERM 1
+#endif
 #ifndef MPM_P2GT_CLAIM
 #define MPM_P2GT_CLAIM 1  // P2G^T work items claimed and decoded by thread 0 (claim_item)
 #endif
@@ -104,6 +107,7 @@ constexpr int kScanTile = MPM_SCAN_THREADS;  // grid blocks per scan tile = thre
 #define MPM_SCATQ 4
 #endif
 constexpr int kScatQ = MPM_SCATQ;  // particles per thread in k_scatter
+constexpr int kCapPerm = 512;    // fused G2P2G: the block's sorted order kept in shared memory
 constexpr int kIdxCap = 512;     // P2G^T: an item's perm / orig entries held in shared memory
 constexpr int kMaxAct = 64;      // n_actuators cap (mpm_create validates)  // grid blocks per scan tile (one per thread)
 constexpr float kEps = 1e-10f;   // step-L epsilon (R7)
@@ -1287,8 +1291,9 @@ __device__ __noinline__ void sort_crowded_cells(int* perm, int* buf, const int* 
 // (storage index, key) pairs, are sorted by (cell, storage index) (stable, R18) into
 // perm[s .. s+n); s_cstart gets the cells' ranges.  CTA-wide (contains barriers).
 template <int D, bool PF_XF = false>
-__device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs& A, int s, int n, int tid,
-                                                int* s_hist, int* s_cstart, int* s_cursor, int* s_sort) {
+__device__ __forceinline__ bool block_cell_sort(const KParams& P, const StepArgs& A, int s, int n, int tid,
+                                                int* s_hist, int* s_cstart, int* s_cursor, int* s_sort,
+                                                int* s_pout = nullptr) {
   const size_t NT = P.NT;
   // (storage index, cell) of this thread's first two particles stay in registers
   int pj[2] = {0, 0}, pc[2] = {0, 0};
@@ -1346,6 +1351,7 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
 #pragma unroll 4
     for (int q = lo; q < hi; ++q) rank += buf[q] < j;
     A.perm[s + lo + rank] = j;
+    if (s_pout && lo + rank < kCapPerm) s_pout[lo + rank] = j;  // the caller's shared copy
   };
 #pragma unroll
   for (int q = 0; q < 2; ++q)
@@ -1356,6 +1362,7 @@ __device__ __forceinline__ void block_cell_sort(const KParams& P, const StepArgs
   }
   if (crowd) sort_crowded_cells(A.perm + s, buf, s_cstart, tid);
   __syncthreads();
+  return crowd;  // uniform; crowded cells are not in s_pout
 }
 
 // Scatter consumer: thread (ox, c), c = cell, accumulates the NSUB nodes c + (ox, *) of the
@@ -1896,9 +1903,9 @@ template <int D, bool COH = false, bool PRM = false>
 __device__ __forceinline__ bool g2p_particle(const KParams& P, const StepArgs& A, const float4* s_v,
                                              const float4& vref, const int* bc, int r, int k, float (&x)[D],
                                              float (&vn)[D], float (&Cn)[D][D], float (&Hn)[D][D], int& u,
-                                             float4* pr = nullptr, int* ai = nullptr) {
+                                             float4* pr = nullptr, int* ai = nullptr, int j_in = -1) {
   const size_t NT = P.NT;
-  const int j = COH ? __ldcg(&A.perm[k]) : __ldg(&A.perm[k]);
+  const int j = j_in >= 0 ? j_in : COH ? __ldcg(&A.perm[k]) : __ldg(&A.perm[k]);
   float H[D][D];  // H = F - I
 #pragma unroll
   for (int a = 0; a < D; ++a) {
@@ -2091,6 +2098,7 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
   int* s_sort = SCAT ? reinterpret_cast<int*>(s_dyn) : s_sort_st;  // the sort is done before the payload is written
   __shared__ WorkSh<D> s_w;
   __shared__ int s_nesc;
+  __shared__ int s_perm[MPM_FUSE_SPERM && SORT ? kCapPerm : 1];  // the sorted order of the block (SORT)
   const int tid = threadIdx.x;
   const int n_occ = A.info_t[I_NOCC];
   const int ox = tid / kCPB;
@@ -2138,10 +2146,12 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
     // grid t's tile first: its loads are independent of the sort and overlap its phases
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
 #endif
+    bool pcrowd = true;
     if (SORT) {
       if (tid < kCPB) s_hist[tid] = 0;
       __syncthreads();
-      block_cell_sort<D, true>(P, A, s0, n0, tid, s_hist, s_cstart, s_cursor, s_sort);
+      pcrowd = block_cell_sort<D, true>(P, A, s0, n0, tid, s_hist, s_cstart, s_cursor, s_sort,
+                                        MPM_FUSE_SPERM ? s_perm : nullptr);
     }
 #if !MPM_FUSE_STAGE_FIRST
     stage_tile<D, false>(P, A, r, bc, s_v, nullptr, 0, vref, aref_unused);
@@ -2158,7 +2168,10 @@ __global__ __launch_bounds__(kThreads, MPM_FUSE_MINB) void k_g2p2g(KParams P, St
         float x[D], vn[D], Cn[D][D], Hn[D][D];
         int u, ai = -1;
         float4 pr;  // m, V, mu, lam
-        const bool ok = g2p_particle<D, SORT, SCAT>(P, A, s_v, vref, bc, r, s + lo + pi, x, vn, Cn, Hn, u, &pr, &ai);
+        // the sorted storage index from the sort's shared copy (no global round trip)
+        const int pj = s + lo + pi - s0;  // position in the whole block's sorted order
+        const int jin = (MPM_FUSE_SPERM && SORT && !pcrowd && pj < kCapPerm) ? s_perm[pj] : -1;
+        const bool ok = g2p_particle<D, SORT, SCAT>(P, A, s_v, vref, bc, r, s + lo + pi, x, vn, Cn, Hn, u, &pr, &ai, jin);
         if constexpr (SCAT) {
           Stencil<D> sc;
           make_stencil<D>(x, P.fres, sc);
