@@ -65,10 +65,10 @@
 #define MPM_GRIDT_FUSED 1  // small problems: gridT folded into P2G^T's tile staging (no k_grid_adj launch)
 #endif
 #ifndef MPM_P2GT_IDXSM
-#define MPM_P2GT_IDXSM 1
+#define MPM_P2GT_IDXSM 1  // P2G^T: each item's perm / orig staged in shared memory with the tile (-0.8 us)
 #endif
 #ifndef MPM_FUSE_SPERM
-#define MPM_FUSE_SPERM 1
+#define MPM_FUSE_SPERM 1  // fused G2P2G: the in-block sort's order kept in shared memory for the producer (-0.5 us)
 #endif
 #ifndef MPM_P2GT_CLAIM
 #define MPM_P2GT_CLAIM 1  // P2G^T work items claimed and decoded by thread 0 (claim_item)
