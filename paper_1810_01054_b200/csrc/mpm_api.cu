@@ -838,7 +838,7 @@ void backward_phase_b(mpm_ctx c, int t) {
   A.gin = c->bcur;
   A.gout = c->bnxt;
   if (has_nbr(c)) launch_band_unpack(c, t, true, A.grid);
-  if (MPM_GRIDT_FUSED && c->split) {  // small problems: gridT inside P2G^T's tile staging; P2G^T
+  if (MPM_GRIDT_FUSED && (c->split || MPM_GRIDT_FUSED >= 2)) {  // small problems: gridT inside P2G^T's tile staging; P2G^T
     A.info_prev = t > c->seg0 ? info_at(c, t - 1) : nullptr;  // also prepares step t-1's adjoint grid
     A.agrid_prev = agrid_of(c, t - 1);
   } else {

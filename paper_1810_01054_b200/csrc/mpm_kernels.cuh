@@ -62,7 +62,8 @@
 #define MPM_P2GT_PARK 3  // record rows parked in shared memory (1: dL/dx, dL/dF; 2: + H; 3: + v, C): -9.5 us
 #endif
 #ifndef MPM_GRIDT_FUSED
-#define MPM_GRIDT_FUSED 1  // small problems: gridT folded into P2G^T's tile staging (no k_grid_adj launch)
+#define MPM_GRIDT_FUSED 1  // gridT folded into P2G^T's tile staging (no k_grid_adj launch): 1 = small
+                           // problems (the SPLIT path), 2 = always (C4: P2G^T +9 us, bench +8 us)
 #endif
 #ifndef MPM_P2GT_IDXSM
 #define MPM_P2GT_IDXSM 1  // P2G^T: each item's perm / orig staged in shared memory with the tile (-0.8 us)
@@ -599,13 +600,6 @@ __device__ __forceinline__ void project_node_adj(const float* vbar, float* g, co
     }
   }
   for (int w = nw - 1; w >= 0; --w) project_wall_adj<D>(vin[w], g, wax[w], wsg[w], wc[w]);
-}
-
-// the wall-band nodes' projection adjoint out of line (rare; keeps its replay arrays out of
-// the register allocation of the kernels that stage tiles)
-template <int D>
-__device__ __noinline__ void band_node_adj(const float* vbar, float* g, const int* node, const KParams& P) {
-  project_node_adj<D>(vbar, g, node, P);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1748,7 +1742,7 @@ __device__ __forceinline__ void fetch_node_slot(const KParams& P, const StepArgs
     vg[0] = fmaf(pm.x, im, P.dt * P.g[0]); vg[1] = fmaf(pm.y, im, P.dt * P.g[1]);
     gv[0] = ad.x; gv[1] = ad.y;
     if constexpr (D == 3) { vg[2] = fmaf(pm.z, im, P.dt * P.g[2]); gv[2] = ad.z; }
-    if (in_band<D>(node, P.res, P.bound)) band_node_adj<D>(vg, gv, node, P);
+    if (in_band<D>(node, P.res, P.bound)) project_node_adj<D>(vg, gv, node, P);
     float pg = 0.f;
 #pragma unroll
     for (int d = 0; d < D; ++d) pg = fmaf(vg[d] - P.dt * P.g[d], gv[d], pg);
@@ -2778,7 +2772,7 @@ __global__ __launch_bounds__(MPM_P2GT_THREADS, MPM_P2GT_MINB) void k_p2g_adj(KPa
   // latency-bound chain; at C4 scale it costs more inside the staging than the k_grid_adj launch
   // it saves: P2G^T +18 us for gridT's 10); its other job moves here: zero the adjoint grid of
   // step t-1 (G2P^T of t-1 accumulates into it) and reset that step's work counters
-  constexpr bool RAW = SPLIT && MPM_GRIDT_FUSED;
+  constexpr bool RAW = (SPLIT || MPM_GRIDT_FUSED >= 2) && MPM_GRIDT_FUSED;
   if (RAW && A.info_prev) adj_prepare(A.info_prev, A.agrid_prev, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   for (;;) {
 #if MPM_P2GT_CLAIM
