@@ -91,3 +91,11 @@ def test_binding_checks_dtype_size_layout_and_device():
     assert _out(np.zeros((3, 2), np.float32), np.float32, (3, 2)) is not None
     with pytest.raises(TypeError):
         _in([1.0, 2.0], np.float32, (2,))
+
+
+def test_bundled_nccl_lookup():
+    """The binding points libmpm's lazy NCCL load at the nvidia-nccl wheel torch bundles (so a
+    later `import torch` keeps its libnccl.so.2), found without importing torch."""
+    from paper_1810_01054_b200 import mpm
+    p = mpm._bundled_nccl()
+    assert p is None or (os.path.basename(p) == "libnccl.so.2" and os.path.exists(p))

@@ -35,6 +35,12 @@ def test_bench_two_ranks_one_json_line(workload):
     d = _run(workload, ("--no-cpu-baseline",))
     assert d["n_gpus"] == 2 and d["steps"] == 2 and d["warmup"] == 3
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    for k in ("metric", "unit", "ms_per_step", "higher_is_better", "scaling", "dtype", "data", "config", "roofline",
+              "clocks", "e2e"):
+        assert k in d, k
+    # C4: one rollout per rank (weak); C5b: the 64 rollouts shared out, C5a: one body split (strong)
+    assert d["scaling"] == ("weak" if workload == "C4" else "strong") and d["higher_is_better"] is True
+    assert d["roofline"]["frac"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
     cfg = d["config"]
     if workload == "C5a":  # one body split into two x-slabs: the job is the whole body
         assert cfg["particles_per_rank"] < 8_355_840 and "slab" in cfg["parallelism"]
