@@ -6,6 +6,8 @@ checkpoint interval (N2), the mass gradient (N3), running-loss seeds on intermed
 (N4) and the horizon -- so that combinations the hand-written cases do not name are
 exercised too.  Bars as in the other parity tests: state at the field scale 1e-4, gradients
 1e-3 norm-wise (R16) and element-wise at the field scale; binning bit-exact at every resident step."""
+import os
+
 import numpy as np
 import pytest
 
@@ -15,14 +17,16 @@ from tests.helpers import assert_grads, oracle_cfg, oracle_params, oracle_state,
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 160
+# MPM_SWEEP_CASES / MPM_SWEEP_SEED (default 160 / 0): a longer or different sweep on demand
+N_CASES = int(os.environ.get("MPM_SWEEP_CASES", "160"))
+SEED0 = int(os.environ.get("MPM_SWEEP_SEED", "0"))
 # per-wall friction draws: sticky (c < 0, R6), frictionless, sliding, and the full stop of
 # step L (c >= 1 stops a node whose |l_n| exceeds l_t / c: R < 0, H(R) = 0)
 FRICTIONS = [-1.0, 0.0, 0.5, 1.0, 2.0]
 
 
 def _case(i):
-    rng = np.random.default_rng(9100 + i)
+    rng = np.random.default_rng(9100 + SEED0 + i)
     d = 2 + i % 2
     res = int(rng.choice([16, 32, 64]))
     n_cells = tuple(int(c) for c in rng.integers(1, 11, d))
@@ -33,7 +37,7 @@ def _case(i):
     T = int(rng.integers(2, 13))
     fric = tuple(float(rng.choice(FRICTIONS)) for _ in range(2 * d)) + (0.0,) * (6 - 2 * d)
     g = tuple(float(v) for v in rng.uniform(-10.0, 10.0, d))
-    sc = scenes.tiny(d, seed=9200 + i, res=res, n_cells=n_cells, center=lo, steps=T, K=K,
+    sc = scenes.tiny(d, seed=9200 + SEED0 + i, res=res, n_cells=n_cells, center=lo, steps=T, K=K,
                      s=float(rng.uniform(0.0, 50.0)), gravity=g, friction=fric)
     opts = dict(material=int(i % 4 == 3), fuse=int(rng.integers(0, 2)),
                 ck=int(rng.choice([0, 0, 2, 3, 5])), mass_grad=bool(rng.integers(0, 2)),
