@@ -96,7 +96,7 @@ def test_random_scene_forward_backward(i):
     assert_grads(pairs, ctx=o)
 
 
-N_BATCH_CASES = 32
+N_BATCH_CASES = int(os.environ.get("MPM_SWEEP_BATCH_CASES", "32"))
 
 
 def _batch_case(i):
@@ -104,7 +104,7 @@ def _batch_case(i):
     each its own block placement, velocities, F0, C0, E, actuation, so the rollouts' blocks
     interleave in the block table differently at every step."""
     import dataclasses
-    rng = np.random.default_rng(9500 + i)
+    rng = np.random.default_rng(9500 + SEED0 + i)
     d = 2 + i % 2
     B = int(rng.integers(2, 5))
     res = int(rng.choice([16, 32]))
@@ -169,7 +169,7 @@ def test_random_batch_forward_backward(i):
         assert_grads(pairs, ctx=(r, o))
 
 
-N_SLAB_CASES = 24
+N_SLAB_CASES = int(os.environ.get("MPM_SWEEP_SLAB_CASES", "24"))
 
 
 def _slab_case(i):
@@ -177,7 +177,7 @@ def _slab_case(i):
     boundaries: random slab count, halo width, grid, body extent, drift speed across the
     slab boundaries, gravity, friction and actuators."""
     from paper_1810_01054_b200 import parallel
-    rng = np.random.default_rng(9800 + i)
+    rng = np.random.default_rng(9800 + SEED0 + i)
     d = 2 + i % 2
     res = int(rng.choice([32, 64])) if d == 3 else int(rng.choice([64, 128]))
     nbp = res // parallel.block_size(d)
@@ -190,7 +190,7 @@ def _slab_case(i):
     fric = tuple(float(rng.choice(FRICTIONS)) for _ in range(2 * d)) + (0.0,) * (6 - 2 * d)
     g = tuple(float(v) for v in rng.uniform(-10.0, 10.0, d))
     v0 = (float(rng.choice([-1.0, 1.0]) * rng.uniform(0.0, 8.0)),) + (0.0,) * (d - 1)
-    sc = scenes.tiny(d, seed=9900 + i, res=res, n_cells=n_cells, center=lo, steps=T,
+    sc = scenes.tiny(d, seed=9900 + SEED0 + i, res=res, n_cells=n_cells, center=lo, steps=T,
                      K=int(rng.integers(0, 3)), s=float(rng.uniform(0.0, 50.0)), gravity=g,
                      friction=fric, v0=v0)
     while G > 2:  # every slab owns particles (the ABI requires n_particles >= 1 per context)
@@ -208,7 +208,7 @@ def test_random_slab_split(i):
     _check_slab_run(sc, T, G, halo, seed=9950 + i)
 
 
-N_CTRL_CASES = 16
+N_CTRL_CASES = int(os.environ.get("MPM_SWEEP_CTRL_CASES", "16"))
 
 
 @pytest.mark.parametrize("i", range(N_CTRL_CASES))
@@ -217,14 +217,14 @@ def test_random_controller(i):
     actuator count, weight scale, bias and target; state, every state/parameter gradient and
     dL/dW, dL/db, dL/dtarget against the controller oracle (oracle/controller.py)."""
     from oracle import controller as ctl
-    rng = np.random.default_rng(10100 + i)
+    rng = np.random.default_rng(10100 + SEED0 + i)
     d = 2 + i % 2
     res = int(rng.choice([16, 32]))
     n_cells = tuple(int(c) for c in rng.integers(2, 9, d))
     lo = tuple(int(rng.integers(1, res - n_cells[a] - 1)) for a in range(d))
     K = int(rng.integers(1, 5))
     T = int(rng.integers(2, 16))
-    sc = scenes.tiny(d, seed=10200 + i, res=res, n_cells=n_cells, center=lo, steps=T, K=K,
+    sc = scenes.tiny(d, seed=10200 + SEED0 + i, res=res, n_cells=n_cells, center=lo, steps=T, K=K,
                      s=float(rng.uniform(10.0, 50.0)),
                      friction=tuple(float(rng.choice([0.0, 0.5])) for _ in range(2 * d)) + (0.0,) * (6 - 2 * d))
     nz = ctl.n_obs(d, K)
